@@ -1,0 +1,248 @@
+/*
+ * include/wfcu.h -- C ABI of libwfcu.so, the B200 (sm_100a) implementation of the
+ * MapReduce word-frequency hot path of arXiv 2206.05269.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no C++ or torch types.
+ * The reference's C++ API (/root/reference/proj/include/wfc/*.hpp) is re-implemented
+ * on top of these entry points by paper_2206_05269_b200/host (libwfc_b200.so), and
+ * INTEGRATION.md shows the binding a reference maintainer would add.  Each entry
+ * point names the reference interface it replaces (paths relative to
+ * /root/reference/).
+ *
+ * Conventions
+ *   - every function returns WFCU_OK (0) or a negative WFCU_ERR_* code and never
+ *     throws; wfcu_last_error() returns the thread-local message of the last
+ *     failure (reference: exceptions, proj/include/wfc/pipeline.hpp:33-41).
+ *   - there is NO CPU fallback: without a usable CUDA device every compute entry
+ *     point returns WFCU_ERR_NO_DEVICE.
+ *   - "host" pointers are ordinary host memory owned by the caller and borrowed
+ *     for the duration of the call (reference: std::span / const& arguments);
+ *     "dev" pointers are device addresses in the current CUDA context (a
+ *     torch.Tensor.data_ptr() works), 16-byte aligned.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = default stream).
+ *   - token keys are exported as packed byte strings in unsigned byte-wise
+ *     lexicographic order = std::map<std::string,...> iteration order
+ *     (proj/include/wfc/reduce.hpp:15).
+ */
+#ifndef WFCU_H
+#define WFCU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WFCU_API __attribute__((visibility("default")))
+
+#define WFCU_OK 0
+#define WFCU_ERR_INVALID_ARGUMENT (-1) /* reference: std::invalid_argument                     */
+#define WFCU_ERR_CUDA (-2)             /* CUDA runtime failure; shim rethrows PipelineError     */
+#define WFCU_ERR_NO_DEVICE (-3)        /* no sm_100 device / driver: the product has no CPU path */
+#define WFCU_ERR_TABLE_FULL (-4)       /* device count table over its load limit                 */
+#define WFCU_ERR_DEFERRED_FULL (-5)    /* slow-path fragment list over capacity                  */
+#define WFCU_ERR_ARENA_FULL (-6)       /* long-token arena / long table over capacity            */
+#define WFCU_ERR_BUFFER_TOO_SMALL (-7) /* caller-provided output buffer too small                */
+#define WFCU_ERR_NOT_SORTED (-8)       /* reduce_sorted on an unsorted list (std::invalid_argument) */
+
+/* MapKind, proj/include/wfc/engine.hpp:12-16; the first three values are the
+ * reference's, `square` is appended for BASELINE.json config 2 (f(x)=x^2). */
+#define WFCU_MAP_IDENTITY 0
+#define WFCU_MAP_SQUARE_ROOT 1
+#define WFCU_MAP_ALTERNATING_HARMONIC_TERM 2
+#define WFCU_MAP_SQUARE 3
+
+#define WFCU_DTYPE_F32 0
+#define WFCU_DTYPE_F64 1
+
+WFCU_API const char* wfcu_last_error(void);
+WFCU_API const char* wfcu_version(void);
+
+/* Number of usable CUDA devices (0 when there is none), and selection of the
+ * device the calling thread works on.  One process per GPU is the intended
+ * deployment (bench.py / torchrun); the library keeps per-device workspaces. */
+WFCU_API int wfcu_device_count(void);
+WFCU_API int wfcu_set_device(int device);
+/* 148 on B200; grids are sized in multiples of this. */
+WFCU_API int wfcu_sm_count(int* out);
+
+/* ------------------------------------------------------------------------- */
+/* Generic map-then-reduce engine  (proj/include/wfc/engine.hpp:25-36,        */
+/* proj/src/engine.cpp:15-98)                                                 */
+/* ------------------------------------------------------------------------- */
+
+/* sum_i map(values[i]) over device-resident values; positions are 1-based and
+ * start at position_base+1 (so a rank holding a slice passes its slice offset).
+ * Grid-stride, 16-byte vector loads, fp64 accumulation, warp-shuffle tree and a
+ * fixed-order final pass: the result is bitwise reproducible run to run and
+ * within 1e-5 relative (in practice ~1e-15) of map_reduce_serial
+ * (proj/src/engine.cpp:82-86).  values may be NULL for
+ * WFCU_MAP_ALTERNATING_HARMONIC_TERM.  *out is a HOST double; the call
+ * synchronises the stream. */
+WFCU_API int wfcu_map_reduce_dev(const void* dev_values, int dtype, uint64_t n, uint64_t position_base,
+                        int map_kind, void* stream, double* out);
+
+/* Same, but leaves the result in a device double (no host sync) -- what bench.py
+ * times for the resident-data number and what precedes the allreduce. */
+WFCU_API int wfcu_map_reduce_dev_async(const void* dev_values, int dtype, uint64_t n, uint64_t position_base,
+                              int map_kind, void* stream, double* dev_out);
+
+/* The reference's blocked engine, reproduced BIT FOR BIT on the device:
+ * ceil(n/block_size) left-to-right block folds (fold_range, engine.cpp:15-20)
+ * combined by the fixed pairwise tree (combine_tree, engine.cpp:23-34).  Equals
+ * map_reduce_blocked(values, map, {block_size, any workers}) exactly
+ * (proj/src/engine.cpp:88-92); block_size == 0 -> WFCU_ERR_INVALID_ARGUMENT
+ * (engine.cpp:38-40). */
+WFCU_API int wfcu_map_reduce_blocked_dev(const void* dev_values, int dtype, uint64_t n, uint64_t position_base,
+                                int map_kind, uint64_t block_size, void* stream, double* out);
+
+/* Host-buffer forms: what wfc::map_reduce_serial / map_reduce_blocked /
+ * alternating_harmonic call (H2D copy inside). */
+WFCU_API int wfcu_map_reduce_host(const void* host_values, int dtype, uint64_t n, int map_kind, double* out);
+WFCU_API int wfcu_map_reduce_blocked_host(const void* host_values, int dtype, uint64_t n, int map_kind,
+                                 uint64_t block_size, double* out);
+WFCU_API int wfcu_alternating_harmonic(uint64_t n, uint64_t block_size, double* out);
+
+/* ------------------------------------------------------------------------- */
+/* Tokenizer + counting map  (proj/src/text.cpp:9-57, proj/src/unicode.cpp,   */
+/* proj/src/pipeline.cpp:131-139  ++counts[word])                             */
+/* ------------------------------------------------------------------------- */
+
+typedef struct wfcu_counter wfcu_counter; /* device-resident word -> count table */
+
+typedef struct wfcu_counter_config {
+    uint64_t table_slots;    /* open-addressing slots (rounded up to 2^k); 0 = default 2^22   */
+    uint64_t deferred_slots; /* capacity of the slow-path fragment list; 0 = default 2^22     */
+    uint64_t arena_bytes;    /* arena for tokens longer than 16 bytes; 0 = default 64 MiB     */
+    uint64_t long_slots;     /* slots of the long-token table; 0 = default 2^20               */
+} wfcu_counter_config;
+
+WFCU_API int wfcu_counter_create(wfcu_counter** out, const wfcu_counter_config* cfg /* NULL = defaults */);
+WFCU_API void wfcu_counter_destroy(wfcu_counter* c);
+/* Empties the table (async on stream). */
+WFCU_API int wfcu_counter_reset(wfcu_counter* c, void* stream);
+
+/* Tokenizes dev_text[0..n) exactly like wfc::tokenize (whitespace split, case
+ * fold, edge trim, UTF-8 rules of proj/src/unicode.cpp) and adds every token to
+ * the table.  The buffer is treated as one document; concatenate documents with
+ * an ASCII whitespace byte between them (document ends are fragment ends,
+ * proj/src/text.cpp:55).  Asynchronous on `stream`; capacity overflows are
+ * reported by wfcu_counter_status / the export calls. */
+WFCU_API int wfcu_counter_count_dev(wfcu_counter* c, const uint8_t* dev_text, uint64_t n, void* stream);
+
+/* Host-buffer form (what wfc::serial_wordcount / run_wordcount call): packs the
+ * documents with '\n' separators into pinned staging memory, copies them to the
+ * device in chunks overlapped with counting, and waits for completion. */
+WFCU_API int wfcu_counter_count_host(wfcu_counter* c, const uint8_t* const* docs, const uint64_t* doc_lens,
+                            uint64_t n_docs);
+
+/* Synchronises and reports overflow conditions (WFCU_ERR_TABLE_FULL, ...). */
+WFCU_API int wfcu_counter_status(wfcu_counter* c, void* stream);
+
+/* Distinct tokens, total tokens and total key bytes currently in the table. */
+WFCU_API int wfcu_counter_stats(wfcu_counter* c, void* stream, uint64_t* distinct, uint64_t* total_tokens,
+                       uint64_t* key_bytes);
+
+/* Exports the table in std::map order: key_bytes (>= key_bytes from stats),
+ * key_lens[distinct], counts[distinct].  Capacities are in elements/bytes. */
+WFCU_API int wfcu_counter_export(wfcu_counter* c, void* stream, uint8_t* key_bytes, uint64_t key_bytes_cap,
+                        uint32_t* key_lens, uint64_t* counts, uint64_t entries_cap);
+
+/* dst[word] += src[word]  (merge_counts, proj/src/reduce.cpp:83-89), on device. */
+WFCU_API int wfcu_counter_merge(wfcu_counter* dst, const wfcu_counter* src, void* stream);
+
+/* Adds explicit (word, count) pairs -- the inverse of export; used to rebuild a
+ * table from a CountMap. */
+WFCU_API int wfcu_counter_add_words(wfcu_counter* c, const uint8_t* key_bytes, const uint32_t* key_lens,
+                           const uint64_t* counts, uint64_t n_words);
+
+/* ------------------------------------------------------------------------- */
+/* Hash-partitioned exchange (replaces the range-partition shuffle,           */
+/* proj/src/shuffle.cpp:9-168, as BASELINE.json asks)           */
+/* ------------------------------------------------------------------------- */
+
+/* Fixed-width wire entry of the all-to-all: 32 bytes.  Keys of at most 16
+ * bytes travel inline (big-endian packed, zero padded); longer tokens travel
+ * in a separate byte stream (wfcu_counter_long_records). */
+typedef struct wfcu_entry {
+    uint64_t k0, k1; /* token bytes 0..7 / 8..15, first byte most significant */
+    uint64_t count;
+    uint64_t aux;    /* reserved (0) */
+} wfcu_entry;
+
+/* owner(word) in [0, n_parts): the partition function of the exchange. */
+WFCU_API uint32_t wfcu_owner_of(const uint8_t* word, uint32_t len, uint32_t n_parts);
+
+/* Groups the table's inline entries by owner: dev_entries receives them
+ * partition by partition, dev_part_counts[n_parts] (device uint64) the size of
+ * each partition.  entries_cap >= distinct.  Asynchronous. */
+WFCU_API int wfcu_counter_partition(wfcu_counter* c, uint32_t n_parts, wfcu_entry* dev_entries,
+                           uint64_t entries_cap, uint64_t* dev_part_counts, void* stream);
+
+/* Inserts n received entries (summing counts of equal keys). Asynchronous. */
+WFCU_API int wfcu_counter_merge_entries(wfcu_counter* c, const wfcu_entry* dev_entries, uint64_t n, void* stream);
+
+/* Long tokens (> 16 bytes) as a self-describing device byte stream of records
+ * {u64 count, u32 len, u32 hash, bytes..., pad to 8}.  *n_bytes (host) gets the
+ * stream length; dev_out may be NULL to query the size. */
+WFCU_API int wfcu_counter_long_records(wfcu_counter* c, uint8_t* dev_out, uint64_t out_cap, uint64_t* n_bytes,
+                              void* stream);
+/* Inserts the records of a stream whose owner (wfcu_owner_of) is `part` of
+ * n_parts (n_parts == 1 keeps everything). */
+WFCU_API int wfcu_counter_merge_long_records(wfcu_counter* c, const uint8_t* dev_records, uint64_t n_bytes,
+                                    uint32_t part, uint32_t n_parts, void* stream);
+
+/* ------------------------------------------------------------------------- */
+/* Tokenizer as a stand-alone stage and the sort + run-length-encode reduce   */
+/* (proj/src/text.cpp:32-63, proj/src/reduce.cpp:8-21)                        */
+/* ------------------------------------------------------------------------- */
+
+typedef struct wfcu_tokens wfcu_tokens; /* device-resident token list in text order */
+
+/* wfc::tokenize on a device buffer: tokens in text order. */
+WFCU_API int wfcu_tokenize_dev(const uint8_t* dev_text, uint64_t n, void* stream, wfcu_tokens** out);
+WFCU_API int wfcu_tokenize_host(const uint8_t* text, uint64_t n, wfcu_tokens** out);
+WFCU_API void wfcu_tokens_destroy(wfcu_tokens* t);
+WFCU_API int wfcu_tokens_stats(const wfcu_tokens* t, uint64_t* n_tokens, uint64_t* n_bytes);
+/* Packed copy-out: token bytes concatenated + per-token lengths. */
+WFCU_API int wfcu_tokens_export(const wfcu_tokens* t, uint8_t* bytes, uint64_t bytes_cap, uint32_t* lens,
+                       uint64_t lens_cap);
+/* Builds a device token list from packed host words (WordList -> device). */
+WFCU_API int wfcu_tokens_from_words(const uint8_t* bytes, const uint32_t* lens, uint64_t n_tokens,
+                           wfcu_tokens** out);
+/* sort_words (proj/src/text.cpp:59-63): stable byte-wise sort, in place. */
+WFCU_API int wfcu_tokens_sort(wfcu_tokens* t, void* stream);
+/* reduce_sorted (proj/src/reduce.cpp:8-21): run-length encodes a sorted list
+ * into the counter; WFCU_ERR_NOT_SORTED if the list is not in order. */
+WFCU_API int wfcu_tokens_reduce_sorted(const wfcu_tokens* t, wfcu_counter* into, void* stream);
+/* The sort + RLE alternative end to end on a device buffer: tokenize, sort,
+ * run-length encode, add the runs to the counter. */
+WFCU_API int wfcu_counter_count_dev_sorted(wfcu_counter* c, const uint8_t* dev_text, uint64_t n, void* stream);
+
+/* ------------------------------------------------------------------------- */
+/* Synthetic corpora for BASELINE.json configs 3-5; host-side */
+/* generator, deterministic for (seed, doc index).                            */
+/* ------------------------------------------------------------------------- */
+
+/* Fills out[0..doc_bytes) with document `doc` of a Zipf(s) corpus over a
+ * `vocab`-word vocabulary.  `speaker` permutes 1 % of the ranks (config 5). */
+WFCU_API int wfcu_synth_document(uint64_t seed, uint64_t doc, uint32_t vocab, double zipf_s, uint32_t speaker,
+                        uint8_t* out, uint64_t doc_bytes);
+/* Documents [doc_begin, doc_end) back to back ('\n' ends every document), using
+ * `threads` host threads (0 = all). */
+WFCU_API int wfcu_synth_corpus(uint64_t seed, uint64_t doc_begin, uint64_t doc_end, uint32_t vocab,
+                      double zipf_s, uint32_t speaker, uint64_t doc_bytes, uint8_t* out, int threads);
+
+/* The reference bench's input recipe (proj/src/cli.cpp:120-125): n draws of
+ * std::mt19937_64(seed) through std::uniform_real_distribution<double>(0,1),
+ * stored as double (WFCU_DTYPE_F64) or rounded to float (WFCU_DTYPE_F32). */
+WFCU_API int wfcu_synth_uniform(uint64_t seed, uint64_t n, int dtype, void* out);
+
+/* Number of kernels this library has launched in this process (bench.py's
+ * gpu_launches evidence). */
+WFCU_API uint64_t wfcu_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WFCU_H */

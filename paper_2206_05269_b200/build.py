@@ -1,0 +1,105 @@
+"""In-tree build of the native libraries (nvcc for sm_100a, g++ for the host shim).
+
+  paper_2206_05269_b200/lib/libwfcu.so      CUDA kernels + the C ABI of include/wfcu.h
+  paper_2206_05269_b200/lib/libwfc_b200.so  C++ drop-in for the reference's wfc:: API
+                                            (host/include/wfc/*.hpp) on top of the C ABI
+  paper_2206_05269_b200/lib/wfc_dropin_tests  the reference-style C++ test binary
+
+The outputs are git-ignored but travel to the GPU box with the gpurun snapshot.
+`python -m paper_2206_05269_b200.build` rebuilds when a source is newer than the output.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+HOST = PKG / "host"
+LIB = PKG / "lib"
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC,-fvisibility=hidden,-O2",
+    "--expt-relaxed-constexpr",
+]
+
+
+def _nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found; the CUDA extension cannot be built")
+
+
+def _stale(out: Path, deps: list[Path]) -> bool:
+    if not out.exists():
+        return True
+    t = out.stat().st_mtime
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def _run(cmd: list[str]) -> None:
+    proc = subprocess.run(cmd, capture_output=True, text=True)
+    if proc.returncode != 0:
+        sys.stderr.write(" ".join(cmd) + "\n" + proc.stdout + proc.stderr)
+        raise RuntimeError(f"build step failed: {cmd[0]} (exit {proc.returncode})")
+
+
+def build_wfcu(force: bool = False, verbose: bool = False) -> Path:
+    LIB.mkdir(exist_ok=True)
+    out = LIB / "libwfcu.so"
+    cu = sorted(CSRC.glob("*.cu"))
+    cpp = sorted(CSRC.glob("*.cpp"))
+    hdr = sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "wfcu.h"]
+    if not force and not _stale(out, cu + cpp + hdr):
+        return out
+    objs = []
+    obj_dir = LIB / "obj"
+    obj_dir.mkdir(exist_ok=True)
+    for src in cu + cpp:
+        obj = obj_dir / (src.name + ".o")
+        if force or _stale(obj, [src] + hdr):
+            cmd = [_nvcc(), *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+            _run(cmd)
+        objs.append(str(obj))
+    _run([_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(out), *objs,
+          "-Xlinker", "--no-undefined", "-lpthread"])
+    return out
+
+
+def build_host(force: bool = False) -> Path | None:
+    """C++ drop-in (libwfc_b200.so) and its test binary; needs libwfcu.so first."""
+    if not HOST.exists():
+        return None
+    LIB.mkdir(exist_ok=True)
+    out = LIB / "libwfc_b200.so"
+    srcs = sorted((HOST / "src").glob("*.cpp"))
+    hdrs = sorted((HOST / "include" / "wfc").glob("*.hpp")) + [ROOT / "include" / "wfcu.h"]
+    cxx = os.environ.get("CXX") or shutil.which("g++") or "g++"
+    common = [cxx, "-std=c++20", "-O2", "-fPIC", "-pthread", f"-I{HOST / 'include'}", f"-I{ROOT / 'include'}"]
+    if force or _stale(out, srcs + hdrs + [LIB / "libwfcu.so"]):
+        _run(common + ["-shared", "-o", str(out), *map(str, srcs), f"-L{LIB}", "-lwfcu", "-Wl,-rpath,$ORIGIN"])
+    tests = sorted((HOST / "tests").glob("*.cpp"))
+    if tests:
+        exe = LIB / "wfc_dropin_tests"
+        if force or _stale(exe, tests + hdrs + [out]):
+            _run(common + ["-o", str(exe), *map(str, tests), f"-L{LIB}", "-lwfc_b200", "-lwfcu", "-Wl,-rpath,$ORIGIN"])
+    return out
+
+
+def build_all(force: bool = False, verbose: bool = False) -> None:
+    build_wfcu(force, verbose)
+    build_host(force)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print("built:", *(p.name for p in sorted(LIB.glob("*")) if p.is_file()))

@@ -1,0 +1,690 @@
+// capi.cu -- the extern "C" surface declared in include/wfcu.h.
+// Thin host logic only: argument checks, workspace ownership, launches.  Every
+// compute step is a kernel in wordcount.cu / mapreduce.cu / table_ops.cu /
+// tokens.cu; there is no CPU implementation of the path behind any entry point.
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/wfcu.h"
+#include "wfcu_dev.cuh"
+
+namespace wfcu {
+// wordcount.cu
+cudaError_t wc_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream, u64* launches);
+// mapreduce.cu
+cudaError_t mr_launch(const void* values, int is_f64, u64 n, u64 base, int kind, int grid, double* partials,
+                      double* dev_out, cudaStream_t s, u64* launches);
+cudaError_t mr_blocked_launch(const void* values, int is_f64, u64 n, u64 base, int kind, u64 block, double* buf_a,
+                              double* buf_b, double* dev_out, int sm_count, cudaStream_t s, u64* launches);
+// table_ops.cu
+cudaError_t tb_compact(const TableView& t, Slot* out, u64 cap, u64* dev_count, int sm, cudaStream_t s, u64* launches);
+cudaError_t tb_key_bytes(const TableView& t, u64* dev_bytes, int sm, cudaStream_t s, u64* launches);
+cudaError_t tb_partition(const TableView& t, u32 n_parts, Slot* out, u64 cap, u64* dev_part_counts, u64* cursors,
+                         int sm, cudaStream_t s, u64* launches);
+cudaError_t tb_merge_entries(const TableView& t, const Slot* in, u64 n, int sm, cudaStream_t s, u64* launches);
+cudaError_t tb_merge_table(const TableView& dst, const TableView& src, int sm, cudaStream_t s, u64* launches);
+cudaError_t tb_long_serialize(const TableView& t, uint8_t* out, u64 cap, u64* dev_bytes, int sm, cudaStream_t s,
+                              u64* launches);
+cudaError_t tb_long_merge(const TableView& t, const uint8_t* recs, u64 n_bytes, u32 part, u32 n_parts, cudaStream_t s,
+                          u64* launches);
+// synth.cpp
+int synth_document(uint64_t seed, uint64_t doc, uint32_t vocab, double s, uint32_t speaker, uint8_t* out, uint64_t doc_bytes);
+int synth_corpus(uint64_t seed, uint64_t doc_begin, uint64_t doc_end, uint32_t vocab, double s, uint32_t speaker,
+                 uint64_t doc_bytes, uint8_t* out, int threads);
+int synth_uniform(uint64_t seed, uint64_t n, int as_f64, void* out);
+}  // namespace wfcu
+
+using namespace wfcu;
+
+// ---- error plumbing -------------------------------------------------------------
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+static int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+#define CUDA_TRY(expr)                                                                           \
+    do {                                                                                         \
+        cudaError_t _e = (expr);                                                                 \
+        if (_e != cudaSuccess) return fail(WFCU_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
+    } while (0)
+
+struct LaunchTally {   // adds to the global launch counter on scope exit
+    u64 n = 0;
+    ~LaunchTally() { g_launches += n; }
+};
+
+// ---- device state -----------------------------------------------------------------
+struct DeviceState {
+    bool ready = false;
+    int sm_count = 0;
+    double* mr_partials = nullptr;   // kMrGridMax doubles
+    double* mr_out = nullptr;        // device result
+    u64* scratch = nullptr;          // 64 u64 of device scratch (counts, cursors)
+};
+static constexpr int kMaxDevices = 64;
+static DeviceState g_dev[kMaxDevices];
+static std::mutex g_dev_mu;
+
+static int current_device_state(DeviceState** out) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count <= 0) {
+        cudaGetLastError();
+        return fail(WFCU_ERR_NO_DEVICE, "no CUDA device available (%s); libwfcu has no CPU path",
+                    e == cudaSuccess ? "device count 0" : cudaGetErrorString(e));
+    }
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    if (dev >= kMaxDevices) return fail(WFCU_ERR_NO_DEVICE, "device index %d out of range", dev);
+    std::lock_guard<std::mutex> lock(g_dev_mu);
+    DeviceState& d = g_dev[dev];
+    if (!d.ready) {
+        cudaDeviceProp prop;
+        CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
+        if (prop.major != 10)
+            return fail(WFCU_ERR_NO_DEVICE, "device %d is sm_%d%d; libwfcu is built for sm_100a only", dev, prop.major,
+                        prop.minor);
+        d.sm_count = prop.multiProcessorCount;
+        CUDA_TRY(cudaMalloc(&d.mr_partials, sizeof(double) * 8192));
+        CUDA_TRY(cudaMalloc(&d.mr_out, sizeof(double)));
+        CUDA_TRY(cudaMalloc(&d.scratch, sizeof(u64) * 64));
+        d.ready = true;
+    }
+    *out = &d;
+    return WFCU_OK;
+}
+
+extern "C" const char* wfcu_last_error(void) { return g_last_error.c_str(); }
+extern "C" const char* wfcu_version(void) { return "wfcu 0.1 (sm_100a)"; }
+extern "C" uint64_t wfcu_launch_count(void) { return g_launches.load(); }
+
+extern "C" int wfcu_device_count(void) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return count;
+}
+extern "C" int wfcu_set_device(int device) {
+    CUDA_TRY(cudaSetDevice(device));
+    return WFCU_OK;
+}
+extern "C" int wfcu_sm_count(int* out) {
+    DeviceState* d;
+    if (int rc = current_device_state(&d)) return rc;
+    *out = d->sm_count;
+    return WFCU_OK;
+}
+
+// ---- map-then-reduce ----------------------------------------------------------------
+static int check_map_args(int dtype, int kind, const void* values, uint64_t n) {
+    if (dtype != WFCU_DTYPE_F32 && dtype != WFCU_DTYPE_F64) return fail(WFCU_ERR_INVALID_ARGUMENT, "unknown dtype %d", dtype);
+    if (kind < 0 || kind > WFCU_MAP_SQUARE) return fail(WFCU_ERR_INVALID_ARGUMENT, "unknown map kind");
+    if (!values && n && kind != WFCU_MAP_ALTERNATING_HARMONIC_TERM)
+        return fail(WFCU_ERR_INVALID_ARGUMENT, "values is null");
+    if (values && (reinterpret_cast<uintptr_t>(values) & 15u))
+        return fail(WFCU_ERR_INVALID_ARGUMENT, "device values must be 16-byte aligned");
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_map_reduce_dev_async(const void* dev_values, int dtype, uint64_t n, uint64_t position_base,
+                                         int map_kind, void* stream, double* dev_out) {
+    DeviceState* d;
+    if (int rc = current_device_state(&d)) return rc;
+    if (int rc = check_map_args(dtype, map_kind, dev_values, n)) return rc;
+    if (!dev_out) return fail(WFCU_ERR_INVALID_ARGUMENT, "dev_out is null");
+    // grid: a multiple of the SM count, never more CTAs than 16-byte vectors need
+    const u64 vec = (dtype == WFCU_DTYPE_F64) ? 2 : 4;
+    u64 want = (n / vec + 256 * 4 - 1) / (256 * 4);
+    int grid = d->sm_count * 8;
+    if (map_kind == WFCU_MAP_ALTERNATING_HARMONIC_TERM) want = (n + 255) / 256;
+    if ((u64)grid > want) grid = (int)std::max<u64>(1, want);
+    LaunchTally tally;
+    CUDA_TRY(mr_launch(dev_values, dtype == WFCU_DTYPE_F64, n, position_base, map_kind, grid, d->mr_partials, dev_out,
+                       (cudaStream_t)stream, &tally.n));
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_map_reduce_dev(const void* dev_values, int dtype, uint64_t n, uint64_t position_base, int map_kind,
+                                   void* stream, double* out) {
+    DeviceState* d;
+    if (int rc = current_device_state(&d)) return rc;
+    if (!out) return fail(WFCU_ERR_INVALID_ARGUMENT, "out is null");
+    if (int rc = wfcu_map_reduce_dev_async(dev_values, dtype, n, position_base, map_kind, stream, d->mr_out)) return rc;
+    CUDA_TRY(cudaMemcpyAsync(out, d->mr_out, sizeof(double), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_map_reduce_blocked_dev(const void* dev_values, int dtype, uint64_t n, uint64_t position_base,
+                                           int map_kind, uint64_t block_size, void* stream, double* out) {
+    DeviceState* d;
+    if (int rc = current_device_state(&d)) return rc;
+    if (block_size == 0) return fail(WFCU_ERR_INVALID_ARGUMENT, "block_size and workers must be >= 1");
+    if (int rc = check_map_args(dtype, map_kind, dev_values, n)) return rc;
+    if (!out) return fail(WFCU_ERR_INVALID_ARGUMENT, "out is null");
+    const u64 nb = (n + block_size - 1) / block_size;
+    double *a = nullptr, *b = nullptr;
+    CUDA_TRY(cudaMalloc(&a, sizeof(double) * std::max<u64>(nb, 1)));
+    if (cudaMalloc(&b, sizeof(double) * std::max<u64>(nb / 2 + 1, 1)) != cudaSuccess) {
+        cudaFree(a);
+        return fail(WFCU_ERR_CUDA, "cudaMalloc of the partials failed");
+    }
+    LaunchTally tally;
+    cudaError_t e = mr_blocked_launch(dev_values, dtype == WFCU_DTYPE_F64, n, position_base, map_kind, block_size, a, b,
+                                      d->mr_out, d->sm_count, (cudaStream_t)stream, &tally.n);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, d->mr_out, sizeof(double), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+    cudaFree(a);
+    cudaFree(b);
+    if (e != cudaSuccess) return fail(WFCU_ERR_CUDA, "blocked map-reduce: %s", cudaGetErrorString(e));
+    return WFCU_OK;
+}
+
+static int upload(const void* host, uint64_t bytes, void** dev) {
+    *dev = nullptr;
+    if (bytes == 0) return WFCU_OK;
+    CUDA_TRY(cudaMalloc(dev, bytes));
+    cudaError_t e = cudaMemcpy(*dev, host, bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(*dev);
+        *dev = nullptr;
+        return fail(WFCU_ERR_CUDA, "H2D copy: %s", cudaGetErrorString(e));
+    }
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_map_reduce_host(const void* host_values, int dtype, uint64_t n, int map_kind, double* out) {
+    DeviceState* d;
+    if (int rc = current_device_state(&d)) return rc;
+    if (!host_values && n && map_kind != WFCU_MAP_ALTERNATING_HARMONIC_TERM)
+        return fail(WFCU_ERR_INVALID_ARGUMENT, "values is null");
+    void* dev = nullptr;
+    const uint64_t esz = dtype == WFCU_DTYPE_F64 ? 8 : 4;
+    if (map_kind != WFCU_MAP_ALTERNATING_HARMONIC_TERM)
+        if (int rc = upload(host_values, n * esz, &dev)) return rc;
+    const int rc = wfcu_map_reduce_dev(dev, dtype, n, 0, map_kind, nullptr, out);
+    cudaFree(dev);
+    return rc;
+}
+
+extern "C" int wfcu_map_reduce_blocked_host(const void* host_values, int dtype, uint64_t n, int map_kind,
+                                            uint64_t block_size, double* out) {
+    DeviceState* d;
+    if (int rc = current_device_state(&d)) return rc;
+    if (block_size == 0) return fail(WFCU_ERR_INVALID_ARGUMENT, "block_size and workers must be >= 1");
+    if (!host_values && n && map_kind != WFCU_MAP_ALTERNATING_HARMONIC_TERM)
+        return fail(WFCU_ERR_INVALID_ARGUMENT, "values is null");
+    void* dev = nullptr;
+    const uint64_t esz = dtype == WFCU_DTYPE_F64 ? 8 : 4;
+    if (map_kind != WFCU_MAP_ALTERNATING_HARMONIC_TERM)
+        if (int rc = upload(host_values, n * esz, &dev)) return rc;
+    const int rc = wfcu_map_reduce_blocked_dev(dev, dtype, n, 0, map_kind, block_size, nullptr, out);
+    cudaFree(dev);
+    return rc;
+}
+
+extern "C" int wfcu_alternating_harmonic(uint64_t n, uint64_t block_size, double* out) {
+    return wfcu_map_reduce_blocked_dev(nullptr, WFCU_DTYPE_F64, n, 0, WFCU_MAP_ALTERNATING_HARMONIC_TERM, block_size,
+                                       nullptr, out);
+}
+
+// ---- counter ------------------------------------------------------------------------
+struct wfcu_counter {
+    int device = 0;
+    int sm_count = 0;
+    TableView v{};
+    u64 table_slots = 0, long_slots = 0;
+    u64* counters = nullptr;    // device: [0] n_used [1] n_tokens [2] n_deferred [3] n_long [4] arena_used
+                                //         [5] status(int) [6..15] scratch
+    // host staging for count_host
+    uint8_t* pinned[2] = {nullptr, nullptr};
+    uint8_t* devbuf[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    u64 chunk_cap = 0;
+    cudaStream_t stream = nullptr;
+};
+
+static u64 round_pow2(u64 x) {
+    u64 p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+static void counter_free(wfcu_counter* c) {
+    if (!c) return;
+    cudaFree(c->v.slots);
+    cudaFree(c->v.deferred);
+    cudaFree(c->v.long_ref);
+    cudaFree(c->v.long_count);
+    cudaFree(c->v.arena);
+    cudaFree(c->counters);
+    for (int i = 0; i < 2; ++i) {
+        if (c->pinned[i]) cudaFreeHost(c->pinned[i]);
+        if (c->devbuf[i]) cudaFree(c->devbuf[i]);
+        if (c->done[i]) cudaEventDestroy(c->done[i]);
+    }
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+extern "C" int wfcu_counter_reset(wfcu_counter* c, void* stream) {
+    if (!c) return fail(WFCU_ERR_INVALID_ARGUMENT, "counter is null");
+    cudaStream_t s = (cudaStream_t)stream;
+    CUDA_TRY(cudaMemsetAsync(c->v.slots, 0, sizeof(Slot) * c->table_slots, s));
+    CUDA_TRY(cudaMemsetAsync(c->v.long_ref, 0, sizeof(u64) * c->long_slots, s));
+    CUDA_TRY(cudaMemsetAsync(c->v.long_count, 0, sizeof(u64) * c->long_slots, s));
+    CUDA_TRY(cudaMemsetAsync(c->counters, 0, sizeof(u64) * 16, s));
+    const u64 arena_start = 8;   // offset 0 means "empty"
+    CUDA_TRY(cudaMemcpyAsync(c->v.arena_used, &arena_start, sizeof(u64), cudaMemcpyHostToDevice, s));
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_counter_create(wfcu_counter** out, const wfcu_counter_config* cfg) {
+    if (!out) return fail(WFCU_ERR_INVALID_ARGUMENT, "out is null");
+    *out = nullptr;
+    DeviceState* d;
+    if (int rc = current_device_state(&d)) return rc;
+    wfcu_counter_config k{};
+    if (cfg) k = *cfg;
+    auto* c = new wfcu_counter;
+    cudaGetDevice(&c->device);
+    c->sm_count = d->sm_count;
+    c->table_slots = round_pow2(k.table_slots ? std::max<u64>(k.table_slots, 1024) : (1ull << 22));
+    c->long_slots = round_pow2(k.long_slots ? std::max<u64>(k.long_slots, 1024) : (1ull << 20));
+    const u64 deferred = k.deferred_slots ? k.deferred_slots : (1ull << 22);
+    const u64 arena = k.arena_bytes ? std::max<u64>(k.arena_bytes, 4096) : (64ull << 20);
+    cudaError_t e = cudaSuccess;
+    auto alloc = [&](void** p, u64 bytes) {
+        if (e == cudaSuccess) e = cudaMalloc(p, bytes);
+    };
+    alloc((void**)&c->v.slots, sizeof(Slot) * c->table_slots);
+    alloc((void**)&c->v.deferred, sizeof(u64) * deferred);
+    alloc((void**)&c->v.long_ref, sizeof(u64) * c->long_slots);
+    alloc((void**)&c->v.long_count, sizeof(u64) * c->long_slots);
+    alloc((void**)&c->v.arena, arena);
+    alloc((void**)&c->counters, sizeof(u64) * 16);
+    if (e != cudaSuccess) {
+        counter_free(c);
+        return fail(WFCU_ERR_CUDA, "counter allocation: %s", cudaGetErrorString(e));
+    }
+    c->v.mask = c->table_slots - 1;
+    c->v.max_used = c->table_slots / 10 * 7;
+    c->v.n_used = c->counters + 0;
+    c->v.n_tokens = c->counters + 1;
+    c->v.n_deferred = c->counters + 2;
+    c->v.n_long = c->counters + 3;
+    c->v.arena_used = c->counters + 4;
+    c->v.status = reinterpret_cast<int*>(c->counters + 5);
+    c->v.deferred_cap = deferred;
+    c->v.long_mask = c->long_slots - 1;
+    c->v.arena_cap = arena;
+    if (int rc = wfcu_counter_reset(c, nullptr)) {
+        counter_free(c);
+        return rc;
+    }
+    if (cudaStreamSynchronize(nullptr) != cudaSuccess) {
+        counter_free(c);
+        return fail(WFCU_ERR_CUDA, "counter reset failed");
+    }
+    *out = c;
+    return WFCU_OK;
+}
+
+extern "C" void wfcu_counter_destroy(wfcu_counter* c) {
+    if (c) cudaSetDevice(c->device);
+    counter_free(c);
+}
+
+extern "C" int wfcu_counter_count_dev(wfcu_counter* c, const uint8_t* dev_text, uint64_t n, void* stream) {
+    if (!c) return fail(WFCU_ERR_INVALID_ARGUMENT, "counter is null");
+    if (n == 0) return WFCU_OK;
+    if (!dev_text) return fail(WFCU_ERR_INVALID_ARGUMENT, "text is null");
+    if (reinterpret_cast<uintptr_t>(dev_text) & 15u)
+        return fail(WFCU_ERR_INVALID_ARGUMENT, "device text must be 16-byte aligned");
+    LaunchTally tally;
+    CUDA_TRY(wc_launch(dev_text, n, c->v, c->sm_count, (cudaStream_t)stream, &tally.n));
+    return WFCU_OK;
+}
+
+static int status_to_rc(int st) {
+    if (st & kStatusTableFull) return fail(WFCU_ERR_TABLE_FULL, "count table over its load limit; recreate with more table_slots");
+    if (st & kStatusDeferredFull) return fail(WFCU_ERR_DEFERRED_FULL, "slow-path fragment list full; recreate with more deferred_slots");
+    if (st & (kStatusArenaFull | kStatusLongFull)) return fail(WFCU_ERR_ARENA_FULL, "long-token arena/table full; recreate with more arena_bytes / long_slots");
+    if (st & kStatusNotSorted) return fail(WFCU_ERR_NOT_SORTED, "reduce_sorted: word list must be sorted");
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_counter_status(wfcu_counter* c, void* stream) {
+    if (!c) return fail(WFCU_ERR_INVALID_ARGUMENT, "counter is null");
+    int st = 0;
+    CUDA_TRY(cudaMemcpyAsync(&st, c->v.status, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    return status_to_rc(st);
+}
+
+extern "C" int wfcu_counter_stats(wfcu_counter* c, void* stream, uint64_t* distinct, uint64_t* total_tokens,
+                                  uint64_t* key_bytes) {
+    if (!c) return fail(WFCU_ERR_INVALID_ARGUMENT, "counter is null");
+    cudaStream_t s = (cudaStream_t)stream;
+    LaunchTally tally;
+    CUDA_TRY(tb_key_bytes(c->v, c->counters + 6, c->sm_count, s, &tally.n));
+    u64 h[8];
+    CUDA_TRY(cudaMemcpyAsync(h, c->counters, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (int rc = status_to_rc((int)(h[5] & 0xFFFFFFFFu))) return rc;
+    if (distinct) *distinct = h[0] + h[3];
+    if (total_tokens) *total_tokens = h[1];
+    if (key_bytes) *key_bytes = h[6];
+    return WFCU_OK;
+}
+
+namespace {
+struct HostEntry {
+    std::string key;
+    u64 count;
+};
+}
+
+// Pulls every (word, count) pair to the host, unordered.
+static int counter_pull(wfcu_counter* c, cudaStream_t s, std::vector<HostEntry>* out) {
+    u64 h[8];
+    CUDA_TRY(cudaMemcpyAsync(h, c->counters, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (int rc = status_to_rc((int)(h[5] & 0xFFFFFFFFu))) return rc;
+    const u64 n_inline = h[0], n_long = h[3], arena_used = h[4];
+    out->clear();
+    out->reserve(n_inline + n_long);
+    LaunchTally tally;
+    if (n_inline) {
+        Slot* dense = nullptr;
+        CUDA_TRY(cudaMalloc(&dense, sizeof(Slot) * n_inline));
+        cudaError_t e = tb_compact(c->v, dense, n_inline, c->counters + 7, c->sm_count, s, &tally.n);
+        std::vector<Slot> hs(n_inline);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(hs.data(), dense, sizeof(Slot) * n_inline, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaFree(dense);
+        if (e != cudaSuccess) return fail(WFCU_ERR_CUDA, "table export: %s", cudaGetErrorString(e));
+        for (const Slot& sl : hs) {
+            uint8_t b[16];
+            key_to_bytes(sl.k0, sl.k1, b);
+            out->push_back({std::string(reinterpret_cast<const char*>(b), key_len(sl.k0, sl.k1)), sl.count});
+        }
+    }
+    if (n_long) {
+        std::vector<u64> refs(c->long_slots), counts(c->long_slots);
+        std::vector<uint8_t> arena(arena_used);
+        CUDA_TRY(cudaMemcpyAsync(refs.data(), c->v.long_ref, sizeof(u64) * c->long_slots, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(counts.data(), c->v.long_count, sizeof(u64) * c->long_slots, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(arena.data(), c->v.arena, arena_used, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        for (u64 i = 0; i < c->long_slots; ++i) {
+            if (!refs[i]) continue;
+            u32 len;
+            std::memcpy(&len, arena.data() + refs[i], 4);
+            out->push_back({std::string(reinterpret_cast<const char*>(arena.data() + refs[i] + 8), len), counts[i]});
+        }
+    }
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_counter_export(wfcu_counter* c, void* stream, uint8_t* key_bytes, uint64_t key_bytes_cap,
+                                   uint32_t* key_lens, uint64_t* counts, uint64_t entries_cap) {
+    if (!c) return fail(WFCU_ERR_INVALID_ARGUMENT, "counter is null");
+    std::vector<HostEntry> rows;
+    if (int rc = counter_pull(c, (cudaStream_t)stream, &rows)) return rc;
+    // std::map order = unsigned byte-wise lexicographic (std::string::compare uses char_traits<char>::compare = memcmp)
+    std::sort(rows.begin(), rows.end(), [](const HostEntry& a, const HostEntry& b) { return a.key < b.key; });
+    u64 total_bytes = 0;
+    for (const auto& r : rows) total_bytes += r.key.size();
+    if (rows.size() > entries_cap || total_bytes > key_bytes_cap)
+        return fail(WFCU_ERR_BUFFER_TOO_SMALL, "export needs %llu entries / %llu key bytes",
+                    (unsigned long long)rows.size(), (unsigned long long)total_bytes);
+    u64 off = 0;
+    for (size_t i = 0; i < rows.size(); ++i) {
+        std::memcpy(key_bytes + off, rows[i].key.data(), rows[i].key.size());
+        off += rows[i].key.size();
+        key_lens[i] = (u32)rows[i].key.size();
+        counts[i] = rows[i].count;
+    }
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_counter_merge(wfcu_counter* dst, const wfcu_counter* src, void* stream) {
+    if (!dst || !src) return fail(WFCU_ERR_INVALID_ARGUMENT, "counter is null");
+    cudaStream_t s = (cudaStream_t)stream;
+    LaunchTally tally;
+    CUDA_TRY(tb_merge_table(dst->v, src->v, dst->sm_count, s, &tally.n));
+    // long tokens: serialise src, re-insert into dst
+    u64 h[8];
+    CUDA_TRY(cudaMemcpyAsync(h, src->counters, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (h[3]) {
+        uint8_t* buf = nullptr;
+        const u64 cap = h[4] + 16 * h[3] + 64;
+        CUDA_TRY(cudaMalloc(&buf, cap));
+        cudaError_t e = tb_long_serialize(src->v, buf, cap, dst->counters + 8, dst->sm_count, s, &tally.n);
+        u64 nbytes = 0;
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&nbytes, dst->counters + 8, sizeof(u64), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e == cudaSuccess) e = tb_long_merge(dst->v, buf, nbytes, 0, 1, s, &tally.n);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaFree(buf);
+        if (e != cudaSuccess) return fail(WFCU_ERR_CUDA, "long-token merge: %s", cudaGetErrorString(e));
+    }
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_counter_add_words(wfcu_counter* c, const uint8_t* key_bytes, const uint32_t* key_lens,
+                                      const uint64_t* counts, uint64_t n_words) {
+    if (!c) return fail(WFCU_ERR_INVALID_ARGUMENT, "counter is null");
+    if (n_words == 0) return WFCU_OK;
+    if (!key_bytes || !key_lens || !counts) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
+    std::vector<Slot> inl;
+    std::vector<uint8_t> longs;
+    u64 off = 0;
+    for (u64 i = 0; i < n_words; ++i) {
+        const u32 len = key_lens[i];
+        if (len == 0) return fail(WFCU_ERR_INVALID_ARGUMENT, "empty word");
+        if (len <= 16) {
+            Slot s{};
+            key_from_bytes(key_bytes + off, len, &s.k0, &s.k1);
+            s.count = counts[i];
+            inl.push_back(s);
+        } else {
+            const u64 need = 16 + ((u64(len) + 7) & ~7ull);
+            const size_t at = longs.size();
+            longs.resize(at + need, 0);
+            const u32 h = fnv32(key_bytes + off, len);
+            std::memcpy(&longs[at], &counts[i], 8);
+            std::memcpy(&longs[at + 8], &len, 4);
+            std::memcpy(&longs[at + 12], &h, 4);
+            std::memcpy(&longs[at + 16], key_bytes + off, len);
+        }
+        off += len;
+    }
+    LaunchTally tally;
+    if (!inl.empty()) {
+        void* dev = nullptr;
+        if (int rc = upload(inl.data(), inl.size() * sizeof(Slot), &dev)) return rc;
+        cudaError_t e = tb_merge_entries(c->v, static_cast<const Slot*>(dev), inl.size(), c->sm_count, nullptr, &tally.n);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
+        cudaFree(dev);
+        if (e != cudaSuccess) return fail(WFCU_ERR_CUDA, "add_words: %s", cudaGetErrorString(e));
+    }
+    if (!longs.empty()) {
+        void* dev = nullptr;
+        if (int rc = upload(longs.data(), longs.size(), &dev)) return rc;
+        cudaError_t e = tb_long_merge(c->v, static_cast<const uint8_t*>(dev), longs.size(), 0, 1, nullptr, &tally.n);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
+        cudaFree(dev);
+        if (e != cudaSuccess) return fail(WFCU_ERR_CUDA, "add_words: %s", cudaGetErrorString(e));
+    }
+    return WFCU_OK;
+}
+
+// ---- host-buffer counting (the reference-facing call) ----------------------------------
+static int ensure_staging(wfcu_counter* c, u64 want) {
+    if (c->chunk_cap >= want) return WFCU_OK;
+    for (int i = 0; i < 2; ++i) {
+        if (c->pinned[i]) cudaFreeHost(c->pinned[i]);
+        if (c->devbuf[i]) cudaFree(c->devbuf[i]);
+        c->pinned[i] = nullptr;
+        c->devbuf[i] = nullptr;
+    }
+    c->chunk_cap = 0;
+    for (int i = 0; i < 2; ++i) {
+        CUDA_TRY(cudaHostAlloc((void**)&c->pinned[i], want, cudaHostAllocDefault));
+        CUDA_TRY(cudaMalloc((void**)&c->devbuf[i], want));
+        if (!c->done[i]) CUDA_TRY(cudaEventCreateWithFlags(&c->done[i], cudaEventDisableTiming));
+    }
+    if (!c->stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->chunk_cap = want;
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_counter_count_host(wfcu_counter* c, const uint8_t* const* docs, const uint64_t* doc_lens,
+                                       uint64_t n_docs) {
+    if (!c) return fail(WFCU_ERR_INVALID_ARGUMENT, "counter is null");
+    if (n_docs == 0) return WFCU_OK;
+    if (!docs || !doc_lens) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
+    u64 max_doc = 0, total = 0;
+    for (u64 d = 0; d < n_docs; ++d) {
+        if (doc_lens[d] && !docs[d]) return fail(WFCU_ERR_INVALID_ARGUMENT, "document %llu is null", (unsigned long long)d);
+        max_doc = std::max<u64>(max_doc, doc_lens[d]);
+        total += doc_lens[d] + 1;
+    }
+    // chunk = whole documents, '\n' after each; 64 MiB unless one document needs more
+    u64 chunk = std::min<u64>(std::max<u64>(total, 1 << 20), 64ull << 20);
+    chunk = std::max<u64>(chunk, max_doc + 1);
+    chunk = (chunk + 15) & ~15ull;
+    if (int rc = ensure_staging(c, chunk)) return rc;
+    // default-stream work issued earlier (reset, count_dev) must be visible to our stream
+    CUDA_TRY(cudaStreamSynchronize(nullptr));
+
+    int cur = 0;
+    u64 fill = 0;
+    bool used[2] = {false, false};
+    auto submit = [&]() -> int {
+        if (fill == 0) return WFCU_OK;
+        CUDA_TRY(cudaMemcpyAsync(c->devbuf[cur], c->pinned[cur], fill, cudaMemcpyHostToDevice, c->stream));
+        if (int rc = wfcu_counter_count_dev(c, c->devbuf[cur], fill, c->stream)) return rc;
+        CUDA_TRY(cudaEventRecord(c->done[cur], c->stream));
+        used[cur] = true;
+        cur ^= 1;
+        fill = 0;
+        if (used[cur]) CUDA_TRY(cudaEventSynchronize(c->done[cur]));   // buffer about to be refilled
+        return WFCU_OK;
+    };
+    for (u64 d = 0; d < n_docs; ++d) {
+        const u64 need = doc_lens[d] + 1;
+        if (fill + need > c->chunk_cap)
+            if (int rc = submit()) return rc;
+        std::memcpy(c->pinned[cur] + fill, docs[d], doc_lens[d]);
+        c->pinned[cur][fill + doc_lens[d]] = '\n';
+        fill += need;
+    }
+    if (int rc = submit()) return rc;
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return wfcu_counter_status(c, c->stream);
+}
+
+// ---- exchange -------------------------------------------------------------------------
+extern "C" uint32_t wfcu_owner_of(const uint8_t* word, uint32_t len, uint32_t n_parts) {
+    if (n_parts <= 1 || !word) return 0;
+    if (len <= 16) {
+        u64 k0, k1;
+        key_from_bytes(word, len, &k0, &k1);
+        return owner_mix32(k0, k1) % n_parts;
+    }
+    return ((fnv32(word, len) * 0x9E3779B1u) >> 7) % n_parts;
+}
+
+extern "C" int wfcu_counter_partition(wfcu_counter* c, uint32_t n_parts, wfcu_entry* dev_entries, uint64_t entries_cap,
+                                      uint64_t* dev_part_counts, void* stream) {
+    if (!c) return fail(WFCU_ERR_INVALID_ARGUMENT, "counter is null");
+    if (n_parts == 0 || n_parts > 4096) return fail(WFCU_ERR_INVALID_ARGUMENT, "n_parts must be in 1..4096");
+    if (!dev_entries || !dev_part_counts) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
+    static_assert(sizeof(wfcu_entry) == sizeof(Slot), "wire entry layout");
+    u64* cursors = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&cursors, sizeof(u64) * n_parts, (cudaStream_t)stream));
+    LaunchTally tally;
+    cudaError_t e = tb_partition(c->v, n_parts, reinterpret_cast<Slot*>(dev_entries), entries_cap,
+                                 reinterpret_cast<u64*>(dev_part_counts), cursors, c->sm_count, (cudaStream_t)stream, &tally.n);
+    cudaFreeAsync(cursors, (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(WFCU_ERR_CUDA, "partition: %s", cudaGetErrorString(e));
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_counter_merge_entries(wfcu_counter* c, const wfcu_entry* dev_entries, uint64_t n, void* stream) {
+    if (!c) return fail(WFCU_ERR_INVALID_ARGUMENT, "counter is null");
+    if (n && !dev_entries) return fail(WFCU_ERR_INVALID_ARGUMENT, "entries is null");
+    LaunchTally tally;
+    CUDA_TRY(tb_merge_entries(c->v, reinterpret_cast<const Slot*>(dev_entries), n, c->sm_count, (cudaStream_t)stream, &tally.n));
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_counter_long_records(wfcu_counter* c, uint8_t* dev_out, uint64_t out_cap, uint64_t* n_bytes,
+                                         void* stream) {
+    if (!c || !n_bytes) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    LaunchTally tally;
+    CUDA_TRY(tb_long_serialize(c->v, dev_out, out_cap, c->counters + 8, c->sm_count, s, &tally.n));
+    CUDA_TRY(cudaMemcpyAsync(n_bytes, c->counters + 8, sizeof(u64), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (dev_out && *n_bytes > out_cap) return fail(WFCU_ERR_BUFFER_TOO_SMALL, "long record stream needs %llu bytes", (unsigned long long)*n_bytes);
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_counter_merge_long_records(wfcu_counter* c, const uint8_t* dev_records, uint64_t n_bytes,
+                                               uint32_t part, uint32_t n_parts, void* stream) {
+    if (!c) return fail(WFCU_ERR_INVALID_ARGUMENT, "counter is null");
+    if (n_bytes && !dev_records) return fail(WFCU_ERR_INVALID_ARGUMENT, "records is null");
+    LaunchTally tally;
+    CUDA_TRY(tb_long_merge(c->v, dev_records, n_bytes, part, n_parts, (cudaStream_t)stream, &tally.n));
+    return WFCU_OK;
+}
+
+// ---- synthetic corpora ------------------------------------------------------------------
+extern "C" int wfcu_synth_document(uint64_t seed, uint64_t doc, uint32_t vocab, double zipf_s, uint32_t speaker,
+                                   uint8_t* out, uint64_t doc_bytes) {
+    if (synth_document(seed, doc, vocab, zipf_s, speaker, out, doc_bytes)) return fail(WFCU_ERR_INVALID_ARGUMENT, "bad synth arguments");
+    return WFCU_OK;
+}
+extern "C" int wfcu_synth_corpus(uint64_t seed, uint64_t doc_begin, uint64_t doc_end, uint32_t vocab, double zipf_s,
+                                 uint32_t speaker, uint64_t doc_bytes, uint8_t* out, int threads) {
+    if (synth_corpus(seed, doc_begin, doc_end, vocab, zipf_s, speaker, doc_bytes, out, threads))
+        return fail(WFCU_ERR_INVALID_ARGUMENT, "bad synth arguments");
+    return WFCU_OK;
+}
+extern "C" int wfcu_synth_uniform(uint64_t seed, uint64_t n, int dtype, void* out) {
+    if (dtype != WFCU_DTYPE_F32 && dtype != WFCU_DTYPE_F64) return fail(WFCU_ERR_INVALID_ARGUMENT, "unknown dtype %d", dtype);
+    if (synth_uniform(seed, n, dtype == WFCU_DTYPE_F64, out)) return fail(WFCU_ERR_INVALID_ARGUMENT, "bad synth arguments");
+    return WFCU_OK;
+}
+
+// ---- tokens API: TEMPORARY stubs, replaced by tokens.cu ------------------------------
+#define WFCU_TODO(name) return fail(WFCU_ERR_CUDA, name ": not implemented yet")
+extern "C" int wfcu_tokenize_dev(const uint8_t*, uint64_t, void*, wfcu_tokens**) { WFCU_TODO("wfcu_tokenize_dev"); }
+extern "C" int wfcu_tokenize_host(const uint8_t*, uint64_t, wfcu_tokens**) { WFCU_TODO("wfcu_tokenize_host"); }
+extern "C" void wfcu_tokens_destroy(wfcu_tokens*) {}
+extern "C" int wfcu_tokens_stats(const wfcu_tokens*, uint64_t*, uint64_t*) { WFCU_TODO("wfcu_tokens_stats"); }
+extern "C" int wfcu_tokens_export(const wfcu_tokens*, uint8_t*, uint64_t, uint32_t*, uint64_t) { WFCU_TODO("wfcu_tokens_export"); }
+extern "C" int wfcu_tokens_from_words(const uint8_t*, const uint32_t*, uint64_t, wfcu_tokens**) { WFCU_TODO("wfcu_tokens_from_words"); }
+extern "C" int wfcu_tokens_sort(wfcu_tokens*, void*) { WFCU_TODO("wfcu_tokens_sort"); }
+extern "C" int wfcu_tokens_reduce_sorted(const wfcu_tokens*, wfcu_counter*, void*) { WFCU_TODO("wfcu_tokens_reduce_sorted"); }
+extern "C" int wfcu_counter_count_dev_sorted(wfcu_counter*, const uint8_t*, uint64_t, void*) { WFCU_TODO("wfcu_counter_count_dev_sorted"); }

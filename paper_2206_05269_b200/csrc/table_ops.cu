@@ -1,0 +1,217 @@
+// table_ops.cu -- kernels that move count-table entries around: export compaction,
+// hash partition by owner GPU (the exchange step that replaces the reference's
+// range-partition shuffle, /root/reference/proj/src/shuffle.cpp:9-168, see
+// SURVEY.md D2), merge-insert of received entries (merge_counts,
+// proj/src/reduce.cpp:83-89) and the long-token record stream.
+#include "wfcu_dev.cuh"
+
+namespace wfcu {
+
+// Dense list of the non-empty inline slots (order unspecified).
+__global__ void tb_compact_kernel(TableView t, Slot* __restrict__ out, u64 out_cap, u64* __restrict__ out_count) {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= t.mask; i += (u64)gridDim.x * blockDim.x) {
+        const Slot s = t.slots[i];
+        if (s.k0 != 0) {
+            const u64 j = atomicAdd(out_count, 1ull);
+            if (j < out_cap) out[j] = Slot{s.k0, s.k1, s.count, 0};
+        }
+    }
+}
+
+// sum of key lengths (inline keys + long records) -> *out_bytes
+__global__ void tb_key_bytes_kernel(TableView t, u64* __restrict__ out_bytes) {
+    u64 local = 0;
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= t.mask; i += stride) {
+        const Slot s = t.slots[i];
+        if (s.k0 != 0) local += key_len(s.k0, s.k1);
+    }
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= t.long_mask; i += stride) {
+        const u64 r = t.long_ref[i];
+        if (r) local += *reinterpret_cast<const u32*>(t.arena + r);
+    }
+    for (int d = 16; d > 0; d >>= 1) local += __shfl_xor_sync(0xFFFFFFFFu, local, d);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(out_bytes, local);
+}
+
+// ---- hash partition ---------------------------------------------------------------
+// pass 1: part_counts[owner] += 1 for every inline entry
+__global__ void tb_partition_count_kernel(TableView t, u32 n_parts, u64* __restrict__ part_counts) {
+    extern __shared__ u32 s_hist[];
+    for (u32 p = threadIdx.x; p < n_parts; p += blockDim.x) s_hist[p] = 0;
+    __syncthreads();
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= t.mask; i += (u64)gridDim.x * blockDim.x) {
+        const Slot s = t.slots[i];
+        if (s.k0 != 0) atomicAdd(&s_hist[owner_mix32(s.k0, s.k1) % n_parts], 1u);
+    }
+    __syncthreads();
+    for (u32 p = threadIdx.x; p < n_parts; p += blockDim.x)
+        if (s_hist[p]) atomicAdd(&part_counts[p], (u64)s_hist[p]);
+}
+// exclusive scan of the (few) partition sizes -> cursors
+__global__ void tb_partition_scan_kernel(const u64* __restrict__ part_counts, u32 n_parts, u64* __restrict__ cursors) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        u64 acc = 0;
+        for (u32 p = 0; p < n_parts; ++p) { cursors[p] = acc; acc += part_counts[p]; }
+    }
+}
+// pass 2: scatter entries into their partition's region
+__global__ void tb_partition_scatter_kernel(TableView t, u32 n_parts, u64* __restrict__ cursors,
+                                            Slot* __restrict__ out, u64 out_cap) {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= t.mask; i += (u64)gridDim.x * blockDim.x) {
+        const Slot s = t.slots[i];
+        if (s.k0 != 0) {
+            const u32 p = owner_mix32(s.k0, s.k1) % n_parts;
+            const u64 j = atomicAdd(&cursors[p], 1ull);
+            if (j < out_cap) out[j] = Slot{s.k0, s.k1, s.count, 0};
+        }
+    }
+}
+
+// counts[key] += count for n received entries; also accounts the tokens
+__global__ void tb_merge_entries_kernel(TableView t, const Slot* __restrict__ in, u64 n) {
+    u64 tokens = 0;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const Slot s = in[i];
+        if (s.k0 != 0 && s.count != 0) {
+            table_add(t, s.k0, s.k1, s.count);
+            tokens += s.count;
+        }
+    }
+    for (int d = 16; d > 0; d >>= 1) tokens += __shfl_xor_sync(0xFFFFFFFFu, tokens, d);
+    if ((threadIdx.x & 31) == 0 && tokens) atomicAdd(t.n_tokens, tokens);
+}
+
+// dst += src for whole tables (inline part)
+__global__ void tb_merge_table_kernel(TableView dst, TableView src) {
+    u64 tokens = 0;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= src.mask; i += (u64)gridDim.x * blockDim.x) {
+        const Slot s = src.slots[i];
+        if (s.k0 != 0 && s.count != 0) {
+            table_add(dst, s.k0, s.k1, s.count);
+            tokens += s.count;
+        }
+    }
+    for (int d = 16; d > 0; d >>= 1) tokens += __shfl_xor_sync(0xFFFFFFFFu, tokens, d);
+    if ((threadIdx.x & 31) == 0 && tokens) atomicAdd(dst.n_tokens, tokens);
+}
+
+// ---- long-token record stream -----------------------------------------------------
+// record: {u64 count, u32 len, u32 hash, bytes..., pad to 8}
+__device__ __forceinline__ u64 long_record_bytes(u32 len) { return 16 + ((u64(len) + 7) & ~7ull); }
+
+// Serialises the long table.  out == nullptr: only sizes (*out_bytes).
+__global__ void tb_long_serialize_kernel(TableView t, uint8_t* __restrict__ out, u64 out_cap, u64* __restrict__ out_bytes) {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= t.long_mask; i += (u64)gridDim.x * blockDim.x) {
+        const u64 r = t.long_ref[i];
+        if (!r) continue;
+        const u32 len = *reinterpret_cast<const u32*>(t.arena + r);
+        const u64 need = long_record_bytes(len);
+        const u64 off = atomicAdd(out_bytes, need);
+        if (out && off + need <= out_cap) {
+            *reinterpret_cast<u64*>(out + off) = t.long_count[i];
+            *reinterpret_cast<u32*>(out + off + 8) = len;
+            *reinterpret_cast<u32*>(out + off + 12) = *reinterpret_cast<const u32*>(t.arena + r + 4);
+            for (u32 k = 0; k < len; ++k) out[off + 16 + k] = t.arena[r + 8 + k];
+            for (u64 k = 16 + len; k < need; ++k) out[off + k] = 0;
+        }
+    }
+}
+
+// Walks a record stream (single thread per CTA-strided record is impossible
+// without an index, so one thread walks; long tokens are rare) and inserts the
+// records owned by `part`.
+__global__ void tb_long_merge_kernel(TableView t, const uint8_t* __restrict__ recs, u64 n_bytes, u32 part, u32 n_parts) {
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    u64 off = 0;
+    while (off + 16 <= n_bytes) {
+        const u64 count = *reinterpret_cast<const u64*>(recs + off);
+        const u32 len = *reinterpret_cast<const u32*>(recs + off + 8);
+        const u32 hash = *reinterpret_cast<const u32*>(recs + off + 12);
+        const u64 need = long_record_bytes(len);
+        if (off + need > n_bytes) break;
+        const bool mine = (n_parts <= 1) || ((hash * 0x9E3779B1u) >> 7) % n_parts == part;
+        if (mine && count) {
+            const u64 rec = arena_alloc(t, len);
+            if (rec) {
+                *reinterpret_cast<u32*>(t.arena + rec) = len;
+                *reinterpret_cast<u32*>(t.arena + rec + 4) = hash;
+                for (u32 k = 0; k < len; ++k) t.arena[rec + 8 + k] = recs[off + 16 + k];
+                __threadfence();
+                long_add(t, rec, count);
+                atomicAdd(t.n_tokens, count);
+            }
+        }
+        off += need;
+    }
+}
+
+// ---- launchers ----------------------------------------------------------------------
+static inline unsigned grid_for(u64 items, int sm_count) {
+    u64 g = (items + 255) / 256;
+    const u64 cap = (u64)sm_count * 8;
+    if (g > cap) g = cap;
+    if (g == 0) g = 1;
+    return (unsigned)g;
+}
+
+cudaError_t tb_compact(const TableView& t, Slot* out, u64 cap, u64* dev_count, int sm, cudaStream_t s, u64* launches) {
+    cudaError_t e = cudaMemsetAsync(dev_count, 0, sizeof(u64), s);
+    if (e != cudaSuccess) return e;
+    tb_compact_kernel<<<grid_for(t.mask + 1, sm), 256, 0, s>>>(t, out, cap, dev_count);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+cudaError_t tb_key_bytes(const TableView& t, u64* dev_bytes, int sm, cudaStream_t s, u64* launches) {
+    cudaError_t e = cudaMemsetAsync(dev_bytes, 0, sizeof(u64), s);
+    if (e != cudaSuccess) return e;
+    tb_key_bytes_kernel<<<grid_for(t.mask + 1, sm), 256, 0, s>>>(t, dev_bytes);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+// cursors: device scratch of n_parts u64
+cudaError_t tb_partition(const TableView& t, u32 n_parts, Slot* out, u64 cap, u64* dev_part_counts, u64* cursors,
+                         int sm, cudaStream_t s, u64* launches) {
+    cudaError_t e = cudaMemsetAsync(dev_part_counts, 0, sizeof(u64) * n_parts, s);
+    if (e != cudaSuccess) return e;
+    const unsigned g = grid_for(t.mask + 1, sm);
+    tb_partition_count_kernel<<<g, 256, n_parts * sizeof(u32), s>>>(t, n_parts, dev_part_counts);
+    tb_partition_scan_kernel<<<1, 32, 0, s>>>(dev_part_counts, n_parts, cursors);
+    tb_partition_scatter_kernel<<<g, 256, 0, s>>>(t, n_parts, cursors, out, cap);
+    *launches += 3;
+    return cudaGetLastError();
+}
+
+cudaError_t tb_merge_entries(const TableView& t, const Slot* in, u64 n, int sm, cudaStream_t s, u64* launches) {
+    if (n == 0) return cudaSuccess;
+    tb_merge_entries_kernel<<<grid_for(n, sm), 256, 0, s>>>(t, in, n);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+cudaError_t tb_merge_table(const TableView& dst, const TableView& src, int sm, cudaStream_t s, u64* launches) {
+    tb_merge_table_kernel<<<grid_for(src.mask + 1, sm), 256, 0, s>>>(dst, src);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+cudaError_t tb_long_serialize(const TableView& t, uint8_t* out, u64 cap, u64* dev_bytes, int sm, cudaStream_t s,
+                              u64* launches) {
+    cudaError_t e = cudaMemsetAsync(dev_bytes, 0, sizeof(u64), s);
+    if (e != cudaSuccess) return e;
+    tb_long_serialize_kernel<<<grid_for(t.long_mask + 1, sm), 256, 0, s>>>(t, out, cap, dev_bytes);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+cudaError_t tb_long_merge(const TableView& t, const uint8_t* recs, u64 n_bytes, u32 part, u32 n_parts, cudaStream_t s,
+                          u64* launches) {
+    if (n_bytes == 0) return cudaSuccess;
+    tb_long_merge_kernel<<<1, 32, 0, s>>>(t, recs, n_bytes, part, n_parts);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+}  // namespace wfcu

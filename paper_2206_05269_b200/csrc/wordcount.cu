@@ -1,0 +1,505 @@
+// wordcount.cu -- fused tokenizer + counting map for sm_100a.
+//
+// Replaces, on the device, the reference's  tokenize -> normalize_word -> ++counts[word]
+// loop (/root/reference/proj/src/text.cpp:9-57, proj/src/unicode.cpp:11-121,
+// proj/src/pipeline.cpp:131-139).  Tokens never reach HBM: bytes are read once,
+// classified, cut into tokens and counted in the same kernel.
+//
+// Kernel K1+K2 (wc_fast_kernel): HBM-bound byte scan.
+//   * every warp owns a contiguous strip of 512-byte rows and streams it through
+//     a private shared-memory ring with 16-byte cp.async (LDGSTS) copies,
+//     RING_ROWS-2 rows ahead -- no CTA-wide barrier in steady state;
+//   * phase 1, one 16-byte chunk per lane: SWAR byte classes (ASCII whitespace,
+//     alphanumeric, >=0x80) -> 16-bit masks; fragment ENDS are found from the
+//     whitespace mask and resolved BACKWARDS against the previous chunk's masks
+//     (shuffle), so no look-ahead is ever needed; the edge trim (first..last
+//     word character) falls out of the alnum mask; a warp prefix sum packs the
+//     resolved (start,len) pairs into a per-warp queue;
+//   * phase 2, one token per lane: unaligned fetch from the ring (3-5 LDS.32 +
+//     funnel shifts), case fold in registers, big-endian pack into the 128-bit
+//     key, then a CTA-wide shared-memory combiner table (the Zipf head: >80 % of
+//     all tokens) with the global table (ATOMG.CAS.128 / RED.ADD.64) behind it.
+//   * anything the byte-class logic cannot decide exactly -- fragments with a
+//     byte >= 0x80, fragments or tokens longer than 16 bytes -- is appended to a
+//     deferred list and handled by wc_slow_kernel, an exact restatement of the
+//     reference's UTF-8 rules (one thread per fragment).
+#include "wfcu_dev.cuh"
+
+namespace wfcu {
+
+constexpr int kRowBytes = 512;              // 32 lanes x 16 bytes
+constexpr int kRingRows = 8;
+constexpr int kRingBytes = kRowBytes * kRingRows;   // per warp
+constexpr int kRingWords = kRingBytes / 4;
+constexpr int kPrefetch = kRingRows - 2;    // rows in flight ahead of the current one
+constexpr int kQueueCap = 512;              // >= 256 = most fragment ends in one row
+constexpr u64 kSlotLocked = 1ull;           // smem slot being claimed (never a valid k0)
+
+// ---- SWAR byte classes: bit 7 of each byte lane is the answer ------------------
+__device__ __forceinline__ u32 space4(u32 x) {
+    const u32 x7 = x & 0x7F7F7F7Fu;
+    const u32 z = (x7 ^ 0x20202020u) + 0x7F7F7F7Fu;  // bit7 clear <=> byte == 0x20
+    const u32 a = x7 + 0x77777777u;                  // bit7 set   <=> byte >= 0x09
+    const u32 b = x7 + 0x72727272u;                  // bit7 set   <=> byte >= 0x0E
+    return (~z | (a & ~b)) & ~x & 0x80808080u;
+}
+__device__ __forceinline__ u32 alnum4(u32 x) {
+    const u32 x7 = x & 0x7F7F7F7Fu;
+    const u32 y = x7 | 0x20202020u;
+    const u32 a1 = y + 0x1F1F1F1Fu;   // >= 'a'
+    const u32 a2 = y + 0x05050505u;   // >  'z'
+    const u32 d1 = x7 + 0x50505050u;  // >= '0'
+    const u32 d2 = x7 + 0x46464646u;  // >  '9'
+    return ((a1 & ~a2) | (d1 & ~d2)) & ~x & 0x80808080u;
+}
+// bytes known to be ASCII: 0x80 where 'A'..'Z'
+__device__ __forceinline__ u32 upper4(u32 x) {
+    const u32 u1 = x + 0x3F3F3F3Fu;   // >= 'A'
+    const u32 u2 = x + 0x25252525u;   // >  'Z'
+    return u1 & ~u2 & 0x80808080u;
+}
+// gather bit 7 of the four byte lanes into a nibble
+__device__ __forceinline__ u32 nib(u32 m) { return (m * 0x00204081u) >> 28; }
+__device__ __forceinline__ u32 mask16(u32 m0, u32 m1, u32 m2, u32 m3) {
+    return nib(m0) | (nib(m1) << 4) | (nib(m2) << 8) | (nib(m3) << 12);
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, u32 src_bytes) {
+    const u32 d = (u32)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gsrc), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// ---- CTA-shared combiner table ---------------------------------------------------
+struct SmemTable {
+    u64* k0;
+    u64* k1;
+    u32* cnt;
+    u32 mask;
+};
+
+// true if the token was counted in shared memory; false -> caller goes global.
+template <int PROBES>
+__device__ __forceinline__ bool smem_add(const SmemTable& t, u64 k0, u64 k1, u32 h) {
+    u32 i = h & t.mask;
+#pragma unroll 1
+    for (int p = 0; p < PROBES; ++p) {
+        u64 c0 = *reinterpret_cast<volatile u64*>(t.k0 + i);
+        if (c0 == 0) {
+            c0 = atomicCAS(t.k0 + i, 0ull, kSlotLocked);
+            if (c0 == 0) {
+                // we own the slot: publish k1 first, then k0
+                *reinterpret_cast<volatile u64*>(t.k1 + i) = k1;
+                __threadfence_block();
+                *reinterpret_cast<volatile u64*>(t.k0 + i) = k0;
+                atomicAdd(t.cnt + i, 1u);
+                return true;
+            }
+        }
+        if (c0 == kSlotLocked) return false;  // being claimed: the global table is always safe
+        if (c0 == k0) {
+            const u64 c1 = *reinterpret_cast<volatile u64*>(t.k1 + i);
+            if (c1 == k1) {
+                atomicAdd(t.cnt + i, 1u);
+                return true;
+            }
+        }
+        i = (i + 1) & t.mask;
+    }
+    return false;
+}
+
+template <int WARPS, int NSLOTS>
+struct FastSmem {
+    u64 k0[NSLOTS];
+    u64 k1[NSLOTS];
+    u32 cnt[NSLOTS];
+    uint4 ring[WARPS][kRingBytes / 16];
+    u32 queue[WARPS][kQueueCap];
+};
+
+// text[0..n): one document (documents are concatenated with whitespace between
+// them by the caller).  Position n acts as a whitespace byte, so does "position -1".
+template <int WARPS, int NSLOTS>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, TableView gt) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    FastSmem<WARPS, NSLOTS>& sm = *reinterpret_cast<FastSmem<WARPS, NSLOTS>*>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    for (int i = tid; i < NSLOTS; i += WARPS * 32) {
+        sm.k0[i] = 0; sm.k1[i] = 0; sm.cnt[i] = 0;
+    }
+    __syncthreads();
+    const SmemTable st{sm.k0, sm.k1, sm.cnt, (u32)(NSLOTS - 1)};
+
+    const u64 n_rows = n / kRowBytes + 1;   // the last row holds the virtual whitespace at n
+    const u64 gw = (u64)blockIdx.x * WARPS + warp;
+    const u64 row_begin = gw * rows_per_warp;
+    u64 row_end = row_begin + rows_per_warp;
+    if (row_end > n_rows) row_end = n_rows;
+
+    uint8_t* ring = reinterpret_cast<uint8_t*>(sm.ring[warp]);
+    const u32* ringw = reinterpret_cast<const u32*>(ring);
+    u32* queue = sm.queue[warp];
+    u32 my_tokens = 0;
+
+    if (row_begin < row_end) {
+        // issue one row: lane copies its 16-byte chunk, zero-filled past n
+        auto issue_row = [&](u64 row) {
+            if (row < row_end) {
+                const u64 g = row * kRowBytes + (u64)lane * 16;
+                u32 nbytes = 0;
+                const uint8_t* src = text;
+                if (g < n) {
+                    nbytes = (n - g >= 16) ? 16u : (u32)(n - g);
+                    src = text + g;
+                }
+                cp_async16(ring + (g & (kRingBytes - 1)), src, nbytes);
+            }
+            cp_async_commit();
+        };
+
+        // masks of the chunk that precedes this lane's chunk (lane 0: carried from the previous row)
+        u32 carryS = 0xFFFFu, carryA = 0, carryH = 0;   // "position -1" is whitespace
+        if (row_begin > 0) {
+            // history row: gives lane 0 its predecessor masks and keeps the bytes in the ring
+            issue_row(row_begin - 1);   // row_begin-1 < row_end always
+            cp_async_wait<0>();
+            __syncwarp();
+            const u64 g = (row_begin - 1) * kRowBytes + (u64)lane * 16;
+            const uint4 w = *reinterpret_cast<const uint4*>(ring + (g & (kRingBytes - 1)));
+            const u32 S = mask16(space4(w.x), space4(w.y), space4(w.z), space4(w.w));
+            const u32 A = mask16(alnum4(w.x), alnum4(w.y), alnum4(w.z), alnum4(w.w));
+            const u32 H = mask16(w.x & 0x80808080u, w.y & 0x80808080u, w.z & 0x80808080u, w.w & 0x80808080u);
+            carryS = __shfl_sync(0xFFFFFFFFu, S, 31);
+            carryA = __shfl_sync(0xFFFFFFFFu, A, 31);
+            carryH = __shfl_sync(0xFFFFFFFFu, H, 31);
+        }
+#pragma unroll
+        for (int p = 0; p < kPrefetch; ++p) issue_row(row_begin + p);
+
+        for (u64 row = row_begin; row < row_end; ++row) {
+            cp_async_wait<kPrefetch - 1>();
+            __syncwarp();
+
+            // ------------------------------ phase 1 ------------------------------
+            const u64 g = row * kRowBytes + (u64)lane * 16;   // global offset of my chunk
+            const uint4 w = *reinterpret_cast<const uint4*>(ring + (g & (kRingBytes - 1)));
+            u32 S = mask16(space4(w.x), space4(w.y), space4(w.z), space4(w.w));
+            const u32 A = mask16(alnum4(w.x), alnum4(w.y), alnum4(w.z), alnum4(w.w));
+            u32 H = 0;
+            const u32 anyhi = (w.x | w.y | w.z | w.w) & 0x80808080u;
+            if (__any_sync(0xFFFFFFFFu, anyhi != 0) || carryH) {
+                H = mask16(w.x & 0x80808080u, w.y & 0x80808080u, w.z & 0x80808080u, w.w & 0x80808080u);
+            }
+            if (g + 16 > n) {   // bytes at and beyond n are whitespace (document end)
+                const u32 valid = (g < n) ? (u32)(n - g) : 0u;
+                S |= (0xFFFFu << valid) & 0xFFFFu;
+            }
+            u32 pS = __shfl_up_sync(0xFFFFFFFFu, S, 1);
+            u32 pA = __shfl_up_sync(0xFFFFFFFFu, A, 1);
+            u32 pH = __shfl_up_sync(0xFFFFFFFFu, H, 1);
+            if (lane == 0) { pS = carryS; pA = carryA; pH = carryH; }
+            carryS = __shfl_sync(0xFFFFFFFFu, S, 31);
+            carryA = __shfl_sync(0xFFFFFFFFu, A, 31);
+            carryH = __shfl_sync(0xFFFFFFFFu, H, 31);
+
+            // bit i of the 32-bit views = byte (g - 16 + i)
+            const u32 S32 = pS | (S << 16);
+            const u32 A32 = pA | (A << 16);
+            const u32 H32 = pH | (H << 16);
+            // fragment ends: whitespace byte whose predecessor is not whitespace
+            u32 E = S & ~((S << 1) | (pS >> 15)) & 0xFFFFu;
+            const u32 cnt = __popc(E);
+            // warp exclusive prefix sum of cnt
+            u32 incl = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const u32 v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                if (lane >= d) incl += v;
+            }
+            const u32 total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+            u32 qi = incl - cnt;
+            while (E) {
+                const u32 j = __ffs(E) - 1;
+                E &= E - 1;
+                const u32 pos = 16 + j;                    // end position in the 32-bit view
+                const u32 below = (1u << pos) - 1;
+                const u32 sp = S32 & below;
+                u32 entry = 0;                              // dead entry: fragment without a word character
+                const u32 start = 32 - __clz(sp);          // first byte of the fragment (0 if sp == 0)
+                const u32 frag = below & ~((1u << start) - 1);
+                const u32 a = A32 & frag;
+                bool defer = (sp == 0) || (H32 & frag);
+                if (!defer && a) {
+                    const u32 first = __ffs(a) - 1;
+                    const u32 tlen = 32 - __clz(a) - first;
+                    if (tlen > 16) {
+                        defer = true;
+                    } else {
+                        const u32 rp = (u32)((g - 16 + first) & (kRingBytes - 1));
+                        entry = 0x40000000u | (tlen << 16) | rp;
+                    }
+                }
+                if (defer) {
+                    const u64 slot = atomicAdd(gt.n_deferred, 1ull);
+                    if (slot < gt.deferred_cap) gt.deferred[slot] = g + j;
+                    else atomicOr(gt.status, kStatusDeferredFull);
+                }
+                queue[qi++] = entry;
+            }
+            __syncwarp();
+
+            // ------------------------------ phase 2 ------------------------------
+            for (u32 q0 = 0; q0 < total; q0 += 32) {
+                const u32 qidx = q0 + lane;
+                const u32 entry = (qidx < total) ? queue[qidx] : 0u;
+                const bool live = (entry >> 30) == 1u;
+                const u32 tlen = (entry >> 16) & 31u;
+                const u32 sp = entry & (kRingBytes - 1);
+                const u32 wi = sp >> 2, sh = (sp & 3u) * 8u;
+                const u32 w0 = ringw[wi & (kRingWords - 1)];
+                const u32 w1 = ringw[(wi + 1) & (kRingWords - 1)];
+                const u32 w2 = ringw[(wi + 2) & (kRingWords - 1)];
+                u32 b0 = __funnelshift_r(w0, w1, sh);
+                u32 b1 = __funnelshift_r(w1, w2, sh);
+                u32 b2 = 0, b3 = 0;
+                if (__any_sync(0xFFFFFFFFu, live && tlen > 8)) {
+                    const u32 w3 = ringw[(wi + 3) & (kRingWords - 1)];
+                    const u32 w4 = ringw[(wi + 4) & (kRingWords - 1)];
+                    b2 = __funnelshift_r(w2, w3, sh);
+                    b3 = __funnelshift_r(w3, w4, sh);
+                }
+                // keep the first tlen bytes (little-endian lanes), fold A-Z
+                auto keep = [](u32 v, int nb) -> u32 {
+                    return nb >= 4 ? v : (nb <= 0 ? 0u : (v & ((1u << (8 * nb)) - 1u)));
+                };
+                b0 = keep(b0, (int)tlen);
+                b1 = keep(b1, (int)tlen - 4);
+                b2 = keep(b2, (int)tlen - 8);
+                b3 = keep(b3, (int)tlen - 12);
+                b0 |= upper4(b0) >> 2;
+                b1 |= upper4(b1) >> 2;
+                b2 |= upper4(b2) >> 2;
+                b3 |= upper4(b3) >> 2;
+                const u64 k0 = ((u64)__byte_perm(b0, 0, 0x0123) << 32) | __byte_perm(b1, 0, 0x0123);
+                const u64 k1 = ((u64)__byte_perm(b2, 0, 0x0123) << 32) | __byte_perm(b3, 0, 0x0123);
+                if (live) {
+                    const u32 h = mix32(k0, k1);
+                    if (!smem_add<4>(st, k0, k1, h)) table_add(gt, k0, k1, 1ull);
+                    ++my_tokens;
+                }
+            }
+            __syncwarp();   // everyone is done with the ring slot the next copy overwrites
+            issue_row(row + kPrefetch);
+        }
+        cp_async_wait<0>();
+    }
+
+    // token total: one atomic per warp
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) my_tokens += __shfl_xor_sync(0xFFFFFFFFu, my_tokens, d);
+    if (lane == 0 && my_tokens) atomicAdd(gt.n_tokens, (u64)my_tokens);
+
+    // flush the combiner into the global table
+    __syncthreads();
+    for (int i = tid; i < NSLOTS; i += WARPS * 32) {
+        const u64 k0 = sm.k0[i];
+        const u32 c = sm.cnt[i];
+        if (k0 > kSlotLocked && c) table_add(gt, k0, sm.k1[i], (u64)c);
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// Slow path: exact restatement of the reference's UTF-8 rules, one thread per
+// deferred fragment.  (/root/reference/proj/src/unicode.cpp:11-121, text.cpp:9-57)
+// ---------------------------------------------------------------------------------
+struct Dec { u32 cp; u32 len; bool valid; };
+
+__device__ __forceinline__ Dec utf8_dec(const uint8_t* s, u64 pos, u64 end) {
+    const Dec bad{0xFFFDu, 1u, false};
+    const u32 b0 = s[pos];
+    if (b0 < 0x80) return Dec{b0, 1u, true};
+    u32 extra, cp, lo = 0x80, hi = 0xBF;
+    if (b0 >= 0xC2 && b0 <= 0xDF) { extra = 1; cp = b0 & 0x1F; }
+    else if (b0 >= 0xE0 && b0 <= 0xEF) {
+        extra = 2; cp = b0 & 0x0F;
+        if (b0 == 0xE0) lo = 0xA0;
+        if (b0 == 0xED) hi = 0x9F;
+    } else if (b0 >= 0xF0 && b0 <= 0xF4) {
+        extra = 3; cp = b0 & 0x07;
+        if (b0 == 0xF0) lo = 0x90;
+        if (b0 == 0xF4) hi = 0x8F;
+    } else return bad;
+    if (pos + extra >= end) return bad;
+    const u32 b1 = s[pos + 1];
+    if (b1 < lo || b1 > hi) return bad;
+    cp = (cp << 6) | (b1 & 0x3F);
+    for (u32 k = 2; k <= extra; ++k) {
+        const u32 b = s[pos + k];
+        if ((b & 0xC0) != 0x80) return bad;
+        cp = (cp << 6) | (b & 0x3F);
+    }
+    return Dec{cp, extra + 1, true};
+}
+
+__device__ __forceinline__ bool uni_space(u32 cp) {
+    if (cp >= 0x09 && cp <= 0x0D) return true;
+    if (cp >= 0x2000 && cp <= 0x200A) return true;
+    return cp == 0x20 || cp == 0x85 || cp == 0xA0 || cp == 0x1680 || cp == 0x2028 || cp == 0x2029 ||
+           cp == 0x202F || cp == 0x205F || cp == 0x3000;
+}
+__device__ __forceinline__ bool word_char(u32 cp) {
+    if (cp < 0x80) {
+        const u32 l = cp | 0x20;
+        return (cp >= '0' && cp <= '9') || (l >= 'a' && l <= 'z');
+    }
+    if (cp == 0xFFFD) return false;
+    if (cp >= 0xA1 && cp <= 0xBF) return cp == 0xAA || cp == 0xB5 || cp == 0xBA;
+    if (cp == 0xD7 || cp == 0xF7) return false;
+    if ((cp >= 0x2000 && cp <= 0x206F) || (cp >= 0x3000 && cp <= 0x303F)) return false;
+    if ((cp >= 0xFF01 && cp <= 0xFF0F) || (cp >= 0xFF1A && cp <= 0xFF20)) return false;
+    if ((cp >= 0xFF3B && cp <= 0xFF40) || (cp >= 0xFF5B && cp <= 0xFF65)) return false;
+    return !uni_space(cp);
+}
+__device__ __forceinline__ u32 lower_cp(u32 cp) {
+    if (cp >= 'A' && cp <= 'Z') return cp + 0x20;
+    if (cp >= 0xC0 && cp <= 0xDE && cp != 0xD7) return cp + 0x20;
+    return cp;
+}
+__device__ __forceinline__ u32 enc_len(u32 cp) { return cp < 0x80 ? 1 : cp < 0x800 ? 2 : cp < 0x10000 ? 3 : 4; }
+__device__ __forceinline__ u32 enc_byte(u32 cp, u32 n, u32 i) {
+    // byte i of the n-byte UTF-8 encoding of cp
+    if (n == 1) return cp;
+    const u32 shift = 6 * (n - 1 - i);
+    if (i == 0) return ((0xF00u >> n) & 0xFF) | (cp >> shift);
+    return 0x80 | ((cp >> shift) & 0x3F);
+}
+
+// Counts the token of one whitespace-free piece [a,b) of the text (normalize_word).
+__device__ void slow_count_piece(const uint8_t* text, u64 a, u64 b, const TableView& gt) {
+    // pass 1: normalised offsets of the first / last word character
+    u64 noff = 0, nfirst = 0, nlast_end = 0, first_b = b, last_e = a;
+    for (u64 pos = a; pos < b;) {
+        const Dec d = utf8_dec(text, pos, b);
+        const u32 cp = lower_cp(d.cp);
+        const u32 el = enc_len(cp);
+        if (word_char(cp)) {
+            if (first_b == b) { first_b = pos; nfirst = noff; }
+            last_e = pos + d.len;
+            nlast_end = noff + el;
+        }
+        noff += el;
+        pos += d.len;
+    }
+    if (first_b == b) return;
+    const u64 nlen = nlast_end - nfirst;
+    atomicAdd(gt.n_tokens, 1ull);
+    if (nlen <= 16) {
+        u64 k0 = 0, k1 = 0;
+        u32 i = 0;
+        for (u64 pos = first_b; pos < last_e;) {
+            const Dec d = utf8_dec(text, pos, b);
+            const u32 cp = lower_cp(d.cp);
+            const u32 el = enc_len(cp);
+            for (u32 k = 0; k < el; ++k, ++i) {
+                const u64 byte = enc_byte(cp, el, k);
+                if (i < 8) k0 |= byte << (56 - 8 * i);
+                else k1 |= byte << (56 - 8 * (i - 8));
+            }
+            pos += d.len;
+        }
+        table_add(gt, k0, k1, 1ull);
+        return;
+    }
+    if (nlen > 0xFFFFFFFFull) { atomicOr(gt.status, kStatusArenaFull); return; }
+    const u64 rec = arena_alloc(gt, (u32)nlen);
+    if (!rec) return;
+    uint8_t* out = gt.arena + rec + 8;
+    u32 h = 2166136261u;
+    u64 i = 0;
+    for (u64 pos = first_b; pos < last_e;) {
+        const Dec d = utf8_dec(text, pos, b);
+        const u32 cp = lower_cp(d.cp);
+        const u32 el = enc_len(cp);
+        for (u32 k = 0; k < el; ++k, ++i) {
+            const u32 byte = enc_byte(cp, el, k);
+            out[i] = (uint8_t)byte;
+            h = (h ^ byte) * 16777619u;
+        }
+        pos += d.len;
+    }
+    *reinterpret_cast<u32*>(gt.arena + rec) = (u32)nlen;
+    *reinterpret_cast<u32*>(gt.arena + rec + 4) = h;
+    __threadfence();
+    long_add(gt, rec, 1ull);
+}
+
+__device__ __forceinline__ bool ascii_space(u32 b) { return b == 0x20 || (b >= 0x09 && b <= 0x0D); }
+
+// One thread per deferred fragment END (offset of the terminating ASCII
+// whitespace byte, or n).  The fragment start is found by scanning backwards.
+__global__ void wc_slow_kernel(const uint8_t* __restrict__ text, u64 n, TableView gt) {
+    u64 count = *gt.n_deferred;
+    if (count > gt.deferred_cap) count = gt.deferred_cap;
+    for (u64 idx = (u64)blockIdx.x * blockDim.x + threadIdx.x; idx < count; idx += (u64)gridDim.x * blockDim.x) {
+        const u64 e = gt.deferred[idx];
+        u64 s = e;
+        while (s > 0 && !ascii_space(text[s - 1])) --s;
+        // split [s,e) on valid non-ASCII whitespace code points (text.cpp:45-55)
+        u64 piece = s;
+        bool in_piece = false;
+        for (u64 pos = s; pos <= e;) {
+            Dec d{0, 1, false};
+            bool boundary = (pos == e);
+            if (!boundary) {
+                d = utf8_dec(text, pos, e);
+                boundary = d.valid && uni_space(d.cp);
+            }
+            if (boundary) {
+                if (in_piece) slow_count_piece(text, piece, pos, gt);
+                in_piece = false;
+            } else if (!in_piece) {
+                piece = pos;
+                in_piece = true;
+            }
+            pos += d.len;
+        }
+    }
+}
+
+__global__ void wc_reset_deferred_kernel(TableView gt) { *gt.n_deferred = 0; }
+
+// ---- host-side launchers (called from capi.cu) -----------------------------------
+constexpr int kFastWarps = 16;
+constexpr int kFastSlots = 4096;
+
+size_t wc_fast_smem_bytes() { return sizeof(FastSmem<kFastWarps, kFastSlots>); }
+
+cudaError_t wc_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream,
+                      u64* launches) {
+    static bool attr_set = false;
+    const size_t smem = wc_fast_smem_bytes();
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(wc_fast_kernel<kFastWarps, kFastSlots>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const u64 n_rows = n / kRowBytes + 1;
+    u64 grid = (u64)sm_count;
+    const u64 total_warps_needed = n_rows;   // at least one row per warp
+    if (grid * kFastWarps > total_warps_needed) grid = (total_warps_needed + kFastWarps - 1) / kFastWarps;
+    if (grid == 0) grid = 1;
+    const u64 rows_per_warp = (n_rows + grid * kFastWarps - 1) / (grid * kFastWarps);
+    wc_fast_kernel<kFastWarps, kFastSlots><<<(unsigned)grid, kFastWarps * 32, smem, stream>>>(text, n, rows_per_warp, gt);
+    wc_slow_kernel<<<sm_count * 2, 128, 0, stream>>>(text, n, gt);
+    wc_reset_deferred_kernel<<<1, 1, 0, stream>>>(gt);
+    *launches += 3;
+    return cudaGetLastError();
+}
+
+}  // namespace wfcu
