@@ -28,7 +28,7 @@
 namespace wfcu {
 
 constexpr int kRowBytes = 512;              // 32 lanes x 16 bytes
-constexpr int kRingRows = 8;
+constexpr int kRingRows = 4;
 constexpr int kRingBytes = kRowBytes * kRingRows;   // per warp
 constexpr int kRingWords = kRingBytes / 4;
 constexpr int kPrefetch = kRingRows - 2;    // rows in flight ahead of the current one
@@ -72,68 +72,95 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// ---- CTA-shared combiner table ---------------------------------------------------
-struct SmemTable {
-    u64* k0;
-    u64* k1;
-    u32* cnt;
-    u32 mask;
-};
-
-// true if the token was counted in shared memory; false -> caller goes global.
-template <int PROBES>
-__device__ __forceinline__ bool smem_add(const SmemTable& t, u64 k0, u64 k1, u32 h) {
-    u32 i = h & t.mask;
-#pragma unroll 1
-    for (int p = 0; p < PROBES; ++p) {
-        u64 c0 = *reinterpret_cast<volatile u64*>(t.k0 + i);
+// ---- CTA-shared combiner tables --------------------------------------------------
+// Two tables so that the common case never touches a second key word:
+//   short  : tokens of <= 8 bytes, key = the bytes, little-endian packed (u64)
+//   medium : tokens of 9..16 bytes, key = two u64
+// Both are 2-way (two candidate slots from one hash), probed with straight-line
+// code.  A key that lands in two slots, or in a slot and the global table, is
+// harmless: the flush adds every slot's count into the global table.  What must
+// never happen is a count credited to a different key, hence the publish order
+// of the medium table (k1 first, then k0 behind a fence).
+__device__ __forceinline__ bool short_add(u64* __restrict__ keys, u32* __restrict__ cnt, u32 mask, u64 key, u32 h) {
+    const u32 i0 = h & mask, i1 = (h >> 16) & mask;
+    const u64 c0 = *reinterpret_cast<volatile u64*>(keys + i0);
+    const u64 c1 = *reinterpret_cast<volatile u64*>(keys + i1);
+    u32 slot;
+    if (c0 == key) slot = i0;
+    else if (c1 == key) slot = i1;
+    else {
+        slot = 0xFFFFFFFFu;
         if (c0 == 0) {
-            c0 = atomicCAS(t.k0 + i, 0ull, kSlotLocked);
+            const u64 old = atomicCAS(keys + i0, 0ull, key);
+            if (old == 0 || old == key) slot = i0;
+        }
+        if (slot == 0xFFFFFFFFu && c1 == 0) {
+            const u64 old = atomicCAS(keys + i1, 0ull, key);
+            if (old == 0 || old == key) slot = i1;
+        }
+        if (slot == 0xFFFFFFFFu) return false;
+    }
+    atomicAdd(cnt + slot, 1u);
+    return true;
+}
+
+__device__ __forceinline__ bool medium_add(u64* __restrict__ k0s, u64* __restrict__ k1s, u32* __restrict__ cnt,
+                                           u32 mask, u64 k0, u64 k1, u32 h) {
+    u32 i = h & mask;
+#pragma unroll 1
+    for (int way = 0; way < 2; ++way) {
+        u64 c0 = *reinterpret_cast<volatile u64*>(k0s + i);
+        if (c0 == 0) {
+            c0 = atomicCAS(k0s + i, 0ull, kSlotLocked);
             if (c0 == 0) {
-                // we own the slot: publish k1 first, then k0
-                *reinterpret_cast<volatile u64*>(t.k1 + i) = k1;
+                *reinterpret_cast<volatile u64*>(k1s + i) = k1;
                 __threadfence_block();
-                *reinterpret_cast<volatile u64*>(t.k0 + i) = k0;
-                atomicAdd(t.cnt + i, 1u);
+                *reinterpret_cast<volatile u64*>(k0s + i) = k0;
+                atomicAdd(cnt + i, 1u);
                 return true;
             }
         }
-        if (c0 == kSlotLocked) return false;  // being claimed: the global table is always safe
-        if (c0 == k0) {
-            const u64 c1 = *reinterpret_cast<volatile u64*>(t.k1 + i);
-            if (c1 == k1) {
-                atomicAdd(t.cnt + i, 1u);
-                return true;
-            }
+        if (c0 == kSlotLocked) return false;   // being claimed: the global table is always safe
+        if (c0 == k0 && *reinterpret_cast<volatile u64*>(k1s + i) == k1) {
+            atomicAdd(cnt + i, 1u);
+            return true;
         }
-        i = (i + 1) & t.mask;
+        i = (h >> 16) & mask;
     }
     return false;
 }
 
-template <int WARPS, int NSLOTS>
+__device__ __forceinline__ u32 bswap32(u32 v) { return __byte_perm(v, 0, 0x0123); }
+// little-endian packed token word pair -> big-endian table key word
+__device__ __forceinline__ u64 le_to_be(u64 v) { return ((u64)bswap32((u32)v) << 32) | bswap32((u32)(v >> 32)); }
+
+constexpr int kMissCap = 64;   // per-warp buffer of keys that go to the global table
+
+template <int WARPS, int NSLOTS, int MSLOTS>
 struct FastSmem {
-    u64 k0[NSLOTS];
-    u64 k1[NSLOTS];
-    u32 cnt[NSLOTS];
+    u64 sk[NSLOTS];
+    u32 scnt[NSLOTS];
+    u64 mk0[MSLOTS];
+    u64 mk1[MSLOTS];
+    u32 mcnt[MSLOTS];
     uint4 ring[WARPS][kRingBytes / 16];
-    u32 queue[WARPS][kQueueCap];
+    ulonglong2 miss[WARPS][kMissCap];
+    uint16_t queue[WARPS][kQueueCap];   // tlen << 11 | ring position
 };
 
 // text[0..n): one document (documents are concatenated with whitespace between
 // them by the caller).  Position n acts as a whitespace byte, so does "position -1".
-template <int WARPS, int NSLOTS>
+template <int WARPS, int NSLOTS, int MSLOTS>
 __global__ void __launch_bounds__(WARPS * 32, 1)
 wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, TableView gt) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    FastSmem<WARPS, NSLOTS>& sm = *reinterpret_cast<FastSmem<WARPS, NSLOTS>*>(smem_raw);
+    FastSmem<WARPS, NSLOTS, MSLOTS>& sm = *reinterpret_cast<FastSmem<WARPS, NSLOTS, MSLOTS>*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const u32 lt_mask = (1u << lane) - 1u;
 
-    for (int i = tid; i < NSLOTS; i += WARPS * 32) {
-        sm.k0[i] = 0; sm.k1[i] = 0; sm.cnt[i] = 0;
-    }
+    for (int i = tid; i < NSLOTS; i += WARPS * 32) { sm.sk[i] = 0; sm.scnt[i] = 0; }
+    for (int i = tid; i < MSLOTS; i += WARPS * 32) { sm.mk0[i] = 0; sm.mk1[i] = 0; sm.mcnt[i] = 0; }
     __syncthreads();
-    const SmemTable st{sm.k0, sm.k1, sm.cnt, (u32)(NSLOTS - 1)};
 
     const u64 n_rows = n / kRowBytes + 1;   // the last row holds the virtual whitespace at n
     const u64 gw = (u64)blockIdx.x * WARPS + warp;
@@ -143,8 +170,78 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
 
     uint8_t* ring = reinterpret_cast<uint8_t*>(sm.ring[warp]);
     const u32* ringw = reinterpret_cast<const u32*>(ring);
-    u32* queue = sm.queue[warp];
+    uint16_t* queue = sm.queue[warp];
+    ulonglong2* missbuf = sm.miss[warp];
     u32 my_tokens = 0;
+    u32 qhead = 0, qtail = 0;     // token queue (warp-uniform)
+    u32 mhead = 0, mtail = 0;     // miss buffer (warp-uniform)
+
+    // 32 buffered keys -> global table, one key per lane
+    auto drain_misses = [&](u32 count) {
+        if (lane < count) {
+            const ulonglong2 k = missbuf[(mhead + lane) & (kMissCap - 1)];
+            table_add(gt, k.x, k.y, 1ull);
+        }
+        mhead += count;
+    };
+
+    // one pass of phase 2: `count` (<= 32) queued tokens, one per lane
+    auto token_pass = [&](u32 count) {
+        const u32 entry = (lane < count) ? queue[(qhead + lane) & (kQueueCap - 1)] : 0u;
+        qhead += count;
+        const u32 tlen = entry >> 11;               // 0: dead entry
+        const u32 sp = entry & (kRingBytes - 1);
+        const u32 wi = sp >> 2, sh = (sp & 3u) * 8u;
+        const u32 w0 = ringw[wi & (kRingWords - 1)];
+        const u32 w1 = ringw[(wi + 1) & (kRingWords - 1)];
+        const u32 w2 = ringw[(wi + 2) & (kRingWords - 1)];
+        u32 b0 = __funnelshift_r(w0, w1, sh);
+        u32 b1 = __funnelshift_r(w1, w2, sh);
+        b0 |= upper4(b0 & 0x7F7F7F7Fu) >> 2;   // fold A-Z (bytes past the token are masked off below)
+        b1 |= upper4(b1 & 0x7F7F7F7Fu) >> 2;
+        bool miss = false;
+        u64 mk0 = 0, mk1 = 0;
+        if (!__any_sync(0xFFFFFFFFu, tlen > 8)) {
+            // every token of this pass fits 8 bytes
+            const u64 key = (((u64)b1 << 32) | b0) & (~0ull >> ((64u - 8u * tlen) & 63u));
+            if (tlen) {
+                u32 h = (u32)key * 0x9E3779B1u ^ (u32)(key >> 32) * 0x85EBCA77u;
+                h ^= h >> 15;
+                h *= 0x2C1B3C6Du;
+                h ^= h >> 13;
+                if (!short_add(sm.sk, sm.scnt, NSLOTS - 1, key, h)) { miss = true; mk0 = le_to_be(key); }
+                ++my_tokens;
+            }
+        } else {
+            const u32 w3 = ringw[(wi + 3) & (kRingWords - 1)];
+            const u32 w4 = ringw[(wi + 4) & (kRingWords - 1)];
+            u32 b2 = __funnelshift_r(w2, w3, sh);
+            u32 b3 = __funnelshift_r(w3, w4, sh);
+            b2 |= upper4(b2 & 0x7F7F7F7Fu) >> 2;
+            b3 |= upper4(b3 & 0x7F7F7F7Fu) >> 2;
+            u64 lo = ((u64)b1 << 32) | b0, hi = ((u64)b3 << 32) | b2;
+            if (tlen <= 8) { lo &= ~0ull >> ((64u - 8u * tlen) & 63u); hi = 0; }
+            else hi &= ~0ull >> ((128u - 8u * tlen) & 63u);
+            if (tlen) {
+                u32 h = (u32)lo * 0x9E3779B1u ^ (u32)(lo >> 32) * 0x85EBCA77u;
+                h ^= (u32)hi * 0xC2B2AE3Du ^ (u32)(hi >> 32) * 0x27D4EB2Fu;
+                h ^= h >> 15;
+                h *= 0x2C1B3C6Du;
+                h ^= h >> 13;
+                const bool ok = (tlen <= 8) ? short_add(sm.sk, sm.scnt, NSLOTS - 1, lo, h)
+                                            : medium_add(sm.mk0, sm.mk1, sm.mcnt, MSLOTS - 1, lo, hi, h);
+                if (!ok) { miss = true; mk0 = le_to_be(lo); mk1 = le_to_be(hi); }
+                ++my_tokens;
+            }
+        }
+        const u32 mm = __ballot_sync(0xFFFFFFFFu, miss);
+        if (mm) {
+            if (miss) missbuf[(mtail + __popc(mm & lt_mask)) & (kMissCap - 1)] = make_ulonglong2(mk0, mk1);
+            mtail += __popc(mm);
+            __syncwarp();
+            if (mtail - mhead >= 32) drain_misses(32);
+        }
+    };
 
     if (row_begin < row_end) {
         // issue one row: lane copies its 16-byte chunk, zero-filled past n
@@ -222,7 +319,9 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
                 if (lane >= d) incl += v;
             }
             const u32 total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-            u32 qi = incl - cnt;
+            const u32 carried = qtail - qhead;          // entries left over from the previous row
+            u32 qi = qtail + incl - cnt;
+            const u32 gbase = (u32)g - 16u;             // ring positions only need the low bits
             while (E) {
                 const u32 j = __ffs(E) - 1;
                 E &= E - 1;
@@ -237,66 +336,33 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
                 if (!defer && a) {
                     const u32 first = __ffs(a) - 1;
                     const u32 tlen = 32 - __clz(a) - first;
-                    if (tlen > 16) {
-                        defer = true;
-                    } else {
-                        const u32 rp = (u32)((g - 16 + first) & (kRingBytes - 1));
-                        entry = 0x40000000u | (tlen << 16) | rp;
-                    }
+                    if (tlen > 16) defer = true;
+                    else entry = (tlen << 11) | ((gbase + first) & (kRingBytes - 1));
                 }
                 if (defer) {
                     const u64 slot = atomicAdd(gt.n_deferred, 1ull);
                     if (slot < gt.deferred_cap) gt.deferred[slot] = g + j;
                     else atomicOr(gt.status, kStatusDeferredFull);
                 }
-                queue[qi++] = entry;
+                queue[(qi++) & (kQueueCap - 1)] = (uint16_t)entry;
             }
+            qtail += total;
             __syncwarp();
 
             // ------------------------------ phase 2 ------------------------------
-            for (u32 q0 = 0; q0 < total; q0 += 32) {
-                const u32 qidx = q0 + lane;
-                const u32 entry = (qidx < total) ? queue[qidx] : 0u;
-                const bool live = (entry >> 30) == 1u;
-                const u32 tlen = (entry >> 16) & 31u;
-                const u32 sp = entry & (kRingBytes - 1);
-                const u32 wi = sp >> 2, sh = (sp & 3u) * 8u;
-                const u32 w0 = ringw[wi & (kRingWords - 1)];
-                const u32 w1 = ringw[(wi + 1) & (kRingWords - 1)];
-                const u32 w2 = ringw[(wi + 2) & (kRingWords - 1)];
-                u32 b0 = __funnelshift_r(w0, w1, sh);
-                u32 b1 = __funnelshift_r(w1, w2, sh);
-                u32 b2 = 0, b3 = 0;
-                if (__any_sync(0xFFFFFFFFu, live && tlen > 8)) {
-                    const u32 w3 = ringw[(wi + 3) & (kRingWords - 1)];
-                    const u32 w4 = ringw[(wi + 4) & (kRingWords - 1)];
-                    b2 = __funnelshift_r(w2, w3, sh);
-                    b3 = __funnelshift_r(w3, w4, sh);
-                }
-                // keep the first tlen bytes (little-endian lanes), fold A-Z
-                auto keep = [](u32 v, int nb) -> u32 {
-                    return nb >= 4 ? v : (nb <= 0 ? 0u : (v & ((1u << (8 * nb)) - 1u)));
-                };
-                b0 = keep(b0, (int)tlen);
-                b1 = keep(b1, (int)tlen - 4);
-                b2 = keep(b2, (int)tlen - 8);
-                b3 = keep(b3, (int)tlen - 12);
-                b0 |= upper4(b0) >> 2;
-                b1 |= upper4(b1) >> 2;
-                b2 |= upper4(b2) >> 2;
-                b3 |= upper4(b3) >> 2;
-                const u64 k0 = ((u64)__byte_perm(b0, 0, 0x0123) << 32) | __byte_perm(b1, 0, 0x0123);
-                const u64 k1 = ((u64)__byte_perm(b2, 0, 0x0123) << 32) | __byte_perm(b3, 0, 0x0123);
-                if (live) {
-                    const u32 h = mix32(k0, k1);
-                    if (!smem_add<4>(st, k0, k1, h)) table_add(gt, k0, k1, 1ull);
-                    ++my_tokens;
-                }
-            }
+            // full 32-token passes; the remainder waits for the next row's tokens
+            u32 consumed = 0;
+            while (qtail - qhead >= 32) { token_pass(32); consumed += 32; }
+            // ... unless it would outlive its bytes in the ring (entries of row-1 may
+            // reach back into row-2, which the next copy overwrites)
+            if (carried > consumed) token_pass(qtail - qhead);
             __syncwarp();   // everyone is done with the ring slot the next copy overwrites
             issue_row(row + kPrefetch);
         }
         cp_async_wait<0>();
+        if (qtail != qhead) token_pass(qtail - qhead);
+        __syncwarp();
+        while (mtail != mhead) drain_misses(min(mtail - mhead, 32u));
     }
 
     // token total: one atomic per warp
@@ -304,12 +370,17 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
     for (int d = 16; d > 0; d >>= 1) my_tokens += __shfl_xor_sync(0xFFFFFFFFu, my_tokens, d);
     if (lane == 0 && my_tokens) atomicAdd(gt.n_tokens, (u64)my_tokens);
 
-    // flush the combiner into the global table
+    // flush the combiners into the global table
     __syncthreads();
     for (int i = tid; i < NSLOTS; i += WARPS * 32) {
-        const u64 k0 = sm.k0[i];
-        const u32 c = sm.cnt[i];
-        if (k0 > kSlotLocked && c) table_add(gt, k0, sm.k1[i], (u64)c);
+        const u64 k = sm.sk[i];
+        const u32 c = sm.scnt[i];
+        if (k != 0 && c) table_add(gt, le_to_be(k), 0ull, (u64)c);
+    }
+    for (int i = tid; i < MSLOTS; i += WARPS * 32) {
+        const u64 k = sm.mk0[i];
+        const u32 c = sm.mcnt[i];
+        if (k > kSlotLocked && c) table_add(gt, le_to_be(k), le_to_be(sm.mk1[i]), (u64)c);
     }
 }
 
@@ -474,20 +545,20 @@ __global__ void wc_slow_kernel(const uint8_t* __restrict__ text, u64 n, TableVie
 __global__ void wc_reset_deferred_kernel(TableView gt) { *gt.n_deferred = 0; }
 
 // ---- host-side launchers (called from capi.cu) -----------------------------------
-constexpr int kFastWarps = 16;
-constexpr int kFastSlots = 4096;
+static_assert(kRingBytes == 2048, "queue entries keep ring positions in 11 bits");
+constexpr int kFastWarps = 24;
+constexpr int kFastSlots = 8192;    // short-token combiner slots (12 bytes each)
+constexpr int kFastMedSlots = 1024; // medium-token combiner slots (20 bytes each)
 
-size_t wc_fast_smem_bytes() { return sizeof(FastSmem<kFastWarps, kFastSlots>); }
+size_t wc_fast_smem_bytes() { return sizeof(FastSmem<kFastWarps, kFastSlots, kFastMedSlots>); }
 
 cudaError_t wc_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream,
                       u64* launches) {
-    static bool attr_set = false;
     const size_t smem = wc_fast_smem_bytes();
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(wc_fast_kernel<kFastWarps, kFastSlots>,
+    {
+        cudaError_t e = cudaFuncSetAttribute(wc_fast_kernel<kFastWarps, kFastSlots, kFastMedSlots>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
     const u64 n_rows = n / kRowBytes + 1;
     u64 grid = (u64)sm_count;
@@ -495,7 +566,7 @@ cudaError_t wc_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_co
     if (grid * kFastWarps > total_warps_needed) grid = (total_warps_needed + kFastWarps - 1) / kFastWarps;
     if (grid == 0) grid = 1;
     const u64 rows_per_warp = (n_rows + grid * kFastWarps - 1) / (grid * kFastWarps);
-    wc_fast_kernel<kFastWarps, kFastSlots><<<(unsigned)grid, kFastWarps * 32, smem, stream>>>(text, n, rows_per_warp, gt);
+    wc_fast_kernel<kFastWarps, kFastSlots, kFastMedSlots><<<(unsigned)grid, kFastWarps * 32, smem, stream>>>(text, n, rows_per_warp, gt);
     wc_slow_kernel<<<sm_count * 2, 128, 0, stream>>>(text, n, gt);
     wc_reset_deferred_kernel<<<1, 1, 0, stream>>>(gt);
     *launches += 3;
