@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""bench.py -- the headline benchmark of the word-frequency hot path on B200.
+
+    python bench.py --gpus N --steps K --warmup W [--impl reference] [--workload cfg3|cfg4]
+
+metric   word-count corpus GB/s (BASELINE.json): bytes of corpus counted per second,
+         whole job over all N GPUs, GB = 1e9 bytes.
+workload cfg3 (default): synthetic Zipf(s=1.1) corpus, 50k-word vocabulary, 954 one-MiB
+         documents (1.0003 GB) PER GPU, documents assigned round-robin (d mod N); at
+         N > 1 every step ends with the hash-partitioned all-to-all merge.  Weak scaling.
+         cfg4: 32 GB total, 1M-word vocabulary, document-sharded over N >= 2 GPUs.
+step     reset the count table + one pass of the fused tokenizer/count kernels over the
+         rank's resident shard (+ partition / all-to-all / merge-insert at N > 1).
+value    inputs resident in HBM, CUDA-event timed, max over ranks.
+e2e      the same step through the host-buffer C-ABI call (wfcu_counter_count_host:
+         pack -> pinned staging -> H2D -> count) plus the export of the ordered table to
+         host memory; wall clock around synchronised steps, max over ranks.
+The reference arm (--impl reference) times the UNMODIFIED reference's run_wordcount
+(oracle/_ref, all host threads) on a bounded sample of the same corpus.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DOC_BYTES = 1 << 20
+SEED = 1
+ZIPF_S = 1.1
+WORKLOADS = {
+    # name: (vocab, docs per GPU (None = total/N), total docs (None = per-GPU * N), scaling)
+    "cfg3": dict(vocab=50000, docs_per_gpu=954, total_docs=None, scaling="weak",
+                 name="word count, synthetic Zipf(1.1) corpus, 50k vocabulary, 1 GB per GPU"),
+    "cfg4": dict(vocab=1000000, docs_per_gpu=None, total_docs=30518, scaling="strong",
+                 name="word count, synthetic Zipf(1.1) corpus, 1M vocabulary, 32 GB document-sharded"),
+}
+METRIC = "wordcount_corpus_GBps"
+UNIT = "GB/s"
+
+
+def measured_peak_gbs():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._pump, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def plan(workload: str, world: int, rank: int, docs_override: int | None):
+    w = WORKLOADS[workload]
+    if w["total_docs"] is None:
+        per = docs_override or w["docs_per_gpu"]
+        total = per * world
+    else:
+        total = docs_override or w["total_docs"]
+    my_docs = list(range(rank, total, world))   # the reference's rule: document d -> worker d mod n
+    return w, total, my_docs
+
+
+def build_corpus(capi, np, torch, vocab: int, docs: list[int], stride: int):
+    """The rank's shard as one pinned host buffer: documents docs[0], docs[0]+stride, ..."""
+    n = len(docs) * DOC_BYTES
+    host = torch.empty(max(n, 16), dtype=torch.uint8).pin_memory()
+    arr = host.numpy()
+    if docs:
+        capi.synth_corpus_strided(SEED, docs[0], stride, len(docs), vocab, ZIPF_S, 0, DOC_BYTES, out=arr)
+    return host, n
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle
+    from paper_2206_05269_b200 import capi
+    oracle.build()
+    cores = os.cpu_count() or 1
+    w, total, _ = plan(args.workload, max(args.gpus, 1), 0, args.docs)
+    use_ref = oracle.ref_available()
+    cpu = oracle.ref() if use_ref else oracle.port()
+
+    def docs_of(k):
+        blob = capi.synth_corpus(SEED, 0, k, w["vocab"], ZIPF_S, 0, DOC_BYTES)
+        return [blob[i * DOC_BYTES:(i + 1) * DOC_BYTES] for i in range(k)]
+
+    def one(docs):
+        t0 = time.perf_counter()
+        if use_ref:
+            table, _ = cpu.run_wordcount(docs, cores)
+        else:
+            table = cpu.wordcount(docs)
+        return time.perf_counter() - t0, len(table)
+
+    # calibrate the bounded sample: ~4 s of CPU work per step, 8..256 documents
+    t_probe, _ = one(docs_of(8))
+    k = int(min(256, max(8, 8 * 4.0 / max(t_probe, 1e-3))))
+    if args.sample_docs:
+        k = args.sample_docs
+    docs = docs_of(k)
+    for _ in range(args.warmup):
+        one(docs)
+    t0 = time.perf_counter()
+    distinct = 0
+    for _ in range(args.steps):
+        _, distinct = one(docs)
+    dt = time.perf_counter() - t0
+    nbytes = k * DOC_BYTES
+    value = nbytes * args.steps / dt / 1e9
+    sample = (f"{k} of {total} one-MiB documents ({nbytes / 1e6:.0f} MB) per step, "
+              f"{'wfc::run_wordcount(corpus, n_workers=%d)' % cores if use_ref else 'oracle port, serial'}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": w["scaling"],
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": w["name"], "vocab": w["vocab"], "zipf_s": ZIPF_S, "doc_bytes": DOC_BYTES, "seed": SEED,
+                   "sample": sample, "distinct_words_in_sample": distinct},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores if use_ref else 1,
+                         "kind": "reference" if use_ref else "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(capi, vocab: int, total_docs: int) -> dict:
+    """The reference CPU path on this box's host cores, bounded sample (rank 0, N=1 only)."""
+    import oracle
+    cores = os.cpu_count() or 1
+    use_ref = oracle.ref_available()
+    cpu = oracle.ref() if use_ref else oracle.port()
+    k = 8
+    blob = capi.synth_corpus(SEED, 0, 64, vocab, ZIPF_S, 0, DOC_BYTES)
+    docs = [blob[i * DOC_BYTES:(i + 1) * DOC_BYTES] for i in range(64)]
+
+    def one(d):
+        t0 = time.perf_counter()
+        cpu.run_wordcount(d, cores) if use_ref else cpu.wordcount(d)
+        return time.perf_counter() - t0
+    t = one(docs[:k])
+    if t < 5.0:      # grow the sample towards ~10-20 s of CPU work, at most 64 documents
+        k = int(min(64, max(k, k * 12.0 / max(t, 1e-3))))
+        t = one(docs[:k])
+    nbytes = k * DOC_BYTES
+    return {"value": nbytes / t / 1e9, "unit": UNIT, "cores": cores if use_ref else 1,
+            "kind": "reference" if use_ref else "port",
+            "sample": f"first {k} of {total_docs} one-MiB documents ({nbytes / 1e6:.0f} MB), one run of "
+                      f"{'wfc::run_wordcount with n_workers=%d' % cores if use_ref else 'the serial oracle port'}, {t:.1f} s"}
+
+
+def run_b200(args) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2206_05269_b200 import capi
+    from paper_2206_05269_b200.exchange import DeviceOps, hash_partition_merge
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device: the product has no CPU path")
+    torch.cuda.set_device(local_rank)
+    device = torch.device("cuda", local_rank)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=device)
+    if world != max(args.gpus, 1) and rank == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+
+    w, total_docs, my_docs = plan(args.workload, world, rank, args.docs)
+    host, nbytes = build_corpus(capi, np, torch, w["vocab"], my_docs, world)
+    dev = host.to(device, non_blocking=True)
+    torch.cuda.synchronize()
+    slots = 1 << 20 if w["vocab"] <= 100000 else 1 << 22
+    local = capi.Counter(table_slots=slots)
+    owned = capi.Counter(table_slots=slots) if world > 1 else None
+    ops = DeviceOps(torch, device)
+    stream = torch.cuda.current_stream(device).cuda_stream
+
+    def step():
+        local.reset(stream)
+        local.count_dev(dev.data_ptr(), nbytes, stream)
+        if world > 1:
+            owned.reset(stream)
+            hash_partition_merge(local, owned, ops, dist)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+    local.status(stream)
+
+    # ---- resident-data timing: exactly K steps, CUDA events, max over ranks --------------------
+    launches0 = capi.launch_count()
+    local.set_timing(True)
+    local.take_kernel_ms()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        barrier()
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        barrier()
+    total_ms = e0.elapsed_time(e1)
+    kernel_ms, kernel_launches = local.take_kernel_ms()
+    local.set_timing(False)
+    launches = capi.launch_count() - launches0
+    t = torch.tensor([total_ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    table = owned if world > 1 else local
+    table.status(stream)
+    distinct, tokens, _ = table.stats(stream)
+    all_bytes = torch.tensor([nbytes, distinct, tokens], dtype=torch.int64, device=device)
+    if world > 1:
+        dist.all_reduce(all_bytes)
+    job_bytes, job_distinct, job_tokens = (int(v) for v in all_bytes.tolist())
+    ms_per_step = total_ms / args.steps
+    value = job_bytes / (ms_per_step * 1e-3) / 1e9
+
+    # ---- end to end through the host-buffer call (pinned staging, H2D, count, export D2H) ------
+    arr = host.numpy()
+    docs = [arr[i * DOC_BYTES:(i + 1) * DOC_BYTES] for i in range(len(my_docs))]
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    d2h = 0
+
+    def e2e_step():
+        nonlocal d2h
+        local.reset()
+        local.count_host(docs)
+        if world > 1:
+            owned.reset(stream)
+            hash_partition_merge(local, owned, ops, dist)
+            torch.cuda.synchronize()
+        blob, lens, counts = (owned if world > 1 else local).export()
+        d2h = blob.nbytes + lens.nbytes + counts.nbytes
+    e2e_step()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    barrier()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    t = torch.tensor([e2e_s], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_value = job_bytes / float(t.item()) / 1e9
+
+    if rank == 0:
+        peak, peak_src = measured_peak_gbs()
+        k_ms = kernel_ms / max(kernel_launches, 1)
+        achieved = nbytes / (k_ms * 1e-3) / 1e9 if k_ms > 0 else 0.0
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": w["scaling"], "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": w["name"], "vocab": w["vocab"], "zipf_s": ZIPF_S, "doc_bytes": DOC_BYTES,
+                       "seed": SEED, "documents": total_docs, "bytes_per_gpu": nbytes, "job_bytes": job_bytes,
+                       "tokens": job_tokens, "distinct_words": job_distinct,
+                       "parallelism": f"document shard d mod {world}" + (", hash-partitioned all-to-all merge" if world > 1 else ""),
+                       "l2": "inputs (1 GB per GPU) larger than the 126 MB L2; no flush needed"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if peak else None, "traffic": None,
+                         "kernel": "wc_fast_kernel", "kernel_ms": k_ms, "kernel_launches": kernel_launches,
+                         "algorithmic_bytes_per_launch": nbytes, "peak_source": peak_src},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": d2h,
+                    "steps": e2e_steps, "api": "wfcu_counter_count_host + wfcu_counter_export"},
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+        }
+        if world == 1 and not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline(capi, w["vocab"], total_docs)
+        if not args.no_mapreduce:
+            line["extra"] = {"mapreduce": mapreduce_line(capi, torch, device, stream, peak)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def mapreduce_line(capi, torch, device, stream, peak) -> dict:
+    """BASELINE.json config 2: sum of x^2 over 2^28 fp32 (1 GiB), resident, event timed."""
+    n = 1 << 28
+    x = torch.rand(n, device=device, dtype=torch.float32)
+    out = torch.zeros(1, device=device, dtype=torch.float64)
+    res = {}
+    for name, kind in (("identity", capi.MAP_IDENTITY), ("square", capi.MAP_SQUARE)):
+        for _ in range(3):
+            capi.map_reduce_dev_async(x.data_ptr(), capi.DTYPE_F32, n, kind, out.data_ptr(), 0, stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            capi.map_reduce_dev_async(x.data_ptr(), capi.DTYPE_F32, n, kind, out.data_ptr(), 0, stream)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 10
+        ref = float((x.double() if kind == capi.MAP_IDENTITY else x.double() ** 2).sum().item())
+        res[name] = {"ms": ms, "GBps": 4 * n / ms / 1e6, "frac_of_hbm_peak": 4 * n / ms / 1e6 / peak,
+                     "rel_err_vs_torch_fp64": abs(float(out.item()) - ref) / max(1.0, abs(ref))}
+    return {"config": "sum f(x) over 2^28 fp32 (torch.rand), 1 GiB, 1 GPU", **res}
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3")
+    ap.add_argument("--docs", type=int, default=None, help="override document count (per GPU for cfg3, total for cfg4)")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--sample-docs", type=int, default=None, help="reference arm: documents per step")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-mapreduce", action="store_true", help="skip the config-2 map-reduce extra")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

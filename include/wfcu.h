@@ -136,6 +136,13 @@ WFCU_API int wfcu_counter_count_dev(wfcu_counter* c, const uint8_t* dev_text, ui
 WFCU_API int wfcu_counter_count_host(wfcu_counter* c, const uint8_t* const* docs, const uint64_t* doc_lens,
                             uint64_t n_docs);
 
+/* Measurement hook: with timing enabled every wfcu_counter_count_dev brackets its
+ * dominant kernel (wc_fast_kernel) with CUDA events on the launching stream;
+ * take_kernel_ms waits for them and returns the summed device time and the
+ * number of launches since the last call. */
+WFCU_API int wfcu_counter_set_timing(wfcu_counter* c, int enabled);
+WFCU_API int wfcu_counter_take_kernel_ms(wfcu_counter* c, double* sum_ms, uint64_t* launches);
+
 /* Synchronises and reports overflow conditions (WFCU_ERR_TABLE_FULL, ...). */
 WFCU_API int wfcu_counter_status(wfcu_counter* c, void* stream);
 
@@ -232,6 +239,12 @@ WFCU_API int wfcu_synth_document(uint64_t seed, uint64_t doc, uint32_t vocab, do
  * `threads` host threads (0 = all). */
 WFCU_API int wfcu_synth_corpus(uint64_t seed, uint64_t doc_begin, uint64_t doc_end, uint32_t vocab,
                       double zipf_s, uint32_t speaker, uint64_t doc_bytes, uint8_t* out, int threads);
+
+/* Documents doc_begin, doc_begin + doc_stride, ... (n_docs of them): the shard of the
+ * rank that owns documents d = doc_begin (mod doc_stride). */
+WFCU_API int wfcu_synth_corpus_strided(uint64_t seed, uint64_t doc_begin, uint64_t doc_stride, uint64_t n_docs,
+                                       uint32_t vocab, double zipf_s, uint32_t speaker, uint64_t doc_bytes,
+                                       uint8_t* out, int threads);
 
 /* The reference bench's input recipe (proj/src/cli.cpp:120-125): n draws of
  * std::mt19937_64(seed) through std::uniform_real_distribution<double>(0,1),

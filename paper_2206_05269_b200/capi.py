@@ -67,6 +67,8 @@ SIGNATURES = {
     "wfcu_counter_reset": (C.c_int, [C.c_void_p, C.c_void_p]),
     "wfcu_counter_count_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "wfcu_counter_count_host": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), u64p, C.c_uint64]),
+    "wfcu_counter_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
+    "wfcu_counter_take_kernel_ms": (C.c_int, [C.c_void_p, f64p, u64p]),
     "wfcu_counter_status": (C.c_int, [C.c_void_p, C.c_void_p]),
     "wfcu_counter_stats": (C.c_int, [C.c_void_p, C.c_void_p, u64p, u64p, u64p]),
     "wfcu_counter_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64]),
@@ -88,6 +90,7 @@ SIGNATURES = {
     "wfcu_counter_count_dev_sorted": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "wfcu_synth_document": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint32, C.c_double, C.c_uint32, C.c_void_p, C.c_uint64]),
     "wfcu_synth_corpus": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, C.c_double, C.c_uint32, C.c_uint64, C.c_void_p, C.c_int]),
+    "wfcu_synth_corpus_strided": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, C.c_double, C.c_uint32, C.c_uint64, C.c_void_p, C.c_int]),
     "wfcu_synth_uniform": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, C.c_void_p]),
     "wfcu_launch_count": (C.c_uint64, []),
 }
@@ -211,11 +214,15 @@ class Counter:
         check(lib.wfcu_counter_create(C.byref(self._h), C.byref(cfg)))
 
     def close(self) -> None:
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:
             lib.wfcu_counter_destroy(self._h)
             self._h = None
 
-    __del__ = close
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     @property
     def handle(self) -> C.c_void_p:
@@ -236,6 +243,14 @@ class Counter:
         ptrs = (C.c_void_p * max(n, 1))(*[a.ctypes.data if a.size else None for a in arrs])
         lens = (C.c_uint64 * max(n, 1))(*[a.size for a in arrs])
         check(lib.wfcu_counter_count_host(self._h, ptrs, lens, n))
+
+    def set_timing(self, enabled: bool) -> None:
+        check(lib.wfcu_counter_set_timing(self._h, int(enabled)))
+
+    def take_kernel_ms(self) -> tuple[float, int]:
+        ms, n = C.c_double(), C.c_uint64()
+        check(lib.wfcu_counter_take_kernel_ms(self._h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
 
     def status(self, stream: int = 0) -> None:
         check(lib.wfcu_counter_status(self._h, C.c_void_p(stream)))
@@ -316,11 +331,15 @@ class Tokens:
         return cls(h)
 
     def close(self) -> None:
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:
             lib.wfcu_tokens_destroy(self._h)
             self._h = None
 
-    __del__ = close
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def stats(self) -> tuple[int, int]:
         n, b = C.c_uint64(), C.c_uint64()
@@ -349,6 +368,18 @@ def synth_corpus(seed: int, doc_begin: int, doc_end: int, vocab: int, zipf_s: fl
         out = np.empty(n, dtype=np.uint8)
     assert out.size >= n and out.dtype == np.uint8
     check(lib.wfcu_synth_corpus(seed, doc_begin, doc_end, vocab, zipf_s, speaker, doc_bytes, _ptr(out), threads))
+    return out[:n]
+
+
+def synth_corpus_strided(seed: int, doc_begin: int, doc_stride: int, n_docs: int, vocab: int, zipf_s: float = 1.1,
+                         speaker: int = 0, doc_bytes: int = 1 << 20, threads: int = 0,
+                         out: np.ndarray | None = None) -> np.ndarray:
+    n = n_docs * doc_bytes
+    if out is None:
+        out = np.empty(n, dtype=np.uint8)
+    assert out.size >= n and out.dtype == np.uint8
+    check(lib.wfcu_synth_corpus_strided(seed, doc_begin, doc_stride, n_docs, vocab, zipf_s, speaker, doc_bytes,
+                                        _ptr(out), threads))
     return out[:n]
 
 

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/wfcu.h"
@@ -16,7 +17,8 @@
 
 namespace wfcu {
 // wordcount.cu
-cudaError_t wc_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream, u64* launches);
+cudaError_t wc_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream, u64* launches,
+                      cudaEvent_t* ev_before_fast, cudaEvent_t* ev_after_fast);
 // mapreduce.cu
 cudaError_t mr_launch(const void* values, int is_f64, u64 n, u64 base, int kind, int grid, double* partials,
                       double* dev_out, cudaStream_t s, u64* launches);
@@ -37,6 +39,8 @@ cudaError_t tb_long_merge(const TableView& t, const uint8_t* recs, u64 n_bytes, 
 int synth_document(uint64_t seed, uint64_t doc, uint32_t vocab, double s, uint32_t speaker, uint8_t* out, uint64_t doc_bytes);
 int synth_corpus(uint64_t seed, uint64_t doc_begin, uint64_t doc_end, uint32_t vocab, double s, uint32_t speaker,
                  uint64_t doc_bytes, uint8_t* out, int threads);
+int synth_corpus_strided(uint64_t seed, uint64_t doc_begin, uint64_t doc_stride, uint64_t n_docs, uint32_t vocab,
+                         double s, uint32_t speaker, uint64_t doc_bytes, uint8_t* out, int threads);
 int synth_uniform(uint64_t seed, uint64_t n, int as_f64, void* out);
 }  // namespace wfcu
 
@@ -257,6 +261,10 @@ struct wfcu_counter {
     cudaEvent_t done[2] = {nullptr, nullptr};
     u64 chunk_cap = 0;
     cudaStream_t stream = nullptr;
+    // optional CUDA-event timing of the dominant kernel (bench.py's roofline leg)
+    bool timing = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;   // one pair per wc_fast launch
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> event_pool;
 };
 
 static u64 round_pow2(u64 x) {
@@ -279,6 +287,8 @@ static void counter_free(wfcu_counter* c) {
         if (c->done[i]) cudaEventDestroy(c->done[i]);
     }
     if (c->stream) cudaStreamDestroy(c->stream);
+    for (auto& pr : c->timed) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+    for (auto& pr : c->event_pool) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
     delete c;
 }
 
@@ -357,7 +367,44 @@ extern "C" int wfcu_counter_count_dev(wfcu_counter* c, const uint8_t* dev_text, 
     if (reinterpret_cast<uintptr_t>(dev_text) & 15u)
         return fail(WFCU_ERR_INVALID_ARGUMENT, "device text must be 16-byte aligned");
     LaunchTally tally;
-    CUDA_TRY(wc_launch(dev_text, n, c->v, c->sm_count, (cudaStream_t)stream, &tally.n));
+    cudaEvent_t* ev0 = nullptr;
+    cudaEvent_t* ev1 = nullptr;
+    if (c->timing) {
+        std::pair<cudaEvent_t, cudaEvent_t> pr{nullptr, nullptr};
+        if (!c->event_pool.empty()) {
+            pr = c->event_pool.back();
+            c->event_pool.pop_back();
+        } else {
+            CUDA_TRY(cudaEventCreate(&pr.first));
+            CUDA_TRY(cudaEventCreate(&pr.second));
+        }
+        c->timed.push_back(pr);
+        ev0 = &c->timed.back().first;
+        ev1 = &c->timed.back().second;
+    }
+    CUDA_TRY(wc_launch(dev_text, n, c->v, c->sm_count, (cudaStream_t)stream, &tally.n, ev0, ev1));
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_counter_set_timing(wfcu_counter* c, int enabled) {
+    if (!c) return fail(WFCU_ERR_INVALID_ARGUMENT, "counter is null");
+    c->timing = enabled != 0;
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_counter_take_kernel_ms(wfcu_counter* c, double* sum_ms, uint64_t* launches) {
+    if (!c || !sum_ms || !launches) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
+    double total = 0.0;
+    for (auto& pr : c->timed) {
+        CUDA_TRY(cudaEventSynchronize(pr.second));
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, pr.first, pr.second));
+        total += ms;
+    }
+    *sum_ms = total;
+    *launches = c->timed.size();
+    for (auto& pr : c->timed) c->event_pool.push_back(pr);
+    c->timed.clear();
     return WFCU_OK;
 }
 
@@ -668,6 +715,13 @@ extern "C" int wfcu_synth_document(uint64_t seed, uint64_t doc, uint32_t vocab, 
 extern "C" int wfcu_synth_corpus(uint64_t seed, uint64_t doc_begin, uint64_t doc_end, uint32_t vocab, double zipf_s,
                                  uint32_t speaker, uint64_t doc_bytes, uint8_t* out, int threads) {
     if (synth_corpus(seed, doc_begin, doc_end, vocab, zipf_s, speaker, doc_bytes, out, threads))
+        return fail(WFCU_ERR_INVALID_ARGUMENT, "bad synth arguments");
+    return WFCU_OK;
+}
+extern "C" int wfcu_synth_corpus_strided(uint64_t seed, uint64_t doc_begin, uint64_t doc_stride, uint64_t n_docs,
+                                         uint32_t vocab, double zipf_s, uint32_t speaker, uint64_t doc_bytes,
+                                         uint8_t* out, int threads) {
+    if (synth_corpus_strided(seed, doc_begin, doc_stride, n_docs, vocab, zipf_s, speaker, doc_bytes, out, threads))
         return fail(WFCU_ERR_INVALID_ARGUMENT, "bad synth arguments");
     return WFCU_OK;
 }

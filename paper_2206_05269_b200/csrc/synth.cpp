@@ -127,16 +127,16 @@ int synth_document(uint64_t seed, uint64_t doc, uint32_t vocab, double s, uint32
     return 0;
 }
 
-int synth_corpus(uint64_t seed, uint64_t doc_begin, uint64_t doc_end, uint32_t vocab, double s, uint32_t speaker,
-                 uint64_t doc_bytes, uint8_t* out, int threads) {
-    if (vocab == 0 || !out || doc_end < doc_begin) return -1;
+// documents doc_begin, doc_begin + stride, ... (n_docs of them), back to back
+int synth_corpus_strided(uint64_t seed, uint64_t doc_begin, uint64_t doc_stride, uint64_t n_docs, uint32_t vocab,
+                         double s, uint32_t speaker, uint64_t doc_bytes, uint8_t* out, int threads) {
+    if (vocab == 0 || !out || doc_stride == 0) return -1;
     const auto v = get_vocabulary(seed, vocab, s, speaker);
-    const uint64_t n_docs = doc_end - doc_begin;
     unsigned nt = threads > 0 ? unsigned(threads) : std::max(1u, std::thread::hardware_concurrency());
     if (nt > n_docs) nt = unsigned(std::max<uint64_t>(1, n_docs));
     auto work = [&](unsigned t) {
         for (uint64_t d = t; d < n_docs; d += nt)
-            make_document(*v, seed + 0x1000003ull * speaker, doc_begin + d, out + d * doc_bytes, doc_bytes);
+            make_document(*v, seed + 0x1000003ull * speaker, doc_begin + d * doc_stride, out + d * doc_bytes, doc_bytes);
     };
     if (nt <= 1) {
         work(0);
@@ -146,6 +146,12 @@ int synth_corpus(uint64_t seed, uint64_t doc_begin, uint64_t doc_end, uint32_t v
         for (auto& th : pool) th.join();
     }
     return 0;
+}
+
+int synth_corpus(uint64_t seed, uint64_t doc_begin, uint64_t doc_end, uint32_t vocab, double s, uint32_t speaker,
+                 uint64_t doc_bytes, uint8_t* out, int threads) {
+    if (doc_end < doc_begin) return -1;
+    return synth_corpus_strided(seed, doc_begin, 1, doc_end - doc_begin, vocab, s, speaker, doc_bytes, out, threads);
 }
 
 // The reference bench's input recipe (/root/reference/proj/src/cli.cpp:120-125):

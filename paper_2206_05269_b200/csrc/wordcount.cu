@@ -553,7 +553,7 @@ constexpr int kFastMedSlots = 1024; // medium-token combiner slots (20 bytes eac
 size_t wc_fast_smem_bytes() { return sizeof(FastSmem<kFastWarps, kFastSlots, kFastMedSlots>); }
 
 cudaError_t wc_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream,
-                      u64* launches) {
+                      u64* launches, cudaEvent_t* ev_before_fast, cudaEvent_t* ev_after_fast) {
     const size_t smem = wc_fast_smem_bytes();
     {
         cudaError_t e = cudaFuncSetAttribute(wc_fast_kernel<kFastWarps, kFastSlots, kFastMedSlots>,
@@ -566,7 +566,9 @@ cudaError_t wc_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_co
     if (grid * kFastWarps > total_warps_needed) grid = (total_warps_needed + kFastWarps - 1) / kFastWarps;
     if (grid == 0) grid = 1;
     const u64 rows_per_warp = (n_rows + grid * kFastWarps - 1) / (grid * kFastWarps);
+    if (ev_before_fast) cudaEventRecord(*ev_before_fast, stream);
     wc_fast_kernel<kFastWarps, kFastSlots, kFastMedSlots><<<(unsigned)grid, kFastWarps * 32, smem, stream>>>(text, n, rows_per_warp, gt);
+    if (ev_after_fast) cudaEventRecord(*ev_after_fast, stream);
     wc_slow_kernel<<<sm_count * 2, 128, 0, stream>>>(text, n, gt);
     wc_reset_deferred_kernel<<<1, 1, 0, stream>>>(gt);
     *launches += 3;

@@ -1,0 +1,159 @@
+"""Multi-GPU merge of per-GPU count tables: hash-partitioned all-to-all over NCCL.
+
+One process per GPU (torchrun).  Replaces the reference's exchange stage
+(/root/reference/proj/src/shuffle.cpp:98-168: range partition of sorted words, n(n-1)
+WCX1 frames, n-way merge) and the merge_counts / boundary_repair that follow it
+(proj/src/reduce.cpp:48-89) -- see SURVEY.md D2: the contract is the final CountMap,
+the shard layout is implementation defined.
+
+    per rank:  local table --K4 partition-by-owner--> n contiguous regions of 32-byte
+               entries --all_to_all(sizes), all_to_all_v(entries)--> K5 merge-insert
+               into the rank's OWNED table (every key lives on exactly one rank, so
+               count_unreduced_words == 0 and no repair pass is needed).
+
+torch.distributed is the plumbing (rendezvous, NCCL all-to-all over NVLink 5 / NVSwitch);
+partition and merge are kernels of libwfcu.so reached through the C ABI.  The `ops`
+argument isolates those device steps so the control flow can be exercised on CPU with
+gloo (tests/test_exchange_gloo.py supplies an oracle-backed stand-in); the product always
+uses DeviceOps and has no CPU path.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+ENTRY_WORDS = 4   # wfcu_entry = 4 x u64 = 32 bytes
+
+
+class DeviceOps:
+    """The device steps of the exchange, through libwfcu.so."""
+
+    def __init__(self, torch, device):
+        from . import capi
+        self.capi = capi
+        self.torch = torch
+        self.device = device
+
+    def stream(self) -> int:
+        return self.torch.cuda.current_stream(self.device).cuda_stream
+
+    def partition(self, counter, n_parts: int):
+        """-> (entries[int64, cap x 4] grouped by owner, part_counts[int64, n_parts]) on device"""
+        t = self.torch
+        distinct, _, _ = counter.stats(self.stream())
+        entries = t.empty((max(distinct, 1), ENTRY_WORDS), dtype=t.int64, device=self.device)
+        counts = t.zeros(n_parts, dtype=t.int64, device=self.device)
+        counter.partition(n_parts, entries.data_ptr(), entries.shape[0], counts.data_ptr(), self.stream())
+        return entries, counts
+
+    def merge_entries(self, counter, entries, n: int) -> None:
+        if n:
+            counter.merge_entries(entries.data_ptr(), n, self.stream())
+
+    def long_records(self, counter):
+        t = self.torch
+        n = counter.long_records(0, 0, self.stream())
+        buf = t.empty(max(n, 8), dtype=t.uint8, device=self.device)
+        if n:
+            counter.long_records(buf.data_ptr(), n, self.stream())
+        return buf[:n]
+
+    def merge_long_records(self, counter, records, part: int, n_parts: int) -> None:
+        if records.numel():
+            counter.merge_long_records(records.data_ptr(), records.numel(), part, n_parts, self.stream())
+
+    def empty_entries(self, n: int):
+        t = self.torch
+        return t.empty((max(n, 1), ENTRY_WORDS), dtype=t.int64, device=self.device)
+
+    def empty_bytes(self, n: int):
+        t = self.torch
+        return t.empty(max(n, 1), dtype=t.uint8, device=self.device)
+
+
+@dataclass
+class ExchangeStats:
+    sent_entries: int
+    received_entries: int
+    sent_bytes: int
+    long_bytes: int
+
+
+def hash_partition_merge(local, owned, ops, dist, group=None) -> ExchangeStats:
+    """Moves every entry of `local` to the rank that owns its key and sums it into `owned`.
+
+    local / owned are counters (capi.Counter for DeviceOps).  Collective: every rank of the
+    group must call it.  After the call the union of the ranks' `owned` tables is the
+    merged CountMap and the tables are pairwise disjoint.
+    """
+    torch = ops.torch
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+
+    entries, send_counts = ops.partition(local, world)
+    if world == 1:
+        n = int(send_counts.sum().item())
+        ops.merge_entries(owned, entries, n)
+        ops.merge_long_records(owned, ops.long_records(local), 0, 1)
+        return ExchangeStats(n, n, 0, 0)
+
+    # sizes first (n x n u64 in total), then the entries themselves
+    recv_counts = torch.empty_like(send_counts)
+    dist.all_to_all_single(recv_counts, send_counts, group=group)
+    send_list = [int(v) for v in send_counts.cpu().tolist()]
+    recv_list = [int(v) for v in recv_counts.cpu().tolist()]
+    n_send, n_recv = sum(send_list), sum(recv_list)
+    recv = ops.empty_entries(n_recv)
+    dist.all_to_all_single(recv[:n_recv], entries[:n_send], output_split_sizes=recv_list,
+                           input_split_sizes=send_list, group=group)
+    ops.merge_entries(owned, recv, n_recv)
+
+    # tokens longer than 16 bytes: rare, variable length -> all-gather the record streams and
+    # let every rank keep the records it owns
+    mine = ops.long_records(local)
+    sizes = torch.zeros(world, dtype=torch.int64, device=send_counts.device)
+    sizes[rank] = mine.numel()
+    dist.all_reduce(sizes, group=group)
+    size_list = [int(v) for v in sizes.cpu().tolist()]
+    long_total = sum(size_list)
+    if long_total:
+        width = max(size_list)
+        padded = ops.empty_bytes(width)
+        padded.zero_()
+        padded[:mine.numel()] = mine
+        gathered = ops.empty_bytes(width * world)
+        parts = [gathered[r * width:(r + 1) * width] for r in range(world)]
+        dist.all_gather(parts, padded[:width], group=group)
+        for r in range(world):
+            if size_list[r]:
+                ops.merge_long_records(owned, gathered[r * width:r * width + size_list[r]], rank, world)
+    return ExchangeStats(n_send, n_recv, n_send * 8 * ENTRY_WORDS, long_total)
+
+
+def allreduce_scalar(partial, dist, group=None, reproducible: bool = True):
+    """Finishes a sharded map-then-reduce: sum of the ranks' partial sums.
+
+    partial: 1-element float64 tensor (device for NCCL).  reproducible=True gathers the n
+    partials and adds them in rank order (bitwise run-to-run stable, the reference's
+    determinism contract, proj/include/wfc/engine.hpp:27-31); False is a plain allreduce.
+    """
+    world = dist.get_world_size(group)
+    if world == 1:
+        return partial.clone()
+    if not reproducible:
+        out = partial.clone()
+        dist.all_reduce(out, group=group)
+        return out
+    parts = [partial.new_empty(partial.shape) for _ in range(world)]
+    dist.all_gather(parts, partial, group=group)
+    acc = parts[0].clone()
+    for p in parts[1:]:
+        acc += p
+    return acc
+
+
+def shard_documents(n_docs: int, rank: int, world: int) -> range:
+    """Round-robin document assignment d = rank (mod world), the reference's rule
+    (/root/reference/proj/src/pipeline.cpp:83)."""
+    return range(rank, n_docs, world)
