@@ -55,59 +55,70 @@ def measured_peak_gbs():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle reasons sampled through NVML DURING the timed region."""
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines: list[str] = []
+        self.samples: list[tuple[int, int]] = []
+        self.max_mhz = None
+        self.stop = threading.Event()
+        self.thread = None
+        self.error = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import pynvml
+            pynvml.nvmlInit()
+            visible = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = self.index
+            if visible:
+                try:
+                    idx = int(visible.split(",")[self.index])
+                except (ValueError, IndexError):
+                    pass
+            self.nvml = pynvml
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
             self.thread = threading.Thread(target=self._pump, daemon=True)
             self.thread.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:   # no NVML: report it, never fake a reading
+            self.error = repr(e)
         return self
 
     def _pump(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+        n = self.nvml
+        while not self.stop.is_set():
+            try:
+                mhz = n.nvmlDeviceGetClockInfo(self.handle, n.NVML_CLOCK_SM)
+                try:
+                    reasons = n.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+                except Exception:
+                    reasons = n.nvmlDeviceGetCurrentClocksThrottleReasons(self.handle)
+                self.samples.append((mhz, reasons))
+            except Exception as e:
+                self.error = repr(e)
+                return
+            time.sleep(0.001)
 
     def __exit__(self, *exc):
-        if self.proc:
-            time.sleep(0.15)
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.thread:
+            self.thread.join(timeout=2)
 
     def summary(self) -> dict:
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for name, val in zip(names, parts[3:7]):
-                if val.lower().startswith("active"):
-                    reasons.add(name)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0, "error": self.error}
+        n = self.nvml
+        names = {"hw_slowdown": getattr(n, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+                 "hw_thermal_slowdown": getattr(n, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+                 "sw_thermal_slowdown": getattr(n, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+                 "sw_power_cap": getattr(n, "nvmlClocksThrottleReasonSwPowerCap", 0x4)}
+        mhz = sorted(m for m, _ in self.samples)
+        seen = 0
+        for _, r in self.samples:
+            seen |= r
+        return {"sm_mhz": mhz[len(mhz) // 2], "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(k for k, bit in names.items() if seen & bit), "samples": len(mhz)}
 
 
 def plan(workload: str, world: int, rank: int, docs_override: int | None):
@@ -193,17 +204,17 @@ def cpu_baseline(capi, vocab: int, total_docs: int) -> dict:
     cores = os.cpu_count() or 1
     use_ref = oracle.ref_available()
     cpu = oracle.ref() if use_ref else oracle.port()
-    k = 8
-    blob = capi.synth_corpus(SEED, 0, 64, vocab, ZIPF_S, 0, DOC_BYTES)
-    docs = [blob[i * DOC_BYTES:(i + 1) * DOC_BYTES] for i in range(64)]
+    k, cap = 8, 256   # run_wordcount keeps every token as a std::string: bound the sample
+    blob = capi.synth_corpus(SEED, 0, cap, vocab, ZIPF_S, 0, DOC_BYTES)
+    docs = [blob[i * DOC_BYTES:(i + 1) * DOC_BYTES] for i in range(cap)]
 
     def one(d):
         t0 = time.perf_counter()
         cpu.run_wordcount(d, cores) if use_ref else cpu.wordcount(d)
         return time.perf_counter() - t0
     t = one(docs[:k])
-    if t < 5.0:      # grow the sample towards ~10-20 s of CPU work, at most 64 documents
-        k = int(min(64, max(k, k * 12.0 / max(t, 1e-3))))
+    if t < 5.0:      # grow the sample towards ~10-20 s of CPU work, at most 256 documents
+        k = int(min(cap, max(k, k * 12.0 / max(t, 1e-3))))
         t = one(docs[:k])
     nbytes = k * DOC_BYTES
     return {"value": nbytes / t / 1e9, "unit": UNIT, "cores": cores if use_ref else 1,

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -35,6 +36,23 @@ cudaError_t tb_long_serialize(const TableView& t, uint8_t* out, u64 cap, u64* de
                               u64* launches);
 cudaError_t tb_long_merge(const TableView& t, const uint8_t* recs, u64 n_bytes, u32 part, u32 n_parts, cudaStream_t s,
                           u64* launches);
+// wordcount.cu (stand-alone tokenizer) and tokens.cu
+cudaError_t wc_tokenize_launch(const uint8_t* text, u64 n, const TableView& gt, const EmitView& em, int sm_count,
+                               cudaStream_t stream, u64* launches);
+struct SortScratch {
+    TokenRec* alt;
+    u64* hist;
+    u64* tmp;
+    int* flag;
+};
+u64 sort_hist_words(u64 n);
+u64 scan_tmp_words(u64 n);
+cudaError_t tokens_sort(TokenRec* recs, u64 n, bool by_position, const uint8_t* arena, const SortScratch& sc, int sm,
+                        cudaStream_t s, u64* launches);
+cudaError_t tokens_rle_flags(const TokenRec* recs, u64 n, const uint8_t* arena, u64* flags, int* status, int sm,
+                             cudaStream_t s, u64* launches);
+cudaError_t tokens_rle_insert(const TokenRec* recs, u64 n, const uint8_t* arena, u64* flags, u64* run_start, u64* tmp,
+                              const TableView& t, int sm, cudaStream_t s, u64* launches);
 // synth.cpp
 int synth_document(uint64_t seed, uint64_t doc, uint32_t vocab, double s, uint32_t speaker, uint8_t* out, uint64_t doc_bytes);
 int synth_corpus(uint64_t seed, uint64_t doc_begin, uint64_t doc_end, uint32_t vocab, double s, uint32_t speaker,
@@ -637,15 +655,42 @@ extern "C" int wfcu_counter_count_host(wfcu_counter* c, const uint8_t* const* do
         if (used[cur]) CUDA_TRY(cudaEventSynchronize(c->done[cur]));   // buffer about to be refilled
         return WFCU_OK;
     };
-    for (u64 d = 0; d < n_docs; ++d) {
-        const u64 need = doc_lens[d] + 1;
-        if (fill + need > c->chunk_cap)
+    // documents [first, d) form one chunk; they are packed by a few host threads
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const unsigned n_threads = std::min(8u, hw);
+    std::vector<u64> offs;
+    auto pack = [&](u64 first, u64 last) {
+        uint8_t* dst = c->pinned[cur];
+        const u64 count = last - first;
+        auto work = [&](unsigned t) {
+            for (u64 i = first + t; i < last; i += n_threads) {
+                std::memcpy(dst + offs[i - first], docs[i], doc_lens[i]);
+                dst[offs[i - first] + doc_lens[i]] = '\n';
+            }
+        };
+        if (count < 4 || n_threads == 1) {
+            for (unsigned t = 0; t < n_threads; ++t) work(t);
+        } else {
+            std::vector<std::thread> pool;
+            for (unsigned t = 1; t < n_threads; ++t) pool.emplace_back(work, t);
+            work(0);
+            for (auto& th : pool) th.join();
+        }
+    };
+    u64 first = 0;
+    for (u64 d = 0; d <= n_docs; ++d) {
+        const u64 need = d < n_docs ? doc_lens[d] + 1 : 0;
+        if (d == n_docs || fill + need > c->chunk_cap) {
+            if (d > first) pack(first, d);
             if (int rc = submit()) return rc;
-        std::memcpy(c->pinned[cur] + fill, docs[d], doc_lens[d]);
-        c->pinned[cur][fill + doc_lens[d]] = '\n';
-        fill += need;
+            first = d;
+            offs.clear();
+        }
+        if (d < n_docs) {
+            offs.push_back(fill);
+            fill += need;
+        }
     }
-    if (int rc = submit()) return rc;
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     return wfcu_counter_status(c, c->stream);
 }
@@ -731,14 +776,281 @@ extern "C" int wfcu_synth_uniform(uint64_t seed, uint64_t n, int dtype, void* ou
     return WFCU_OK;
 }
 
-// ---- tokens API: TEMPORARY stubs, replaced by tokens.cu ------------------------------
-#define WFCU_TODO(name) return fail(WFCU_ERR_CUDA, name ": not implemented yet")
-extern "C" int wfcu_tokenize_dev(const uint8_t*, uint64_t, void*, wfcu_tokens**) { WFCU_TODO("wfcu_tokenize_dev"); }
-extern "C" int wfcu_tokenize_host(const uint8_t*, uint64_t, wfcu_tokens**) { WFCU_TODO("wfcu_tokenize_host"); }
-extern "C" void wfcu_tokens_destroy(wfcu_tokens*) {}
-extern "C" int wfcu_tokens_stats(const wfcu_tokens*, uint64_t*, uint64_t*) { WFCU_TODO("wfcu_tokens_stats"); }
-extern "C" int wfcu_tokens_export(const wfcu_tokens*, uint8_t*, uint64_t, uint32_t*, uint64_t) { WFCU_TODO("wfcu_tokens_export"); }
-extern "C" int wfcu_tokens_from_words(const uint8_t*, const uint32_t*, uint64_t, wfcu_tokens**) { WFCU_TODO("wfcu_tokens_from_words"); }
-extern "C" int wfcu_tokens_sort(wfcu_tokens*, void*) { WFCU_TODO("wfcu_tokens_sort"); }
-extern "C" int wfcu_tokens_reduce_sorted(const wfcu_tokens*, wfcu_counter*, void*) { WFCU_TODO("wfcu_tokens_reduce_sorted"); }
-extern "C" int wfcu_counter_count_dev_sorted(wfcu_counter*, const uint8_t*, uint64_t, void*) { WFCU_TODO("wfcu_counter_count_dev_sorted"); }
+// ---- token lists: tokenize / sort_words / reduce_sorted ---------------------------------
+struct wfcu_tokens {
+    int device = 0;
+    int sm_count = 0;
+    TokenRec* recs = nullptr;
+    u64 n = 0;
+    uint8_t* arena = nullptr;   // long-token records {u32 len, u32 hash, bytes}, offset 0 unused
+    u64 arena_used = 0;
+    u64 arena_cap = 0;
+    bool sorted = false;        // WordList::sorted (proj/include/wfc/text.hpp:18-21)
+};
+
+static void tokens_free(wfcu_tokens* t) {
+    if (!t) return;
+    cudaFree(t->recs);
+    cudaFree(t->arena);
+    delete t;
+}
+
+extern "C" void wfcu_tokens_destroy(wfcu_tokens* t) {
+    if (t) cudaSetDevice(t->device);
+    tokens_free(t);
+}
+
+namespace {
+struct DevBuf {   // RAII device allocation
+    void* p = nullptr;
+    cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes ? bytes : 16); }
+    ~DevBuf() { cudaFree(p); }
+    template <typename T> T* as() { return static_cast<T*>(p); }
+};
+}  // namespace
+
+static int sort_device_tokens(wfcu_tokens* t, bool by_position, cudaStream_t s) {
+    if (t->n < 2) return WFCU_OK;
+    DevBuf alt, hist, tmp, flag;
+    const u64 hw = sort_hist_words(t->n);
+    CUDA_TRY(alt.alloc(sizeof(TokenRec) * t->n));
+    CUDA_TRY(hist.alloc(sizeof(u64) * hw));
+    CUDA_TRY(tmp.alloc(sizeof(u64) * scan_tmp_words(hw)));
+    CUDA_TRY(flag.alloc(sizeof(int)));
+    SortScratch sc{alt.as<TokenRec>(), hist.as<u64>(), tmp.as<u64>(), flag.as<int>()};
+    LaunchTally tally;
+    CUDA_TRY(tokens_sort(t->recs, t->n, by_position, t->arena, sc, t->sm_count, s, &tally.n));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return WFCU_OK;
+}
+
+// Runs the tokenizer kernels; the records come out in no particular order.
+static int tokenize_unordered(const uint8_t* dev_text, uint64_t n, cudaStream_t s, wfcu_tokens** out) {
+    *out = nullptr;
+    DeviceState* d;
+    if (int rc = current_device_state(&d)) return rc;
+    if (n && !dev_text) return fail(WFCU_ERR_INVALID_ARGUMENT, "text is null");
+    if (reinterpret_cast<uintptr_t>(dev_text) & 15u) return fail(WFCU_ERR_INVALID_ARGUMENT, "device text must be 16-byte aligned");
+    auto* t = new wfcu_tokens;
+    cudaGetDevice(&t->device);
+    t->sm_count = d->sm_count;
+    if (n == 0) {
+        *out = t;
+        return WFCU_OK;
+    }
+    u64 cap = n / 5 + 1024;                 // records; grown to the exact count on overflow
+    u64 deferred_cap = n / 16 + 1024;       // grown on overflow
+    u64 arena_cap = std::max<u64>(1 << 20, n / 4);
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        DevBuf recs, deferred, arena, counters;
+        cudaError_t e = recs.alloc(sizeof(TokenRec) * cap);
+        if (e == cudaSuccess) e = deferred.alloc(sizeof(u64) * deferred_cap);
+        if (e == cudaSuccess) e = arena.alloc(arena_cap);
+        if (e == cudaSuccess) e = counters.alloc(sizeof(u64) * 16);
+        if (e == cudaSuccess) e = cudaMemsetAsync(counters.p, 0, sizeof(u64) * 16, s);
+        const u64 arena_start = 8;
+        u64* cnt = counters.as<u64>();
+        if (e == cudaSuccess) e = cudaMemcpyAsync(cnt + 4, &arena_start, sizeof(u64), cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) {
+            tokens_free(t);
+            return fail(WFCU_ERR_CUDA, "tokenize allocation: %s", cudaGetErrorString(e));
+        }
+        TableView v{};
+        v.n_used = cnt + 0; v.n_tokens = cnt + 1; v.n_deferred = cnt + 2; v.n_long = cnt + 3; v.arena_used = cnt + 4;
+        v.status = reinterpret_cast<int*>(cnt + 5);
+        v.deferred = deferred.as<u64>(); v.deferred_cap = deferred_cap;
+        v.arena = arena.as<uint8_t>(); v.arena_cap = arena_cap;
+        EmitView em{recs.as<TokenRec>(), cap, cnt + 6};
+        LaunchTally tally;
+        e = wc_tokenize_launch(dev_text, n, v, em, d->sm_count, s, &tally.n);
+        u64 h[8];
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) {
+            tokens_free(t);
+            return fail(WFCU_ERR_CUDA, "tokenize: %s", cudaGetErrorString(e));
+        }
+        const int st = (int)(h[5] & 0xFFFFFFFFu);
+        const u64 produced = h[6];
+        if (produced > cap || (st & (kStatusDeferredFull | kStatusArenaFull))) {
+            // grow what overflowed and run again (n_out keeps counting past cap, so it is exact
+            // unless the deferred list or the arena cut the run short)
+            if (produced > cap) cap = produced + 1024;
+            if (st & kStatusDeferredFull) { deferred_cap = n / 2 + 1024; cap = std::max<u64>(cap, n / 2 + 1024); }
+            if (st & kStatusArenaFull) arena_cap = 3 * n + 4096;
+            continue;
+        }
+        t->recs = recs.as<TokenRec>();
+        recs.p = nullptr;
+        t->arena = arena.as<uint8_t>();
+        arena.p = nullptr;
+        t->n = produced;
+        t->arena_used = h[4];
+        t->arena_cap = arena_cap;
+        *out = t;
+        return WFCU_OK;
+    }
+    tokens_free(t);
+    return fail(WFCU_ERR_ARENA_FULL, "tokenize: capacities still too small after regrowing");
+}
+
+extern "C" int wfcu_tokenize_dev(const uint8_t* dev_text, uint64_t n, void* stream, wfcu_tokens** out) {
+    if (!out) return fail(WFCU_ERR_INVALID_ARGUMENT, "out is null");
+    if (int rc = tokenize_unordered(dev_text, n, (cudaStream_t)stream, out)) return rc;
+    if (int rc = sort_device_tokens(*out, /*by_position=*/true, (cudaStream_t)stream)) {
+        tokens_free(*out);
+        *out = nullptr;
+        return rc;
+    }
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_tokenize_host(const uint8_t* text, uint64_t n, wfcu_tokens** out) {
+    if (!out) return fail(WFCU_ERR_INVALID_ARGUMENT, "out is null");
+    DeviceState* d;
+    if (int rc = current_device_state(&d)) return rc;
+    if (n && !text) return fail(WFCU_ERR_INVALID_ARGUMENT, "text is null");
+    void* dev = nullptr;
+    if (int rc = upload(text, n, &dev)) return rc;
+    const int rc = wfcu_tokenize_dev(static_cast<const uint8_t*>(dev), n, nullptr, out);
+    cudaFree(dev);
+    return rc;
+}
+
+extern "C" int wfcu_tokens_stats(const wfcu_tokens* t, uint64_t* n_tokens, uint64_t* n_bytes) {
+    if (!t) return fail(WFCU_ERR_INVALID_ARGUMENT, "tokens is null");
+    if (n_tokens) *n_tokens = t->n;
+    if (n_bytes) {
+        // lengths are recomputed on the host from the records (cheap next to the D2H copy)
+        std::vector<TokenRec> h(t->n);
+        std::vector<uint8_t> arena(t->arena_used);
+        if (t->n) CUDA_TRY(cudaMemcpy(h.data(), t->recs, sizeof(TokenRec) * t->n, cudaMemcpyDeviceToHost));
+        if (t->arena_used > 8) CUDA_TRY(cudaMemcpy(arena.data(), t->arena, t->arena_used, cudaMemcpyDeviceToHost));
+        u64 total = 0;
+        for (const TokenRec& r : h) {
+            if (r.ext) {
+                u32 len;
+                std::memcpy(&len, arena.data() + r.ext, 4);
+                total += len;
+            } else {
+                total += key_len(r.k0, r.k1);
+            }
+        }
+        *n_bytes = total;
+    }
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_tokens_export(const wfcu_tokens* t, uint8_t* bytes, uint64_t bytes_cap, uint32_t* lens,
+                                  uint64_t lens_cap) {
+    if (!t) return fail(WFCU_ERR_INVALID_ARGUMENT, "tokens is null");
+    if (t->n > lens_cap) return fail(WFCU_ERR_BUFFER_TOO_SMALL, "export needs %llu lengths", (unsigned long long)t->n);
+    std::vector<TokenRec> h(t->n);
+    std::vector<uint8_t> arena(t->arena_used);
+    if (t->n) CUDA_TRY(cudaMemcpy(h.data(), t->recs, sizeof(TokenRec) * t->n, cudaMemcpyDeviceToHost));
+    if (t->arena_used > 8) CUDA_TRY(cudaMemcpy(arena.data(), t->arena, t->arena_used, cudaMemcpyDeviceToHost));
+    u64 off = 0;
+    for (u64 i = 0; i < t->n; ++i) {
+        const TokenRec& r = h[i];
+        if (r.ext) {
+            u32 len;
+            std::memcpy(&len, arena.data() + r.ext, 4);
+            if (off + len > bytes_cap) return fail(WFCU_ERR_BUFFER_TOO_SMALL, "export byte buffer too small");
+            std::memcpy(bytes + off, arena.data() + r.ext + 8, len);
+            lens[i] = len;
+            off += len;
+        } else {
+            uint8_t b[16];
+            key_to_bytes(r.k0, r.k1, b);
+            const u32 len = key_len(r.k0, r.k1);
+            if (off + len > bytes_cap) return fail(WFCU_ERR_BUFFER_TOO_SMALL, "export byte buffer too small");
+            std::memcpy(bytes + off, b, len);
+            lens[i] = len;
+            off += len;
+        }
+    }
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_tokens_from_words(const uint8_t* bytes, const uint32_t* lens, uint64_t n_tokens, wfcu_tokens** out) {
+    if (!out) return fail(WFCU_ERR_INVALID_ARGUMENT, "out is null");
+    *out = nullptr;
+    DeviceState* d;
+    if (int rc = current_device_state(&d)) return rc;
+    if (n_tokens && (!bytes || !lens)) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
+    std::vector<TokenRec> recs(n_tokens);
+    std::vector<uint8_t> arena(8, 0);
+    u64 off = 0;
+    for (u64 i = 0; i < n_tokens; ++i) {
+        const u32 len = lens[i];
+        if (len == 0) return fail(WFCU_ERR_INVALID_ARGUMENT, "empty word at index %llu", (unsigned long long)i);
+        TokenRec r{};
+        key_from_bytes(bytes + off, std::min<u32>(len, 16), &r.k0, &r.k1);
+        r.pos = i;
+        if (len > 16) {
+            const size_t at = arena.size();
+            arena.resize(at + 8 + ((size_t(len) + 7) & ~size_t(7)), 0);
+            const u32 h = fnv32(bytes + off, len);
+            std::memcpy(&arena[at], &len, 4);
+            std::memcpy(&arena[at + 4], &h, 4);
+            std::memcpy(&arena[at + 8], bytes + off, len);
+            r.ext = at;
+        }
+        recs[i] = r;
+        off += len;
+    }
+    auto* t = new wfcu_tokens;
+    cudaGetDevice(&t->device);
+    t->sm_count = d->sm_count;
+    t->n = n_tokens;
+    t->arena_used = arena.size();
+    t->arena_cap = arena.size();
+    void* p = nullptr;
+    if (int rc = upload(recs.data(), sizeof(TokenRec) * n_tokens, &p)) { tokens_free(t); return rc; }
+    t->recs = static_cast<TokenRec*>(p);
+    if (int rc = upload(arena.data(), arena.size(), &p)) { tokens_free(t); return rc; }
+    t->arena = static_cast<uint8_t*>(p);
+    *out = t;
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_tokens_sort(wfcu_tokens* t, void* stream) {
+    if (!t) return fail(WFCU_ERR_INVALID_ARGUMENT, "tokens is null");
+    if (int rc = sort_device_tokens(t, /*by_position=*/false, (cudaStream_t)stream)) return rc;
+    t->sorted = true;
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_tokens_reduce_sorted(const wfcu_tokens* t, wfcu_counter* into, void* stream) {
+    if (!t || !into) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
+    if (t->n == 0) return WFCU_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    DevBuf flags, starts, tmp, status;
+    CUDA_TRY(flags.alloc(sizeof(u64) * t->n));
+    CUDA_TRY(starts.alloc(sizeof(u64) * t->n));
+    CUDA_TRY(tmp.alloc(sizeof(u64) * scan_tmp_words(t->n)));
+    CUDA_TRY(status.alloc(sizeof(int)));
+    CUDA_TRY(cudaMemsetAsync(status.p, 0, sizeof(int), s));
+    LaunchTally tally;
+    CUDA_TRY(tokens_rle_flags(t->recs, t->n, t->arena, flags.as<u64>(), status.as<int>(), into->sm_count, s, &tally.n));
+    int st = 0;
+    CUDA_TRY(cudaMemcpyAsync(&st, status.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    // the reference checks the `sorted` flag (reduce.cpp:9); here the order itself is checked
+    if (st & kStatusNotSorted) return fail(WFCU_ERR_NOT_SORTED, "reduce_sorted: word list must be sorted");
+    CUDA_TRY(tokens_rle_insert(t->recs, t->n, t->arena, flags.as<u64>(), starts.as<u64>(), tmp.as<u64>(), into->v,
+                               into->sm_count, s, &tally.n));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_counter_count_dev_sorted(wfcu_counter* c, const uint8_t* dev_text, uint64_t n, void* stream) {
+    if (!c) return fail(WFCU_ERR_INVALID_ARGUMENT, "counter is null");
+    if (n == 0) return WFCU_OK;
+    wfcu_tokens* t = nullptr;
+    if (int rc = tokenize_unordered(dev_text, n, (cudaStream_t)stream, &t)) return rc;
+    int rc = wfcu_tokens_sort(t, stream);
+    if (rc == WFCU_OK) rc = wfcu_tokens_reduce_sorted(t, c, stream);
+    tokens_free(t);
+    return rc;
+}

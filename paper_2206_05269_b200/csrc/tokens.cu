@@ -1,0 +1,363 @@
+// tokens.cu -- device-resident token lists: the stand-alone tokenizer, the stable
+// byte-wise sort and the run-length-encode reduce, i.e. the reference's
+//   tokenize      /root/reference/proj/src/text.cpp:32-57
+//   sort_words    proj/src/text.cpp:59-63      (std::stable_sort of std::string)
+//   reduce_sorted proj/src/reduce.cpp:8-21     (RLE into the count map)
+// kept as the alternative to the hash-count path for high-cardinality vocabularies.
+//
+// A token is a 32-byte TokenRec: its first 16 bytes big-endian packed (so unsigned
+// integer order on (k0,k1) IS byte-wise lexicographic order), an arena reference for
+// the rare token longer than 16 bytes, and its text position.
+//   * sort: hand-written stable LSD radix sort, 8-bit digits, keys (is_long, k1, k0);
+//     digit passes whose histogram has a single bin are skipped (k1 is all zero for
+//     corpora of short words); ties between long tokens that share a 16-byte prefix
+//     are ordered by an exact string fix-up pass.
+//   * RLE: head flags by adjacent comparison -> exclusive scan -> run starts ->
+//     counts[key] += run length in the table.
+#include "wfcu_dev.cuh"
+
+namespace wfcu {
+
+// ---------------------------------------------------------------------------------
+// exclusive scan of u64 (three-phase, up to 2^30 elements)
+// ---------------------------------------------------------------------------------
+constexpr int kScanBlock = 1024;
+
+__global__ void scan_reduce_kernel(const u64* __restrict__ in, u64 n, u64* __restrict__ block_sums) {
+    __shared__ u64 warp_sums[32];
+    const u64 i = (u64)blockIdx.x * kScanBlock + threadIdx.x;
+    u64 v = i < n ? in[i] : 0;
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, d);
+    if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = warp_sums[threadIdx.x];
+        for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, d);
+        if (threadIdx.x == 0) block_sums[blockIdx.x] = v;
+    }
+}
+
+// exclusive scan inside each block of kScanBlock elements, plus block_offsets[block]
+__global__ void scan_block_kernel(const u64* __restrict__ in, u64 n, const u64* __restrict__ block_offsets,
+                                  u64* __restrict__ out) {
+    __shared__ u64 warp_sums[32];
+    const u64 i = (u64)blockIdx.x * kScanBlock + threadIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const u64 x = i < n ? in[i] : 0;
+    u64 v = x;
+    for (int d = 1; d < 32; d <<= 1) {
+        const u64 t = __shfl_up_sync(0xFFFFFFFFu, v, d);
+        if (lane >= d) v += t;
+    }
+    if (lane == 31) warp_sums[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        u64 w = warp_sums[lane];
+        for (int d = 1; d < 32; d <<= 1) {
+            const u64 t = __shfl_up_sync(0xFFFFFFFFu, w, d);
+            if (lane >= d) w += t;
+        }
+        warp_sums[lane] = w;
+    }
+    __syncthreads();
+    const u64 base = (block_offsets ? block_offsets[blockIdx.x] : 0) + (warp ? warp_sums[warp - 1] : 0);
+    if (i < n) out[i] = base + v - x;
+}
+
+// out = exclusive_scan(in) ; tmp must hold ceil(n/1024) + ceil(n/1024^2) + 2 u64.  in may alias out.
+cudaError_t exclusive_scan_u64(const u64* in, u64* out, u64 n, u64* tmp, cudaStream_t s, u64* launches) {
+    if (n == 0) return cudaSuccess;
+    const u64 nb = (n + kScanBlock - 1) / kScanBlock;
+    if (nb == 1) {
+        scan_block_kernel<<<1, kScanBlock, 0, s>>>(in, n, nullptr, out);
+        *launches += 1;
+        return cudaGetLastError();
+    }
+    u64* sums = tmp;
+    scan_reduce_kernel<<<(unsigned)nb, kScanBlock, 0, s>>>(in, n, sums);
+    *launches += 1;
+    cudaError_t e = exclusive_scan_u64(sums, sums, nb, tmp + nb, s, launches);
+    if (e != cudaSuccess) return e;
+    scan_block_kernel<<<(unsigned)nb, kScanBlock, 0, s>>>(in, n, sums, out);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------
+// stable LSD radix sort of TokenRec
+// ---------------------------------------------------------------------------------
+constexpr int kSortWarps = 4;          // warps per CTA, one tile each
+constexpr int kTileItems = 2048;       // records per warp tile
+
+// pass: 0..7 -> byte of k1 (least significant first), 8..15 -> byte of k0, 16 -> pos bytes via separate kernel mode
+__device__ __forceinline__ u32 digit_of(const TokenRec& r, int mode, int pass) {
+    if (mode == 0) return (u32)((pass < 8 ? r.k1 >> (8 * pass) : r.k0 >> (8 * (pass - 8))) & 0xFF);
+    if (mode == 1) return (u32)((r.pos >> (8 * pass)) & 0xFF);   // text order
+    return r.ext ? 1u : 0u;                                      // mode 2: long tokens after equal inline ones
+}
+
+// hist[digit * n_tiles + tile]
+__global__ void sort_hist_kernel(const TokenRec* __restrict__ in, u64 n, u64 n_tiles, int mode, int pass,
+                                 u64* __restrict__ hist) {
+    __shared__ u32 sh[kSortWarps][256];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const u64 tile = (u64)blockIdx.x * kSortWarps + warp;
+    for (int d = lane; d < 256; d += 32) sh[warp][d] = 0;
+    __syncwarp();
+    if (tile < n_tiles) {
+        const u64 lo = tile * kTileItems;
+        const u64 hi = min(lo + (u64)kTileItems, n);
+        for (u64 i = lo + lane; i < hi; i += 32) atomicAdd(&sh[warp][digit_of(in[i], mode, pass)], 1u);
+    }
+    __syncwarp();
+    if (tile < n_tiles)
+        for (int d = lane; d < 256; d += 32) hist[(u64)d * n_tiles + tile] = sh[warp][d];
+}
+
+// single-bin test: flag[0] = 1 when every record has the same digit (pass can be skipped)
+__global__ void sort_single_bin_kernel(const u64* __restrict__ hist, u64 n_tiles, u64 n, int* __restrict__ flag) {
+    __shared__ int found;
+    if (threadIdx.x == 0) found = 0;
+    __syncthreads();
+    // digit d is "the" bin when its counts over all tiles sum to n
+    const int d = threadIdx.x;   // 256 threads
+    u64 sum = 0;
+    for (u64 t = 0; t < n_tiles; ++t) sum += hist[(u64)d * n_tiles + t];
+    if (sum == n) found = 1;
+    __syncthreads();
+    if (threadIdx.x == 0) *flag = found;
+}
+
+// offs = exclusive scan of hist (digit-major), scatter keeps the tile order inside a digit
+__global__ void sort_scatter_kernel(const TokenRec* __restrict__ in, TokenRec* __restrict__ out, u64 n, u64 n_tiles,
+                                    int mode, int pass, const u64* __restrict__ offs, const int* __restrict__ skip) {
+    if (*skip) return;   // the caller swaps buffers only when the pass ran; see radix_pass
+    __shared__ u64 sh[kSortWarps][256];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const u64 tile = (u64)blockIdx.x * kSortWarps + warp;
+    if (tile >= n_tiles) return;
+    for (int d = lane; d < 256; d += 32) sh[warp][d] = offs[(u64)d * n_tiles + tile];
+    __syncwarp();
+    const u64 lo = tile * kTileItems;
+    const u64 hi = min(lo + (u64)kTileItems, n);
+    const u32 lt = (1u << lane) - 1u;
+    for (u64 base = lo; base < hi; base += 32) {
+        const u64 i = base + lane;
+        const bool live = i < hi;
+        TokenRec r{};
+        u32 d = 0xFFFFFFFFu;
+        if (live) {
+            r = in[i];
+            d = digit_of(r, mode, pass);
+        }
+        const u32 peers = __match_any_sync(0xFFFFFFFFu, d);
+        u64 dst = 0;
+        if (live) dst = sh[warp][d] + __popc(peers & lt);
+        __syncwarp();
+        if (live && (peers & lt) == 0) sh[warp][d] += __popc(peers);   // lowest lane of each digit group
+        __syncwarp();
+        if (live) out[dst] = r;
+    }
+}
+
+// when a pass is skipped the data stays in `in`; copy so that the ping-pong stays uniform
+__global__ void sort_copy_if_skipped_kernel(const TokenRec* __restrict__ in, TokenRec* __restrict__ out, u64 n,
+                                            const int* __restrict__ skip) {
+    if (!*skip) return;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) out[i] = in[i];
+}
+
+// ---- long-token tie fix-up ---------------------------------------------------------
+__device__ __forceinline__ int long_compare(const uint8_t* arena, u64 a, u64 b) {
+    const u32 la = *reinterpret_cast<const u32*>(arena + a), lb = *reinterpret_cast<const u32*>(arena + b);
+    const uint8_t* pa = arena + a + 8;
+    const uint8_t* pb = arena + b + 8;
+    const u32 m = la < lb ? la : lb;
+    for (u32 i = 16; i < m; ++i) {   // the first 16 bytes are known equal
+        if (pa[i] != pb[i]) return pa[i] < pb[i] ? -1 : 1;
+    }
+    return la < lb ? -1 : (la > lb ? 1 : 0);
+}
+
+// After the radix passes, long tokens with the same 16-byte prefix are adjacent and in
+// original order; order each such run by the full string (stable insertion sort, one
+// thread per run -- long tokens are rare).
+__global__ void sort_long_fixup_kernel(TokenRec* __restrict__ recs, u64 n, const uint8_t* __restrict__ arena) {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const TokenRec r = recs[i];
+        if (!r.ext) continue;
+        if (i > 0) {
+            const TokenRec p = recs[i - 1];
+            if (p.ext && p.k0 == r.k0 && p.k1 == r.k1) continue;   // not a run head
+        }
+        u64 end = i + 1;
+        while (end < n && recs[end].ext && recs[end].k0 == r.k0 && recs[end].k1 == r.k1) ++end;
+        for (u64 a = i + 1; a < end; ++a) {
+            const TokenRec x = recs[a];
+            u64 b = a;
+            while (b > i && long_compare(arena, recs[b - 1].ext, x.ext) > 0) {
+                recs[b] = recs[b - 1];
+                --b;
+            }
+            recs[b] = x;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// run-length encode
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ int rec_compare(const TokenRec& a, const TokenRec& b, const uint8_t* arena) {
+    if (a.k0 != b.k0) return a.k0 < b.k0 ? -1 : 1;
+    if (a.k1 != b.k1) return a.k1 < b.k1 ? -1 : 1;
+    if (!a.ext && !b.ext) return 0;
+    if (!a.ext) return -1;   // a 16-byte token sorts before a longer one with that prefix
+    if (!b.ext) return 1;
+    return long_compare(arena, a.ext, b.ext);
+}
+
+// flags[i] = 1 when record i starts a run; sets kStatusNotSorted in *status on a descent
+__global__ void rle_flags_kernel(const TokenRec* __restrict__ recs, u64 n, const uint8_t* __restrict__ arena,
+                                 u64* __restrict__ flags, int* __restrict__ status) {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        u64 f = 1;
+        if (i > 0) {
+            const int c = rec_compare(recs[i - 1], recs[i], arena);
+            if (c > 0) atomicOr(status, kStatusNotSorted);
+            f = c != 0;
+        }
+        flags[i] = f;
+    }
+}
+
+// run_start[scan[i]] = i for heads; n_runs = scan[n-1] + flags[n-1]
+__global__ void rle_starts_kernel(const u64* __restrict__ flags_scan, const TokenRec* __restrict__ recs, u64 n,
+                                  const uint8_t* __restrict__ arena, u64* __restrict__ run_start) {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const bool head = (i == 0) || rec_compare(recs[i - 1], recs[i], arena) != 0;
+        if (head) run_start[flags_scan[i]] = i;
+    }
+}
+
+// counts[key of run r] += length of run r
+__global__ void rle_insert_kernel(const TokenRec* __restrict__ recs, u64 n, const uint8_t* __restrict__ arena,
+                                  const u64* __restrict__ run_start, const u64* __restrict__ flags_scan, TableView t) {
+    // heads before the last record, plus the last record's own run
+    const bool last_is_head = (n == 1) || rec_compare(recs[n - 2], recs[n - 1], arena) != 0;
+    const u64 n_runs = flags_scan[n - 1] + (last_is_head ? 1 : 0);
+    u64 tokens = 0;
+    for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < n_runs; r += (u64)gridDim.x * blockDim.x) {
+        const u64 lo = run_start[r];
+        const u64 hi = (r + 1 < n_runs) ? run_start[r + 1] : n;
+        const TokenRec rec = recs[lo];
+        const u64 len = hi - lo;
+        tokens += len;
+        if (!rec.ext) {
+            table_add(t, rec.k0, rec.k1, len);
+        } else {
+            const u32 blen = *reinterpret_cast<const u32*>(arena + rec.ext);
+            const u64 dst = arena_alloc(t, blen);
+            if (dst) {
+                *reinterpret_cast<u32*>(t.arena + dst) = blen;
+                *reinterpret_cast<u32*>(t.arena + dst + 4) = *reinterpret_cast<const u32*>(arena + rec.ext + 4);
+                for (u32 k = 0; k < blen; ++k) t.arena[dst + 8 + k] = arena[rec.ext + 8 + k];
+                __threadfence();
+                long_add(t, dst, len);
+            }
+        }
+    }
+    for (int d = 16; d > 0; d >>= 1) tokens += __shfl_xor_sync(0xFFFFFFFFu, tokens, d);
+    if ((threadIdx.x & 31) == 0 && tokens) atomicAdd(t.n_tokens, tokens);
+}
+
+// ---------------------------------------------------------------------------------
+// host-side drivers
+// ---------------------------------------------------------------------------------
+static inline unsigned blocks_for(u64 items, int threads, int sm) {
+    u64 g = (items + threads - 1) / threads;
+    const u64 cap = (u64)sm * 16;
+    if (g > cap) g = cap;
+    if (g == 0) g = 1;
+    return (unsigned)g;
+}
+
+struct SortScratch {
+    TokenRec* alt;   // n records
+    u64* hist;       // 256 * n_tiles
+    u64* tmp;        // scan scratch
+    int* flag;       // skip flag
+};
+
+u64 sort_n_tiles(u64 n) { return (n + kTileItems - 1) / kTileItems; }
+u64 sort_hist_words(u64 n) { return 256 * sort_n_tiles(n); }
+u64 scan_tmp_words(u64 n) { return (n / kScanBlock + 2) + (n / ((u64)kScanBlock * kScanBlock) + 2) + 8; }
+
+// One stable radix pass; data ends up in `b` (either scattered or copied).
+static cudaError_t radix_pass(TokenRec* a, TokenRec* b, u64 n, int mode, int pass, const SortScratch& sc, int sm,
+                              cudaStream_t s, u64* launches) {
+    const u64 n_tiles = sort_n_tiles(n);
+    const unsigned grid = (unsigned)((n_tiles + kSortWarps - 1) / kSortWarps);
+    sort_hist_kernel<<<grid, kSortWarps * 32, 0, s>>>(a, n, n_tiles, mode, pass, sc.hist);
+    sort_single_bin_kernel<<<1, 256, 0, s>>>(sc.hist, n_tiles, n, sc.flag);
+    *launches += 2;
+    cudaError_t e = exclusive_scan_u64(sc.hist, sc.hist, 256 * n_tiles, sc.tmp, s, launches);
+    if (e != cudaSuccess) return e;
+    sort_scatter_kernel<<<grid, kSortWarps * 32, 0, s>>>(a, b, n, n_tiles, mode, pass, sc.hist, sc.flag);
+    sort_copy_if_skipped_kernel<<<blocks_for(n, 256, sm), 256, 0, s>>>(a, b, n, sc.flag);
+    *launches += 2;
+    return cudaGetLastError();
+}
+
+// mode 1: restore text order (sort by pos); mode 0: sort_words order.  Result in `recs`.
+cudaError_t tokens_sort(TokenRec* recs, u64 n, bool by_position, const uint8_t* arena, const SortScratch& sc, int sm,
+                        cudaStream_t s, u64* launches) {
+    if (n < 2) return cudaSuccess;
+    TokenRec* a = recs;
+    TokenRec* b = sc.alt;
+    cudaError_t e = cudaSuccess;
+    auto run = [&](int mode, int pass) {
+        if (e != cudaSuccess) return;
+        e = radix_pass(a, b, n, mode, pass, sc, sm, s, launches);
+        TokenRec* t = a; a = b; b = t;
+    };
+    if (by_position) {
+        for (int p = 0; p < 6; ++p) run(1, p);          // 48-bit offsets
+    } else {
+        run(2, 0);                                      // least significant: inline before long
+        for (int p = 0; p < 16; ++p) run(0, p);
+    }
+    if (e != cudaSuccess) return e;
+    if (a != recs) {
+        e = cudaMemcpyAsync(recs, a, sizeof(TokenRec) * n, cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) return e;
+    }
+    if (!by_position) {
+        sort_long_fixup_kernel<<<blocks_for(n, 256, sm), 256, 0, s>>>(recs, n, arena);
+        *launches += 1;
+    }
+    return cudaGetLastError();
+}
+
+// step 1: head flags + sortedness check (status gets kStatusNotSorted on a descent)
+cudaError_t tokens_rle_flags(const TokenRec* recs, u64 n, const uint8_t* arena, u64* flags, int* status, int sm,
+                             cudaStream_t s, u64* launches) {
+    if (n == 0) return cudaSuccess;
+    rle_flags_kernel<<<blocks_for(n, 256, sm), 256, 0, s>>>(recs, n, arena, flags, status);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+// step 2: flags (from step 1) / run_start: n u64 each; tmp: scan scratch
+cudaError_t tokens_rle_insert(const TokenRec* recs, u64 n, const uint8_t* arena, u64* flags, u64* run_start, u64* tmp,
+                              const TableView& t, int sm, cudaStream_t s, u64* launches) {
+    if (n == 0) return cudaSuccess;
+    const unsigned g = blocks_for(n, 256, sm);
+    cudaError_t e = exclusive_scan_u64(flags, flags, n, tmp, s, launches);
+    if (e != cudaSuccess) return e;
+    rle_starts_kernel<<<g, 256, 0, s>>>(flags, recs, n, arena, run_start);
+    rle_insert_kernel<<<g, 256, 0, s>>>(recs, n, arena, run_start, flags, t);
+    *launches += 2;
+    return cudaGetLastError();
+}
+
+}  // namespace wfcu

@@ -52,6 +52,22 @@ struct TableView {
     int* status;
 };
 
+// One token of a device-resident token list (wfcu_tokens), 32 bytes.
+//   k0,k1 : first 16 bytes of the token, big-endian packed, zero padded
+//   ext   : 0 for tokens of <= 16 bytes; otherwise the arena offset of the full
+//           record {u32 len, u32 hash, bytes...}
+//   pos   : byte offset of the token in the text (text order = pos order)
+struct __align__(32) TokenRec {
+    u64 k0, k1, ext, pos;
+};
+
+// Where the kernels put tokens when they run as a stand-alone tokenizer.
+struct EmitView {
+    TokenRec* out;
+    u64 cap;
+    u64* n_out;
+};
+
 // ---- hashing -----------------------------------------------------------------
 // 32-bit mix of the 128-bit key.  Only used to pick a slot / an owner, never as
 // an identity.

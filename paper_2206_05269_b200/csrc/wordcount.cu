@@ -150,9 +150,11 @@ struct FastSmem {
 
 // text[0..n): one document (documents are concatenated with whitespace between
 // them by the caller).  Position n acts as a whitespace byte, so does "position -1".
-template <int WARPS, int NSLOTS, int MSLOTS>
+// EMIT = false: count into the tables.  EMIT = true: stand-alone tokenizer, every
+// token becomes a TokenRec appended to `em` (order restored later by sorting on pos).
+template <int WARPS, int NSLOTS, int MSLOTS, bool EMIT>
 __global__ void __launch_bounds__(WARPS * 32, 1)
-wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, TableView gt) {
+wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, TableView gt, EmitView em) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     FastSmem<WARPS, NSLOTS, MSLOTS>& sm = *reinterpret_cast<FastSmem<WARPS, NSLOTS, MSLOTS>*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -185,8 +187,9 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
         mhead += count;
     };
 
-    // one pass of phase 2: `count` (<= 32) queued tokens, one per lane
-    auto token_pass = [&](u32 count) {
+    // one pass of phase 2: `count` (<= 32) queued tokens, one per lane; `row_end_off`
+    // is the global offset just past the row being processed
+    auto token_pass = [&](u32 count, u64 row_end_off) {
         const u32 entry = (lane < count) ? queue[(qhead + lane) & (kQueueCap - 1)] : 0u;
         qhead += count;
         const u32 tlen = entry >> 11;               // 0: dead entry
@@ -201,6 +204,29 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
         b1 |= upper4(b1 & 0x7F7F7F7Fu) >> 2;
         bool miss = false;
         u64 mk0 = 0, mk1 = 0;
+        if (EMIT) {
+            const u32 w3 = ringw[(wi + 3) & (kRingWords - 1)];
+            const u32 w4 = ringw[(wi + 4) & (kRingWords - 1)];
+            u32 b2 = __funnelshift_r(w2, w3, sh);
+            u32 b3 = __funnelshift_r(w3, w4, sh);
+            b2 |= upper4(b2 & 0x7F7F7F7Fu) >> 2;
+            b3 |= upper4(b3 & 0x7F7F7F7Fu) >> 2;
+            u64 lo = ((u64)b1 << 32) | b0, hi = ((u64)b3 << 32) | b2;
+            if (tlen <= 8) { lo &= ~0ull >> ((64u - 8u * tlen) & 63u); hi = 0; }
+            else hi &= ~0ull >> ((128u - 8u * tlen) & 63u);
+            const u32 live = __ballot_sync(0xFFFFFFFFu, tlen != 0);
+            u64 base = 0;
+            if (lane == 0 && live) base = atomicAdd(em.n_out, (u64)__popc(live));
+            base = __shfl_sync(0xFFFFFFFFu, base, 0);
+            if (tlen) {
+                const u64 at = base + __popc(live & lt_mask);
+                // token start: within one ring length before the end of the current row
+                const u32 back = ((u32)row_end_off - sp) & (kRingBytes - 1);
+                if (at < em.cap) em.out[at] = TokenRec{le_to_be(lo), le_to_be(hi), 0ull, row_end_off - (back ? back : kRingBytes)};
+                ++my_tokens;
+            }
+            return;
+        }
         if (!__any_sync(0xFFFFFFFFu, tlen > 8)) {
             // every token of this pass fits 8 bytes
             const u64 key = (((u64)b1 << 32) | b0) & (~0ull >> ((64u - 8u * tlen) & 63u));
@@ -352,15 +378,16 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
             // ------------------------------ phase 2 ------------------------------
             // full 32-token passes; the remainder waits for the next row's tokens
             u32 consumed = 0;
-            while (qtail - qhead >= 32) { token_pass(32); consumed += 32; }
+            const u64 row_end_off = (row + 1) * kRowBytes;
+            while (qtail - qhead >= 32) { token_pass(32, row_end_off); consumed += 32; }
             // ... unless it would outlive its bytes in the ring (entries of row-1 may
             // reach back into row-2, which the next copy overwrites)
-            if (carried > consumed) token_pass(qtail - qhead);
+            if (carried > consumed) token_pass(qtail - qhead, row_end_off);
             __syncwarp();   // everyone is done with the ring slot the next copy overwrites
             issue_row(row + kPrefetch);
         }
         cp_async_wait<0>();
-        if (qtail != qhead) token_pass(qtail - qhead);
+        if (qtail != qhead) token_pass(qtail - qhead, row_end * kRowBytes);
         __syncwarp();
         while (mtail != mhead) drain_misses(min(mtail - mhead, 32u));
     }
@@ -372,15 +399,17 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
 
     // flush the combiners into the global table
     __syncthreads();
-    for (int i = tid; i < NSLOTS; i += WARPS * 32) {
-        const u64 k = sm.sk[i];
-        const u32 c = sm.scnt[i];
-        if (k != 0 && c) table_add(gt, le_to_be(k), 0ull, (u64)c);
-    }
-    for (int i = tid; i < MSLOTS; i += WARPS * 32) {
-        const u64 k = sm.mk0[i];
-        const u32 c = sm.mcnt[i];
-        if (k > kSlotLocked && c) table_add(gt, le_to_be(k), le_to_be(sm.mk1[i]), (u64)c);
+    if constexpr (!EMIT) {
+        for (int i = tid; i < NSLOTS; i += WARPS * 32) {
+            const u64 k = sm.sk[i];
+            const u32 c = sm.scnt[i];
+            if (k != 0 && c) table_add(gt, le_to_be(k), 0ull, (u64)c);
+        }
+        for (int i = tid; i < MSLOTS; i += WARPS * 32) {
+            const u64 k = sm.mk0[i];
+            const u32 c = sm.mcnt[i];
+            if (k > kSlotLocked && c) table_add(gt, le_to_be(k), le_to_be(sm.mk1[i]), (u64)c);
+        }
     }
 }
 
@@ -450,8 +479,9 @@ __device__ __forceinline__ u32 enc_byte(u32 cp, u32 n, u32 i) {
     return 0x80 | ((cp >> shift) & 0x3F);
 }
 
-// Counts the token of one whitespace-free piece [a,b) of the text (normalize_word).
-__device__ void slow_count_piece(const uint8_t* text, u64 a, u64 b, const TableView& gt) {
+// Counts (or, when em != nullptr, emits) the token of one whitespace-free piece
+// [a,b) of the text (normalize_word).
+__device__ void slow_count_piece(const uint8_t* text, u64 a, u64 b, const TableView& gt, const EmitView* em) {
     // pass 1: normalised offsets of the first / last word character
     u64 noff = 0, nfirst = 0, nlast_end = 0, first_b = b, last_e = a;
     for (u64 pos = a; pos < b;) {
@@ -483,7 +513,12 @@ __device__ void slow_count_piece(const uint8_t* text, u64 a, u64 b, const TableV
             }
             pos += d.len;
         }
-        table_add(gt, k0, k1, 1ull);
+        if (em) {
+            const u64 at = atomicAdd(em->n_out, 1ull);
+            if (at < em->cap) em->out[at] = TokenRec{k0, k1, 0ull, first_b};
+        } else {
+            table_add(gt, k0, k1, 1ull);
+        }
         return;
     }
     if (nlen > 0xFFFFFFFFull) { atomicOr(gt.status, kStatusArenaFull); return; }
@@ -491,7 +526,7 @@ __device__ void slow_count_piece(const uint8_t* text, u64 a, u64 b, const TableV
     if (!rec) return;
     uint8_t* out = gt.arena + rec + 8;
     u32 h = 2166136261u;
-    u64 i = 0;
+    u64 i = 0, p0 = 0, p1 = 0;
     for (u64 pos = first_b; pos < last_e;) {
         const Dec d = utf8_dec(text, pos, b);
         const u32 cp = lower_cp(d.cp);
@@ -500,11 +535,18 @@ __device__ void slow_count_piece(const uint8_t* text, u64 a, u64 b, const TableV
             const u32 byte = enc_byte(cp, el, k);
             out[i] = (uint8_t)byte;
             h = (h ^ byte) * 16777619u;
+            if (i < 8) p0 |= (u64)byte << (56 - 8 * i);
+            else if (i < 16) p1 |= (u64)byte << (56 - 8 * (i - 8));
         }
         pos += d.len;
     }
     *reinterpret_cast<u32*>(gt.arena + rec) = (u32)nlen;
     *reinterpret_cast<u32*>(gt.arena + rec + 4) = h;
+    if (em) {
+        const u64 at = atomicAdd(em->n_out, 1ull);
+        if (at < em->cap) em->out[at] = TokenRec{p0, p1, rec, first_b};
+        return;
+    }
     __threadfence();
     long_add(gt, rec, 1ull);
 }
@@ -513,7 +555,7 @@ __device__ __forceinline__ bool ascii_space(u32 b) { return b == 0x20 || (b >= 0
 
 // One thread per deferred fragment END (offset of the terminating ASCII
 // whitespace byte, or n).  The fragment start is found by scanning backwards.
-__global__ void wc_slow_kernel(const uint8_t* __restrict__ text, u64 n, TableView gt) {
+__global__ void wc_slow_kernel(const uint8_t* __restrict__ text, u64 n, TableView gt, EmitView em, int emit) {
     u64 count = *gt.n_deferred;
     if (count > gt.deferred_cap) count = gt.deferred_cap;
     for (u64 idx = (u64)blockIdx.x * blockDim.x + threadIdx.x; idx < count; idx += (u64)gridDim.x * blockDim.x) {
@@ -531,7 +573,7 @@ __global__ void wc_slow_kernel(const uint8_t* __restrict__ text, u64 n, TableVie
                 boundary = d.valid && uni_space(d.cp);
             }
             if (boundary) {
-                if (in_piece) slow_count_piece(text, piece, pos, gt);
+                if (in_piece) slow_count_piece(text, piece, pos, gt, emit ? &em : nullptr);
                 in_piece = false;
             } else if (!in_piece) {
                 piece = pos;
@@ -552,12 +594,14 @@ constexpr int kFastMedSlots = 1024; // medium-token combiner slots (20 bytes eac
 
 size_t wc_fast_smem_bytes() { return sizeof(FastSmem<kFastWarps, kFastSlots, kFastMedSlots>); }
 
-cudaError_t wc_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream,
-                      u64* launches, cudaEvent_t* ev_before_fast, cudaEvent_t* ev_after_fast) {
+template <bool EMIT>
+static cudaError_t wc_launch_impl(const uint8_t* text, u64 n, const TableView& gt, const EmitView& em, int sm_count,
+                                  cudaStream_t stream, u64* launches, cudaEvent_t* ev_before_fast,
+                                  cudaEvent_t* ev_after_fast) {
     const size_t smem = wc_fast_smem_bytes();
+    auto kernel = wc_fast_kernel<kFastWarps, kFastSlots, kFastMedSlots, EMIT>;
     {
-        cudaError_t e = cudaFuncSetAttribute(wc_fast_kernel<kFastWarps, kFastSlots, kFastMedSlots>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
     const u64 n_rows = n / kRowBytes + 1;
@@ -567,12 +611,26 @@ cudaError_t wc_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_co
     if (grid == 0) grid = 1;
     const u64 rows_per_warp = (n_rows + grid * kFastWarps - 1) / (grid * kFastWarps);
     if (ev_before_fast) cudaEventRecord(*ev_before_fast, stream);
-    wc_fast_kernel<kFastWarps, kFastSlots, kFastMedSlots><<<(unsigned)grid, kFastWarps * 32, smem, stream>>>(text, n, rows_per_warp, gt);
+    kernel<<<(unsigned)grid, kFastWarps * 32, smem, stream>>>(text, n, rows_per_warp, gt, em);
     if (ev_after_fast) cudaEventRecord(*ev_after_fast, stream);
-    wc_slow_kernel<<<sm_count * 2, 128, 0, stream>>>(text, n, gt);
+    wc_slow_kernel<<<sm_count * 2, 128, 0, stream>>>(text, n, gt, em, EMIT ? 1 : 0);
     wc_reset_deferred_kernel<<<1, 1, 0, stream>>>(gt);
     *launches += 3;
     return cudaGetLastError();
+}
+
+// count text[0..n) into the tables of gt
+cudaError_t wc_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream,
+                      u64* launches, cudaEvent_t* ev_before_fast, cudaEvent_t* ev_after_fast) {
+    return wc_launch_impl<false>(text, n, gt, EmitView{nullptr, 0, nullptr}, sm_count, stream, launches,
+                                 ev_before_fast, ev_after_fast);
+}
+
+// stand-alone tokenizer: append every token of text[0..n) to em (gt supplies the
+// deferred list, the long-token arena and the status word; its tables stay untouched)
+cudaError_t wc_tokenize_launch(const uint8_t* text, u64 n, const TableView& gt, const EmitView& em, int sm_count,
+                               cudaStream_t stream, u64* launches) {
+    return wc_launch_impl<true>(text, n, gt, em, sm_count, stream, launches, nullptr, nullptr);
 }
 
 }  // namespace wfcu

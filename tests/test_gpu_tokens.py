@@ -1,0 +1,107 @@
+"""GPU parity: stand-alone tokenizer, sort_words and reduce_sorted vs the oracle.
+
+reference: tokenize proj/src/text.cpp:32-57, sort_words :59-63, reduce_sorted
+proj/src/reduce.cpp:8-21 (goldens: proj/tests/text_test.cpp:94-169, reduce_test.cpp:28-58)
+"""
+import random
+
+import pytest
+
+from helpers import random_text, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("text", [
+    b"I want to test MapReduce",
+    b"MapReduce is a cool algorithm to test.",
+    b"",
+    b"--- a !!! b ...",
+    "a b c one\ttwo\nthree".encode(),
+    b"Dog dog. DOG!",
+    b"x" * 40 + b" y " + b"Z" * 17 + b" " + b"z" * 16,
+])
+def test_tokenize_goldens(capi, cuda, port, text):
+    toks = capi.Tokens.tokenize_host(text)
+    assert toks.words() == port.tokenize(text)
+
+
+@pytest.mark.parametrize("flavour", ["ascii", "long", "unicode"])
+@pytest.mark.parametrize("size", [1, 17, 513, 5000, 200003])
+def test_tokenize_matches_oracle_in_text_order(capi, cuda, port, flavour, size):
+    text = random_text(random.Random(size + len(flavour)), size, flavour)
+    toks = capi.Tokens.tokenize_host(text)
+    want = port.tokenize(text)
+    assert toks.stats()[0] == len(want)
+    assert toks.words() == want
+
+
+def test_sort_words_goldens(capi, cuda):
+    # proj/tests/text_test.cpp:143-154
+    t = capi.Tokens.from_words([b"i", b"want", b"to", b"test", b"mapreduce"])
+    t.sort()
+    assert t.words() == [b"i", b"mapreduce", b"test", b"to", b"want"]
+    t = capi.Tokens.from_words([b"mapreduce", b"is", b"a", b"cool", b"algorithm", b"to", b"test"])
+    t.sort()
+    assert t.words() == [b"a", b"algorithm", b"cool", b"is", b"mapreduce", b"test", b"to"]
+    e = capi.Tokens.from_words([])
+    e.sort()
+    assert e.words() == []
+
+
+@pytest.mark.parametrize("flavour", ["ascii", "long", "unicode"])
+def test_sort_words_matches_oracle(capi, cuda, port, flavour):
+    text = random_text(random.Random(5), 60000, flavour)
+    words = port.tokenize(text)
+    # long tokens sharing a 16-byte prefix, a 16-byte token equal to that prefix, NULs inside
+    words += [b"p" * 16 + b"zz", b"p" * 16, b"p" * 16 + b"a", b"p" * 16 + b"zz", b"p" * 17, b"a\x00b", b"a", b"a\x00"[:1]]
+    t = capi.Tokens.from_words(words)
+    t.sort()
+    assert t.words() == port.sort_words(words) == sorted(words)
+
+
+def test_reduce_sorted_goldens(capi, cuda, port):
+    # proj/tests/reduce_test.cpp:28-43
+    t = capi.Tokens.from_words([b"a", b"algorithm", b"cool", b"i", b"is", b"mapreduce"])
+    c = capi.Counter(table_slots=1024)
+    t.reduce_sorted(c)
+    assert c.to_dict() == {b"a": 1, b"algorithm": 1, b"cool": 1, b"i": 1, b"is": 1, b"mapreduce": 1}
+    t = capi.Tokens.from_words([b"mapreduce", b"test", b"test", b"to", b"to", b"want"])
+    c = capi.Counter(table_slots=1024)
+    t.reduce_sorted(c)
+    assert c.to_dict() == {b"mapreduce": 1, b"test": 2, b"to": 2, b"want": 1}
+    # unsorted input is rejected like the reference's std::invalid_argument (reduce.cpp:9)
+    bad = capi.Tokens.from_words([b"b", b"a"])
+    with pytest.raises(capi.InvalidArgument):
+        bad.reduce_sorted(capi.Counter(table_slots=1024))
+    empty = capi.Tokens.from_words([])
+    c = capi.Counter(table_slots=1024)
+    empty.reduce_sorted(c)
+    assert c.to_dict() == {}
+
+
+@pytest.mark.parametrize("flavour", ["ascii", "long", "unicode"])
+def test_sort_then_rle_equals_hash_count(capi, cuda, port, flavour):
+    """the sort + RLE alternative and the hash-count path give the same table"""
+    text = random_text(random.Random(9), 150000, flavour)
+    dev, n = to_dev(cuda, text)
+    a = capi.Counter(table_slots=1 << 16)
+    a.count_dev_sorted(dev.data_ptr(), n)
+    want = port.wordcount([text])
+    assert a.to_dict() == want
+    assert a.stats()[1] == sum(want.values())
+    toks = capi.Tokens.tokenize_dev(dev.data_ptr(), n)
+    toks.sort()
+    b = capi.Counter(table_slots=1 << 16)
+    toks.reduce_sorted(b)
+    assert b.to_dict() == want
+    runs = port.reduce_sorted(port.sort_words(port.tokenize(text)))
+    assert dict(runs) == want
+
+
+def test_sorted_count_on_zipf_corpus(capi, cuda, port):
+    corpus = capi.synth_corpus(seed=3, doc_begin=0, doc_end=8, vocab=50000)
+    dev, n = to_dev(cuda, corpus)
+    c = capi.Counter(table_slots=1 << 18)
+    c.count_dev_sorted(dev.data_ptr(), n)
+    assert c.to_dict() == port.wordcount([corpus])
