@@ -1,0 +1,79 @@
+"""CPU: the C-ABI library loads, exports every symbol include/wfcu.h declares, and its
+host-side pieces (synthetic corpora, owner function, no-device behaviour) are right."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "wfcu.h")).read()
+    return sorted(set(re.findall(r"WFCU_API\s+[\w\s\*]+?\b(wfcu_\w+)\s*\(", text)))
+
+
+def test_every_declared_symbol_is_exported(capi):
+    names = declared_symbols()
+    assert len(names) >= 40
+    lib = ctypes.CDLL(str(capi.LIB_PATH))
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    assert sorted(capi.SIGNATURES) == names        # the Python binding covers the whole header
+
+
+def test_no_device_is_an_error_not_a_fallback(capi):
+    if capi.device_count() > 0:
+        pytest.skip("a GPU is visible here")
+    with pytest.raises(capi.WfcuError) as e:
+        capi.Counter()
+    assert e.value.code == capi.ERR_NO_DEVICE
+    with pytest.raises(capi.WfcuError) as e:
+        capi.map_reduce_host(np.ones(4), capi.MAP_IDENTITY)
+    assert e.value.code == capi.ERR_NO_DEVICE
+    with pytest.raises(capi.WfcuError):
+        capi.Tokens.tokenize_host(b"a b")
+
+
+def test_synthetic_corpus_is_deterministic_and_per_document(capi):
+    a = capi.synth_corpus(1, 0, 6, 50000, doc_bytes=8192)
+    b = capi.synth_corpus(1, 0, 6, 50000, doc_bytes=8192, threads=1)
+    assert (a == b).all()
+    docs = a.reshape(6, 8192)
+    for d in range(6):      # document d depends only on (seed, d)
+        assert (capi.synth_corpus(1, d, d + 1, 50000, doc_bytes=8192) == docs[d]).all()
+    assert (capi.synth_corpus_strided(1, 1, 2, 3, 50000, doc_bytes=8192).reshape(3, 8192) == docs[1::2]).all()
+    assert not (capi.synth_corpus(2, 0, 1, 50000, doc_bytes=8192) == docs[0]).all()
+    assert docs[:, -1].tolist() == [10] * 6                 # every document ends with '\n'
+    assert set(np.unique(a).tolist()) <= set(b" \n.,;!?" + bytes(range(65, 91)) + bytes(range(97, 123)) + b"0123456789")
+
+
+def test_synthetic_corpus_is_zipfian(capi, port):
+    text = capi.synth_corpus(1, 0, 4, 50000)
+    counts = port.wordcount([text])
+    total = sum(counts.values())
+    top = max(counts.values())
+    assert 0.12 < top / total < 0.16          # Zipf(1.1) over 50k words: top word ~13.9 %
+    assert 6.5 < text.size / total < 8.0      # ~7.3 bytes per token
+    lens = {len(w) for w in counts}
+    assert min(lens) >= 4 and max(lens) <= 8  # W=4 plus a 0..4 letter prefix
+    sp = capi.synth_corpus(1, 0, 1, 50000, speaker=3)
+    assert any(w.endswith(b"3") for w in port.wordcount([sp]))   # speaker-specific words
+
+
+def test_owner_function_is_a_partition(capi):
+    words = [b"w%05d" % i for i in range(2000)] + [b"x" * 17, b"y" * 40, "café".encode()]
+    for n in (1, 2, 3, 8):
+        owners = [capi.owner_of(w, n) for w in words]
+        assert all(0 <= o < n for o in owners)
+        if n > 1:
+            hist = np.bincount(owners, minlength=n)
+            assert hist.min() > len(words) / n * 0.7      # roughly balanced
+
+
+def test_pack_unpack_roundtrip(capi):
+    words = [b"a", b"", b"hello", bytes(range(256))]
+    blob, lens = capi.pack_words(words)
+    assert capi.unpack_words(blob, lens) == words
