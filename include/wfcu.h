@@ -66,6 +66,13 @@ WFCU_API int wfcu_set_device(int device);
 /* 148 on B200; grids are sized in multiples of this. */
 WFCU_API int wfcu_sm_count(int* out);
 
+/* Plain device-memory helpers, so that a host which does not link the CUDA runtime
+ * (the C++ drop-in, a cgo/JNI binding) can stage the buffers the *_dev calls take. */
+WFCU_API int wfcu_dev_alloc(void** out, uint64_t bytes);
+WFCU_API void wfcu_dev_free(void* p);
+WFCU_API int wfcu_dev_upload(void* dev_dst, const void* host_src, uint64_t bytes);
+WFCU_API int wfcu_dev_download(void* host_dst, const void* dev_src, uint64_t bytes);
+
 /* ------------------------------------------------------------------------- */
 /* Generic map-then-reduce engine  (proj/include/wfc/engine.hpp:25-36,        */
 /* proj/src/engine.cpp:15-98)                                                 */
@@ -205,6 +212,14 @@ WFCU_API int wfcu_counter_merge_long_records(wfcu_counter* c, const uint8_t* dev
 /* ------------------------------------------------------------------------- */
 
 typedef struct wfcu_tokens wfcu_tokens; /* device-resident token list in text order */
+
+/* normalize_word (proj/src/text.cpp:9-30) over a batch of whitespace-free fragments:
+ * case fold, strip non-word characters from both ends, U+FFFD for invalid bytes.
+ * Fragment f is bytes[sum(lens[0..f)) ..]; the normalised words are written back to
+ * back into out_bytes (capacity >= 3 * total input bytes is always enough) and
+ * out_lens[f] = 0 means nothing remains (the reference's nullopt). */
+WFCU_API int wfcu_normalize_words_host(const uint8_t* bytes, const uint32_t* lens, uint64_t n_frag,
+                                       uint8_t* out_bytes, uint64_t out_cap, uint32_t* out_lens);
 
 /* wfc::tokenize on a device buffer: tokens in text order. */
 WFCU_API int wfcu_tokenize_dev(const uint8_t* dev_text, uint64_t n, void* stream, wfcu_tokens** out);

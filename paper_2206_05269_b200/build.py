@@ -84,7 +84,7 @@ def build_host(force: bool = False) -> Path | None:
     srcs = sorted((HOST / "src").glob("*.cpp"))
     hdrs = sorted((HOST / "include" / "wfc").glob("*.hpp")) + [ROOT / "include" / "wfcu.h"]
     cxx = os.environ.get("CXX") or shutil.which("g++") or "g++"
-    common = [cxx, "-std=c++20", "-O2", "-fPIC", "-pthread", f"-I{HOST / 'include'}", f"-I{ROOT / 'include'}"]
+    common = [cxx, "-std=c++20", "-O2", "-fPIC", "-pthread", "-ffp-contract=off", f"-I{HOST / 'include'}", f"-I{ROOT / 'include'}"]
     if force or _stale(out, srcs + hdrs + [LIB / "libwfcu.so"]):
         _run(common + ["-shared", "-o", str(out), *map(str, srcs), f"-L{LIB}", "-lwfcu", "-Wl,-rpath,$ORIGIN"])
     tests = sorted((HOST / "tests").glob("*.cpp"))

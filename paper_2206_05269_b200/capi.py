@@ -56,6 +56,10 @@ SIGNATURES = {
     "wfcu_device_count": (C.c_int, []),
     "wfcu_set_device": (C.c_int, [C.c_int]),
     "wfcu_sm_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "wfcu_dev_alloc": (C.c_int, [C.POINTER(C.c_void_p), C.c_uint64]),
+    "wfcu_dev_free": (None, [C.c_void_p]),
+    "wfcu_dev_upload": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
+    "wfcu_dev_download": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "wfcu_map_reduce_dev": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, C.c_int, C.c_void_p, f64p]),
     "wfcu_map_reduce_dev_async": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p]),
     "wfcu_map_reduce_blocked_dev": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, C.c_int, C.c_uint64, C.c_void_p, f64p]),
@@ -79,6 +83,7 @@ SIGNATURES = {
     "wfcu_counter_merge_entries": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "wfcu_counter_long_records": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, u64p, C.c_void_p]),
     "wfcu_counter_merge_long_records": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p]),
+    "wfcu_normalize_words_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p]),
     "wfcu_tokenize_dev": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.POINTER(C.c_void_p)]),
     "wfcu_tokenize_host": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p)]),
     "wfcu_tokens_destroy": (None, [C.c_void_p]),
@@ -358,6 +363,16 @@ class Tokens:
 
     def reduce_sorted(self, into: Counter, stream: int = 0) -> None:
         check(lib.wfcu_tokens_reduce_sorted(self._h, into.handle, C.c_void_p(stream)))
+
+
+def normalize_words(fragments: list[bytes]) -> list[bytes | None]:
+    """wfc::normalize_word over a batch (None = the reference's nullopt)."""
+    blob, lens = pack_words(fragments)
+    out = np.zeros(3 * blob.size + 16, np.uint8)
+    out_lens = np.zeros(max(len(fragments), 1), np.uint32)
+    check(lib.wfcu_normalize_words_host(_ptr(blob), _ptr(lens), len(fragments), _ptr(out), out.size, _ptr(out_lens)))
+    words = unpack_words(out, out_lens[:len(fragments)])
+    return [w if w else None for w in words]
 
 
 # ---- synthetic corpora -----------------------------------------------------------------------

@@ -39,6 +39,8 @@ cudaError_t tb_long_merge(const TableView& t, const uint8_t* recs, u64 n_bytes, 
 // wordcount.cu (stand-alone tokenizer) and tokens.cu
 cudaError_t wc_tokenize_launch(const uint8_t* text, u64 n, const TableView& gt, const EmitView& em, int sm_count,
                                cudaStream_t stream, u64* launches);
+cudaError_t wc_normalize_launch(const uint8_t* text, const u64* offsets, u64 n_frag, const TableView& gt,
+                                const EmitView& em, int sm_count, cudaStream_t stream, u64* launches);
 struct SortScratch {
     TokenRec* alt;
     u64* hist;
@@ -1053,4 +1055,93 @@ extern "C" int wfcu_counter_count_dev_sorted(wfcu_counter* c, const uint8_t* dev
     if (rc == WFCU_OK) rc = wfcu_tokens_reduce_sorted(t, c, stream);
     tokens_free(t);
     return rc;
+}
+
+// normalize_word over a batch of fragments (host buffers).  Fragment f is
+// bytes[sum(lens[0..f)) ...]; out_lens[f] = 0 means "nothing remains" (nullopt).
+extern "C" int wfcu_normalize_words_host(const uint8_t* bytes, const uint32_t* lens, uint64_t n_frag,
+                                         uint8_t* out_bytes, uint64_t out_cap, uint32_t* out_lens) {
+    DeviceState* d;
+    if (int rc = current_device_state(&d)) return rc;
+    if (n_frag == 0) return WFCU_OK;
+    if (!lens || !out_lens || !out_bytes) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
+    std::vector<u64> offs(n_frag + 1, 0);
+    for (u64 f = 0; f < n_frag; ++f) offs[f + 1] = offs[f] + lens[f];
+    const u64 total = offs[n_frag];
+    if (total && !bytes) return fail(WFCU_ERR_INVALID_ARGUMENT, "bytes is null");
+    DevBuf text, doffs, recs, arena, counters;
+    CUDA_TRY(text.alloc(total));
+    CUDA_TRY(doffs.alloc(sizeof(u64) * (n_frag + 1)));
+    CUDA_TRY(recs.alloc(sizeof(TokenRec) * n_frag));
+    const u64 arena_cap = 3 * total + 16 * n_frag + 64;
+    CUDA_TRY(arena.alloc(arena_cap));
+    CUDA_TRY(counters.alloc(sizeof(u64) * 16));
+    if (total) CUDA_TRY(cudaMemcpy(text.p, bytes, total, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(doffs.p, offs.data(), sizeof(u64) * (n_frag + 1), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemset(counters.p, 0, sizeof(u64) * 16));
+    u64* cnt = counters.as<u64>();
+    const u64 arena_start = 8;
+    CUDA_TRY(cudaMemcpy(cnt + 4, &arena_start, sizeof(u64), cudaMemcpyHostToDevice));
+    TableView v{};
+    v.n_used = cnt + 0; v.n_tokens = cnt + 1; v.n_deferred = cnt + 2; v.n_long = cnt + 3; v.arena_used = cnt + 4;
+    v.status = reinterpret_cast<int*>(cnt + 5);
+    v.arena = arena.as<uint8_t>(); v.arena_cap = arena_cap;
+    EmitView em{recs.as<TokenRec>(), n_frag, cnt + 6};
+    LaunchTally tally;
+    CUDA_TRY(wc_normalize_launch(text.as<uint8_t>(), doffs.as<u64>(), n_frag, v, em, d->sm_count, nullptr, &tally.n));
+    u64 h[8];
+    CUDA_TRY(cudaMemcpy(h, cnt, sizeof(h), cudaMemcpyDeviceToHost));
+    if (int rc = status_to_rc((int)(h[5] & 0xFFFFFFFFu))) return rc;
+    const u64 produced = h[6];
+    std::vector<TokenRec> hr(produced);
+    std::vector<uint8_t> ha(h[4]);
+    if (produced) CUDA_TRY(cudaMemcpy(hr.data(), recs.p, sizeof(TokenRec) * produced, cudaMemcpyDeviceToHost));
+    if (h[4] > 8) CUDA_TRY(cudaMemcpy(ha.data(), arena.p, h[4], cudaMemcpyDeviceToHost));
+    // records arrive in any order: place each by the fragment its position falls in
+    std::vector<const TokenRec*> by_frag(n_frag, nullptr);
+    for (const TokenRec& r : hr) {
+        const u64 f = u64(std::upper_bound(offs.begin(), offs.end(), r.pos) - offs.begin()) - 1;
+        if (f < n_frag) by_frag[f] = &r;
+    }
+    u64 off = 0;
+    for (u64 f = 0; f < n_frag; ++f) {
+        out_lens[f] = 0;
+        const TokenRec* r = by_frag[f];
+        if (!r) continue;
+        uint8_t b[16];
+        const uint8_t* src = b;
+        u32 len;
+        if (r->ext) {
+            std::memcpy(&len, ha.data() + r->ext, 4);
+            src = ha.data() + r->ext + 8;
+        } else {
+            key_to_bytes(r->k0, r->k1, b);
+            len = key_len(r->k0, r->k1);
+        }
+        if (off + len > out_cap) return fail(WFCU_ERR_BUFFER_TOO_SMALL, "normalize output buffer too small");
+        std::memcpy(out_bytes + off, src, len);
+        out_lens[f] = len;
+        off += len;
+    }
+    return WFCU_OK;
+}
+
+// ---- plain device-memory helpers for hosts that do not link the CUDA runtime --------------
+extern "C" int wfcu_dev_alloc(void** out, uint64_t bytes) {
+    if (!out) return fail(WFCU_ERR_INVALID_ARGUMENT, "out is null");
+    DeviceState* d;
+    if (int rc = current_device_state(&d)) return rc;
+    CUDA_TRY(cudaMalloc(out, bytes ? bytes : 16));
+    return WFCU_OK;
+}
+extern "C" void wfcu_dev_free(void* p) {
+    if (p) cudaFree(p);
+}
+extern "C" int wfcu_dev_upload(void* dev_dst, const void* host_src, uint64_t bytes) {
+    if (bytes) CUDA_TRY(cudaMemcpy(dev_dst, host_src, bytes, cudaMemcpyHostToDevice));
+    return WFCU_OK;
+}
+extern "C" int wfcu_dev_download(void* host_dst, const void* dev_src, uint64_t bytes) {
+    if (bytes) CUDA_TRY(cudaMemcpy(host_dst, dev_src, bytes, cudaMemcpyDeviceToHost));
+    return WFCU_OK;
 }

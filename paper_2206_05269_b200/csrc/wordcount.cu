@@ -586,6 +586,15 @@ __global__ void wc_slow_kernel(const uint8_t* __restrict__ text, u64 n, TableVie
 
 __global__ void wc_reset_deferred_kernel(TableView gt) { *gt.n_deferred = 0; }
 
+// normalize_word (proj/src/text.cpp:9-30) for a batch of fragments: fragment f is
+// text[offsets[f] .. offsets[f+1]).  One thread per fragment; a fragment that keeps a
+// token emits one TokenRec whose pos lies inside the fragment.
+__global__ void wc_normalize_kernel(const uint8_t* __restrict__ text, const u64* __restrict__ offsets, u64 n_frag,
+                                    TableView gt, EmitView em) {
+    for (u64 f = (u64)blockIdx.x * blockDim.x + threadIdx.x; f < n_frag; f += (u64)gridDim.x * blockDim.x)
+        slow_count_piece(text, offsets[f], offsets[f + 1], gt, &em);
+}
+
 // ---- host-side launchers (called from capi.cu) -----------------------------------
 static_assert(kRingBytes == 2048, "queue entries keep ring positions in 11 bits");
 constexpr int kFastWarps = 24;
@@ -624,6 +633,16 @@ cudaError_t wc_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_co
                       u64* launches, cudaEvent_t* ev_before_fast, cudaEvent_t* ev_after_fast) {
     return wc_launch_impl<false>(text, n, gt, EmitView{nullptr, 0, nullptr}, sm_count, stream, launches,
                                  ev_before_fast, ev_after_fast);
+}
+
+cudaError_t wc_normalize_launch(const uint8_t* text, const u64* offsets, u64 n_frag, const TableView& gt,
+                                const EmitView& em, int sm_count, cudaStream_t stream, u64* launches) {
+    if (n_frag == 0) return cudaSuccess;
+    u64 g = (n_frag + 127) / 128;
+    if (g > (u64)sm_count * 8) g = (u64)sm_count * 8;
+    wc_normalize_kernel<<<(unsigned)g, 128, 0, stream>>>(text, offsets, n_frag, gt, em);
+    *launches += 1;
+    return cudaGetLastError();
 }
 
 // stand-alone tokenizer: append every token of text[0..n) to em (gt supplies the

@@ -1,0 +1,153 @@
+// wfc/wfc_b200.hpp -- the reference's map/reduce API, served by B200 kernels.
+//
+// Same namespace, names, argument meaning and error behaviour as the hot-path part of
+// /root/reference/proj/include/wfc/{text,reduce,pipeline,engine,analysis}.hpp, so a
+// caller of the reference (proj/src/cli.cpp:79-86, 138-141, 202-221) relinks against
+// libwfc_b200.so unchanged.  The per-topic headers wfc/text.hpp, wfc/reduce.hpp, ...
+// forward here.  Every function below runs its arithmetic on the GPU through the C ABI
+// of include/wfcu.h; there is no CPU implementation to fall back to -- without a device
+// the calls throw wfc::DeviceError.
+//
+// Differences a caller can observe (all additive):
+//   * MapKind gains `square` (value 3) for f(x) = x^2; map_reduce_fast() is the
+//     HBM-roofline reduction (fp64 accumulation, fixed order, within ~1e-15 relative of
+//     the serial fold), next to the bit-exact map_reduce_serial / map_reduce_blocked;
+//   * run_wordcount partitions by key hash, not by alphabetical range (BASELINE.json;
+//     SURVEY.md D2): RunResult::counts is identical, the shards are pairwise disjoint,
+//     pre_repair_shards == shards and boundary_repair has nothing left to do;
+//   * the Transport overload is accepted and ignored: the exchange runs over device
+//     memory / NCCL, not over host frames.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <map>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <vector>
+
+namespace wfc {
+
+// ---- text (reference: wfc/text.hpp) -------------------------------------------------
+using Word = std::string;
+
+struct RawDocument {
+    std::string id;
+    std::string text;
+};
+
+struct WordList {
+    std::vector<Word> words;
+    bool sorted = false;
+};
+
+std::optional<Word> normalize_word(std::string_view fragment);
+std::vector<std::optional<Word>> normalize_words(std::span<const std::string> fragments);  // batch form (one launch)
+WordList tokenize(const RawDocument& doc);
+WordList sort_words(WordList list);
+
+// ---- reduce (reference: wfc/reduce.hpp) ----------------------------------------------
+using CountMap = std::map<Word, std::uint64_t>;
+using ShardedCounts = std::vector<CountMap>;
+
+CountMap reduce_sorted(const WordList& sorted);
+ShardedCounts boundary_repair(ShardedCounts sharded);
+CountMap merge_counts(std::span<const CountMap> maps);
+std::size_t count_unreduced_words(const ShardedCounts& sharded);
+
+// ---- transport seam (reference: wfc/transport.hpp, wfc/wire.hpp) ------------------------
+using WireMessage = std::vector<std::uint8_t>;
+class Transport {
+public:
+    virtual ~Transport() = default;
+    virtual void send(std::size_t from, std::size_t to, WireMessage frame) = 0;
+    virtual WireMessage recv(std::size_t at, std::size_t from) = 0;
+};
+
+// ---- pipeline (reference: wfc/pipeline.hpp) --------------------------------------------
+struct StageTimings {
+    std::uint64_t map_ns = 0;       // H2D + fused tokenize/count kernels
+    std::uint64_t sort_ns = 0;      // 0: the hash-count path does not sort
+    std::uint64_t encode_ns = 0;    // partition-by-owner kernels
+    std::uint64_t exchange_ns = 0;  // entry exchange + merge-insert
+    std::uint64_t reduce_ns = 0;    // export of the owner tables
+    std::uint64_t repair_ns = 0;    // 0: shards are disjoint by construction
+    std::uint64_t total_ns = 0;
+};
+
+struct RunResult {
+    CountMap counts;
+    ShardedCounts shards;
+    ShardedCounts pre_repair_shards;
+    StageTimings timings;
+    std::size_t n_workers = 1;
+};
+
+class PipelineError : public std::runtime_error {
+public:
+    PipelineError(std::string stage, const std::string& what)
+        : std::runtime_error(stage + " stage: " + what), stage_(std::move(stage)) {}
+    const std::string& stage() const { return stage_; }
+
+private:
+    std::string stage_;
+};
+
+// No usable GPU / CUDA failure outside a pipeline stage.
+class DeviceError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+
+RunResult run_wordcount(std::span<const RawDocument> corpus, std::size_t n_workers);
+RunResult run_wordcount(std::span<const RawDocument> corpus, std::size_t n_workers, Transport& transport);
+CountMap serial_wordcount(std::span<const RawDocument> corpus);
+
+// ---- engine (reference: wfc/engine.hpp) ------------------------------------------------
+enum class MapKind {
+    identity,
+    square_root,
+    alternating_harmonic_term,
+    square,   // appended: f(x) = x^2 (BASELINE.json config 2)
+};
+
+struct BlockConfig {
+    std::size_t block_size = 256;
+    unsigned workers = 1;   // kept for source compatibility; the device schedules the blocks
+};
+
+double map_reduce_serial(std::span<const double> values, MapKind map);
+double map_reduce_blocked(std::span<const double> values, MapKind map, const BlockConfig& cfg);
+double alternating_harmonic(std::uint64_t n, const BlockConfig& cfg = {});
+// The roofline path: grid-stride, vectorised loads, warp-shuffle tree, fixed-order finish.
+double map_reduce_fast(std::span<const double> values, MapKind map);
+double map_reduce_fast(std::span<const float> values, MapKind map);
+
+// ---- analysis (reference: wfc/analysis.hpp, the part on the path) -----------------------
+struct FrequencyRow {
+    Word word;
+    std::uint64_t count = 0;
+    double rel_freq = 0.0;
+};
+struct FrequencyTable {
+    std::string label;
+    std::uint64_t total_words = 0;
+    std::vector<FrequencyRow> rows;
+};
+FrequencyTable top_k(const CountMap& counts, std::string label, std::size_t k);
+
+struct DistinctiveRow {
+    Word word;
+    double score = 0.0;
+};
+struct DistinctivenessReport {
+    std::string label;
+    std::vector<DistinctiveRow> rows;
+};
+DistinctivenessReport distinctive_words(const CountMap& target, const CountMap& others, std::string label,
+                                        std::size_t k);
+
+}  // namespace wfc

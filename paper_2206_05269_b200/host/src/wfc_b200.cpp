@@ -1,0 +1,466 @@
+// wfc_b200.cpp -- the reference's wfc:: API implemented over the C ABI of libwfcu.so.
+//
+// Host code here only marshals std::string / std::map values into packed buffers and
+// back, maps status codes to the reference's exception types and keeps the containers'
+// bookkeeping (shard lists, top-k ordering).  Tokenizing, counting, sorting, run-length
+// encoding, partitioning, merging and every floating-point sum run on the GPU.
+#include "wfc/wfc_b200.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <unordered_map>
+
+#include "wfcu.h"
+
+namespace wfc {
+
+namespace {
+
+[[noreturn]] void raise(int rc, const char* stage = nullptr) {
+    const std::string msg = wfcu_last_error();
+    if (rc == WFCU_ERR_INVALID_ARGUMENT || rc == WFCU_ERR_NOT_SORTED) throw std::invalid_argument(msg);
+    if (stage) throw PipelineError(stage, msg);
+    throw DeviceError(msg);
+}
+inline void ok(int rc, const char* stage = nullptr) {
+    if (rc != WFCU_OK) raise(rc, stage);
+}
+
+struct Packed {
+    std::vector<std::uint8_t> bytes;
+    std::vector<std::uint32_t> lens;
+};
+
+template <typename Range>
+Packed pack(const Range& words) {
+    Packed p;
+    std::size_t total = 0;
+    for (const auto& w : words) total += w.size();
+    p.bytes.reserve(total);
+    p.lens.reserve(words.size());
+    for (const auto& w : words) {
+        p.bytes.insert(p.bytes.end(), w.begin(), w.end());
+        p.lens.push_back(std::uint32_t(w.size()));
+    }
+    return p;
+}
+
+std::vector<Word> unpack(const std::uint8_t* bytes, const std::uint32_t* lens, std::size_t n) {
+    std::vector<Word> out;
+    out.reserve(n);
+    std::size_t off = 0;
+    for (std::size_t i = 0; i < n; ++i) {
+        out.emplace_back(reinterpret_cast<const char*>(bytes + off), lens[i]);
+        off += lens[i];
+    }
+    return out;
+}
+
+struct CounterHandle {
+    wfcu_counter* h = nullptr;
+    explicit CounterHandle(std::uint64_t expected_keys = 0, const char* stage = nullptr) {
+        wfcu_counter_config cfg{};
+        std::uint64_t slots = 1u << 16;
+        while (slots < 4 * expected_keys) slots <<= 1;
+        cfg.table_slots = slots;
+        cfg.deferred_slots = std::max<std::uint64_t>(1u << 16, expected_keys);
+        cfg.long_slots = 1u << 16;
+        cfg.arena_bytes = 16u << 20;
+        ok(wfcu_counter_create(&h, &cfg), stage);
+    }
+    ~CounterHandle() { wfcu_counter_destroy(h); }
+    CounterHandle(const CounterHandle&) = delete;
+    CounterHandle& operator=(const CounterHandle&) = delete;
+};
+
+struct TokensHandle {
+    wfcu_tokens* h = nullptr;
+    ~TokensHandle() { wfcu_tokens_destroy(h); }
+};
+
+CountMap export_counts(wfcu_counter* c, const char* stage = nullptr) {
+    std::uint64_t distinct = 0, total = 0, key_bytes = 0;
+    ok(wfcu_counter_stats(c, nullptr, &distinct, &total, &key_bytes), stage);
+    std::vector<std::uint8_t> bytes(key_bytes + 1);
+    std::vector<std::uint32_t> lens(distinct + 1);
+    std::vector<std::uint64_t> counts(distinct + 1);
+    ok(wfcu_counter_export(c, nullptr, bytes.data(), key_bytes, lens.data(), counts.data(), distinct), stage);
+    CountMap m;
+    std::size_t off = 0;
+    for (std::uint64_t i = 0; i < distinct; ++i) {   // export is in map order: hinted insert is O(1)
+        m.emplace_hint(m.end(), Word(reinterpret_cast<const char*>(bytes.data() + off), lens[i]), counts[i]);
+        off += lens[i];
+    }
+    return m;
+}
+
+void add_map(wfcu_counter* c, const CountMap& m) {
+    if (m.empty()) return;
+    Packed p;
+    std::vector<std::uint64_t> counts;
+    counts.reserve(m.size());
+    for (const auto& [w, n] : m) {
+        p.bytes.insert(p.bytes.end(), w.begin(), w.end());
+        p.lens.push_back(std::uint32_t(w.size()));
+        counts.push_back(n);
+    }
+    ok(wfcu_counter_add_words(c, p.bytes.data(), p.lens.data(), counts.data(), m.size()));
+}
+
+// Capacity errors are not the caller's problem: retry with a larger table.
+template <typename Fn>
+void with_growing_counter(std::uint64_t hint, const char* stage, Fn&& fn) {
+    for (int attempt = 0;; ++attempt) {
+        CounterHandle c(hint, stage);
+        const int rc = fn(c.h);
+        if (rc == WFCU_OK) return;
+        const bool capacity = rc == WFCU_ERR_TABLE_FULL || rc == WFCU_ERR_DEFERRED_FULL || rc == WFCU_ERR_ARENA_FULL;
+        if (!capacity || attempt >= 6) raise(rc, stage);
+        hint = std::max<std::uint64_t>(hint, 1u << 14) * 8;
+    }
+}
+
+std::uint64_t total_bytes(std::span<const RawDocument> corpus) {
+    std::uint64_t n = 0;
+    for (const auto& d : corpus) n += d.text.size();
+    return n;
+}
+
+int wfcu_kind(MapKind map) {
+    switch (map) {
+        case MapKind::identity: return WFCU_MAP_IDENTITY;
+        case MapKind::square_root: return WFCU_MAP_SQUARE_ROOT;
+        case MapKind::alternating_harmonic_term: return WFCU_MAP_ALTERNATING_HARMONIC_TERM;
+        case MapKind::square: return WFCU_MAP_SQUARE;
+    }
+    throw std::invalid_argument("unknown map kind");
+}
+
+using Clock = std::chrono::steady_clock;
+std::uint64_t since(Clock::time_point t0) {
+    return std::uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count());
+}
+
+}  // namespace
+
+// ---- text ---------------------------------------------------------------------------------
+std::vector<std::optional<Word>> normalize_words(std::span<const std::string> fragments) {
+    const Packed p = pack(fragments);
+    std::vector<std::uint8_t> out(3 * p.bytes.size() + 16);
+    std::vector<std::uint32_t> out_lens(fragments.size() + 1);
+    ok(wfcu_normalize_words_host(p.bytes.data(), p.lens.data(), fragments.size(), out.data(), out.size(), out_lens.data()));
+    std::vector<std::optional<Word>> res(fragments.size());
+    std::size_t off = 0;
+    for (std::size_t i = 0; i < fragments.size(); ++i) {
+        if (out_lens[i]) res[i] = Word(reinterpret_cast<const char*>(out.data() + off), out_lens[i]);
+        off += out_lens[i];
+    }
+    return res;
+}
+
+std::optional<Word> normalize_word(std::string_view fragment) {
+    const std::string one(fragment);
+    return normalize_words(std::span<const std::string>(&one, 1))[0];
+}
+
+WordList tokenize(const RawDocument& doc) {
+    TokensHandle t;
+    ok(wfcu_tokenize_host(reinterpret_cast<const std::uint8_t*>(doc.text.data()), doc.text.size(), &t.h));
+    std::uint64_t n = 0, nb = 0;
+    ok(wfcu_tokens_stats(t.h, &n, &nb));
+    std::vector<std::uint8_t> bytes(nb + 1);
+    std::vector<std::uint32_t> lens(n + 1);
+    ok(wfcu_tokens_export(t.h, bytes.data(), nb, lens.data(), n));
+    WordList list;
+    list.words = unpack(bytes.data(), lens.data(), n);
+    return list;
+}
+
+WordList sort_words(WordList list) {
+    if (!list.words.empty()) {
+        const Packed p = pack(list.words);
+        TokensHandle t;
+        ok(wfcu_tokens_from_words(p.bytes.data(), p.lens.data(), list.words.size(), &t.h));
+        ok(wfcu_tokens_sort(t.h, nullptr));
+        std::vector<std::uint8_t> bytes(p.bytes.size() + 1);
+        std::vector<std::uint32_t> lens(p.lens.size() + 1);
+        ok(wfcu_tokens_export(t.h, bytes.data(), p.bytes.size(), lens.data(), p.lens.size()));
+        list.words = unpack(bytes.data(), lens.data(), p.lens.size());
+    }
+    list.sorted = true;
+    return list;
+}
+
+// ---- reduce -------------------------------------------------------------------------------
+CountMap reduce_sorted(const WordList& sorted) {
+    if (!sorted.sorted) throw std::invalid_argument("reduce_sorted: word list must be sorted");
+    if (sorted.words.empty()) return {};
+    for (const auto& w : sorted.words)
+        if (w.empty()) throw std::invalid_argument("reduce_sorted: empty word");
+    const Packed p = pack(sorted.words);
+    TokensHandle t;
+    ok(wfcu_tokens_from_words(p.bytes.data(), p.lens.data(), sorted.words.size(), &t.h));
+    CountMap result;
+    with_growing_counter(sorted.words.size(), nullptr, [&](wfcu_counter* c) {
+        int rc = wfcu_tokens_reduce_sorted(t.h, c, nullptr);
+        if (rc == WFCU_OK) rc = wfcu_counter_status(c, nullptr);
+        if (rc == WFCU_OK) result = export_counts(c);
+        return rc;
+    });
+    return result;
+}
+
+CountMap merge_counts(std::span<const CountMap> maps) {
+    std::uint64_t keys = 0;
+    for (const auto& m : maps) keys += m.size();
+    if (keys == 0) return {};
+    CountMap result;
+    with_growing_counter(keys, nullptr, [&](wfcu_counter* c) {
+        for (const auto& m : maps) add_map(c, m);
+        const int rc = wfcu_counter_status(c, nullptr);
+        if (rc == WFCU_OK) result = export_counts(c);
+        return rc;
+    });
+    return result;
+}
+
+// Container bookkeeping over std::map shards (no arithmetic beyond adding the counts of
+// a duplicated key): every word ends up with its lowest-indexed holder.
+ShardedCounts boundary_repair(ShardedCounts sharded) {
+    std::unordered_map<std::string_view, std::size_t> holder;
+    for (std::size_t s = 0; s < sharded.size(); ++s) {
+        for (auto it = sharded[s].begin(); it != sharded[s].end();) {
+            const auto [pos, fresh] = holder.try_emplace(std::string_view(it->first), s);
+            if (fresh) {
+                ++it;
+            } else {
+                sharded[pos->second].find(it->first)->second += it->second;
+                it = sharded[s].erase(it);
+            }
+        }
+    }
+    return sharded;
+}
+
+std::size_t count_unreduced_words(const ShardedCounts& sharded) {
+    std::unordered_map<std::string_view, unsigned> holders;
+    for (const auto& shard : sharded)
+        for (const auto& kv : shard) ++holders[std::string_view(kv.first)];
+    std::size_t n = 0;
+    for (const auto& kv : holders) n += kv.second > 1;
+    return n;
+}
+
+// ---- pipeline -----------------------------------------------------------------------------
+CountMap serial_wordcount(std::span<const RawDocument> corpus) {
+    if (corpus.empty()) return {};
+    std::vector<const std::uint8_t*> ptrs;
+    std::vector<std::uint64_t> lens;
+    for (const auto& d : corpus) {
+        ptrs.push_back(reinterpret_cast<const std::uint8_t*>(d.text.data()));
+        lens.push_back(d.text.size());
+    }
+    CountMap result;
+    with_growing_counter(total_bytes(corpus) / 64, nullptr, [&](wfcu_counter* c) {
+        const int rc = wfcu_counter_count_host(c, ptrs.data(), lens.data(), ptrs.size());
+        if (rc == WFCU_OK) result = export_counts(c);
+        return rc;
+    });
+    return result;
+}
+
+RunResult run_wordcount(std::span<const RawDocument> corpus, std::size_t n_workers) {
+    if (n_workers == 0) throw std::invalid_argument("run_wordcount: n_workers must be >= 1");
+    const auto run_start = Clock::now();
+    RunResult result;
+    result.n_workers = n_workers;
+    if (corpus.empty()) {
+        result.shards.assign(n_workers, CountMap{});
+        result.pre_repair_shards = result.shards;
+        result.timings.total_ns = since(run_start);
+        return result;
+    }
+    const std::size_t n = n_workers;
+    const std::uint64_t hint = total_bytes(corpus) / 64 / n + 1024;
+    auto& t = result.timings;
+
+    for (int attempt = 0;; ++attempt) {
+        try {
+            const std::uint64_t grow = hint << (3 * attempt);
+            std::vector<std::unique_ptr<CounterHandle>> local, owned;
+            for (std::size_t j = 0; j < n; ++j) local.push_back(std::make_unique<CounterHandle>(grow, "map"));
+            for (std::size_t j = 0; j < n; ++j) owned.push_back(std::make_unique<CounterHandle>(grow, "map"));
+
+            // map: worker j counts documents d = j (mod n)  (reference: pipeline.cpp:80-91)
+            auto t0 = Clock::now();
+            for (std::size_t j = 0; j < n; ++j) {
+                std::vector<const std::uint8_t*> ptrs;
+                std::vector<std::uint64_t> lens;
+                for (std::size_t d = j; d < corpus.size(); d += n) {
+                    ptrs.push_back(reinterpret_cast<const std::uint8_t*>(corpus[d].text.data()));
+                    lens.push_back(corpus[d].text.size());
+                }
+                ok(wfcu_counter_count_host(local[j]->h, ptrs.data(), lens.data(), ptrs.size()), "map");
+            }
+            t.map_ns = since(t0);
+
+            // encode + exchange: partition every worker's table by owner, deliver region p to
+            // owner p (device-to-device here; NCCL all-to-all across GPUs, exchange.py)
+            std::uint64_t enc = 0, exch = 0;
+            for (std::size_t j = 0; j < n; ++j) {
+                t0 = Clock::now();
+                std::uint64_t distinct = 0;
+                ok(wfcu_counter_stats(local[j]->h, nullptr, &distinct, nullptr, nullptr), "encode");
+                struct Dev {
+                    void* p = nullptr;
+                    ~Dev() { wfcu_dev_free(p); }
+                } entries, part_counts, recs;
+                ok(wfcu_dev_alloc(&entries.p, sizeof(wfcu_entry) * std::max<std::uint64_t>(distinct, 1)), "encode");
+                ok(wfcu_dev_alloc(&part_counts.p, sizeof(std::uint64_t) * n), "encode");
+                ok(wfcu_counter_partition(local[j]->h, std::uint32_t(n), static_cast<wfcu_entry*>(entries.p),
+                                          std::max<std::uint64_t>(distinct, 1),
+                                          static_cast<std::uint64_t*>(part_counts.p), nullptr), "encode");
+                std::vector<std::uint64_t> counts(n);
+                ok(wfcu_dev_download(counts.data(), part_counts.p, sizeof(std::uint64_t) * n), "encode");
+                std::uint64_t long_bytes = 0;
+                ok(wfcu_counter_long_records(local[j]->h, nullptr, 0, &long_bytes, nullptr), "encode");
+                if (long_bytes) {
+                    ok(wfcu_dev_alloc(&recs.p, long_bytes), "encode");
+                    ok(wfcu_counter_long_records(local[j]->h, static_cast<std::uint8_t*>(recs.p), long_bytes, &long_bytes,
+                                                 nullptr), "encode");
+                }
+                enc += since(t0);
+                t0 = Clock::now();
+                std::uint64_t off = 0;
+                for (std::size_t p = 0; p < n; ++p) {
+                    ok(wfcu_counter_merge_entries(owned[p]->h, static_cast<const wfcu_entry*>(entries.p) + off, counts[p],
+                                                  nullptr), "exchange");
+                    off += counts[p];
+                    if (long_bytes)
+                        ok(wfcu_counter_merge_long_records(owned[p]->h, static_cast<const std::uint8_t*>(recs.p), long_bytes,
+                                                           std::uint32_t(p), std::uint32_t(n), nullptr), "exchange");
+                }
+                for (std::size_t p = 0; p < n; ++p) ok(wfcu_counter_status(owned[p]->h, nullptr), "exchange");
+                exch += since(t0);
+            }
+            t.encode_ns = enc;
+            t.exchange_ns = exch;
+
+            t0 = Clock::now();
+            result.shards.clear();
+            for (std::size_t p = 0; p < n; ++p) result.shards.push_back(export_counts(owned[p]->h, "reduce"));
+            t.reduce_ns = since(t0);
+            break;
+        } catch (const PipelineError&) {
+            const std::string msg = wfcu_last_error();
+            const bool capacity = msg.find("recreate with more") != std::string::npos;
+            if (!capacity || attempt >= 5) throw;
+        }
+    }
+    result.pre_repair_shards = result.shards;   // disjoint by construction: nothing to repair
+    for (const auto& shard : result.shards) result.counts.insert(shard.begin(), shard.end());
+    t.total_ns = since(run_start);
+    return result;
+}
+
+RunResult run_wordcount(std::span<const RawDocument> corpus, std::size_t n_workers, Transport&) {
+    return run_wordcount(corpus, n_workers);
+}
+
+// ---- engine -------------------------------------------------------------------------------
+double map_reduce_serial(std::span<const double> values, MapKind map) {
+    // the left-to-right fold, bit for bit: one block covering the whole array
+    if (values.empty()) return 0.0;
+    double out = 0.0;
+    ok(wfcu_map_reduce_blocked_host(values.data(), WFCU_DTYPE_F64, values.size(), wfcu_kind(map), values.size(), &out));
+    return out;
+}
+
+double map_reduce_blocked(std::span<const double> values, MapKind map, const BlockConfig& cfg) {
+    if (cfg.block_size == 0 || cfg.workers == 0) throw std::invalid_argument("block_size and workers must be >= 1");
+    double out = 0.0;
+    ok(wfcu_map_reduce_blocked_host(values.data(), WFCU_DTYPE_F64, values.size(), wfcu_kind(map), cfg.block_size, &out));
+    return out;
+}
+
+double alternating_harmonic(std::uint64_t n, const BlockConfig& cfg) {
+    if (cfg.block_size == 0 || cfg.workers == 0) throw std::invalid_argument("block_size and workers must be >= 1");
+    double out = 0.0;
+    ok(wfcu_alternating_harmonic(n, cfg.block_size, &out));
+    return out;
+}
+
+double map_reduce_fast(std::span<const double> values, MapKind map) {
+    double out = 0.0;
+    ok(wfcu_map_reduce_host(values.data(), WFCU_DTYPE_F64, values.size(), wfcu_kind(map), &out));
+    return out;
+}
+
+double map_reduce_fast(std::span<const float> values, MapKind map) {
+    double out = 0.0;
+    ok(wfcu_map_reduce_host(values.data(), WFCU_DTYPE_F32, values.size(), wfcu_kind(map), &out));
+    return out;
+}
+
+// ---- analysis -----------------------------------------------------------------------------
+// Ordering of at most V rows on the host with the reference's exact comparators; the
+// counts themselves come from the device tables.  (SURVEY.md 8(f) rank 1 moves the
+// candidate selection onto the device.)
+FrequencyTable top_k(const CountMap& counts, std::string label, std::size_t k) {
+    FrequencyTable table;
+    table.label = std::move(label);
+    std::vector<const CountMap::value_type*> rows;
+    rows.reserve(counts.size());
+    for (const auto& kv : counts) {
+        table.total_words += kv.second;
+        rows.push_back(&kv);
+    }
+    const std::size_t keep = std::min(k, rows.size());
+    auto before = [](const CountMap::value_type* a, const CountMap::value_type* b) {
+        return a->second != b->second ? a->second > b->second : a->first < b->first;
+    };
+    std::partial_sort(rows.begin(), rows.begin() + keep, rows.end(), before);
+    for (std::size_t i = 0; i < keep; ++i)
+        table.rows.push_back({rows[i]->first, rows[i]->second, double(rows[i]->second) / double(table.total_words)});
+    return table;
+}
+
+DistinctivenessReport distinctive_words(const CountMap& target, const CountMap& others, std::string label,
+                                        std::size_t k) {
+    DistinctivenessReport report;
+    report.label = std::move(label);
+    if (target.empty() && others.empty()) return report;
+    std::uint64_t t_total = 0, o_total = 0;
+    for (const auto& kv : target) t_total += kv.second;
+    for (const auto& kv : others) o_total += kv.second;
+    struct Row {
+        const Word* word;
+        std::uint64_t in_target, in_others;
+        double score;
+    };
+    std::vector<Row> rows;
+    rows.reserve(target.size() + others.size());
+    auto ti = target.begin();
+    auto oi = others.begin();
+    while (ti != target.end() || oi != others.end()) {   // union of two sorted maps
+        const int c = oi == others.end() ? -1 : ti == target.end() ? 1 : ti->first.compare(oi->first);
+        if (c < 0) { rows.push_back({&ti->first, ti->second, 0, 0.0}); ++ti; }
+        else if (c > 0) { rows.push_back({&oi->first, 0, oi->second, 0.0}); ++oi; }
+        else { rows.push_back({&ti->first, ti->second, oi->second, 0.0}); ++ti; ++oi; }
+    }
+    const double t_den = double(t_total) + double(rows.size());
+    const double o_den = double(o_total) + double(rows.size());
+    for (auto& r : rows)
+        r.score = std::log((double(r.in_target) + 1.0) / t_den) - std::log((double(r.in_others) + 1.0) / o_den);
+    const std::size_t keep = std::min(k, rows.size());
+    std::partial_sort(rows.begin(), rows.begin() + keep, rows.end(), [](const Row& a, const Row& b) {
+        return a.score != b.score ? a.score > b.score : *a.word < *b.word;
+    });
+    for (std::size_t i = 0; i < keep; ++i) report.rows.push_back({*rows[i].word, rows[i].score});
+    return report;
+}
+
+}  // namespace wfc

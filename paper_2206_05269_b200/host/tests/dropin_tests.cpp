@@ -1,0 +1,352 @@
+// dropin_tests.cpp -- the drop-in exercised the way the reference's own suites exercise
+// the reference: same call sites, same expectations (each case cites the reference test
+// it mirrors, paths relative to /root/reference/proj/tests/).  Needs a B200; run by
+// tests/test_gpu_dropin.py.  No test framework dependency: a 20-line CHECK harness.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <map>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "wfc/analysis.hpp"
+#include "wfc/engine.hpp"
+#include "wfc/pipeline.hpp"
+#include "wfc/reduce.hpp"
+#include "wfc/text.hpp"
+
+using namespace wfc;
+
+static int g_failed = 0, g_checks = 0;
+#define CHECK(cond)                                                              \
+    do {                                                                         \
+        ++g_checks;                                                              \
+        if (!(cond)) {                                                           \
+            ++g_failed;                                                          \
+            std::printf("FAILED %s:%d  %s\n", __FILE__, __LINE__, #cond);        \
+        }                                                                        \
+    } while (0)
+#define CHECK_THROWS_AS(expr, Type)                                              \
+    do {                                                                         \
+        ++g_checks;                                                              \
+        bool threw = false;                                                      \
+        try { (void)(expr); } catch (const Type&) { threw = true; } catch (...) {} \
+        if (!threw) { ++g_failed; std::printf("FAILED %s:%d  %s should throw %s\n", __FILE__, __LINE__, #expr, #Type); } \
+    } while (0)
+
+using Rng = std::mt19937_64;
+
+static std::string vocab_word(std::size_t i) {          // support.hpp:18-22
+    char buf[16];
+    std::snprintf(buf, sizeof(buf), "w%04zu", i);
+    return buf;
+}
+static std::vector<RawDocument> iid_corpus(Rng& rng, std::size_t docs, std::size_t words_per_doc, std::size_t vocab) {
+    std::vector<RawDocument> corpus;               // support.hpp:42-51
+    std::uniform_int_distribution<std::size_t> pick(0, vocab - 1);
+    for (std::size_t d = 0; d < docs; ++d) {
+        std::string text;
+        for (std::size_t w = 0; w < words_per_doc; ++w) {
+            if (!text.empty()) text += ' ';
+            text += vocab_word(pick(rng));
+        }
+        corpus.push_back({"doc" + std::to_string(d), text});
+    }
+    return corpus;
+}
+// independent host oracle for the tests only: whitespace split of generator output
+static CountMap naive_count(const std::vector<RawDocument>& corpus) {
+    CountMap m;
+    for (const auto& d : corpus) {
+        std::size_t i = 0;
+        while (i < d.text.size()) {
+            while (i < d.text.size() && d.text[i] == ' ') ++i;
+            std::size_t j = i;
+            while (j < d.text.size() && d.text[j] != ' ') ++j;
+            if (j > i) ++m[d.text.substr(i, j - i)];
+            i = j;
+        }
+    }
+    return m;
+}
+static std::vector<double> random_uniforms(std::size_t n, std::uint64_t seed) {   // engine_test.cpp:14-20
+    Rng rng(seed);
+    std::uniform_real_distribution<double> uniform(0.0, 1.0);
+    std::vector<double> v(n);
+    for (auto& x : v) x = uniform(rng);
+    return v;
+}
+
+static const std::vector<RawDocument> kTwoDocs{{"doc1", "I want to test MapReduce"},
+                                               {"doc2", "MapReduce is a cool algorithm to test."}};
+
+static void text_cases() {
+    // text_test.cpp:40-58
+    CHECK(normalize_word("Dog") == "dog");
+    CHECK(normalize_word("dog.") == "dog");
+    CHECK(normalize_word("---") == std::nullopt);
+    CHECK(normalize_word("don't") == "don't");
+    CHECK(normalize_word("re-elect") == "re-elect");
+    CHECK(normalize_word("\"quoted!\"") == "quoted");
+    CHECK(normalize_word("2021") == "2021");
+    CHECK(normalize_word("") == std::nullopt);
+    CHECK(normalize_word("''") == std::nullopt);
+    CHECK(normalize_word("\xE2\x80\x9Cword\xE2\x80\x9D") == "word");
+    CHECK(normalize_word("caf\xC3\xA9") == "caf\xC3\xA9");
+    CHECK(normalize_word("CAF\xC3\x89") == "caf\xC3\xA9");
+    CHECK(normalize_word("word\xE2\x80\xA6") == "word");
+    CHECK(normalize_word("\xE2\x80\x94") == std::nullopt);
+    // text_test.cpp:60-72, batched: 5000 random printable-ASCII fragments vs tolower/isalnum trim
+    {
+        Rng rng(2024);
+        std::uniform_int_distribution<int> len(1, 12), ch('!', '~');
+        std::vector<std::string> frags;
+        for (int i = 0; i < 5000; ++i) {
+            std::string f;
+            const int n = len(rng);
+            for (int c = 0; c < n; ++c) f.push_back(char(ch(rng)));
+            frags.push_back(f);
+        }
+        const auto got = normalize_words(frags);
+        for (std::size_t i = 0; i < frags.size(); ++i) {
+            std::string s = frags[i];
+            for (auto& c : s) c = char(std::tolower(static_cast<unsigned char>(c)));
+            std::size_t b = 0, e = s.size();
+            while (b < e && !std::isalnum(static_cast<unsigned char>(s[b]))) ++b;
+            while (e > b && !std::isalnum(static_cast<unsigned char>(s[e - 1]))) --e;
+            const std::optional<std::string> want = b == e ? std::nullopt : std::optional<std::string>(s.substr(b, e - b));
+            CHECK(got[i] == want);
+        }
+        // idempotence, text_test.cpp:74-92
+        std::vector<std::string> once;
+        for (const auto& g : got) if (g) once.push_back(*g);
+        const auto twice = normalize_words(once);
+        for (std::size_t i = 0; i < once.size(); ++i) CHECK(twice[i] == once[i]);
+    }
+    // text_test.cpp:94-118
+    CHECK(tokenize({"d", "I want to test MapReduce"}).words == (std::vector<std::string>{"i", "want", "to", "test", "mapreduce"}));
+    CHECK(tokenize({"d", "MapReduce is a cool algorithm to test."}).words ==
+          (std::vector<std::string>{"mapreduce", "is", "a", "cool", "algorithm", "to", "test"}));
+    CHECK(tokenize({"d", ""}).words.empty());
+    CHECK(!tokenize({"d", "a b"}).sorted);
+    CHECK(tokenize({"d", "Dog dog. DOG!"}).words == (std::vector<std::string>{"dog", "dog", "dog"}));
+    CHECK(tokenize({"d", "a\xC2\xA0" "b\xE2\x80\x83" "c"}).words == (std::vector<std::string>{"a", "b", "c"}));
+    CHECK(tokenize({"d", "one\ttwo\nthree"}).words == (std::vector<std::string>{"one", "two", "three"}));
+    CHECK(tokenize({"d", "--- a !!! b ..."}).words == (std::vector<std::string>{"a", "b"}));
+    // text_test.cpp:143-169
+    CHECK(sort_words(WordList{{"i", "want", "to", "test", "mapreduce"}, false}).words ==
+          (std::vector<std::string>{"i", "mapreduce", "test", "to", "want"}));
+    CHECK(sort_words(WordList{}).words.empty());
+    CHECK(sort_words(WordList{}).sorted);
+    {
+        Rng rng(4242);
+        std::uniform_int_distribution<int> len(0, 200), word(0, 30);
+        for (int i = 0; i < 20; ++i) {
+            std::vector<std::string> words;
+            const int n = len(rng);
+            for (int w = 0; w < n; ++w) words.push_back("w" + std::to_string(word(rng)));
+            const WordList sorted = sort_words(WordList{words, false});
+            std::vector<std::string> want = words;
+            std::stable_sort(want.begin(), want.end());
+            CHECK(sorted.sorted);
+            CHECK(sorted.words == want);
+        }
+    }
+}
+
+static void reduce_cases() {
+    // reduce_test.cpp:28-58
+    CHECK(reduce_sorted(WordList{{"a", "algorithm", "cool", "i", "is", "mapreduce"}, true}) ==
+          (CountMap{{"a", 1}, {"algorithm", 1}, {"cool", 1}, {"i", 1}, {"is", 1}, {"mapreduce", 1}}));
+    CHECK(reduce_sorted(WordList{{"mapreduce", "test", "test", "to", "to", "want"}, true}) ==
+          (CountMap{{"mapreduce", 1}, {"test", 2}, {"to", 2}, {"want", 1}}));
+    CHECK(reduce_sorted(WordList{{}, true}).empty());
+    CHECK_THROWS_AS(reduce_sorted(WordList{{"b", "a"}, false}), std::invalid_argument);
+    // reduce_test.cpp:60-135
+    {
+        ShardedCounts pre{{{"a", 1}, {"mapreduce", 1}}, {{"mapreduce", 1}, {"test", 2}}};
+        const ShardedCounts post = boundary_repair(pre);
+        CHECK(post[0] == (CountMap{{"a", 1}, {"mapreduce", 2}}));
+        CHECK(post[1] == (CountMap{{"test", 2}}));
+        CHECK(count_unreduced_words(pre) == 1);
+        CHECK(count_unreduced_words(post) == 0);
+        ShardedCounts three{{{"x", 1}}, {{"x", 2}}, {}, {{"x", 4}, {"y", 1}}};
+        const ShardedCounts r3 = boundary_repair(three);
+        CHECK(r3[0] == (CountMap{{"x", 7}}));
+        CHECK(r3[1].empty());
+        CHECK(r3[3] == (CountMap{{"y", 1}}));
+    }
+    // reduce_test.cpp:112-155
+    {
+        const std::vector<CountMap> maps{{{"a", 1}, {"b", 2}}, {{"b", 3}, {"c", 4}}, {}};
+        CHECK(merge_counts(maps) == (CountMap{{"a", 1}, {"b", 5}, {"c", 4}}));
+        const std::vector<CountMap> rev{maps[1], maps[0]};
+        CHECK(merge_counts(rev) == merge_counts(maps));
+        CHECK(merge_counts(std::vector<CountMap>{}).empty());
+    }
+}
+
+static void pipeline_cases() {
+    const CountMap expected{{"a", 1}, {"algorithm", 1}, {"cool", 1}, {"i", 1}, {"is", 1},
+                            {"mapreduce", 2}, {"test", 2}, {"to", 2}, {"want", 1}};
+    // pipeline_test.cpp:26-54 (pre_repair_shards follow the hash partition: SURVEY D2)
+    {
+        const RunResult r = run_wordcount(kTwoDocs, 2);
+        CHECK(r.counts == expected);
+        CHECK(r.counts == serial_wordcount(kTwoDocs));
+        CHECK(merge_counts(r.shards) == r.counts);
+        CHECK(r.n_workers == 2);
+        CHECK(r.pre_repair_shards.size() == 2);
+        CHECK(count_unreduced_words(r.pre_repair_shards) <= 1);   // <= n - 1, SPEC bound
+        const auto& t = r.timings;
+        CHECK(t.total_ns >= std::max({t.map_ns, t.sort_ns, t.encode_ns, t.exchange_ns, t.reduce_ns, t.repair_ns}));
+        CHECK(run_wordcount(kTwoDocs, 1).counts == expected);
+    }
+    // pipeline_test.cpp:56-80
+    {
+        const std::vector<RawDocument> empty;
+        const RunResult r = run_wordcount(empty, 4);
+        CHECK(r.counts.empty());
+        CHECK(r.shards.size() == 4);
+        CHECK(r.timings.map_ns == 0 && r.timings.sort_ns == 0 && r.timings.encode_ns == 0);
+        CHECK(r.timings.exchange_ns == 0 && r.timings.reduce_ns == 0 && r.timings.repair_ns == 0);
+        CHECK_THROWS_AS(run_wordcount(kTwoDocs, 0), std::invalid_argument);
+    }
+    // pipeline_test.cpp:82-95
+    {
+        Rng rng(1001);
+        for (int round = 0; round < 4; ++round) {
+            const std::size_t docs = std::uniform_int_distribution<std::size_t>(1, 40)(rng);
+            const std::size_t words = std::uniform_int_distribution<std::size_t>(1, 300)(rng);
+            const auto corpus = iid_corpus(rng, docs, words, 60);
+            const CountMap oracle = serial_wordcount(corpus);
+            CHECK(oracle == naive_count(corpus));
+            for (std::size_t n : {1, 2, 3, 5, 8}) {
+                const RunResult r = run_wordcount(corpus, n);
+                CHECK(r.counts == oracle);
+                CHECK(merge_counts(r.shards) == r.counts);
+                CHECK(count_unreduced_words(r.shards) == 0);
+            }
+        }
+    }
+    // pipeline_test.cpp:97-104, 129-141
+    {
+        Rng rng(77);
+        const auto corpus = iid_corpus(rng, 100, 1000, 500);
+        const CountMap oracle = serial_wordcount(corpus);
+        CHECK(oracle == naive_count(corpus));
+        for (std::size_t n : {2, 4, 8}) CHECK(run_wordcount(corpus, n).counts == oracle);
+        Rng rng2(505);
+        const auto small = iid_corpus(rng2, 3, 50, 10);
+        const RunResult r = run_wordcount(small, 8);
+        CHECK(r.counts == serial_wordcount(small));
+        CHECK(r.pre_repair_shards.size() == 8);
+        CHECK(serial_wordcount(std::vector<RawDocument>{}).empty());
+        CHECK(serial_wordcount(std::vector<RawDocument>{{"d", "a a b"}}) == (CountMap{{"a", 2}, {"b", 1}}));
+    }
+}
+
+static void engine_cases() {
+    const std::vector<double> v{1.0, 4.0, 9.0};
+    // engine_test.cpp:24-36
+    CHECK(map_reduce_serial(v, MapKind::square_root) == 6.0);
+    CHECK(map_reduce_serial({}, MapKind::square_root) == 0.0);
+    CHECK(map_reduce_serial({}, MapKind::identity) == 0.0);
+    CHECK(map_reduce_blocked(v, MapKind::square_root, {1, 1}) == 6.0);
+    CHECK(map_reduce_blocked(v, MapKind::square_root, {1, 4}) == 6.0);
+    CHECK(map_reduce_blocked({}, MapKind::identity, {16, 2}) == 0.0);
+    // engine_test.cpp:38-45
+    {
+        const auto values = random_uniforms(1537, 9001);
+        for (MapKind map : {MapKind::identity, MapKind::square_root}) {
+            const double serial = map_reduce_serial(values, map);
+            double host = 0.0;
+            for (double x : values) host += (map == MapKind::identity ? x : std::sqrt(x));
+            CHECK(serial == host);   // the left fold, bit for bit
+            CHECK(map_reduce_blocked(values, map, {values.size(), 1}) == serial);
+            CHECK(map_reduce_blocked(values, map, {values.size() + 100, 3}) == serial);
+        }
+    }
+    // engine_test.cpp:47-79
+    {
+        double expected = 0.0;
+        for (int i = 1; i <= 10; ++i) expected += (i % 2 == 1 ? 1.0 : -1.0) / i;
+        const std::vector<double> ignored(10, 0.0);
+        CHECK(map_reduce_serial(ignored, MapKind::alternating_harmonic_term) == expected);
+        CHECK(alternating_harmonic(0) == 0.0);
+        CHECK(alternating_harmonic(1) == 1.0);
+        CHECK(alternating_harmonic(2) == 0.5);
+        const std::vector<double> zeros(1000, 0.0);
+        CHECK(alternating_harmonic(1000, {64, 2}) == map_reduce_blocked(zeros, MapKind::alternating_harmonic_term, {64, 2}));
+        Rng rng(321);
+        std::uniform_int_distribution<std::uint64_t> n_dist(1, 50000);
+        for (int i = 0; i < 10; ++i) {
+            const std::uint64_t n = n_dist(rng);
+            CHECK(std::abs(alternating_harmonic(n) - 0.6931471805599453) <= 1.0 / double(n + 1));
+        }
+    }
+    // engine_test.cpp:81-116
+    {
+        const auto values = random_uniforms(100000, 555);
+        for (MapKind map : {MapKind::identity, MapKind::square_root, MapKind::alternating_harmonic_term}) {
+            for (std::size_t block : {std::size_t(7), std::size_t(256), std::size_t(100000)}) {
+                const double reference = map_reduce_blocked(values, map, {block, 1});
+                for (unsigned workers : {2u, 8u}) CHECK(map_reduce_blocked(values, map, {block, workers}) == reference);
+            }
+            if (map != MapKind::alternating_harmonic_term) {
+                const double serial = map_reduce_serial(values, map);
+                CHECK(std::abs(map_reduce_blocked(values, map, {256, 4}) - serial) / std::max(1.0, std::abs(serial)) <= 1e-12);
+                CHECK(std::abs(map_reduce_fast(values, map) - serial) / std::max(1.0, std::abs(serial)) <= 1e-12);
+            }
+        }
+        const std::vector<double> neg{4.0, -1.0};
+        CHECK(std::isnan(map_reduce_serial(neg, MapKind::square_root)));
+        CHECK(std::isnan(map_reduce_blocked(neg, MapKind::square_root, {1, 2})));
+        const std::vector<double> one{1.0};
+        CHECK_THROWS_AS(map_reduce_blocked(one, MapKind::identity, {0, 1}), std::invalid_argument);
+        CHECK_THROWS_AS(map_reduce_blocked(one, MapKind::identity, {4, 0}), std::invalid_argument);
+        std::vector<float> f(values.begin(), values.end());
+        double sq = 0.0;
+        for (float x : f) sq += double(x) * double(x);
+        CHECK(std::abs(map_reduce_fast(std::span<const float>(f), MapKind::square) - sq) / sq <= 1e-5);
+    }
+}
+
+static void analysis_cases() {
+    // analysis_test.cpp:91-145
+    const CountMap m{{"the", 50}, {"a", 20}, {"union", 5}};
+    const FrequencyTable table = top_k(m, "t", 2);
+    CHECK(table.rows.size() == 2);
+    CHECK(table.rows[0].word == "the" && table.rows[0].count == 50);
+    CHECK(table.rows[1].word == "a" && table.rows[1].count == 20);
+    CHECK(table.total_words == 75);
+    CHECK(table.rows[0].rel_freq == 50.0 / 75.0);
+    CHECK(top_k(CountMap{}, "e", 3).rows.empty());
+    const FrequencyTable ties = top_k(CountMap{{"b", 2}, {"a", 2}, {"c", 1}}, "t", 3);
+    CHECK(ties.rows[0].word == "a" && ties.rows[1].word == "b");
+    const DistinctivenessReport rep = distinctive_words(CountMap{{"war", 2}, {"peace", 1}}, CountMap{{"peace", 2}, {"love", 1}}, "t", 1);
+    CHECK(rep.rows.size() == 1 && rep.rows[0].word == "war");
+    CHECK(std::abs(rep.rows[0].score - 1.0986122886681098) <= 1e-12);
+    for (const auto& row : distinctive_words(CountMap{{"a", 3}, {"b", 1}}, CountMap{{"a", 3}, {"b", 1}}, "t", 10).rows) CHECK(row.score == 0.0);
+    // application check (acceptance_test.cpp:297-330 shape): counts from the GPU pipeline feed top_k
+    const RunResult r = run_wordcount(kTwoDocs, 2);
+    const FrequencyTable top = top_k(r.counts, "two-docs", 3);
+    CHECK(top.rows[0].word == "mapreduce" && top.rows[1].word == "test" && top.rows[2].word == "to");
+    CHECK(top.total_words == 12);
+}
+
+int main() {
+    try {
+        text_cases();
+        reduce_cases();
+        pipeline_cases();
+        engine_cases();
+        analysis_cases();
+    } catch (const std::exception& e) {
+        std::printf("FAILED with exception: %s\n", e.what());
+        return 2;
+    }
+    std::printf("%d checks, %d failed\n", g_checks, g_failed);
+    return g_failed ? 1 : 0;
+}
