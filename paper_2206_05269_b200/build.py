@@ -65,7 +65,7 @@ def build_wfcu(force: bool = False, verbose: bool = False) -> Path:
     for src in cu + cpp:
         obj = obj_dir / (src.name + ".o")
         if force or _stale(obj, [src] + hdr):
-            cmd = [_nvcc(), *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+            cmd = [_nvcc(), *NVCC_FLAGS, *os.environ.get("WFCU_NVCC_EXTRA", "").split(), "-c", str(src), "-o", str(obj)]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
             _run(cmd)

@@ -81,27 +81,33 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // harmless: the flush adds every slot's count into the global table.  What must
 // never happen is a count credited to a different key, hence the publish order
 // of the medium table (k1 first, then k0 behind a fence).
-__device__ __forceinline__ bool short_add(u64* __restrict__ keys, u32* __restrict__ cnt, u32 mask, u64 key, u32 h) {
-    const u32 i0 = h & mask, i1 = (h >> 16) & mask;
+// Straight-line hit path: two candidate slots, both loaded up front, slot chosen by
+// selects.  Claiming an empty slot is the rare case (only while the table fills) and is
+// entered through a warp-uniform branch so that the steady state carries no divergence
+// bookkeeping.  live = this lane holds a token.
+__device__ __forceinline__ bool short_add(u64* __restrict__ keys, u32* __restrict__ cnt, u32 mask, u64 key, u32 h,
+                                          bool live) {
+    const u32 i0 = (h >> 19) & mask, i1 = (h >> 6) & mask;   // best-mixed bits of a multiplicative hash
     const u64 c0 = *reinterpret_cast<volatile u64*>(keys + i0);
     const u64 c1 = *reinterpret_cast<volatile u64*>(keys + i1);
-    u32 slot;
-    if (c0 == key) slot = i0;
-    else if (c1 == key) slot = i1;
-    else {
-        slot = 0xFFFFFFFFu;
-        if (c0 == 0) {
-            const u64 old = atomicCAS(keys + i0, 0ull, key);
-            if (old == 0 || old == key) slot = i0;
+    const bool hit0 = c0 == key, hit1 = c1 == key;
+    u32 slot = hit0 ? i0 : i1;
+    bool found = (hit0 || hit1) && live;
+    const bool can_claim = live && !found && (c0 == 0 || c1 == 0);
+    if (__any_sync(0xFFFFFFFFu, can_claim)) {
+        if (can_claim) {
+            if (c0 == 0) {
+                const u64 old = atomicCAS(keys + i0, 0ull, key);
+                if (old == 0 || old == key) { slot = i0; found = true; }
+            }
+            if (!found && c1 == 0) {
+                const u64 old = atomicCAS(keys + i1, 0ull, key);
+                if (old == 0 || old == key) { slot = i1; found = true; }
+            }
         }
-        if (slot == 0xFFFFFFFFu && c1 == 0) {
-            const u64 old = atomicCAS(keys + i1, 0ull, key);
-            if (old == 0 || old == key) slot = i1;
-        }
-        if (slot == 0xFFFFFFFFu) return false;
     }
-    atomicAdd(cnt + slot, 1u);
-    return true;
+    if (found) atomicAdd(cnt + slot, 1u);
+    return found;
 }
 
 __device__ __forceinline__ bool medium_add(u64* __restrict__ k0s, u64* __restrict__ k1s, u32* __restrict__ cnt,
@@ -230,14 +236,13 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
         if (!__any_sync(0xFFFFFFFFu, tlen > 8)) {
             // every token of this pass fits 8 bytes
             const u64 key = (((u64)b1 << 32) | b0) & (~0ull >> ((64u - 8u * tlen) & 63u));
-            if (tlen) {
-                u32 h = (u32)key * 0x9E3779B1u ^ (u32)(key >> 32) * 0x85EBCA77u;
-                h ^= h >> 15;
-                h *= 0x2C1B3C6Du;
-                h ^= h >> 13;
-                if (!short_add(sm.sk, sm.scnt, NSLOTS - 1, key, h)) { miss = true; mk0 = le_to_be(key); }
-                ++my_tokens;
-            }
+            // multiplies run on the FMA pipe, which this ALU-bound kernel leaves mostly idle
+            u32 h = (u32)key * 0x9E3779B1u + (u32)(key >> 32) * 0x85EBCA77u;
+            h ^= h >> 16;
+            h *= 0x2C1B3C6Du;
+            const bool live = tlen != 0;
+            if (!short_add(sm.sk, sm.scnt, NSLOTS - 1, key, h, live) && live) { miss = true; mk0 = le_to_be(key); }
+            my_tokens += live;
         } else {
             const u32 w3 = ringw[(wi + 3) & (kRingWords - 1)];
             const u32 w4 = ringw[(wi + 4) & (kRingWords - 1)];
@@ -248,14 +253,15 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
             u64 lo = ((u64)b1 << 32) | b0, hi = ((u64)b3 << 32) | b2;
             if (tlen <= 8) { lo &= ~0ull >> ((64u - 8u * tlen) & 63u); hi = 0; }
             else hi &= ~0ull >> ((128u - 8u * tlen) & 63u);
+            u32 h = (u32)lo * 0x9E3779B1u + (u32)(lo >> 32) * 0x85EBCA77u;
+            h += (u32)hi * 0xC2B2AE3Du + (u32)(hi >> 32) * 0x27D4EB2Fu;
+            h ^= h >> 16;
+            h *= 0x2C1B3C6Du;
+            // short_add votes across the warp: every lane calls it, medium lanes as idle
+            const bool is_short = tlen != 0 && tlen <= 8;
+            bool ok = short_add(sm.sk, sm.scnt, NSLOTS - 1, lo, h, is_short);
+            if (tlen > 8) ok = medium_add(sm.mk0, sm.mk1, sm.mcnt, MSLOTS - 1, lo, hi, h);
             if (tlen) {
-                u32 h = (u32)lo * 0x9E3779B1u ^ (u32)(lo >> 32) * 0x85EBCA77u;
-                h ^= (u32)hi * 0xC2B2AE3Du ^ (u32)(hi >> 32) * 0x27D4EB2Fu;
-                h ^= h >> 15;
-                h *= 0x2C1B3C6Du;
-                h ^= h >> 13;
-                const bool ok = (tlen <= 8) ? short_add(sm.sk, sm.scnt, NSLOTS - 1, lo, h)
-                                            : medium_add(sm.mk0, sm.mk1, sm.mcnt, MSLOTS - 1, lo, hi, h);
                 if (!ok) { miss = true; mk0 = le_to_be(lo); mk1 = le_to_be(hi); }
                 ++my_tokens;
             }
@@ -274,13 +280,18 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
         auto issue_row = [&](u64 row) {
             if (row < row_end) {
                 const u64 g = row * kRowBytes + (u64)lane * 16;
-                u32 nbytes = 0;
-                const uint8_t* src = text;
-                if (g < n) {
-                    nbytes = (n - g >= 16) ? 16u : (u32)(n - g);
-                    src = text + g;
+                uint8_t* dst = ring + ((u32)g & (kRingBytes - 1));
+                if ((row + 1) * kRowBytes <= n) {          // interior row (warp-uniform): no clamping
+                    cp_async16(dst, text + g, 16u);
+                } else {
+                    u32 nbytes = 0;
+                    const uint8_t* src = text;
+                    if (g < n) {
+                        nbytes = (n - g >= 16) ? 16u : (u32)(n - g);
+                        src = text + g;
+                    }
+                    cp_async16(dst, src, nbytes);
                 }
-                cp_async16(ring + (g & (kRingBytes - 1)), src, nbytes);
             }
             cp_async_commit();
         };
@@ -318,9 +329,11 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
             if (__any_sync(0xFFFFFFFFu, anyhi != 0) || carryH) {
                 H = mask16(w.x & 0x80808080u, w.y & 0x80808080u, w.z & 0x80808080u, w.w & 0x80808080u);
             }
-            if (g + 16 > n) {   // bytes at and beyond n are whitespace (document end)
-                const u32 valid = (g < n) ? (u32)(n - g) : 0u;
-                S |= (0xFFFFu << valid) & 0xFFFFu;
+            if ((row + 1) * kRowBytes > n) {   // last row (warp-uniform): bytes at and beyond n are whitespace
+                if (g + 16 > n) {
+                    const u32 valid = (g < n) ? (u32)(n - g) : 0u;
+                    S |= (0xFFFFu << valid) & 0xFFFFu;
+                }
             }
             u32 pS = __shfl_up_sync(0xFFFFFFFFu, S, 1);
             u32 pA = __shfl_up_sync(0xFFFFFFFFu, A, 1);
@@ -348,29 +361,52 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
             const u32 carried = qtail - qhead;          // entries left over from the previous row
             u32 qi = qtail + incl - cnt;
             const u32 gbase = (u32)g - 16u;             // ring positions only need the low bits
-            while (E) {
-                const u32 j = __ffs(E) - 1;
-                E &= E - 1;
-                const u32 pos = 16 + j;                    // end position in the 32-bit view
-                const u32 below = (1u << pos) - 1;
-                const u32 sp = S32 & below;
-                u32 entry = 0;                              // dead entry: fragment without a word character
-                const u32 start = 32 - __clz(sp);          // first byte of the fragment (0 if sp == 0)
-                const u32 frag = below & ~((1u << start) - 1);
-                const u32 a = A32 & frag;
-                bool defer = (sp == 0) || (H32 & frag);
-                if (!defer && a) {
-                    const u32 first = __ffs(a) - 1;
-                    const u32 tlen = 32 - __clz(a) - first;
-                    if (tlen > 16) defer = true;
-                    else entry = (tlen << 11) | ((gbase + first) & (kRingBytes - 1));
+            // Slow-path candidates are decided once per warp: a byte >= 0x80 nearby, no
+            // whitespace at all in the previous chunk, or a first fragment that reaches more
+            // than 16 bytes back (only the FIRST end of a chunk can: later fragments start
+            // inside the chunk).  Ordinary text takes the check-free loop.
+            const u32 hbS = 31 - __clz(pS | 1u);                       // highest whitespace bit of the previous chunk
+            const bool lane_rare = (H32 != 0) || (E != 0 && (pS == 0 || (u32)(__ffs(E) - 1) > hbS + 1));
+            if (!__any_sync(0xFFFFFFFFu, lane_rare)) {
+                while (E) {
+                    const u32 j = __ffs(E) - 1;
+                    E &= E - 1;
+                    const u32 below = (0x10000u << j) - 1;             // bits below the end (32-bit view)
+                    const u32 start = 32 - __clz(S32 & below);         // first byte of the fragment
+                    const u32 a = A32 & below & ~((1u << start) - 1);
+                    u32 entry = 0;                                     // dead: no word character
+                    if (a) {
+                        const u32 first = __ffs(a) - 1;
+                        const u32 tlen = 32 - __clz(a) - first;        // <= 16 by the test above
+                        entry = (tlen << 11) | ((gbase + first) & (kRingBytes - 1));
+                    }
+                    queue[(qi++) & (kQueueCap - 1)] = (uint16_t)entry;
                 }
-                if (defer) {
-                    const u64 slot = atomicAdd(gt.n_deferred, 1ull);
-                    if (slot < gt.deferred_cap) gt.deferred[slot] = g + j;
-                    else atomicOr(gt.status, kStatusDeferredFull);
+            } else {
+                while (E) {
+                    const u32 j = __ffs(E) - 1;
+                    E &= E - 1;
+                    const u32 pos = 16 + j;                    // end position in the 32-bit view
+                    const u32 below = (1u << pos) - 1;
+                    const u32 sp = S32 & below;
+                    u32 entry = 0;                              // dead entry: fragment without a word character
+                    const u32 start = 32 - __clz(sp);          // first byte of the fragment (0 if sp == 0)
+                    const u32 frag = below & ~((1u << start) - 1);
+                    const u32 a = A32 & frag;
+                    bool defer = (sp == 0) || (H32 & frag);
+                    if (!defer && a) {
+                        const u32 first = __ffs(a) - 1;
+                        const u32 tlen = 32 - __clz(a) - first;
+                        if (tlen > 16) defer = true;
+                        else entry = (tlen << 11) | ((gbase + first) & (kRingBytes - 1));
+                    }
+                    if (defer) {
+                        const u64 slot = atomicAdd(gt.n_deferred, 1ull);
+                        if (slot < gt.deferred_cap) gt.deferred[slot] = g + j;
+                        else atomicOr(gt.status, kStatusDeferredFull);
+                    }
+                    queue[(qi++) & (kQueueCap - 1)] = (uint16_t)entry;
                 }
-                queue[(qi++) & (kQueueCap - 1)] = (uint16_t)entry;
             }
             qtail += total;
             __syncwarp();
@@ -597,9 +633,19 @@ __global__ void wc_normalize_kernel(const uint8_t* __restrict__ text, const u64*
 
 // ---- host-side launchers (called from capi.cu) -----------------------------------
 static_assert(kRingBytes == 2048, "queue entries keep ring positions in 11 bits");
-constexpr int kFastWarps = 24;
-constexpr int kFastSlots = 8192;    // short-token combiner slots (12 bytes each)
-constexpr int kFastMedSlots = 1024; // medium-token combiner slots (20 bytes each)
+#ifndef WFCU_FAST_WARPS
+#define WFCU_FAST_WARPS 28
+#endif
+#ifndef WFCU_FAST_SLOTS
+#define WFCU_FAST_SLOTS 8192
+#endif
+#ifndef WFCU_FAST_MED_SLOTS
+#define WFCU_FAST_MED_SLOTS 512
+#endif
+constexpr int kFastWarps = WFCU_FAST_WARPS;
+constexpr int kFastSlots = WFCU_FAST_SLOTS;         // short-token combiner slots (12 bytes each)
+constexpr int kFastMedSlots = WFCU_FAST_MED_SLOTS;  // medium-token combiner slots (20 bytes each)
+static_assert(sizeof(FastSmem<kFastWarps, kFastSlots, kFastMedSlots>) <= 227 * 1024, "shared memory budget");
 
 size_t wc_fast_smem_bytes() { return sizeof(FastSmem<kFastWarps, kFastSlots, kFastMedSlots>); }
 
