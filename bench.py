@@ -234,13 +234,18 @@ def run_b200(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.backend == "gloo":
+        local_rank = local_rank % max(torch.cuda.device_count(), 1)
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device: the product has no CPU path")
     torch.cuda.set_device(local_rank)
     device = torch.device("cuda", local_rank)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=device)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:   # gloo carries CUDA tensors through the host: lets 2 ranks share one GPU in tests
+            dist.init_process_group("gloo")
     if world != max(args.gpus, 1) and rank == 0:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
 
@@ -395,6 +400,8 @@ def main() -> None:
     ap.add_argument("--docs", type=int, default=None, help="override document count (per GPU for cfg3, total for cfg4)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--sample-docs", type=int, default=None, help="reference arm: documents per step")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                    help="collective backend at N > 1 (gloo only for single-GPU testing of the N > 1 path)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-mapreduce", action="store_true", help="skip the config-2 map-reduce extra")
     args = ap.parse_args()

@@ -99,3 +99,27 @@ def test_device_ops_single_rank_path(capi, cuda, port):
     stats = hash_partition_merge(local, owned, DeviceOps(cuda, cuda.device("cuda", 0)), OneRank)
     assert owned.to_dict() == port.wordcount([text])
     assert stats.sent_entries == stats.received_entries
+
+
+def test_bench_two_ranks_on_one_gpu(capi, cuda):
+    """bench.py's N > 1 path (shard, count, partition, all-to-all, merge, e2e) with two ranks sharing
+    the GPU over gloo; the merged table must equal a single-rank count of the same documents."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", "29533", os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "2",
+           "--warmup", "1", "--docs", "6", "--backend", "gloo", "--no-mapreduce", "--e2e-steps", "1"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=root)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["config"]["documents"] == 12 and line["value"] > 0 and line["e2e"]["value"] > 0
+    # the same 12 documents counted by one rank
+    corpus = capi.synth_corpus(1, 0, 12, 50000)
+    dev, n = to_dev(cuda, corpus)
+    c = capi.Counter(table_slots=1 << 18)
+    c.count_dev(dev.data_ptr(), n)
+    distinct, tokens, _ = c.stats()
+    assert line["config"]["distinct_words"] == distinct and line["config"]["tokens"] == tokens
