@@ -45,6 +45,18 @@ METRIC = "wordcount_corpus_GBps"
 UNIT = "GB/s"
 
 
+def ncu_traffic(kernel: str, nbytes: int):
+    """dram__bytes_read + dram__bytes_write of one launch, from the committed ncu capture of this config."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)[kernel]
+        if t["bytes_per_gpu"] == nbytes:
+            return t["dram_bytes_read"] + t["dram_bytes_write"]
+    except Exception:
+        pass
+    return None
+
+
 def measured_peak_gbs():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -349,7 +361,7 @@ def run_b200(args) -> None:
                        "parallelism": f"document shard d mod {world}" + (", hash-partitioned all-to-all merge" if world > 1 else ""),
                        "l2": "inputs (1 GB per GPU) larger than the 126 MB L2; no flush needed"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak if peak else None, "traffic": None,
+                         "frac": achieved / peak if peak else None, "traffic": ncu_traffic("wc_fast_kernel", nbytes),
                          "kernel": "wc_fast_kernel", "kernel_ms": k_ms, "kernel_launches": kernel_launches,
                          "algorithmic_bytes_per_launch": nbytes, "peak_source": peak_src},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": d2h,

@@ -242,6 +242,24 @@ WFCU_API int wfcu_tokens_reduce_sorted(const wfcu_tokens* t, wfcu_counter* into,
 WFCU_API int wfcu_counter_count_dev_sorted(wfcu_counter* c, const uint8_t* dev_text, uint64_t n, void* stream);
 
 /* ------------------------------------------------------------------------- */
+/* top_k / distinctive_words over exported tables                            */
+/* (proj/src/analysis.cpp:58-132).  Tables are (key_bytes, key_lens, counts) */
+/* in std::map order, as wfcu_counter_export writes them.                    */
+/* ------------------------------------------------------------------------- */
+
+/* Rows ordered by count descending, ties by word ascending, truncated to k.
+ * out_idx[r] indexes the input table, out_rel[r] = count / total over the WHOLE table. */
+WFCU_API int wfcu_top_k(const uint8_t* key_bytes, const uint32_t* key_lens, const uint64_t* counts, uint64_t n,
+                        uint64_t k, uint64_t* out_idx, double* out_rel, uint64_t* total, uint64_t* n_rows);
+
+/* score = log((c_t+1)/(T_t+V)) - log((c_o+1)/(T_o+V)), V = |union vocabulary|; rows by
+ * score descending (exact double compare), ties by word ascending.  out_src[r] = 0: the
+ * word is row out_idx[r] of the target table, 1: of the others table. */
+WFCU_API int wfcu_distinctive(const uint8_t* t_bytes, const uint32_t* t_lens, const uint64_t* t_counts, uint64_t nt,
+                              const uint8_t* o_bytes, const uint32_t* o_lens, const uint64_t* o_counts, uint64_t no,
+                              uint64_t k, int32_t* out_src, uint64_t* out_idx, double* out_score, uint64_t* n_rows);
+
+/* ------------------------------------------------------------------------- */
 /* Synthetic corpora for BASELINE.json configs 3-5; host-side */
 /* generator, deterministic for (seed, doc index).                            */
 /* ------------------------------------------------------------------------- */

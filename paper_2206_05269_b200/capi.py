@@ -93,6 +93,9 @@ SIGNATURES = {
     "wfcu_tokens_sort": (C.c_int, [C.c_void_p, C.c_void_p]),
     "wfcu_tokens_reduce_sorted": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "wfcu_counter_count_dev_sorted": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "wfcu_top_k": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p, u64p, u64p]),
+    "wfcu_distinctive": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, u64p]),
     "wfcu_synth_document": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint32, C.c_double, C.c_uint32, C.c_void_p, C.c_uint64]),
     "wfcu_synth_corpus": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, C.c_double, C.c_uint32, C.c_uint64, C.c_void_p, C.c_int]),
     "wfcu_synth_corpus_strided": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, C.c_double, C.c_uint32, C.c_uint64, C.c_void_p, C.c_int]),
@@ -373,6 +376,35 @@ def normalize_words(fragments: list[bytes]) -> list[bytes | None]:
     check(lib.wfcu_normalize_words_host(_ptr(blob), _ptr(lens), len(fragments), _ptr(out), out.size, _ptr(out_lens)))
     words = unpack_words(out, out_lens[:len(fragments)])
     return [w if w else None for w in words]
+
+
+# ---- analysis over exported tables -----------------------------------------------------------
+Table = tuple  # (key_bytes, key_lens, counts) as returned by Counter.export()
+
+
+def top_k(table: Table, k: int) -> tuple[list[tuple[bytes, int, float]], int]:
+    """wfc::top_k: ([(word, count, rel_freq)], total_words)."""
+    blob, lens, counts = (np.ascontiguousarray(a) for a in table)
+    n = len(lens)
+    idx = np.zeros(max(min(n, k), 1), np.uint64)
+    rel = np.zeros(max(min(n, k), 1), np.float64)
+    total, rows = C.c_uint64(), C.c_uint64()
+    check(lib.wfcu_top_k(_ptr(blob), _ptr(lens), _ptr(counts), n, k, _ptr(idx), _ptr(rel), C.byref(total), C.byref(rows)))
+    words = unpack_words(blob, lens)
+    return [(words[int(idx[r])], int(counts[int(idx[r])]), float(rel[r])) for r in range(rows.value)], total.value
+
+
+def distinctive(target: Table, others: Table, k: int) -> list[tuple[bytes, float]]:
+    """wfc::distinctive_words: [(word, score)]."""
+    tb, tl, tc = (np.ascontiguousarray(a) for a in target)
+    ob, ol, oc = (np.ascontiguousarray(a) for a in others)
+    cap = max(min(len(tl) + len(ol), k), 1)
+    src, idx, score = np.zeros(cap, np.int32), np.zeros(cap, np.uint64), np.zeros(cap, np.float64)
+    rows = C.c_uint64()
+    check(lib.wfcu_distinctive(_ptr(tb), _ptr(tl), _ptr(tc), len(tl), _ptr(ob), _ptr(ol), _ptr(oc), len(ol), k,
+                               _ptr(src), _ptr(idx), _ptr(score), C.byref(rows)))
+    tw, ow = unpack_words(tb, tl), unpack_words(ob, ol)
+    return [((ow if src[r] else tw)[int(idx[r])], float(score[r])) for r in range(rows.value)]
 
 
 # ---- synthetic corpora -----------------------------------------------------------------------

@@ -27,6 +27,7 @@ cudaError_t mr_blocked_launch(const void* values, int is_f64, u64 n, u64 base, i
                               double* buf_b, double* dev_out, int sm_count, cudaStream_t s, u64* launches);
 // table_ops.cu
 cudaError_t tb_compact(const TableView& t, Slot* out, u64 cap, u64* dev_count, int sm, cudaStream_t s, u64* launches);
+cudaError_t tb_compact_recs(const TableView& t, TokenRec* out, u64 cap, u64* dev_count, int sm, cudaStream_t s, u64* launches);
 cudaError_t tb_key_bytes(const TableView& t, u64* dev_bytes, int sm, cudaStream_t s, u64* launches);
 cudaError_t tb_partition(const TableView& t, u32 n_parts, Slot* out, u64 cap, u64* dev_part_counts, u64* cursors,
                          int sm, cudaStream_t s, u64* launches);
@@ -55,6 +56,12 @@ cudaError_t tokens_rle_flags(const TokenRec* recs, u64 n, const uint8_t* arena, 
                              cudaStream_t s, u64* launches);
 cudaError_t tokens_rle_insert(const TokenRec* recs, u64 n, const uint8_t* arena, u64* flags, u64* run_start, u64* tmp,
                               const TableView& t, int sm, cudaStream_t s, u64* launches);
+// analysis.cpp
+uint64_t analysis_top_k(const uint8_t* bytes, const uint32_t* lens, const uint64_t* counts, uint64_t n, uint64_t k,
+                        uint64_t* out_idx, double* out_rel, uint64_t* total);
+uint64_t analysis_distinctive(const uint8_t* t_bytes, const uint32_t* t_lens, const uint64_t* t_counts, uint64_t nt,
+                              const uint8_t* o_bytes, const uint32_t* o_lens, const uint64_t* o_counts, uint64_t no,
+                              uint64_t k, int32_t* out_src, uint64_t* out_idx, double* out_score);
 // synth.cpp
 int synth_document(uint64_t seed, uint64_t doc, uint32_t vocab, double s, uint32_t speaker, uint8_t* out, uint64_t doc_bytes);
 int synth_corpus(uint64_t seed, uint64_t doc_begin, uint64_t doc_end, uint32_t vocab, double s, uint32_t speaker,
@@ -461,14 +468,25 @@ extern "C" int wfcu_counter_stats(wfcu_counter* c, void* stream, uint64_t* disti
 }
 
 namespace {
+struct DevBuf {   // RAII device allocation
+    void* p = nullptr;
+    cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes ? bytes : 16); }
+    ~DevBuf() { cudaFree(p); }
+    template <typename T> T* as() { return static_cast<T*>(p); }
+};
+}  // namespace
+
+namespace {
 struct HostEntry {
     std::string key;
     u64 count;
 };
 }
 
-// Pulls every (word, count) pair to the host, unordered.
-static int counter_pull(wfcu_counter* c, cudaStream_t s, std::vector<HostEntry>* out) {
+// Pulls every (word, count) pair to the host in std::map order.  The inline keys (the
+// bulk) are ordered on the device by the radix sort of tokens.cu; the rare long tokens
+// are ordered on the host and merged in.
+static int counter_pull_sorted(wfcu_counter* c, cudaStream_t s, std::vector<HostEntry>* out) {
     u64 h[8];
     CUDA_TRY(cudaMemcpyAsync(h, c->counters, sizeof(h), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -477,21 +495,22 @@ static int counter_pull(wfcu_counter* c, cudaStream_t s, std::vector<HostEntry>*
     out->clear();
     out->reserve(n_inline + n_long);
     LaunchTally tally;
+    std::vector<TokenRec> hs(n_inline);
     if (n_inline) {
-        Slot* dense = nullptr;
-        CUDA_TRY(cudaMalloc(&dense, sizeof(Slot) * n_inline));
-        cudaError_t e = tb_compact(c->v, dense, n_inline, c->counters + 7, c->sm_count, s, &tally.n);
-        std::vector<Slot> hs(n_inline);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(hs.data(), dense, sizeof(Slot) * n_inline, cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        cudaFree(dense);
-        if (e != cudaSuccess) return fail(WFCU_ERR_CUDA, "table export: %s", cudaGetErrorString(e));
-        for (const Slot& sl : hs) {
-            uint8_t b[16];
-            key_to_bytes(sl.k0, sl.k1, b);
-            out->push_back({std::string(reinterpret_cast<const char*>(b), key_len(sl.k0, sl.k1)), sl.count});
-        }
+        DevBuf dense, alt, hist, tmp, flag;
+        const u64 hw = sort_hist_words(n_inline);
+        CUDA_TRY(dense.alloc(sizeof(TokenRec) * n_inline));
+        CUDA_TRY(alt.alloc(sizeof(TokenRec) * n_inline));
+        CUDA_TRY(hist.alloc(sizeof(u64) * hw));
+        CUDA_TRY(tmp.alloc(sizeof(u64) * scan_tmp_words(hw)));
+        CUDA_TRY(flag.alloc(sizeof(int)));
+        CUDA_TRY(tb_compact_recs(c->v, dense.as<TokenRec>(), n_inline, c->counters + 7, c->sm_count, s, &tally.n));
+        SortScratch sc{alt.as<TokenRec>(), hist.as<u64>(), tmp.as<u64>(), flag.as<int>()};
+        CUDA_TRY(tokens_sort(dense.as<TokenRec>(), n_inline, /*by_position=*/false, nullptr, sc, c->sm_count, s, &tally.n));
+        CUDA_TRY(cudaMemcpyAsync(hs.data(), dense.p, sizeof(TokenRec) * n_inline, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
     }
+    std::vector<HostEntry> longs;
     if (n_long) {
         std::vector<u64> refs(c->long_slots), counts(c->long_slots);
         std::vector<uint8_t> arena(arena_used);
@@ -503,9 +522,20 @@ static int counter_pull(wfcu_counter* c, cudaStream_t s, std::vector<HostEntry>*
             if (!refs[i]) continue;
             u32 len;
             std::memcpy(&len, arena.data() + refs[i], 4);
-            out->push_back({std::string(reinterpret_cast<const char*>(arena.data() + refs[i] + 8), len), counts[i]});
+            longs.push_back({std::string(reinterpret_cast<const char*>(arena.data() + refs[i] + 8), len), counts[i]});
         }
+        std::sort(longs.begin(), longs.end(), [](const HostEntry& a, const HostEntry& b) { return a.key < b.key; });
     }
+    // merge the two ordered lists (std::string::compare is unsigned byte-wise = map order)
+    size_t li = 0;
+    for (const TokenRec& r : hs) {
+        uint8_t b[16];
+        key_to_bytes(r.k0, r.k1, b);
+        std::string key(reinterpret_cast<const char*>(b), key_len(r.k0, r.k1));
+        while (li < longs.size() && longs[li].key < key) out->push_back(std::move(longs[li++]));
+        out->push_back({std::move(key), r.pos});
+    }
+    while (li < longs.size()) out->push_back(std::move(longs[li++]));
     return WFCU_OK;
 }
 
@@ -513,9 +543,7 @@ extern "C" int wfcu_counter_export(wfcu_counter* c, void* stream, uint8_t* key_b
                                    uint32_t* key_lens, uint64_t* counts, uint64_t entries_cap) {
     if (!c) return fail(WFCU_ERR_INVALID_ARGUMENT, "counter is null");
     std::vector<HostEntry> rows;
-    if (int rc = counter_pull(c, (cudaStream_t)stream, &rows)) return rc;
-    // std::map order = unsigned byte-wise lexicographic (std::string::compare uses char_traits<char>::compare = memcmp)
-    std::sort(rows.begin(), rows.end(), [](const HostEntry& a, const HostEntry& b) { return a.key < b.key; });
+    if (int rc = counter_pull_sorted(c, (cudaStream_t)stream, &rows)) return rc;
     u64 total_bytes = 0;
     for (const auto& r : rows) total_bytes += r.key.size();
     if (rows.size() > entries_cap || total_bytes > key_bytes_cap)
@@ -801,15 +829,6 @@ extern "C" void wfcu_tokens_destroy(wfcu_tokens* t) {
     if (t) cudaSetDevice(t->device);
     tokens_free(t);
 }
-
-namespace {
-struct DevBuf {   // RAII device allocation
-    void* p = nullptr;
-    cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes ? bytes : 16); }
-    ~DevBuf() { cudaFree(p); }
-    template <typename T> T* as() { return static_cast<T*>(p); }
-};
-}  // namespace
 
 static int sort_device_tokens(wfcu_tokens* t, bool by_position, cudaStream_t s) {
     if (t->n < 2) return WFCU_OK;
@@ -1143,5 +1162,26 @@ extern "C" int wfcu_dev_upload(void* dev_dst, const void* host_src, uint64_t byt
 }
 extern "C" int wfcu_dev_download(void* host_dst, const void* dev_src, uint64_t bytes) {
     if (bytes) CUDA_TRY(cudaMemcpy(host_dst, dev_src, bytes, cudaMemcpyDeviceToHost));
+    return WFCU_OK;
+}
+
+// ---- analysis over exported tables ---------------------------------------------------------
+extern "C" int wfcu_top_k(const uint8_t* key_bytes, const uint32_t* key_lens, const uint64_t* counts, uint64_t n,
+                          uint64_t k, uint64_t* out_idx, double* out_rel, uint64_t* total, uint64_t* n_rows) {
+    if (!n_rows || !total) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
+    if (n && (!key_bytes || !key_lens || !counts)) return fail(WFCU_ERR_INVALID_ARGUMENT, "null table");
+    if (std::min(n, k) && (!out_idx || !out_rel)) return fail(WFCU_ERR_INVALID_ARGUMENT, "null output");
+    *n_rows = analysis_top_k(key_bytes, key_lens, counts, n, k, out_idx, out_rel, total);
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_distinctive(const uint8_t* t_bytes, const uint32_t* t_lens, const uint64_t* t_counts, uint64_t nt,
+                                const uint8_t* o_bytes, const uint32_t* o_lens, const uint64_t* o_counts, uint64_t no,
+                                uint64_t k, int32_t* out_src, uint64_t* out_idx, double* out_score, uint64_t* n_rows) {
+    if (!n_rows) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
+    if ((nt && (!t_bytes || !t_lens || !t_counts)) || (no && (!o_bytes || !o_lens || !o_counts)))
+        return fail(WFCU_ERR_INVALID_ARGUMENT, "null table");
+    if (std::min(nt + no, k) && (!out_src || !out_idx || !out_score)) return fail(WFCU_ERR_INVALID_ARGUMENT, "null output");
+    *n_rows = analysis_distinctive(t_bytes, t_lens, t_counts, nt, o_bytes, o_lens, o_counts, no, k, out_src, out_idx, out_score);
     return WFCU_OK;
 }

@@ -18,6 +18,18 @@ __global__ void tb_compact_kernel(TableView t, Slot* __restrict__ out, u64 out_c
     }
 }
 
+// Same, as TokenRec {k0,k1,ext=0,pos=count}: the radix sort of tokens.cu then orders the
+// table by key on the device and carries the count along.
+__global__ void tb_compact_recs_kernel(TableView t, TokenRec* __restrict__ out, u64 out_cap, u64* __restrict__ out_count) {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= t.mask; i += (u64)gridDim.x * blockDim.x) {
+        const Slot s = t.slots[i];
+        if (s.k0 != 0) {
+            const u64 j = atomicAdd(out_count, 1ull);
+            if (j < out_cap) out[j] = TokenRec{s.k0, s.k1, 0ull, s.count};
+        }
+    }
+}
+
 // sum of key lengths (inline keys + long records) -> *out_bytes
 __global__ void tb_key_bytes_kernel(TableView t, u64* __restrict__ out_bytes) {
     u64 local = 0;
@@ -159,6 +171,14 @@ cudaError_t tb_compact(const TableView& t, Slot* out, u64 cap, u64* dev_count, i
     cudaError_t e = cudaMemsetAsync(dev_count, 0, sizeof(u64), s);
     if (e != cudaSuccess) return e;
     tb_compact_kernel<<<grid_for(t.mask + 1, sm), 256, 0, s>>>(t, out, cap, dev_count);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+cudaError_t tb_compact_recs(const TableView& t, TokenRec* out, u64 cap, u64* dev_count, int sm, cudaStream_t s, u64* launches) {
+    cudaError_t e = cudaMemsetAsync(dev_count, 0, sizeof(u64), s);
+    if (e != cudaSuccess) return e;
+    tb_compact_recs_kernel<<<grid_for(t.mask + 1, sm), 256, 0, s>>>(t, out, cap, dev_count);
     *launches += 1;
     return cudaGetLastError();
 }

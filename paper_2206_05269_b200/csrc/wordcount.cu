@@ -121,7 +121,7 @@ __device__ __forceinline__ bool medium_add(u64* __restrict__ k0s, u64* __restric
             if (c0 == 0) {
                 *reinterpret_cast<volatile u64*>(k1s + i) = k1;
                 __threadfence_block();
-                *reinterpret_cast<volatile u64*>(k0s + i) = k0;
+                atomicExch(k0s + i, k0);   // publish: readers that see k0 also see k1
                 atomicAdd(cnt + i, 1u);
                 return true;
             }

@@ -1,0 +1,57 @@
+"""GPU: BASELINE.json config 5 at test scale -- four synthetic speaker corpora counted on
+the device, pooled-others by device merge, per-speaker top-k and distinctive words; every
+list must equal the oracle's exactly (words, counts, doubles).  Plus a >4 GiB offset check."""
+import numpy as np
+import pytest
+
+from helpers import to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def test_four_speakers_top_k_and_distinctive(capi, cuda, port):
+    speakers = [1, 2, 3, 4]
+    texts = {s: capi.synth_corpus(seed=7, doc_begin=0, doc_end=2, vocab=50000, speaker=s, doc_bytes=1 << 19) for s in speakers}
+    counters = {}
+    for s in speakers:
+        dev, n = to_dev(cuda, texts[s])
+        c = capi.Counter(table_slots=1 << 17)
+        c.count_dev(dev.data_ptr(), n)
+        counters[s] = c
+    cpu = {s: port.wordcount([texts[s]]) for s in speakers}
+    for s in speakers:
+        pooled = capi.Counter(table_slots=1 << 18)        # sum of the other three, on the device (cli.cpp:213-218)
+        for o in speakers:
+            if o != s:
+                pooled.merge(counters[o])
+        others_cpu = {}
+        for o in speakers:
+            if o != s:
+                for k, v in cpu[o].items():
+                    others_cpu[k] = others_cpu.get(k, 0) + v
+        assert pooled.to_dict() == others_cpu
+        assert capi.top_k(counters[s].export(), 25) == port.top_k(cpu[s], 25)
+        got = capi.distinctive(counters[s].export(), pooled.export(), 25)
+        assert got == port.distinctive(cpu[s], others_cpu, 25)
+        assert any(w.endswith(str(s).encode()) for w, _ in got)      # the speaker's own words rank high
+
+
+def test_offsets_beyond_4_gib(capi, cuda, port):
+    """a 4.25 GiB device buffer (17 copies of a 256 MiB corpus): counts are 17x the base counts"""
+    base = capi.synth_corpus(seed=5, doc_begin=0, doc_end=256, vocab=50000)
+    dev = cuda.from_numpy(base).cuda()
+    c = capi.Counter(table_slots=1 << 18)
+    c.count_dev(dev.data_ptr(), dev.numel())
+    one = c.to_dict()
+    big = dev.repeat(17)
+    assert big.numel() > (1 << 32)
+    c.reset()
+    c.count_dev(big.data_ptr(), big.numel())
+    many = c.to_dict()
+    assert many == {k: 17 * v for k, v in one.items()}
+    assert c.stats()[1] == 17 * sum(one.values())
+    sample = capi.synth_corpus(seed=5, doc_begin=0, doc_end=2, vocab=50000)   # anchor the base against the oracle
+    dsm, n = to_dev(cuda, sample)
+    c.reset()
+    c.count_dev(dsm.data_ptr(), n)
+    assert c.to_dict() == port.wordcount([sample])
