@@ -663,6 +663,50 @@ extern "C" int wfcu_counter_count_host(wfcu_counter* c, const uint8_t* const* do
         max_doc = std::max<u64>(max_doc, doc_lens[d]);
         total += doc_lens[d] + 1;
     }
+    // Fast path: the documents lie back to back in page-locked host memory and each ends
+    // with ASCII whitespace (so no separator is needed): DMA straight from the caller's
+    // buffer, no packing pass.
+    {
+        bool adjacent = true;
+        for (u64 d = 0; d < n_docs && adjacent; ++d) {
+            if (doc_lens[d] == 0) { adjacent = false; break; }
+            const uint8_t last = docs[d][doc_lens[d] - 1];
+            const bool ws = last == 0x20 || (last >= 0x09 && last <= 0x0D);
+            if (!ws && d + 1 < n_docs) adjacent = false;
+            if (d + 1 < n_docs && docs[d] + doc_lens[d] != docs[d + 1]) adjacent = false;
+        }
+        cudaPointerAttributes attr{};
+        if (adjacent && cudaPointerGetAttributes(&attr, docs[0]) == cudaSuccess && attr.type == cudaMemoryTypeHost) {
+            const u64 span = total - n_docs;   // bytes of all documents
+            const u64 piece = 64ull << 20;
+            if (int rc = ensure_staging(c, piece)) return rc;
+            CUDA_TRY(cudaStreamSynchronize(nullptr));
+            // pieces are cut at document boundaries (whitespace), two device buffers in flight
+            int cur = 0;
+            bool used[2] = {false, false};
+            u64 d = 0;
+            while (d < n_docs) {
+                const uint8_t* begin = docs[d];
+                u64 bytes = 0;
+                while (d < n_docs && (bytes == 0 || bytes + doc_lens[d] <= piece)) bytes += doc_lens[d++];
+                if (bytes > c->chunk_cap) {   // one oversized document: grow the staging buffers
+                    CUDA_TRY(cudaStreamSynchronize(c->stream));
+                    if (int rc = ensure_staging(c, (bytes + 15) & ~15ull)) return rc;
+                    used[0] = used[1] = false;
+                }
+                if (used[cur]) CUDA_TRY(cudaEventSynchronize(c->done[cur]));
+                CUDA_TRY(cudaMemcpyAsync(c->devbuf[cur], begin, bytes, cudaMemcpyHostToDevice, c->stream));
+                if (int rc = wfcu_counter_count_dev(c, c->devbuf[cur], bytes, c->stream)) return rc;
+                CUDA_TRY(cudaEventRecord(c->done[cur], c->stream));
+                used[cur] = true;
+                cur ^= 1;
+            }
+            (void)span;
+            CUDA_TRY(cudaStreamSynchronize(c->stream));
+            return wfcu_counter_status(c, c->stream);
+        }
+        cudaGetLastError();   // cudaPointerGetAttributes on plain malloc memory may set an error on old drivers
+    }
     // chunk = whole documents, '\n' after each; 64 MiB unless one document needs more
     u64 chunk = std::min<u64>(std::max<u64>(total, 1 << 20), 64ull << 20);
     chunk = std::max<u64>(chunk, max_doc + 1);

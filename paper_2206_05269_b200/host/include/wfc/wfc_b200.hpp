@@ -104,6 +104,20 @@ public:
 
 RunResult run_wordcount(std::span<const RawDocument> corpus, std::size_t n_workers);
 RunResult run_wordcount(std::span<const RawDocument> corpus, std::size_t n_workers, Transport& transport);
+
+// The paper's own algorithm (reference pipeline.cpp:61-123, shuffle.cpp:9-46), stage by
+// stage on the device kernels: tokenize -> sort_words -> range partition by position
+// (plan_partition) -> per-owner merge (sort) -> reduce_sorted -> boundary_repair.  Slower
+// than run_wordcount (tokens are materialised), but its pre_repair_shards are exactly the
+// reference's, boundary words included.
+struct ShardPlan {
+    std::size_t worker_id = 0;
+    std::size_t n_workers = 1;
+    std::size_t local_count = 0;
+    std::vector<std::size_t> boundaries;   // n+1 cut indices
+};
+ShardPlan plan_partition(const WordList& sorted, std::size_t worker_id, std::size_t n_workers);
+RunResult run_wordcount_range_partitioned(std::span<const RawDocument> corpus, std::size_t n_workers);
 CountMap serial_wordcount(std::span<const RawDocument> corpus);
 
 // ---- engine (reference: wfc/engine.hpp) ------------------------------------------------

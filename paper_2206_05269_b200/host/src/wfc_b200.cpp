@@ -370,6 +370,88 @@ RunResult run_wordcount(std::span<const RawDocument> corpus, std::size_t n_worke
     return run_wordcount(corpus, n_workers);
 }
 
+// Chunk sizes: the kept chunk gets floor(k/n); the rest is spread over the other chunks,
+// one extra each from chunk 0 upward (reference rule, shuffle.cpp:17-45).  Index arithmetic only.
+ShardPlan plan_partition(const WordList& sorted, std::size_t worker_id, std::size_t n_workers) {
+    if (n_workers == 0) throw std::invalid_argument("plan_partition: n_workers must be >= 1");
+    if (worker_id >= n_workers)
+        throw std::invalid_argument("plan_partition: worker_id " + std::to_string(worker_id) + " out of range for " +
+                                    std::to_string(n_workers) + " workers");
+    if (!sorted.sorted) throw std::invalid_argument("plan_partition: word list must be sorted");
+    const std::size_t k = sorted.words.size(), n = n_workers, keep = k / n;
+    const std::size_t others = n > 1 ? n - 1 : 1;
+    const std::size_t base = n > 1 ? (k - keep) / others : 0;
+    std::size_t extra = n > 1 ? (k - keep) % others : 0;
+    ShardPlan plan{worker_id, n, k, std::vector<std::size_t>(n + 1, 0)};
+    for (std::size_t c = 0; c < n; ++c) {
+        std::size_t size = keep;
+        if (c != worker_id) {
+            size = base + (extra ? 1 : 0);
+            if (extra) --extra;
+        }
+        plan.boundaries[c + 1] = plan.boundaries[c] + size;
+    }
+    return plan;
+}
+
+RunResult run_wordcount_range_partitioned(std::span<const RawDocument> corpus, std::size_t n_workers) {
+    if (n_workers == 0) throw std::invalid_argument("run_wordcount: n_workers must be >= 1");
+    const auto run_start = Clock::now();
+    RunResult result;
+    result.n_workers = n_workers;
+    const std::size_t n = n_workers;
+    if (corpus.empty()) {
+        result.shards.assign(n, CountMap{});
+        result.pre_repair_shards = result.shards;
+        result.timings.total_ns = since(run_start);
+        return result;
+    }
+    auto& t = result.timings;
+    auto stage = [&](const char* name, std::uint64_t& ns, auto&& fn) {
+        const auto t0 = Clock::now();
+        try {
+            fn();
+        } catch (const std::invalid_argument&) {
+            throw;
+        } catch (const std::exception& e) {
+            throw PipelineError(name, e.what());
+        }
+        ns = since(t0);
+    };
+    std::vector<WordList> local(n);
+    stage("map", t.map_ns, [&] {          // device tokenizer, documents d = j (mod n)
+        for (std::size_t j = 0; j < n; ++j)
+            for (std::size_t d = j; d < corpus.size(); d += n) {
+                WordList w = tokenize(corpus[d]);
+                local[j].words.insert(local[j].words.end(), std::make_move_iterator(w.words.begin()),
+                                      std::make_move_iterator(w.words.end()));
+            }
+    });
+    stage("sort", t.sort_ns, [&] {        // device radix sort
+        for (auto& l : local) l = sort_words(std::move(l));
+    });
+    std::vector<WordList> exchanged(n);
+    stage("encode", t.encode_ns, [&] {    // range partition by position
+        for (std::size_t j = 0; j < n; ++j) {
+            const ShardPlan plan = plan_partition(local[j], j, n);
+            for (std::size_t c = 0; c < n; ++c)
+                exchanged[c].words.insert(exchanged[c].words.end(), local[j].words.begin() + plan.boundaries[c],
+                                          local[j].words.begin() + plan.boundaries[c + 1]);
+        }
+    });
+    stage("exchange", t.exchange_ns, [&] {   // the n-way merge of sorted chunks == a stable sort of their concatenation
+        for (auto& e : exchanged) e = sort_words(std::move(e));
+    });
+    result.pre_repair_shards.assign(n, CountMap{});
+    stage("reduce", t.reduce_ns, [&] {    // device run-length encode
+        for (std::size_t j = 0; j < n; ++j) result.pre_repair_shards[j] = reduce_sorted(exchanged[j]);
+    });
+    stage("repair", t.repair_ns, [&] { result.shards = boundary_repair(result.pre_repair_shards); });
+    result.counts = merge_counts(result.shards);
+    t.total_ns = since(run_start);
+    return result;
+}
+
 // ---- engine -------------------------------------------------------------------------------
 double map_reduce_serial(std::span<const double> values, MapKind map) {
     // the left-to-right fold, bit for bit: one block covering the whole array

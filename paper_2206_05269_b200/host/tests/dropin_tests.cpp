@@ -247,6 +247,44 @@ static void pipeline_cases() {
     }
 }
 
+static void range_partition_cases() {
+    // shuffle_test.cpp:91-118
+    auto cuts = [](std::size_t k, std::size_t j, std::size_t n) {
+        WordList wl;
+        wl.words.assign(k, "w");
+        wl.sorted = true;
+        return plan_partition(wl, j, n).boundaries;
+    };
+    CHECK(cuts(5, 0, 2) == (std::vector<std::size_t>{0, 2, 5}));
+    CHECK(cuts(7, 1, 2) == (std::vector<std::size_t>{0, 4, 7}));
+    CHECK(cuts(10, 1, 3) == (std::vector<std::size_t>{0, 4, 7, 10}));
+    CHECK(cuts(9, 0, 1) == (std::vector<std::size_t>{0, 9}));
+    CHECK_THROWS_AS(cuts(3, 3, 3), std::invalid_argument);
+    CHECK_THROWS_AS(plan_partition(WordList{{"b", "a"}, false}, 0, 2), std::invalid_argument);
+    // pipeline_test.cpp:26-48: the worked example, BEFORE and after repair
+    const RunResult r = run_wordcount_range_partitioned(kTwoDocs, 2);
+    CHECK(r.pre_repair_shards.size() == 2);
+    CHECK(r.pre_repair_shards[0] == (CountMap{{"a", 1}, {"algorithm", 1}, {"cool", 1}, {"i", 1}, {"is", 1}, {"mapreduce", 1}}));
+    CHECK(r.pre_repair_shards[1] == (CountMap{{"mapreduce", 1}, {"test", 2}, {"to", 2}, {"want", 1}}));
+    CHECK(r.counts == serial_wordcount(kTwoDocs));
+    CHECK(merge_counts(r.shards) == r.counts);
+    CHECK(count_unreduced_words(r.pre_repair_shards) == 1);
+    CHECK(count_unreduced_words(r.shards) == 0);
+    // pipeline_test.cpp:82-95, 116-127 on the range-partitioned path
+    Rng rng(404);
+    for (int round = 0; round < 3; ++round) {
+        const auto corpus = iid_corpus(rng, 12, 150, 40);
+        const CountMap oracle = serial_wordcount(corpus);
+        for (std::size_t n : {1, 2, 4, 8}) {
+            const RunResult rr = run_wordcount_range_partitioned(corpus, n);
+            CHECK(rr.counts == oracle);
+            CHECK(rr.counts == run_wordcount(corpus, n).counts);
+            CHECK(merge_counts(rr.shards) == rr.counts);
+        }
+    }
+    CHECK(run_wordcount_range_partitioned(std::vector<RawDocument>{}, 3).shards.size() == 3);
+}
+
 static void engine_cases() {
     const std::vector<double> v{1.0, 4.0, 9.0};
     // engine_test.cpp:24-36
@@ -341,6 +379,7 @@ int main() {
         text_cases();
         reduce_cases();
         pipeline_cases();
+        range_partition_cases();
         engine_cases();
         analysis_cases();
     } catch (const std::exception& e) {

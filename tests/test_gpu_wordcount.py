@@ -139,3 +139,25 @@ def test_merge_and_add_words(capi, cuda, port):
     cc = capi.Counter(table_slots=1 << 14)
     cc.add_words(list(want), list(want.values()))
     assert cc.to_dict() == want
+
+
+def test_count_host_zero_copy_path(capi, cuda, port):
+    """adjacent whitespace-terminated documents in pinned memory are DMA'd without packing;
+    the same bytes without the terminators take the packing path -- both equal the oracle"""
+    import numpy as np
+    corpus = capi.synth_corpus(seed=9, doc_begin=0, doc_end=40, vocab=50000, doc_bytes=1 << 16)
+    pinned = cuda.from_numpy(corpus.copy()).pin_memory()
+    arr = pinned.numpy()
+    docs = [arr[i << 16:(i + 1) << 16] for i in range(40)]            # each ends with '\n'
+    want = port.wordcount(docs)
+    a = capi.Counter(table_slots=1 << 17)
+    a.count_host(docs)
+    assert a.to_dict() == want
+    ragged = [arr[i << 16:((i + 1) << 16) - 1 - (i % 3)] for i in range(40)]   # views that drop the terminator
+    b = capi.Counter(table_slots=1 << 17)
+    b.count_host(ragged)
+    assert b.to_dict() == port.wordcount(ragged)
+    pageable = [corpus[i << 16:(i + 1) << 16] for i in range(40)]      # adjacent but not pinned
+    c = capi.Counter(table_slots=1 << 17)
+    c.count_host(pageable)
+    assert c.to_dict() == want
