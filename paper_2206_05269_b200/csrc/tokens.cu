@@ -9,9 +9,10 @@
 // integer order on (k0,k1) IS byte-wise lexicographic order), an arena reference for
 // the rare token longer than 16 bytes, and its text position.
 //   * sort: hand-written stable LSD radix sort, 8-bit digits, keys (is_long, k1, k0);
-//     digit passes whose histogram has a single bin are skipped (k1 is all zero for
-//     corpora of short words); ties between long tokens that share a 16-byte prefix
-//     are ordered by an exact string fix-up pass.
+//     one OR/AND reduction over the keys finds the byte positions that vary at all and
+//     only those passes run (k1 is all zero for corpora of short words: 8 passes gone);
+//     ties between long tokens that share a 16-byte prefix are ordered by an exact
+//     string fix-up pass.
 //   * RLE: head flags by adjacent comparison -> exclusive scan -> run starts ->
 //     counts[key] += run length in the table.
 #include "wfcu_dev.cuh"
@@ -114,24 +115,9 @@ __global__ void sort_hist_kernel(const TokenRec* __restrict__ in, u64 n, u64 n_t
         for (int d = lane; d < 256; d += 32) hist[(u64)d * n_tiles + tile] = sh[warp][d];
 }
 
-// single-bin test: flag[0] = 1 when every record has the same digit (pass can be skipped)
-__global__ void sort_single_bin_kernel(const u64* __restrict__ hist, u64 n_tiles, u64 n, int* __restrict__ flag) {
-    __shared__ int found;
-    if (threadIdx.x == 0) found = 0;
-    __syncthreads();
-    // digit d is "the" bin when its counts over all tiles sum to n
-    const int d = threadIdx.x;   // 256 threads
-    u64 sum = 0;
-    for (u64 t = 0; t < n_tiles; ++t) sum += hist[(u64)d * n_tiles + t];
-    if (sum == n) found = 1;
-    __syncthreads();
-    if (threadIdx.x == 0) *flag = found;
-}
-
 // offs = exclusive scan of hist (digit-major), scatter keeps the tile order inside a digit
 __global__ void sort_scatter_kernel(const TokenRec* __restrict__ in, TokenRec* __restrict__ out, u64 n, u64 n_tiles,
-                                    int mode, int pass, const u64* __restrict__ offs, const int* __restrict__ skip) {
-    if (*skip) return;   // the caller swaps buffers only when the pass ran; see radix_pass
+                                    int mode, int pass, const u64* __restrict__ offs) {
     __shared__ u64 sh[kSortWarps][256];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const u64 tile = (u64)blockIdx.x * kSortWarps + warp;
@@ -160,11 +146,26 @@ __global__ void sort_scatter_kernel(const TokenRec* __restrict__ in, TokenRec* _
     }
 }
 
-// when a pass is skipped the data stays in `in`; copy so that the ping-pong stays uniform
-__global__ void sort_copy_if_skipped_kernel(const TokenRec* __restrict__ in, TokenRec* __restrict__ out, u64 n,
-                                            const int* __restrict__ skip) {
-    if (!*skip) return;
-    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) out[i] = in[i];
+// OR / AND of every key word over all records: a byte position whose OR equals its AND is
+// constant and its radix pass can be skipped without being launched.
+// out[0..3] = OR(k0), AND(k0), OR(k1), AND(k1); out[4] = #records with ext != 0; out[5] = OR/AND of pos (two words)
+__global__ void sort_key_range_kernel(const TokenRec* __restrict__ in, u64 n, u64* __restrict__ out) {
+    u64 o0 = 0, a0 = ~0ull, o1 = 0, a1 = ~0ull, op = 0, ap = ~0ull, nl = 0;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const TokenRec r = in[i];
+        o0 |= r.k0; a0 &= r.k0; o1 |= r.k1; a1 &= r.k1; op |= r.pos; ap &= r.pos;
+        nl += r.ext != 0;
+    }
+    for (int d = 16; d > 0; d >>= 1) {
+        o0 |= __shfl_xor_sync(0xFFFFFFFFu, o0, d); a0 &= __shfl_xor_sync(0xFFFFFFFFu, a0, d);
+        o1 |= __shfl_xor_sync(0xFFFFFFFFu, o1, d); a1 &= __shfl_xor_sync(0xFFFFFFFFu, a1, d);
+        op |= __shfl_xor_sync(0xFFFFFFFFu, op, d); ap &= __shfl_xor_sync(0xFFFFFFFFu, ap, d);
+        nl += __shfl_xor_sync(0xFFFFFFFFu, nl, d);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicOr(out + 0, o0); atomicAnd(out + 1, a0); atomicOr(out + 2, o1); atomicAnd(out + 3, a1);
+        atomicAdd(out + 4, nl); atomicOr(out + 5, op); atomicAnd(out + 6, ap);
+    }
 }
 
 // ---- long-token tie fix-up ---------------------------------------------------------
@@ -290,7 +291,7 @@ struct SortScratch {
 
 u64 sort_n_tiles(u64 n) { return (n + kTileItems - 1) / kTileItems; }
 u64 sort_hist_words(u64 n) { return 256 * sort_n_tiles(n); }
-u64 scan_tmp_words(u64 n) { return (n / kScanBlock + 2) + (n / ((u64)kScanBlock * kScanBlock) + 2) + 8; }
+u64 scan_tmp_words(u64 n) { return (n / kScanBlock + 2) + (n / ((u64)kScanBlock * kScanBlock) + 2) + 16; }
 
 // One stable radix pass; data ends up in `b` (either scattered or copied).
 static cudaError_t radix_pass(TokenRec* a, TokenRec* b, u64 n, int mode, int pass, const SortScratch& sc, int sm,
@@ -298,40 +299,55 @@ static cudaError_t radix_pass(TokenRec* a, TokenRec* b, u64 n, int mode, int pas
     const u64 n_tiles = sort_n_tiles(n);
     const unsigned grid = (unsigned)((n_tiles + kSortWarps - 1) / kSortWarps);
     sort_hist_kernel<<<grid, kSortWarps * 32, 0, s>>>(a, n, n_tiles, mode, pass, sc.hist);
-    sort_single_bin_kernel<<<1, 256, 0, s>>>(sc.hist, n_tiles, n, sc.flag);
-    *launches += 2;
-    cudaError_t e = exclusive_scan_u64(sc.hist, sc.hist, 256 * n_tiles, sc.tmp, s, launches);
+    *launches += 1;
+    cudaError_t e = exclusive_scan_u64(sc.hist, sc.hist, 256 * n_tiles, sc.tmp + 8, s, launches);
     if (e != cudaSuccess) return e;
-    sort_scatter_kernel<<<grid, kSortWarps * 32, 0, s>>>(a, b, n, n_tiles, mode, pass, sc.hist, sc.flag);
-    sort_copy_if_skipped_kernel<<<blocks_for(n, 256, sm), 256, 0, s>>>(a, b, n, sc.flag);
-    *launches += 2;
+    sort_scatter_kernel<<<grid, kSortWarps * 32, 0, s>>>(a, b, n, n_tiles, mode, pass, sc.hist);
+    *launches += 1;
     return cudaGetLastError();
 }
 
 // mode 1: restore text order (sort by pos); mode 0: sort_words order.  Result in `recs`.
+// sc.tmp doubles as the 8-word scratch of the key-range reduction (synchronises the stream once).
 cudaError_t tokens_sort(TokenRec* recs, u64 n, bool by_position, const uint8_t* arena, const SortScratch& sc, int sm,
                         cudaStream_t s, u64* launches) {
     if (n < 2) return cudaSuccess;
+    // which digit positions vary at all?
+    const u64 init[8] = {0, ~0ull, 0, ~0ull, 0, 0, ~0ull, 0};
+    cudaError_t e = cudaMemcpyAsync(sc.tmp, init, sizeof(init), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+    sort_key_range_kernel<<<blocks_for(n, 256, sm), 256, 0, s>>>(recs, n, sc.tmp);
+    *launches += 1;
+    u64 range[8];
+    e = cudaMemcpyAsync(range, sc.tmp, sizeof(range), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return e;
+    const u64 vary_k0 = range[0] ^ range[1], vary_k1 = range[2] ^ range[3], vary_pos = range[5] ^ range[6];
+    const bool mixed_long = range[4] != 0 && range[4] != n;
+
     TokenRec* a = recs;
     TokenRec* b = sc.alt;
-    cudaError_t e = cudaSuccess;
     auto run = [&](int mode, int pass) {
         if (e != cudaSuccess) return;
         e = radix_pass(a, b, n, mode, pass, sc, sm, s, launches);
         TokenRec* t = a; a = b; b = t;
     };
     if (by_position) {
-        for (int p = 0; p < 6; ++p) run(1, p);          // 48-bit offsets
+        for (int p = 0; p < 8; ++p)
+            if ((vary_pos >> (8 * p)) & 0xFF) run(1, p);
     } else {
-        run(2, 0);                                      // least significant: inline before long
-        for (int p = 0; p < 16; ++p) run(0, p);
+        if (mixed_long) run(2, 0);                      // least significant: inline before long
+        for (int p = 0; p < 8; ++p)
+            if ((vary_k1 >> (8 * p)) & 0xFF) run(0, p);
+        for (int p = 0; p < 8; ++p)
+            if ((vary_k0 >> (8 * p)) & 0xFF) run(0, 8 + p);
     }
     if (e != cudaSuccess) return e;
     if (a != recs) {
         e = cudaMemcpyAsync(recs, a, sizeof(TokenRec) * n, cudaMemcpyDeviceToDevice, s);
         if (e != cudaSuccess) return e;
     }
-    if (!by_position) {
+    if (!by_position && range[4] != 0) {
         sort_long_fixup_kernel<<<blocks_for(n, 256, sm), 256, 0, s>>>(recs, n, arena);
         *launches += 1;
     }
