@@ -393,6 +393,7 @@ extern "C" int wfcu_counter_count_dev(wfcu_counter* c, const uint8_t* dev_text, 
     if (!dev_text) return fail(WFCU_ERR_INVALID_ARGUMENT, "text is null");
     if (reinterpret_cast<uintptr_t>(dev_text) & 15u)
         return fail(WFCU_ERR_INVALID_ARGUMENT, "device text must be 16-byte aligned");
+    if (n >= (1ull << 40)) return fail(WFCU_ERR_INVALID_ARGUMENT, "one call counts at most 2^40 bytes; split the buffer at whitespace");
     LaunchTally tally;
     cudaEvent_t* ev0 = nullptr;
     cudaEvent_t* ev1 = nullptr;

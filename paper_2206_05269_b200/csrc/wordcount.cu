@@ -277,13 +277,18 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
 
     if (row_begin < row_end) {
         // issue one row: lane copies its 16-byte chunk, zero-filled past n
-        auto issue_row = [&](u64 row) {
-            if (row < row_end) {
-                const u64 g = row * kRowBytes + (u64)lane * 16;
-                uint8_t* dst = ring + ((u32)g & (kRingBytes - 1));
-                if ((row + 1) * kRowBytes <= n) {          // interior row (warp-uniform): no clamping
-                    cp_async16(dst, text + g, 16u);
+        // rows are indexed in 32 bits inside the loop (the launcher caps n at 2^40 bytes)
+        const u32 r_begin = (u32)row_begin, r_end = (u32)row_end;
+        const u32 full_rows = (u32)(n / kRowBytes);        // rows [0, full_rows) lie entirely inside the text
+        const uint8_t* lane_src = text + lane * 16;
+        uint8_t* lane_dst = ring + lane * 16;
+        auto issue_row = [&](u32 row) {
+            if (row < r_end) {
+                uint8_t* dst = lane_dst + (row & (kRingRows - 1)) * kRowBytes;
+                if (row < full_rows) {                     // interior row (warp-uniform): no clamping
+                    cp_async16(dst, lane_src + (u64)row * kRowBytes, 16u);
                 } else {
+                    const u64 g = (u64)row * kRowBytes + (u64)lane * 16;
                     u32 nbytes = 0;
                     const uint8_t* src = text;
                     if (g < n) {
@@ -300,7 +305,7 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
         u32 carryS = 0xFFFFu, carryA = 0, carryH = 0;   // "position -1" is whitespace
         if (row_begin > 0) {
             // history row: gives lane 0 its predecessor masks and keeps the bytes in the ring
-            issue_row(row_begin - 1);   // row_begin-1 < row_end always
+            issue_row(r_begin - 1);   // row_begin-1 < row_end always
             cp_async_wait<0>();
             __syncwarp();
             const u64 g = (row_begin - 1) * kRowBytes + (u64)lane * 16;
@@ -313,15 +318,14 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
             carryH = __shfl_sync(0xFFFFFFFFu, H, 31);
         }
 #pragma unroll
-        for (int p = 0; p < kPrefetch; ++p) issue_row(row_begin + p);
+        for (int p = 0; p < kPrefetch; ++p) issue_row(r_begin + p);
 
-        for (u64 row = row_begin; row < row_end; ++row) {
+        for (u32 row = r_begin; row < r_end; ++row) {
             cp_async_wait<kPrefetch - 1>();
             __syncwarp();
 
             // ------------------------------ phase 1 ------------------------------
-            const u64 g = row * kRowBytes + (u64)lane * 16;   // global offset of my chunk
-            const uint4 w = *reinterpret_cast<const uint4*>(ring + (g & (kRingBytes - 1)));
+            const uint4 w = *reinterpret_cast<const uint4*>(lane_dst + (row & (kRingRows - 1)) * kRowBytes);
             u32 S = mask16(space4(w.x), space4(w.y), space4(w.z), space4(w.w));
             const u32 A = mask16(alnum4(w.x), alnum4(w.y), alnum4(w.z), alnum4(w.w));
             u32 H = 0;
@@ -329,7 +333,8 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
             if (__any_sync(0xFFFFFFFFu, anyhi != 0) || carryH) {
                 H = mask16(w.x & 0x80808080u, w.y & 0x80808080u, w.z & 0x80808080u, w.w & 0x80808080u);
             }
-            if ((row + 1) * kRowBytes > n) {   // last row (warp-uniform): bytes at and beyond n are whitespace
+            if (row >= full_rows) {   // last row (warp-uniform): bytes at and beyond n are whitespace
+                const u64 g = (u64)row * kRowBytes + (u64)lane * 16;
                 if (g + 16 > n) {
                     const u32 valid = (g < n) ? (u32)(n - g) : 0u;
                     S |= (0xFFFFu << valid) & 0xFFFFu;
@@ -360,7 +365,7 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
             const u32 total = __shfl_sync(0xFFFFFFFFu, incl, 31);
             const u32 carried = qtail - qhead;          // entries left over from the previous row
             u32 qi = qtail + incl - cnt;
-            const u32 gbase = (u32)g - 16u;             // ring positions only need the low bits
+            const u32 gbase = row * kRowBytes + lane * 16 - 16u;   // ring positions only need the low bits
             // Slow-path candidates are decided once per warp: a byte >= 0x80 nearby, no
             // whitespace at all in the previous chunk, or a first fragment that reaches more
             // than 16 bytes back (only the FIRST end of a chunk can: later fragments start
@@ -402,7 +407,7 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
                     }
                     if (defer) {
                         const u64 slot = atomicAdd(gt.n_deferred, 1ull);
-                        if (slot < gt.deferred_cap) gt.deferred[slot] = g + j;
+                        if (slot < gt.deferred_cap) gt.deferred[slot] = (u64)row * kRowBytes + (u64)lane * 16 + j;
                         else atomicOr(gt.status, kStatusDeferredFull);
                     }
                     queue[(qi++) & (kQueueCap - 1)] = (uint16_t)entry;
@@ -414,7 +419,7 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
             // ------------------------------ phase 2 ------------------------------
             // full 32-token passes; the remainder waits for the next row's tokens
             u32 consumed = 0;
-            const u64 row_end_off = (row + 1) * kRowBytes;
+            const u64 row_end_off = EMIT ? ((u64)row + 1) * kRowBytes : 0;   // only the tokenizer needs positions
             while (qtail - qhead >= 32) { token_pass(32, row_end_off); consumed += 32; }
             // ... unless it would outlive its bytes in the ring (entries of row-1 may
             // reach back into row-2, which the next copy overwrites)
