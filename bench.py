@@ -133,6 +133,34 @@ class ClockSampler:
                 "reasons": sorted(k for k, bit in names.items() if seen & bit), "samples": len(mhz)}
 
 
+def bind_to_gpu_numa_node(torch, index: int) -> dict:
+    """Pinned host buffers should live on the NUMA node the GPU hangs off, or PCIe reads cross the
+    socket interconnect.  Bind this process to that node's cores before any host allocation
+    (first-touch places the pages); returns what was done for the JSON line."""
+    info = {"node": None, "cpus": None}
+    try:
+        p = torch.cuda.get_device_properties(index)
+        bdf = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bdf}/numa_node") as f:
+            node = int(f.read().strip())
+        if node < 0:
+            return info
+        with open(f"/sys/devices/system/node/node{node}/cpulist") as f:
+            spec = f.read().strip()
+        cpus = set()
+        for part in spec.split(","):
+            lo, _, hi = part.partition("-")
+            cpus.update(range(int(lo), int(hi or lo) + 1))
+        allowed = os.sched_getaffinity(0)
+        use = cpus & allowed
+        if use:
+            os.sched_setaffinity(0, use)
+            info = {"node": node, "cpus": len(use)}
+    except Exception:
+        pass
+    return info
+
+
 def plan(workload: str, world: int, rank: int, docs_override: int | None):
     w = WORKLOADS[workload]
     if w["total_docs"] is None:
@@ -261,6 +289,8 @@ def run_b200(args) -> None:
     if world != max(args.gpus, 1) and rank == 0:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
 
+    all_cpus = os.sched_getaffinity(0)
+    numa = bind_to_gpu_numa_node(torch, local_rank)
     w, total_docs, my_docs = plan(args.workload, world, rank, args.docs)
     host, nbytes = build_corpus(capi, np, torch, w["vocab"], my_docs, world)
     dev = host.to(device, non_blocking=True)
@@ -369,7 +399,9 @@ def run_b200(args) -> None:
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
         }
+        line["host_numa"] = numa
         if world == 1 and not args.no_cpu:
+            os.sched_setaffinity(0, all_cpus)      # the CPU baseline gets every core of the box
             line["cpu_baseline"] = cpu_baseline(capi, w["vocab"], total_docs)
         if not args.no_mapreduce:
             line["extra"] = {"mapreduce": mapreduce_line(capi, torch, device, stream, peak)}
@@ -417,6 +449,15 @@ def main() -> None:
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-mapreduce", action="store_true", help="skip the config-2 map-reduce extra")
     args = ap.parse_args()
+    # the native libraries are built in-tree; make sure they exist and are current (rank 0 builds, a no-op when fresh)
+    from paper_2206_05269_b200 import build as native
+    if int(os.environ.get("LOCAL_RANK", "0")) == 0:
+        native.build_all()
+    else:
+        for _ in range(600):
+            if (native.LIB / "libwfcu.so").exists():
+                break
+            time.sleep(0.5)
     if args.impl == "reference":
         run_reference(args)
     else:

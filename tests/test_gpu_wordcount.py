@@ -161,3 +161,18 @@ def test_count_host_zero_copy_path(capi, cuda, port):
     c = capi.Counter(table_slots=1 << 17)
     c.count_host(pageable)
     assert c.to_dict() == want
+
+
+def test_deferred_list_overflow_is_reported(capi, cuda, port):
+    """a corpus of non-ASCII words overflows a tiny slow-path list: loud error, and the same
+    text counts exactly once the capacity is raised (what the C++ drop-in's retry does)"""
+    text = (" ".join("héllo%d" % (i % 50) for i in range(20000))).encode()
+    dev, n = to_dev(cuda, text)
+    small = capi.Counter(table_slots=1 << 12, deferred_slots=1024)
+    small.count_dev(dev.data_ptr(), n)
+    with pytest.raises(capi.WfcuError) as e:
+        small.status()
+    assert e.value.code == capi.ERR_DEFERRED_FULL
+    big = capi.Counter(table_slots=1 << 12, deferred_slots=1 << 16)
+    big.count_dev(dev.data_ptr(), n)
+    assert big.to_dict() == port.wordcount([text])
