@@ -188,10 +188,15 @@ typedef struct wfcu_entry {
 WFCU_API uint32_t wfcu_owner_of(const uint8_t* word, uint32_t len, uint32_t n_parts);
 
 /* Groups the table's inline entries by owner: dev_entries receives them
- * partition by partition, dev_part_counts[n_parts] (device uint64) the size of
- * each partition.  entries_cap >= distinct.  Asynchronous. */
+ * partition by partition, dev_part_counts (device uint64, n_parts + 1 slots) the size
+ * of each partition and, in the last slot, the byte length of the long-token record
+ * stream.  entries_cap >= distinct (wfcu_counter_max_entries is always enough).
+ * Asynchronous: nothing here synchronises the stream. */
 WFCU_API int wfcu_counter_partition(wfcu_counter* c, uint32_t n_parts, wfcu_entry* dev_entries,
                            uint64_t entries_cap, uint64_t* dev_part_counts, void* stream);
+
+/* Upper bound of the number of inline entries the table can hold (its load limit). */
+WFCU_API uint64_t wfcu_counter_max_entries(const wfcu_counter* c);
 
 /* Inserts n received entries (summing counts of equal keys). Asynchronous. */
 WFCU_API int wfcu_counter_merge_entries(wfcu_counter* c, const wfcu_entry* dev_entries, uint64_t n, void* stream);

@@ -80,6 +80,7 @@ SIGNATURES = {
     "wfcu_counter_add_words": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64]),
     "wfcu_owner_of": (C.c_uint32, [C.c_void_p, C.c_uint32, C.c_uint32]),
     "wfcu_counter_partition": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
+    "wfcu_counter_max_entries": (C.c_uint64, [C.c_void_p]),
     "wfcu_counter_merge_entries": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "wfcu_counter_long_records": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, u64p, C.c_void_p]),
     "wfcu_counter_merge_long_records": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p]),
@@ -293,6 +294,9 @@ class Counter:
     def partition(self, n_parts: int, entries_ptr: int, entries_cap: int, part_counts_ptr: int, stream: int = 0) -> None:
         check(lib.wfcu_counter_partition(self._h, n_parts, C.c_void_p(entries_ptr), entries_cap,
                                          C.c_void_p(part_counts_ptr), C.c_void_p(stream)))
+
+    def max_entries(self) -> int:
+        return int(lib.wfcu_counter_max_entries(self._h))
 
     def merge_entries(self, entries_ptr: int, n: int, stream: int = 0) -> None:
         check(lib.wfcu_counter_merge_entries(self._h, C.c_void_p(entries_ptr), n, C.c_void_p(stream)))

@@ -770,15 +770,22 @@ extern "C" int wfcu_counter_partition(wfcu_counter* c, uint32_t n_parts, wfcu_en
     if (n_parts == 0 || n_parts > 4096) return fail(WFCU_ERR_INVALID_ARGUMENT, "n_parts must be in 1..4096");
     if (!dev_entries || !dev_part_counts) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
     static_assert(sizeof(wfcu_entry) == sizeof(Slot), "wire entry layout");
+    cudaStream_t s = (cudaStream_t)stream;
     u64* cursors = nullptr;
-    CUDA_TRY(cudaMallocAsync((void**)&cursors, sizeof(u64) * n_parts, (cudaStream_t)stream));
+    CUDA_TRY(cudaMallocAsync((void**)&cursors, sizeof(u64) * n_parts, s));
     LaunchTally tally;
     cudaError_t e = tb_partition(c->v, n_parts, reinterpret_cast<Slot*>(dev_entries), entries_cap,
-                                 reinterpret_cast<u64*>(dev_part_counts), cursors, c->sm_count, (cudaStream_t)stream, &tally.n);
-    cudaFreeAsync(cursors, (cudaStream_t)stream);
+                                 reinterpret_cast<u64*>(dev_part_counts), cursors, c->sm_count, s, &tally.n);
+    cudaFreeAsync(cursors, s);
+    // slot n_parts: bytes of the long-token record stream (0 for almost every corpus), so that the
+    // caller learns it from the same device array and needs no extra synchronisation
+    if (e == cudaSuccess)
+        e = tb_long_serialize(c->v, nullptr, 0, reinterpret_cast<u64*>(dev_part_counts) + n_parts, c->sm_count, s, &tally.n);
     if (e != cudaSuccess) return fail(WFCU_ERR_CUDA, "partition: %s", cudaGetErrorString(e));
     return WFCU_OK;
 }
+
+extern "C" uint64_t wfcu_counter_max_entries(const wfcu_counter* c) { return c ? c->v.max_used + 1 : 0; }
 
 extern "C" int wfcu_counter_merge_entries(wfcu_counter* c, const wfcu_entry* dev_entries, uint64_t n, void* stream) {
     if (!c) return fail(WFCU_ERR_INVALID_ARGUMENT, "counter is null");

@@ -21,8 +21,6 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-import numpy as np
-
 ENTRY_WORDS = 4   # wfcu_entry = 4 x u64 = 32 bytes
 
 
@@ -39,25 +37,25 @@ class DeviceOps:
         return self.torch.cuda.current_stream(self.device).cuda_stream
 
     def partition(self, counter, n_parts: int):
-        """-> (entries[int64, cap x 4] grouped by owner, part_counts[int64, n_parts]) on device"""
+        """-> (entries[int64, cap x 4] grouped by owner, counts[int64, n_parts + 1]) on device;
+        counts[n_parts] = bytes of the long-token record stream.  No host synchronisation."""
         t = self.torch
-        distinct, _, _ = counter.stats(self.stream())
-        entries = t.empty((max(distinct, 1), ENTRY_WORDS), dtype=t.int64, device=self.device)
-        counts = t.zeros(n_parts, dtype=t.int64, device=self.device)
-        counter.partition(n_parts, entries.data_ptr(), entries.shape[0], counts.data_ptr(), self.stream())
+        cap = counter.max_entries()
+        entries = t.empty((cap, ENTRY_WORDS), dtype=t.int64, device=self.device)
+        counts = t.zeros(n_parts + 1, dtype=t.int64, device=self.device)
+        counter.partition(n_parts, entries.data_ptr(), cap, counts.data_ptr(), self.stream())
         return entries, counts
 
     def merge_entries(self, counter, entries, n: int) -> None:
         if n:
             counter.merge_entries(entries.data_ptr(), n, self.stream())
 
-    def long_records(self, counter):
+    def long_records(self, counter, n_bytes: int):
         t = self.torch
-        n = counter.long_records(0, 0, self.stream())
-        buf = t.empty(max(n, 8), dtype=t.uint8, device=self.device)
-        if n:
-            counter.long_records(buf.data_ptr(), n, self.stream())
-        return buf[:n]
+        buf = t.empty(max(n_bytes, 8), dtype=t.uint8, device=self.device)
+        if n_bytes:
+            counter.long_records(buf.data_ptr(), n_bytes, self.stream())
+        return buf[:n_bytes]
 
     def merge_long_records(self, counter, records, part: int, n_parts: int) -> None:
         if records.numel():
@@ -80,7 +78,7 @@ class ExchangeStats:
     long_bytes: int
 
 
-def hash_partition_merge(local, owned, ops, dist, group=None) -> ExchangeStats:
+def hash_partition_merge(local, owned, ops, dist, group=None, force_collectives: bool = False) -> ExchangeStats:
     """Moves every entry of `local` to the rank that owns its key and sums it into `owned`.
 
     local / owned are counters (capi.Counter for DeviceOps).  Collective: every rank of the
@@ -91,18 +89,23 @@ def hash_partition_merge(local, owned, ops, dist, group=None) -> ExchangeStats:
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
 
-    entries, send_counts = ops.partition(local, world)
-    if world == 1:
-        n = int(send_counts.sum().item())
-        ops.merge_entries(owned, entries, n)
-        ops.merge_long_records(owned, ops.long_records(local), 0, 1)
-        return ExchangeStats(n, n, 0, 0)
+    entries, counts = ops.partition(local, world)
+    if world == 1 and not force_collectives:   # force_collectives: tests drive the NCCL calls with one rank
+        host = [int(v) for v in counts.cpu().tolist()]
+        ops.merge_entries(owned, entries, host[0])
+        if host[1]:
+            ops.merge_long_records(owned, ops.long_records(local, host[1]), 0, 1)
+        return ExchangeStats(host[0], host[0], 0, host[1])
 
-    # sizes first (n x n u64 in total), then the entries themselves
-    recv_counts = torch.empty_like(send_counts)
-    dist.all_to_all_single(recv_counts, send_counts, group=group)
-    send_list = [int(v) for v in send_counts.cpu().tolist()]
-    recv_list = [int(v) for v in recv_counts.cpu().tolist()]
+    # one small all-to-all tells every peer how many entries it gets from me and how long my
+    # long-token stream is; one host read of the result is the only synchronisation of the step
+    send_meta = torch.stack([counts[:world], counts[world].expand(world)], dim=1).contiguous()   # [world, 2]
+    recv_meta = torch.empty_like(send_meta)
+    dist.all_to_all_single(recv_meta, send_meta, group=group)
+    meta = torch.cat([send_meta, recv_meta], dim=1).cpu().tolist()        # the step's single D2H
+    send_list = [int(r[0]) for r in meta]
+    recv_list = [int(r[2]) for r in meta]
+    long_sizes = [int(r[3]) for r in meta]                                 # peer r's long-stream bytes
     n_send, n_recv = sum(send_list), sum(recv_list)
     recv = ops.empty_entries(n_recv)
     dist.all_to_all_single(recv[:n_recv], entries[:n_send], output_split_sizes=recv_list,
@@ -110,15 +113,11 @@ def hash_partition_merge(local, owned, ops, dist, group=None) -> ExchangeStats:
     ops.merge_entries(owned, recv, n_recv)
 
     # tokens longer than 16 bytes: rare, variable length -> all-gather the record streams and
-    # let every rank keep the records it owns
-    mine = ops.long_records(local)
-    sizes = torch.zeros(world, dtype=torch.int64, device=send_counts.device)
-    sizes[rank] = mine.numel()
-    dist.all_reduce(sizes, group=group)
-    size_list = [int(v) for v in sizes.cpu().tolist()]
-    long_total = sum(size_list)
+    # let every rank keep the records it owns (skipped entirely when nobody has any)
+    long_total = sum(long_sizes)
     if long_total:
-        width = max(size_list)
+        mine = ops.long_records(local, long_sizes[rank])
+        width = max(long_sizes)
         padded = ops.empty_bytes(width)
         padded.zero_()
         padded[:mine.numel()] = mine
@@ -126,8 +125,8 @@ def hash_partition_merge(local, owned, ops, dist, group=None) -> ExchangeStats:
         parts = [gathered[r * width:(r + 1) * width] for r in range(world)]
         dist.all_gather(parts, padded[:width], group=group)
         for r in range(world):
-            if size_list[r]:
-                ops.merge_long_records(owned, gathered[r * width:r * width + size_list[r]], rank, world)
+            if long_sizes[r]:
+                ops.merge_long_records(owned, gathered[r * width:r * width + long_sizes[r]], rank, world)
     return ExchangeStats(n_send, n_recv, n_send * 8 * ENTRY_WORDS, long_total)
 
 

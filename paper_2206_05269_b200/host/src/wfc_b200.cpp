@@ -319,7 +319,7 @@ RunResult run_wordcount(std::span<const RawDocument> corpus, std::size_t n_worke
                     ~Dev() { wfcu_dev_free(p); }
                 } entries, part_counts, recs;
                 ok(wfcu_dev_alloc(&entries.p, sizeof(wfcu_entry) * std::max<std::uint64_t>(distinct, 1)), "encode");
-                ok(wfcu_dev_alloc(&part_counts.p, sizeof(std::uint64_t) * n), "encode");
+                ok(wfcu_dev_alloc(&part_counts.p, sizeof(std::uint64_t) * (n + 1)), "encode");
                 ok(wfcu_counter_partition(local[j]->h, std::uint32_t(n), static_cast<wfcu_entry*>(entries.p),
                                           std::max<std::uint64_t>(distinct, 1),
                                           static_cast<std::uint64_t*>(part_counts.p), nullptr), "encode");

@@ -16,7 +16,7 @@ c2 = capi.Counter(table_slots=1 << 14, deferred_slots=1 << 14, arena_bytes=1 << 
 c2.count_dev_sorted(dev.data_ptr(), dev.numel())
 assert c2.to_dict() == c.to_dict()
 t = capi.Tokens.tokenize_dev(dev.data_ptr(), dev.numel()); assert t.words() == oracle.port().tokenize(text)
-ent = torch.empty((c.stats()[0], 4), dtype=torch.int64, device="cuda"); cnt = torch.zeros(3, dtype=torch.int64, device="cuda")
+ent = torch.empty((c.stats()[0], 4), dtype=torch.int64, device="cuda"); cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
 c.partition(3, ent.data_ptr(), ent.shape[0], cnt.data_ptr()); torch.cuda.synchronize()
 x = capi.synth_uniform(1, 100003, np.float32)
 print(capi.map_reduce_host(x, 3), capi.map_reduce_blocked_host(x, 1, 7), "sanitize workload ok")

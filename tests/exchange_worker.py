@@ -49,18 +49,20 @@ class OracleOps:
                 rows[capi.owner_of(w, n_parts)].append([*key_words(w), c, 0])
         flat = [r for part in rows for r in part]
         entries = torch.tensor(flat, dtype=torch.int64).reshape(-1, 4) if flat else torch.zeros((1, 4), dtype=torch.int64)
-        return entries, torch.tensor([len(p) for p in rows], dtype=torch.int64)
+        long_bytes = sum(16 + len(w) + (-len(w) % 8) for w in counter.table if len(w) > 16)
+        return entries, torch.tensor([len(p) for p in rows] + [long_bytes], dtype=torch.int64)
 
     def merge_entries(self, counter, entries, n):
         for k0, k1, c, _ in entries[:n].tolist():
             w = word_of(k0, k1)
             counter.table[w] = counter.table.get(w, 0) + c
 
-    def long_records(self, counter):
+    def long_records(self, counter, n_bytes):
         out = bytearray()
         for w, c in counter.table.items():
             if len(w) > 16:
                 out += struct.pack("<QII", c, len(w), 0) + w + b"\0" * (-len(w) % 8)
+        assert len(out) == n_bytes
         return torch.tensor(list(out), dtype=torch.uint8)
 
     def merge_long_records(self, counter, records, part, n_parts):

@@ -25,11 +25,12 @@ def run_workers(capi, torch, docs, n_workers, slots=1 << 14):
     for j, c in enumerate(local):
         distinct = c.stats()[0]
         entries = torch.empty((max(distinct, 1), 4), dtype=torch.int64, device="cuda")
-        counts = torch.zeros(n_workers, dtype=torch.int64, device="cuda")
+        counts = torch.zeros(n_workers + 1, dtype=torch.int64, device="cuda")
         c.partition(n_workers, entries.data_ptr(), entries.shape[0], counts.data_ptr())
         torch.cuda.synchronize()
-        offs = np.concatenate([[0], np.cumsum(counts.cpu().numpy())])
+        offs = np.concatenate([[0], np.cumsum(counts.cpu().numpy()[:n_workers])])
         nlong = c.long_records()
+        assert nlong == int(counts[n_workers])
         rec = torch.empty(max(nlong, 8), dtype=torch.uint8, device="cuda")
         if nlong:
             c.long_records(rec.data_ptr(), nlong)
@@ -123,3 +124,38 @@ def test_bench_two_ranks_on_one_gpu(capi, cuda):
     c.count_dev(dev.data_ptr(), n)
     distinct, tokens, _ = c.stats()
     assert line["config"]["distinct_words"] == distinct and line["config"]["tokens"] == tokens
+
+
+def test_nccl_collective_path_with_one_rank(capi, cuda, port):
+    """the exact NCCL calls of the multi-GPU merge (all_to_all_single with split sizes on int64
+    entry tensors, all_reduce, all_gather) driven through a 1-rank NCCL group on this GPU"""
+    import os
+    import subprocess
+    import sys
+    import textwrap
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = textwrap.dedent("""
+        import os, sys, random
+        sys.path.insert(0, %r); sys.path.insert(0, os.path.join(%r, "tests"))
+        import torch, torch.distributed as dist
+        from helpers import random_text, to_dev
+        from paper_2206_05269_b200 import capi
+        from paper_2206_05269_b200.exchange import DeviceOps, hash_partition_merge, allreduce_scalar
+        import oracle
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        text = random_text(random.Random(5), 60000, "unicode") + b" " + b"Z" * 33 + b" " + random_text(random.Random(6), 60000, "ascii")
+        dev, n = to_dev(torch, text)
+        local, owned = capi.Counter(table_slots=1 << 15), capi.Counter(table_slots=1 << 15)
+        local.count_dev(dev.data_ptr(), n)
+        st = hash_partition_merge(local, owned, DeviceOps(torch, torch.device("cuda", 0)), dist, force_collectives=True)
+        torch.cuda.synchronize()
+        assert owned.to_dict() == oracle.port().wordcount([text])
+        x = torch.tensor([1.25], dtype=torch.float64, device="cuda")
+        assert float(allreduce_scalar(x, dist)) == 1.25 and float(allreduce_scalar(x, dist, reproducible=False)) == 1.25
+        dist.destroy_process_group()
+        print("nccl path ok", st.sent_entries, st.long_bytes)
+    """ % (root, root))
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29544")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0 and "nccl path ok" in out.stdout, out.stderr[-3000:]
