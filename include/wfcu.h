@@ -162,6 +162,14 @@ WFCU_API int wfcu_counter_stats(wfcu_counter* c, void* stream, uint64_t* distinc
 WFCU_API int wfcu_counter_export(wfcu_counter* c, void* stream, uint8_t* key_bytes, uint64_t key_bytes_cap,
                         uint32_t* key_lens, uint64_t* counts, uint64_t entries_cap);
 
+/* top_k (proj/src/analysis.cpp:58-75) without exporting the table: rows by count
+ * descending, ties by word ascending, at most k; rel_freq = count / total words of the
+ * WHOLE table.  The table is ordered by count on the device and only rows that can make
+ * the cut are downloaded.  key_bytes_cap >= 16 * k covers tables without long tokens. */
+WFCU_API int wfcu_counter_top_k(wfcu_counter* c, uint64_t k, void* stream, uint8_t* key_bytes, uint64_t key_bytes_cap,
+                                uint32_t* key_lens, uint64_t* counts, double* rel_freq, uint64_t rows_cap,
+                                uint64_t* n_rows, uint64_t* total_words);
+
 /* dst[word] += src[word]  (merge_counts, proj/src/reduce.cpp:83-89), on device. */
 WFCU_API int wfcu_counter_merge(wfcu_counter* dst, const wfcu_counter* src, void* stream);
 

@@ -76,6 +76,8 @@ SIGNATURES = {
     "wfcu_counter_status": (C.c_int, [C.c_void_p, C.c_void_p]),
     "wfcu_counter_stats": (C.c_int, [C.c_void_p, C.c_void_p, u64p, u64p, u64p]),
     "wfcu_counter_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64]),
+    "wfcu_counter_top_k": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_uint64, u64p, u64p]),
     "wfcu_counter_merge": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "wfcu_counter_add_words": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64]),
     "wfcu_owner_of": (C.c_uint32, [C.c_void_p, C.c_uint32, C.c_uint32]),
@@ -281,6 +283,24 @@ class Counter:
     def to_dict(self, stream: int = 0) -> dict[bytes, int]:
         blob, lens, counts = self.export(stream)
         return dict(zip(unpack_words(blob, lens), (int(c) for c in counts)))
+
+    def top_k(self, k: int, stream: int = 0) -> tuple[list[tuple[bytes, int, float]], int]:
+        """wfc::top_k straight from the device table: ([(word, count, rel_freq)], total_words)."""
+        cap = max(k, 1)
+        blob = np.zeros(64 * cap + 4096, np.uint8)
+        lens, counts, rel = np.zeros(cap, np.uint32), np.zeros(cap, np.uint64), np.zeros(cap, np.float64)
+        rows, total = C.c_uint64(), C.c_uint64()
+        while True:
+            rc = lib.wfcu_counter_top_k(self._h, k, C.c_void_p(stream), _ptr(blob), blob.size, _ptr(lens), _ptr(counts),
+                                        _ptr(rel), cap, C.byref(rows), C.byref(total))
+            if rc == ERR_BUFFER_TOO_SMALL and blob.size < (1 << 30):   # very long tokens among the leaders
+                blob = np.zeros(blob.size * 8, np.uint8)
+                continue
+            check(rc)
+            break
+        n = rows.value
+        words = unpack_words(blob, lens[:n])
+        return [(words[r], int(counts[r]), float(rel[r])) for r in range(n)], total.value
 
     def merge(self, other: "Counter", stream: int = 0) -> None:
         check(lib.wfcu_counter_merge(self._h, other._h, C.c_void_p(stream)))

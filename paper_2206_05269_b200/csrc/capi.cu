@@ -28,6 +28,7 @@ cudaError_t mr_blocked_launch(const void* values, int is_f64, u64 n, u64 base, i
 // table_ops.cu
 cudaError_t tb_compact(const TableView& t, Slot* out, u64 cap, u64* dev_count, int sm, cudaStream_t s, u64* launches);
 cudaError_t tb_compact_recs(const TableView& t, TokenRec* out, u64 cap, u64* dev_count, int sm, cudaStream_t s, u64* launches);
+cudaError_t tb_lower_bound_pos(const TokenRec* recs, u64 n, u64 value, u64* dev_out, cudaStream_t s, u64* launches);
 cudaError_t tb_key_bytes(const TableView& t, u64* dev_bytes, int sm, cudaStream_t s, u64* launches);
 cudaError_t tb_partition(const TableView& t, u32 n_parts, Slot* out, u64 cap, u64* dev_part_counts, u64* cursors,
                          int sm, cudaStream_t s, u64* launches);
@@ -557,6 +558,84 @@ extern "C" int wfcu_counter_export(wfcu_counter* c, void* stream, uint8_t* key_b
         key_lens[i] = (u32)rows[i].key.size();
         counts[i] = rows[i].count;
     }
+    return WFCU_OK;
+}
+
+// top_k straight from the device table (proj/src/analysis.cpp:58-75): the compacted slots are
+// ordered by count on the device, the count of the k-th row is the threshold, and only rows at
+// or above it (ties included) come back to be put in the reference's exact order.
+extern "C" int wfcu_counter_top_k(wfcu_counter* c, uint64_t k, void* stream, uint8_t* key_bytes, uint64_t key_bytes_cap,
+                                  uint32_t* key_lens, uint64_t* counts, double* rel_freq, uint64_t rows_cap,
+                                  uint64_t* n_rows, uint64_t* total_words) {
+    if (!c || !n_rows || !total_words) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    u64 h[8];
+    CUDA_TRY(cudaMemcpyAsync(h, c->counters, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (int rc = status_to_rc((int)(h[5] & 0xFFFFFFFFu))) return rc;
+    const u64 n_inline = h[0], n_long = h[3], arena_used = h[4];
+    *total_words = h[1];
+    *n_rows = 0;
+    std::vector<HostEntry> cand;
+    LaunchTally tally;
+    if (n_inline && k) {
+        DevBuf dense, alt, hist, tmp, flag;
+        const u64 hw = sort_hist_words(n_inline);
+        CUDA_TRY(dense.alloc(sizeof(TokenRec) * n_inline));
+        CUDA_TRY(alt.alloc(sizeof(TokenRec) * n_inline));
+        CUDA_TRY(hist.alloc(sizeof(u64) * hw));
+        CUDA_TRY(tmp.alloc(sizeof(u64) * scan_tmp_words(hw)));
+        CUDA_TRY(flag.alloc(sizeof(int)));
+        CUDA_TRY(tb_compact_recs(c->v, dense.as<TokenRec>(), n_inline, c->counters + 7, c->sm_count, s, &tally.n));
+        SortScratch sc{alt.as<TokenRec>(), hist.as<u64>(), tmp.as<u64>(), flag.as<int>()};
+        CUDA_TRY(tokens_sort(dense.as<TokenRec>(), n_inline, /*by_position=*/true, nullptr, sc, c->sm_count, s, &tally.n));
+        // threshold = count of the k-th largest inline row (long rows can only push it up)
+        const u64 kth = n_inline > k ? n_inline - k : 0;
+        TokenRec pivot;
+        CUDA_TRY(cudaMemcpyAsync(&pivot, dense.as<TokenRec>() + kth, sizeof(TokenRec), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        CUDA_TRY(tb_lower_bound_pos(dense.as<TokenRec>(), n_inline, pivot.pos, c->counters + 9, s, &tally.n));
+        u64 first = 0;
+        CUDA_TRY(cudaMemcpyAsync(&first, c->counters + 9, sizeof(u64), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        std::vector<TokenRec> hs(n_inline - first);
+        CUDA_TRY(cudaMemcpyAsync(hs.data(), dense.as<TokenRec>() + first, sizeof(TokenRec) * hs.size(), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        for (const TokenRec& r : hs) {
+            uint8_t b[16];
+            key_to_bytes(r.k0, r.k1, b);
+            cand.push_back({std::string(reinterpret_cast<const char*>(b), key_len(r.k0, r.k1)), r.pos});
+        }
+    }
+    if (n_long && k) {   // rare: every long row is a candidate
+        std::vector<u64> refs(c->long_slots), cnts(c->long_slots);
+        std::vector<uint8_t> arena(arena_used);
+        CUDA_TRY(cudaMemcpyAsync(refs.data(), c->v.long_ref, sizeof(u64) * c->long_slots, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(cnts.data(), c->v.long_count, sizeof(u64) * c->long_slots, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(arena.data(), c->v.arena, arena_used, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        for (u64 i = 0; i < c->long_slots; ++i) {
+            if (!refs[i]) continue;
+            u32 len;
+            std::memcpy(&len, arena.data() + refs[i], 4);
+            cand.push_back({std::string(reinterpret_cast<const char*>(arena.data() + refs[i] + 8), len), cnts[i]});
+        }
+    }
+    const u64 keep = std::min<u64>(k, cand.size());
+    std::partial_sort(cand.begin(), cand.begin() + keep, cand.end(), [](const HostEntry& a, const HostEntry& b) {
+        return a.count != b.count ? a.count > b.count : a.key < b.key;
+    });
+    u64 off = 0;
+    if (keep > rows_cap) return fail(WFCU_ERR_BUFFER_TOO_SMALL, "top_k needs %llu rows", (unsigned long long)keep);
+    for (u64 r = 0; r < keep; ++r) {
+        if (off + cand[r].key.size() > key_bytes_cap) return fail(WFCU_ERR_BUFFER_TOO_SMALL, "top_k key buffer too small");
+        std::memcpy(key_bytes + off, cand[r].key.data(), cand[r].key.size());
+        off += cand[r].key.size();
+        key_lens[r] = (u32)cand[r].key.size();
+        counts[r] = cand[r].count;
+        rel_freq[r] = double(cand[r].count) / double(*total_words);
+    }
+    *n_rows = keep;
     return WFCU_OK;
 }
 

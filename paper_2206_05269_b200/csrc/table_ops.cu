@@ -30,6 +30,17 @@ __global__ void tb_compact_recs_kernel(TableView t, TokenRec* __restrict__ out, 
     }
 }
 
+// recs sorted by pos ascending: *out = first index whose pos >= value (single thread, log n steps)
+__global__ void tb_lower_bound_pos_kernel(const TokenRec* __restrict__ recs, u64 n, u64 value, u64* __restrict__ out) {
+    if (blockIdx.x || threadIdx.x) return;
+    u64 lo = 0, hi = n;
+    while (lo < hi) {
+        const u64 mid = (lo + hi) / 2;
+        if (recs[mid].pos < value) lo = mid + 1; else hi = mid;
+    }
+    *out = lo;
+}
+
 // sum of key lengths (inline keys + long records) -> *out_bytes
 __global__ void tb_key_bytes_kernel(TableView t, u64* __restrict__ out_bytes) {
     u64 local = 0;
@@ -179,6 +190,12 @@ cudaError_t tb_compact_recs(const TableView& t, TokenRec* out, u64 cap, u64* dev
     cudaError_t e = cudaMemsetAsync(dev_count, 0, sizeof(u64), s);
     if (e != cudaSuccess) return e;
     tb_compact_recs_kernel<<<grid_for(t.mask + 1, sm), 256, 0, s>>>(t, out, cap, dev_count);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+cudaError_t tb_lower_bound_pos(const TokenRec* recs, u64 n, u64 value, u64* dev_out, cudaStream_t s, u64* launches) {
+    tb_lower_bound_pos_kernel<<<1, 1, 0, s>>>(recs, n, value, dev_out);
     *launches += 1;
     return cudaGetLastError();
 }

@@ -55,3 +55,19 @@ def test_offsets_beyond_4_gib(capi, cuda, port):
     c.reset()
     c.count_dev(dsm.data_ptr(), n)
     assert c.to_dict() == port.wordcount([sample])
+
+
+@pytest.mark.parametrize("k", [0, 1, 5, 25, 1000, 10 ** 6])
+def test_device_top_k_equals_reference_order(capi, cuda, port, k):
+    """wfcu_counter_top_k (count order on the device, ties resolved exactly) == top_k over the export"""
+    import random
+    from helpers import random_text
+    corpus = capi.synth_corpus(seed=11, doc_begin=0, doc_end=3, vocab=50000, doc_bytes=1 << 19).tobytes()
+    extra = random_text(random.Random(2), 30000, "unicode") + b" " + (b"Q" * 40 + b" ") * 700 + b"zz " * 900
+    text = corpus + b" " + extra
+    dev, n = to_dev(cuda, text)
+    c = capi.Counter(table_slots=1 << 17)
+    c.count_dev(dev.data_ptr(), n)
+    want = port.top_k(port.wordcount([text]), k)
+    assert c.top_k(k) == want
+    assert capi.top_k(c.export(), k) == want
