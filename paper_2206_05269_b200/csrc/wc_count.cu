@@ -1,0 +1,519 @@
+// wc_count.cu -- fused tokenizer + counting map for sm_100a, third generation.
+//
+// Replaces, on the device, the reference's  tokenize -> normalize_word -> ++counts[word]
+// loop (/root/reference/proj/src/text.cpp:9-57, proj/src/unicode.cpp:90-121,
+// proj/src/pipeline.cpp:131-139).  Bytes are read from HBM once; tokens never reach HBM.
+//
+// The kernel is bound by instruction issue, not by HBM, so every
+// choice below is about warp-instructions per corpus byte:
+//   * a ROW is 1 KiB = two interleaved 512-byte halves; lane l owns bytes [16l,16l+16) of
+//     each half, so both 16-byte global loads of a warp are fully coalesced and both
+//     16-byte shared stores are conflict free, while the per-row bookkeeping (shuffles,
+//     prefix sum, loop control) is paid once per 1 KiB;
+//   * phase 1 classifies 4 bytes per operation (SWAR range tests, answer in bit 7 of each
+//     byte lane), folds A-Z in the same registers, and gathers the flag bits into 16-bit
+//     masks with dp4a -- integer dot products run on the FMA pipe, which byte work leaves idle;
+//     the FOLDED bytes are what the warp's shared-memory ring keeps;
+//   * token boundaries are found bit-parallel: with N = non-space bits and A = alnum bits
+//     of the fragments that END in the lane's chunk, F = A & ~(N + A) is the first word
+//     character of every fragment (the carry of the addition runs along each fragment),
+//     and the same expression on the bit-reversed masks gives the last one.  The k-th F
+//     pairs with the k-th L: a token is (position, length), no per-byte loop, no look-ahead
+//     (everything is resolved backwards from the whitespace byte that ends the fragment);
+//   * phase 2 takes one queued token per lane: unaligned fetch of the folded bytes from
+//     the ring, length mask from a table, multiply hash, one 16-byte load of a two-key
+//     bucket of the CTA-wide combiner, shared-memory atomic count.  Misses are buffered
+//     per warp and go to the global table (ATOMG.CAS.128 / RED.ADD.64) 32 at a time;
+//   * whatever byte-class logic cannot decide exactly -- a byte >= 0x80 in the fragment,
+//     a fragment whose start is out of sight, a token longer than 16 bytes -- is appended
+//     to the deferred list and handled by wc_slow_kernel (wordcount.cu), an exact
+//     restatement of the reference's UTF-8 rules.
+#include "wfcu_dev.cuh"
+
+namespace wfcu {
+
+namespace cnt3 {
+
+constexpr int kHalf = 512;                         // 32 lanes x 16 bytes
+constexpr int kRow = 2 * kHalf;
+constexpr int kGuard = 32;                         // bytes in front of a ring slot; the last 16 mirror the previous row's tail
+constexpr int kSlotStride = kGuard + kRow;         // 1056
+constexpr int kRingBytes = 2 * kSlotStride + 32;   // two slots + slack for the unaligned fetch
+constexpr int kQueueCap = 512;                     // u16 entries per warp: (len-1) << 12 | ring position, 0 = dead
+constexpr int kMissCap = 64;
+constexpr u32 kFull = 0xFFFFFFFFu;
+constexpr u64 kSlotLocked = 1ull;
+
+// ---- SWAR byte classes: bit 7 of each byte lane is the answer ----------------------
+// ASCII = true: caller guarantees no byte has bit 7 set.
+template <bool ASCII>
+__device__ __forceinline__ void classify4(u32 x, u32& s, u32& t, u32& u, u32& f) {
+    const u32 M = 0x80808080u;
+    const u32 v = ASCII ? x : (x & 0x7F7F7F7Fu);
+    const u32 y = v | 0x20202020u;
+    t = (y + 0x1F1F1F1Fu) & ~(y + 0x05050505u) & M;          // 'a'..'z' after folding
+    u = (v + 0x50505050u) & ~(v + 0x46464646u) & M;          // '0'..'9'
+    const u32 z = (v ^ 0x20202020u) + 0x7F7F7F7Fu;           // bit 7 clear <=> byte == 0x20
+    s = (~z | ((v + 0x77777777u) & ~(v + 0x72727272u))) & M; // 0x20 or 0x09..0x0D
+    if (!ASCII) { t &= ~x; u &= ~x; s &= ~x; }
+    f = x | (t >> 2);                                        // A-Z -> a-z (a-z unchanged)
+}
+
+// flags (0x80 per byte) of two words -> 128 * (8-bit mask), accumulated on the FMA pipe
+__device__ __forceinline__ u32 gather8(u32 f0, u32 f1, u32 acc) {
+    return __dp4a(f0, 0x08040201u, __dp4a(f1, 0x80402010u, acc));
+}
+
+struct Masks { u32 s7, a7, h7; };   // 16-bit masks of one 16-byte chunk, scaled by 128
+
+template <bool ASCII>
+__device__ __forceinline__ Masks classify16(const uint4& x, uint4& f) {
+    u32 s0, s1, s2, s3, t0, t1, t2, t3, u0, u1, u2, u3;
+    classify4<ASCII>(x.x, s0, t0, u0, f.x);
+    classify4<ASCII>(x.y, s1, t1, u1, f.y);
+    classify4<ASCII>(x.z, s2, t2, u2, f.z);
+    classify4<ASCII>(x.w, s3, t3, u3, f.w);
+    Masks m;
+    m.s7 = gather8(s2, s3, 0) * 256u + gather8(s0, s1, 0);
+    m.a7 = gather8(t2, t3, gather8(u2, u3, 0)) * 256u + gather8(t0, t1, gather8(u0, u1, 0));
+    m.h7 = 0;
+    if (!ASCII) {
+        const u32 M = 0x80808080u;
+        m.h7 = gather8(x.z & M, x.w & M, 0) * 256u + gather8(x.x & M, x.y & M, 0);
+    }
+    return m;
+}
+// pack the masks of the lane's two chunks: low 16 bits = half a, high 16 bits = half b
+__device__ __forceinline__ u32 pack7(u32 a7, u32 b7) { return (b7 << 9) | (a7 >> 7); }
+
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ u32 bswap32(u32 v) { return __byte_perm(v, 0, 0x0123); }
+__device__ __forceinline__ u64 le_to_be(u64 v) { return ((u64)bswap32((u32)v) << 32) | bswap32((u32)(v >> 32)); }
+
+template <int WARPS, int SETS, int MSLOTS>
+struct __align__(1024) Smem {
+    uint16_t queue[WARPS][kQueueCap];          // 1 KiB per warp, 1 KiB aligned (index wrap by OR)
+    ulonglong2 sk[SETS];                       // short combiner: two keys (tokens <= 8 bytes, little-endian) per set
+    uint2 scnt[SETS];                          //                 and their counts
+    u64 mk0[MSLOTS];                           // medium combiner (9..16 bytes): key low, key high, count
+    u64 mk1[MSLOTS];
+    u64 lomask[16];                            // [len-1] -> mask of key bytes 0..7
+    u64 himask[16];                            // [len-1] -> mask of key bytes 8..15
+    ulonglong2 miss[WARPS][kMissCap];
+    uint4 ring[WARPS][kRingBytes / 16];
+    u32 mcnt[MSLOTS];
+};
+
+// Medium tokens (9..16 bytes): 2-way, k1 is written before k0 is published.
+__device__ __forceinline__ bool medium_add(u64* __restrict__ k0s, u64* __restrict__ k1s, u32* __restrict__ cnt,
+                                           u32 mask, u64 k0, u64 k1, u32 h) {
+    u32 i = h & mask;
+#pragma unroll 1
+    for (int way = 0; way < 2; ++way) {
+        u64 c0 = *reinterpret_cast<volatile u64*>(k0s + i);
+        if (c0 == 0) {
+            c0 = atomicCAS(k0s + i, 0ull, kSlotLocked);
+            if (c0 == 0) {
+                *reinterpret_cast<volatile u64*>(k1s + i) = k1;
+                __threadfence_block();
+                atomicExch(k0s + i, k0);
+                atomicAdd(cnt + i, 1u);
+                return true;
+            }
+        }
+        if (c0 == kSlotLocked) return false;
+        if (c0 == k0 && *reinterpret_cast<volatile u64*>(k1s + i) == k1) {
+            atomicAdd(cnt + i, 1u);
+            return true;
+        }
+        i = (h >> 16) & mask;
+    }
+    return false;
+}
+
+}  // namespace cnt3
+
+using namespace cnt3;
+
+// text[0..n): documents concatenated with whitespace between them by the caller.
+// Position n acts as a whitespace byte, so does "position -1".
+template <int WARPS, int SETS, int MSLOTS>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, TableView gt) {
+    extern __shared__ uint8_t smem_raw[];
+    typedef Smem<WARPS, SETS, MSLOTS> SM;
+    const u32 sbase = (u32)__cvta_generic_to_shared(smem_raw);
+    SM& sm = *reinterpret_cast<SM*>(smem_raw + ((1024u - (sbase & 1023u)) & 1023u));
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const u32 lt_mask = (1u << lane) - 1u;
+
+    for (int i = tid; i < SETS; i += WARPS * 32) { sm.sk[i] = make_ulonglong2(0, 0); sm.scnt[i] = make_uint2(0, 0); }
+    for (int i = tid; i < MSLOTS; i += WARPS * 32) { sm.mk0[i] = 0; sm.mk1[i] = 0; sm.mcnt[i] = 0; }
+    if (tid < 16) {
+        sm.lomask[tid] = tid < 8 ? (~0ull >> (56 - 8 * tid)) : ~0ull;
+        sm.himask[tid] = tid < 8 ? 0ull : (~0ull >> (120 - 8 * tid));
+    }
+    for (int i = lane; i < kRingBytes / 16; i += 32) sm.ring[warp][i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+
+    const u32 n_rows = (u32)(n / kRow) + 1;            // the last row holds the virtual whitespace at n
+    const u32 full_rows = (u32)(n / kRow);             // rows [0, full_rows) lie entirely inside the text
+    const u32 gw = blockIdx.x * WARPS + warp;
+    const u64 rb64 = (u64)gw * rows_per_warp;
+    const u32 r_begin = rb64 < n_rows ? (u32)rb64 : n_rows;
+    const u32 r_end = (rb64 + rows_per_warp < n_rows) ? (u32)(rb64 + rows_per_warp) : n_rows;
+
+    uint8_t* ring = reinterpret_cast<uint8_t*>(sm.ring[warp]);
+    uint16_t* queue = sm.queue[warp];
+    ulonglong2* missbuf = sm.miss[warp];
+    u32 my_tokens = 0;
+    u32 qhead = 0, qtail = 0;     // token queue (warp-uniform, free running)
+    u32 mhead = 0, mtail = 0;     // miss buffer (warp-uniform, free running)
+
+    // 32 buffered keys -> global table, one key per lane
+    auto drain_misses = [&](u32 count) {
+        if (lane < count) {
+            const ulonglong2 k = missbuf[(mhead + lane) & (kMissCap - 1)];
+            table_add(gt, k.x, k.y, 1ull);
+        }
+        mhead += count;
+    };
+    auto push_misses = [&](bool miss, u64 k0, u64 k1) {
+        const u32 mm = __ballot_sync(kFull, miss);
+        if (mm) {
+            if (miss) missbuf[(mtail + __popc(mm & lt_mask)) & (kMissCap - 1)] = make_ulonglong2(k0, k1);
+            mtail += __popc(mm);
+            __syncwarp();
+            if (mtail - mhead >= 32) drain_misses(32);
+        }
+    };
+
+    // Two candidate slots in one 16-byte bucket; straight-line hit path, claims behind a
+    // warp-uniform branch (only while the table fills).  A key present in two places (two
+    // buckets can never hold it, but the global table may) is harmless: the flush adds.
+    const u32 sk_s = (u32)__cvta_generic_to_shared(sm.sk);
+    auto short_add = [&](u64 key, u32 h, bool live) -> bool {
+        const u32 set = h >> 20 & (SETS - 1);   // SETS <= 4096
+        ulonglong2 c;   // one LDS.128; a stale value only costs a redundant claim attempt (keys never change once set)
+        asm volatile("ld.shared.v2.u64 {%0,%1}, [%2];" : "=l"(c.x), "=l"(c.y) : "r"(sk_s + set * 16u));
+        const bool hit0 = c.x == key, hit1 = c.y == key;
+        u32 way = hit1 ? 1u : 0u;
+        bool found = (hit0 || hit1) && live;
+        // a valid key never has a zero low word (its first byte is a word character)
+        const bool can_claim = live && !found && ((u32)c.x == 0 || (u32)c.y == 0);
+        if (__any_sync(kFull, can_claim)) {
+            if (can_claim) {
+                u64* slot = reinterpret_cast<u64*>(&sm.sk[set]);
+                if ((u32)c.x == 0) {
+                    const u64 old = atomicCAS(slot, 0ull, key);
+                    if (old == 0 || old == key) { way = 0; found = true; }
+                }
+                if (!found) {
+                    const u64 old = atomicCAS(slot + 1, 0ull, key);
+                    if (old == 0 || old == key) { way = 1; found = true; }
+                }
+            }
+        }
+        if (found) atomicAdd(reinterpret_cast<u32*>(&sm.scnt[set]) + way, 1u);
+        return found;
+    };
+
+    // one pass of phase 2: `count` (<= 32) queued tokens, one per lane
+    auto token_pass = [&](u32 count) {
+        const u32 e = (lane < count) ? queue[(qhead + lane) & (kQueueCap - 1)] : 0u;
+        qhead += count;
+        const bool live = e != 0;
+        const u32* wp = reinterpret_cast<const u32*>(ring + (e & 0xFFCu));
+        const u32 sh = e << 3;                       // funnel shifts use the low 5 bits: (pos & 3) * 8
+        const u32 li = (e >> 9) & 0x78u;             // (len-1) * 8
+        const u32 w0 = wp[0], w1 = wp[1], w2 = wp[2];
+        u32 b0 = __funnelshift_r(w0, w1, sh);
+        u32 b1 = __funnelshift_r(w1, w2, sh);
+        const uint2 lm = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(sm.lomask) + li);
+        b0 &= lm.x; b1 &= lm.y;
+        bool miss = false;
+        u64 mk0 = 0, mk1 = 0;
+        if (!__any_sync(kFull, e >= 0x8000u)) {
+            // every token of this pass fits 8 bytes
+            const u64 key = ((u64)b1 << 32) | b0;
+            u32 h = b0 * 0x9E3779B1u + b1 * 0x85EBCA77u;
+            h ^= h >> 16;
+            h *= 0x2C1B3C6Du;
+            if (!short_add(key, h, live) && live) { miss = true; mk0 = le_to_be(key); }
+            my_tokens += live;
+        } else {
+            const u32 w3 = wp[3], w4 = wp[4];
+            u32 b2 = __funnelshift_r(w2, w3, sh);
+            u32 b3 = __funnelshift_r(w3, w4, sh);
+            const uint2 hm = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(sm.himask) + li);
+            b2 &= hm.x; b3 &= hm.y;
+            const u64 lo = ((u64)b1 << 32) | b0, hi = ((u64)b3 << 32) | b2;
+            u32 h = b0 * 0x9E3779B1u + b1 * 0x85EBCA77u;
+            h += b2 * 0xC2B2AE3Du + b3 * 0x27D4EB2Fu;
+            h ^= h >> 16;
+            h *= 0x2C1B3C6Du;
+            const bool is_medium = e >= 0x8000u;
+            bool ok = short_add(lo, h, live && !is_medium);      // votes across the warp: every lane calls it
+            if (is_medium) ok = medium_add(sm.mk0, sm.mk1, sm.mcnt, MSLOTS - 1, lo, hi, h);
+            if (live) {
+                if (!ok) { miss = true; mk0 = le_to_be(lo); mk1 = le_to_be(hi); }
+                ++my_tokens;
+            }
+        }
+        push_misses(miss, mk0, mk1);
+    };
+
+    if (r_begin < r_end) {
+        // lane's two chunks of a row: bytes [16l,16l+16) of each half; zero past n
+        auto load_row = [&](u32 row, uint4& xa, uint4& xb) {
+            if (row < full_rows) {
+                const uint4* p = reinterpret_cast<const uint4*>(text + (u64)row * kRow) + lane;
+                xa = ldg_stream(p);
+                xb = ldg_stream(p + 32);
+            } else {
+                xa = make_uint4(0, 0, 0, 0);
+                xb = xa;
+                if (row < r_end) {      // the last row of the text
+#pragma unroll
+                    for (int half = 0; half < 2; ++half) {
+                        const u64 g = (u64)row * kRow + (u64)half * kHalf + (u64)lane * 16;
+                        uint4 v = make_uint4(0, 0, 0, 0);
+                        if (g + 16 <= n) {
+                            v = *reinterpret_cast<const uint4*>(text + g);
+                        } else if (g < n) {
+                            u32 w[4] = {0, 0, 0, 0};
+                            for (u32 k = 0; k < (u32)(n - g); ++k) w[k >> 2] |= (u32)text[g + k] << (8 * (k & 3));
+                            v = make_uint4(w[0], w[1], w[2], w[3]);
+                        }
+                        if (half == 0) xa = v; else xb = v;
+                    }
+                }
+            }
+        };
+
+        // masks of the chunk in front of the strip (16 bits): "position -1" is whitespace
+        u32 carryS = 0xFFFFu, carryA = 0, carryH = 0;
+        if (r_begin > 0) {
+            // the 16 bytes in front of the strip: predecessor masks for lane 0, folded bytes for the guard
+            const uint4 x = *reinterpret_cast<const uint4*>(text + (u64)r_begin * kRow - 16);
+            uint4 f;
+            const Masks m = classify16<false>(x, f);
+            carryS = m.s7 >> 7; carryA = m.a7 >> 7; carryH = m.h7 >> 7;
+            if (lane == 0) *reinterpret_cast<uint4*>(ring + (r_begin & 1u) * kSlotStride + 16) = f;
+        }
+        uint4 nxa, nxb;
+        load_row(r_begin, nxa, nxb);
+
+        for (u32 row = r_begin; row < r_end; ++row) {
+            const uint4 xa = nxa, xb = nxb;
+            load_row(row + 1, nxa, nxb);
+            const u32 slotpos = (row & 1u) * kSlotStride;
+
+            // ------------------------------ phase 1 ------------------------------
+            u32 S, A, H = 0;
+            uint4 fa, fb;
+            const u32 anyhi = (xa.x | xa.y | xa.z | xa.w | xb.x | xb.y | xb.z | xb.w) & 0x80808080u;
+            const bool ascii_row = !__any_sync(kFull, anyhi != 0) && carryH == 0;
+            if (ascii_row) {
+                const Masks ma = classify16<true>(xa, fa), mb = classify16<true>(xb, fb);
+                S = pack7(ma.s7, mb.s7);
+                A = pack7(ma.a7, mb.a7);
+            } else {
+                const Masks ma = classify16<false>(xa, fa), mb = classify16<false>(xb, fb);
+                S = pack7(ma.s7, mb.s7);
+                A = pack7(ma.a7, mb.a7);
+                H = pack7(ma.h7, mb.h7);
+            }
+            if (row >= full_rows) {   // last row (warp-uniform): bytes at and beyond n are whitespace
+                const u64 ga = (u64)row * kRow + (u64)lane * 16, gb = ga + kHalf;
+                const u32 va = ga >= n ? 0u : (n - ga >= 16 ? 16u : (u32)(n - ga));
+                const u32 vb = gb >= n ? 0u : (n - gb >= 16 ? 16u : (u32)(n - gb));
+                S |= ((0xFFFFu << va) & 0xFFFFu) | (((0xFFFFu << vb) & 0xFFFFu) << 16);
+            }
+            uint4* slot = reinterpret_cast<uint4*>(ring + slotpos + kGuard);
+            slot[lane] = fa;
+            slot[32 + lane] = fb;
+            if (lane == 31) *reinterpret_cast<uint4*>(ring + (slotpos ^ kSlotStride) + 16) = fb;   // next row's guard
+
+            // predecessor chunks: low half = chunk in front of a, high half = chunk in front of b
+            const u32 s31 = __shfl_sync(kFull, S, 31), a31 = __shfl_sync(kFull, A, 31);
+            u32 pS = __shfl_up_sync(kFull, S, 1), pA = __shfl_up_sync(kFull, A, 1), pH = 0;
+            if (lane == 0) { pS = carryS | (s31 << 16); pA = carryA | (a31 << 16); }
+            carryS = s31 >> 16; carryA = a31 >> 16;
+            if (!ascii_row) {
+                const u32 h31 = __shfl_sync(kFull, H, 31);
+                pH = __shfl_up_sync(kFull, H, 1);
+                if (lane == 0) pH = carryH | (h31 << 16);
+                carryH = h31 >> 16;
+            }
+            // fragment ends: whitespace byte whose predecessor is not whitespace
+            const u32 E = S & ~(((S << 1) & 0xFFFEFFFEu) | ((pS >> 15) & 0x00010001u));
+            // 32-bit views, bit i = byte (chunk start - 16 + i)
+            const u32 VSa = __byte_perm(pS, S, 0x5410), VSb = __byte_perm(pS, S, 0x7632);
+            const u32 VAa = __byte_perm(pA, A, 0x5410), VAb = __byte_perm(pA, A, 0x7632);
+            const u32 Ta = E << 16, Tb = E & 0xFFFF0000u;           // ends in view coordinates
+            const u32 base_a = slotpos + kGuard + lane * 16 - 16;   // ring position of view bit 0
+            const u32 base_b = base_a + kHalf;
+
+            // A fragment that ends in the chunk but has no whitespace in the 16 bytes in front
+            // of the chunk may start out of sight: the careful loop decides end by end.
+            bool careful = !ascii_row ||
+                           __any_sync(kFull, (Ta != 0 && (pS & 0xFFFFu) == 0) || (Tb != 0 && (pS >> 16) == 0));
+            u32 total;
+            for (;;) {
+                u32 Fra = 0, Lra = 0, Frb = 0, Lrb = 0, cnt;
+                if (!careful) {
+                    // first / last word character of every fragment that ends in the chunk
+                    auto first_last = [](u32 VS, u32 VA, u32 T, u32 prev16, u32& Fr, u32& Lr) {
+                        const u32 mt = T ? ((1u << (31 - __clz(T))) - 1u) : 0u;      // below the highest end
+                        const u32 ml = (2u << (31 - __clz(prev16 | 1u))) - 1u;       // up to the last whitespace in front
+                        const u32 K = mt & ~ml;
+                        const u32 NK = ~VS & K, AK = VA & K;
+                        const u32 F = AK & ~(NK + AK);
+                        const u32 Nr = __brev(NK), Ar = __brev(AK);
+                        Lr = Ar & ~(Nr + Ar);
+                        Fr = __brev(F);
+                    };
+                    first_last(VSa, VAa, Ta, pS & 0xFFFFu, Fra, Lra);
+                    first_last(VSb, VAb, Tb, pS >> 16, Frb, Lrb);
+                    cnt = __popc(Fra) + __popc(Frb);
+                } else {
+                    cnt = __popc(E);
+                }
+                u32 incl = cnt;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const u32 v = __shfl_up_sync(kFull, incl, d);
+                    if (lane >= d) incl += v;
+                }
+                total = __shfl_sync(kFull, incl, 31);
+                if ((qtail - qhead) + total > (u32)kQueueCap) {   // pathological row (tokens of 1-2 bytes): make room first
+                    token_pass(qtail - qhead);
+                    __syncwarp();
+                }
+                u32 qi = qtail + incl - cnt;
+                if (!careful) {
+                    u32 mx = 0;
+                    auto emit_fast = [&](u32 Fr, u32 Lr, u32 base) {
+                        while (Fr) {
+                            const u32 fr = 31 - __clz(Fr), lr = 31 - __clz(Lr);
+                            Fr ^= 1u << fr;
+                            Lr ^= 1u << lr;
+                            const u32 tl1 = fr - lr;                  // length - 1
+                            mx = max(mx, tl1);
+                            queue[(qi++) & (kQueueCap - 1)] = (uint16_t)((tl1 << 12) | (base + 31 - fr));
+                        }
+                    };
+                    emit_fast(Fra, Lra, base_a);
+                    emit_fast(Frb, Lrb, base_b);
+                    if (!__any_sync(kFull, mx > 15)) break;
+                    careful = true;      // a token longer than 16 bytes: redo the row end by end
+                    continue;
+                }
+                auto emit_careful = [&](u32 VS, u32 VA, u32 VH, u32 T, u32 base, u64 gchunk) {
+                    u32 Ew = T >> 16;
+                    while (Ew) {
+                        const u32 j = __ffs(Ew) - 1;
+                        Ew &= Ew - 1;
+                        const u32 below = (0x10000u << j) - 1u;            // bits below the end
+                        const u32 sp = VS & below;
+                        const u32 start = 32 - __clz(sp);                   // first byte of the fragment (0 if sp == 0)
+                        const u32 frag = below & ~((1u << start) - 1u);
+                        const u32 a = VA & frag;
+                        u32 entry = 0;                                      // dead: no word character, or deferred
+                        bool defer = (sp == 0) || (VH & frag);
+                        if (!defer && a) {
+                            const u32 first = __ffs(a) - 1;
+                            const u32 tlen = 32 - __clz(a) - first;
+                            if (tlen > 16) defer = true;
+                            else entry = ((tlen - 1) << 12) | (base + first);
+                        }
+                        if (defer) {
+                            const u64 slot_i = atomicAdd(gt.n_deferred, 1ull);
+                            if (slot_i < gt.deferred_cap) gt.deferred[slot_i] = gchunk + j;
+                            else atomicOr(gt.status, kStatusDeferredFull);
+                        }
+                        queue[(qi++) & (kQueueCap - 1)] = (uint16_t)entry;
+                    }
+                };
+                const u64 ga = (u64)row * kRow + (u64)lane * 16;
+                emit_careful(VSa, VAa, __byte_perm(pH, H, 0x5410), Ta, base_a, ga);
+                emit_careful(VSb, VAb, __byte_perm(pH, H, 0x7632), Tb, base_b, ga + kHalf);
+                break;
+            }
+            const u32 still_carried = qtail - qhead;    // 0 if room had to be made
+            qtail += total;
+            __syncwarp();
+
+            // ------------------------------ phase 2 ------------------------------
+            // full 32-token passes; the remainder waits for the next row's tokens ...
+            u32 consumed = 0;
+            while (qtail - qhead >= 32) { token_pass(32); consumed += 32; }
+            // ... unless it would outlive its bytes in the ring (the next row overwrites the
+            // slot of the previous one)
+            if (still_carried > consumed) token_pass(qtail - qhead);
+            __syncwarp();
+        }
+        if (qtail != qhead) token_pass(qtail - qhead);
+        __syncwarp();
+        while (mtail != mhead) drain_misses(min(mtail - mhead, 32u));
+    }
+
+    // token total: one atomic per warp
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) my_tokens += __shfl_xor_sync(kFull, my_tokens, d);
+    if (lane == 0 && my_tokens) atomicAdd(gt.n_tokens, (u64)my_tokens);
+
+    // flush the combiners into the global table
+    __syncthreads();
+    for (int i = tid; i < 2 * SETS; i += WARPS * 32) {
+        const u64 k = reinterpret_cast<const u64*>(sm.sk)[i];
+        const u32 c = reinterpret_cast<const u32*>(sm.scnt)[i];
+        if (k != 0 && c) table_add(gt, le_to_be(k), 0ull, (u64)c);
+    }
+    for (int i = tid; i < MSLOTS; i += WARPS * 32) {
+        const u64 k = sm.mk0[i];
+        const u32 c = sm.mcnt[i];
+        if (k > kSlotLocked && c) table_add(gt, le_to_be(k), le_to_be(sm.mk1[i]), (u64)c);
+    }
+}
+
+// ---- host-side launcher (called from wordcount.cu) ---------------------------------
+#ifndef WFCU_COUNT_WARPS
+#define WFCU_COUNT_WARPS 28
+#endif
+#ifndef WFCU_COUNT_SETS
+#define WFCU_COUNT_SETS 4096
+#endif
+#ifndef WFCU_COUNT_MED_SLOTS
+#define WFCU_COUNT_MED_SLOTS 512
+#endif
+constexpr int kCountWarps = WFCU_COUNT_WARPS;
+constexpr int kCountSets = WFCU_COUNT_SETS;             // two 8-byte keys + two counts per set (24 bytes)
+constexpr int kCountMedSlots = WFCU_COUNT_MED_SLOTS;    // 20 bytes each
+typedef Smem<kCountWarps, kCountSets, kCountMedSlots> CountSmem;
+static_assert(sizeof(CountSmem) + 1024 <= 227 * 1024, "shared memory budget");
+static_assert(kCountSets <= 4096 && (kCountSets & (kCountSets - 1)) == 0, "set index is taken from 12 hash bits");
+static_assert(2 * kSlotStride + 20 <= 4096, "queue entries keep ring positions in 12 bits");
+
+cudaError_t wc_count_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream) {
+    const size_t smem = sizeof(CountSmem) + 1024;   // + slack for the 1 KiB alignment
+    auto kernel = wc_count_kernel<kCountWarps, kCountSets, kCountMedSlots>;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const u64 n_rows = n / kRow + 1;
+    u64 grid = (u64)sm_count;
+    if (grid * kCountWarps > n_rows) grid = (n_rows + kCountWarps - 1) / kCountWarps;   // at least one row per warp
+    if (grid == 0) grid = 1;
+    const u64 rows_per_warp = (n_rows + grid * kCountWarps - 1) / (grid * kCountWarps);
+    kernel<<<(unsigned)grid, kCountWarps * 32, smem, stream>>>(text, n, (u32)rows_per_warp, gt);
+    return cudaGetLastError();
+}
+
+}  // namespace wfcu

@@ -23,6 +23,8 @@
 //     byte >= 0x80, fragments or tokens longer than 16 bytes -- is appended to a
 //     deferred list and handled by wc_slow_kernel, an exact restatement of the
 //     reference's UTF-8 rules (one thread per fragment).
+#include <cstdlib>
+
 #include "wfcu_dev.cuh"
 
 namespace wfcu {
@@ -654,6 +656,14 @@ static_assert(sizeof(FastSmem<kFastWarps, kFastSlots, kFastMedSlots>) <= 227 * 1
 
 size_t wc_fast_smem_bytes() { return sizeof(FastSmem<kFastWarps, kFastSlots, kFastMedSlots>); }
 
+// wc_count.cu: the counting kernel (third generation).  wc_fast_kernel<.., EMIT = false> stays
+// selectable (WFCU_COUNT_KERNEL=2 in the environment) for A/B runs on the same box.
+cudaError_t wc_count_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream);
+static bool use_gen2_count_kernel() {
+    static const bool v = [] { const char* e = getenv("WFCU_COUNT_KERNEL"); return e && e[0] == '2'; }();
+    return v;
+}
+
 template <bool EMIT>
 static cudaError_t wc_launch_impl(const uint8_t* text, u64 n, const TableView& gt, const EmitView& em, int sm_count,
                                   cudaStream_t stream, u64* launches, cudaEvent_t* ev_before_fast,
@@ -671,7 +681,12 @@ static cudaError_t wc_launch_impl(const uint8_t* text, u64 n, const TableView& g
     if (grid == 0) grid = 1;
     const u64 rows_per_warp = (n_rows + grid * kFastWarps - 1) / (grid * kFastWarps);
     if (ev_before_fast) cudaEventRecord(*ev_before_fast, stream);
-    kernel<<<(unsigned)grid, kFastWarps * 32, smem, stream>>>(text, n, rows_per_warp, gt, em);
+    if (!EMIT && !use_gen2_count_kernel()) {
+        cudaError_t e = wc_count_launch(text, n, gt, sm_count, stream);
+        if (e != cudaSuccess) return e;
+    } else {
+        kernel<<<(unsigned)grid, kFastWarps * 32, smem, stream>>>(text, n, rows_per_warp, gt, em);
+    }
     if (ev_after_fast) cudaEventRecord(*ev_after_fast, stream);
     wc_slow_kernel<<<sm_count * 2, 128, 0, stream>>>(text, n, gt, em, EMIT ? 1 : 0);
     wc_reset_deferred_kernel<<<1, 1, 0, stream>>>(gt);
