@@ -28,6 +28,8 @@
 //     a fragment whose start is out of sight, a token longer than 16 bytes -- is appended
 //     to the deferred list and handled by wc_slow_kernel (wordcount.cu), an exact
 //     restatement of the reference's UTF-8 rules.
+#include <type_traits>
+
 #include "wfcu_dev.cuh"
 
 namespace wfcu {
@@ -90,6 +92,22 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
     uint4 v;
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+
+// PTX shifts clamp: a shift amount >= 32 gives 0 (C++ leaves it undefined)
+__device__ __forceinline__ u32 shr_clamp(u32 v, u32 s) {
+    u32 r;
+    asm("shr.b32 %0, %1, %2;" : "=r"(r) : "r"(v), "r"(s));
+    return r;
+}
+// warp inclusive prefix sum; the shuffle's own predicate replaces the lane compare
+__device__ __forceinline__ u32 warp_inclusive_sum(u32 v) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        asm volatile("{ .reg .pred p; .reg .u32 t; shfl.sync.up.b32 t|p, %0, %1, 0, 0xffffffff; @p add.u32 %0, %0, t; }"
+                     : "+r"(v) : "r"(d));
+    }
     return v;
 }
 
@@ -170,27 +188,40 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
     const u32 r_end = (rb64 + rows_per_warp < n_rows) ? (u32)(rb64 + rows_per_warp) : n_rows;
 
     uint8_t* ring = reinterpret_cast<uint8_t*>(sm.ring[warp]);
-    uint16_t* queue = sm.queue[warp];
-    ulonglong2* missbuf = sm.miss[warp];
-    u32 my_tokens = 0;
-    u32 qhead = 0, qtail = 0;     // token queue (warp-uniform, free running)
+    uint4* missbuf = reinterpret_cast<uint4*>(sm.miss[warp]);
+    const u32 q_s = (u32)__cvta_generic_to_shared(sm.queue[warp]);   // 1 KiB aligned: index wrap is an OR
+    u32 my_tokens = 0;            // per lane (careful rows)
+    u32 warp_tokens = 0;          // warp-uniform (fast rows)
+    u32 qhead = 0, qtail = 0;     // token queue (warp-uniform, free running, in entries)
+    u32 qrd = lane * 2;           // byte offset of this lane's entry in the next pass (free running)
     u32 mhead = 0, mtail = 0;     // miss buffer (warp-uniform, free running)
 
-    // 32 buffered keys -> global table, one key per lane
+    auto q_store = [&](u32 off2, u32 v) {
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(q_s | (off2 & (2 * kQueueCap - 2))), "r"(v) : "memory");
+    };
+    auto q_load = [&](u32 off2) {
+        u32 v;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(q_s | (off2 & (2 * kQueueCap - 2))) : "memory");
+        return v;
+    };
+
+    // 32 buffered keys (little-endian packed) -> global table, one key per lane
     auto drain_misses = [&](u32 count) {
         if (lane < count) {
-            const ulonglong2 k = missbuf[(mhead + lane) & (kMissCap - 1)];
-            table_add(gt, k.x, k.y, 1ull);
+            const uint4 k = missbuf[(mhead + lane) & (kMissCap - 1)];
+            table_add(gt, ((u64)bswap32(k.x) << 32) | bswap32(k.y), ((u64)bswap32(k.z) << 32) | bswap32(k.w), 1ull);
         }
         mhead += count;
     };
-    auto push_misses = [&](bool miss, u64 k0, u64 k1) {
+    // branch-free append; the drain is the only (warp-uniform) branch
+    auto push_misses = [&](bool miss, u32 k0, u32 k1, u32 k2, u32 k3) {
         const u32 mm = __ballot_sync(kFull, miss);
-        if (mm) {
-            if (miss) missbuf[(mtail + __popc(mm & lt_mask)) & (kMissCap - 1)] = make_ulonglong2(k0, k1);
-            mtail += __popc(mm);
+        const u32 at = (mtail + __popc(mm & lt_mask)) & (kMissCap - 1);
+        if (miss) missbuf[at] = make_uint4(k0, k1, k2, k3);
+        mtail += __popc(mm);
+        if (mtail - mhead >= 32) {
             __syncwarp();
-            if (mtail - mhead >= 32) drain_misses(32);
+            drain_misses(32);
         }
     };
 
@@ -198,19 +229,20 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
     // warp-uniform branch (only while the table fills).  A key present in two places (two
     // buckets can never hold it, but the global table may) is harmless: the flush adds.
     const u32 sk_s = (u32)__cvta_generic_to_shared(sm.sk);
-    auto short_add = [&](u64 key, u32 h, bool live) -> bool {
-        const u32 set = h >> 20 & (SETS - 1);   // SETS <= 4096
-        ulonglong2 c;   // one LDS.128; a stale value only costs a redundant claim attempt (keys never change once set)
-        asm volatile("ld.shared.v2.u64 {%0,%1}, [%2];" : "=l"(c.x), "=l"(c.y) : "r"(sk_s + set * 16u));
-        const bool hit0 = c.x == key, hit1 = c.y == key;
+    auto short_add = [&](u32 b0, u32 b1, u32 h, bool live) -> bool {
+        const u32 set = (h >> 20) & (SETS - 1);   // SETS <= 4096
+        u32 c0l, c0h, c1l, c1h;   // one LDS.128; a stale value only costs a redundant claim attempt (keys never change once set)
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(c0l), "=r"(c0h), "=r"(c1l), "=r"(c1h) : "r"(sk_s + set * 16u));
+        const bool hit0 = c0l == b0 && c0h == b1, hit1 = c1l == b0 && c1h == b1;
         u32 way = hit1 ? 1u : 0u;
         bool found = (hit0 || hit1) && live;
         // a valid key never has a zero low word (its first byte is a word character)
-        const bool can_claim = live && !found && ((u32)c.x == 0 || (u32)c.y == 0);
+        const bool can_claim = live && !found && (c0l == 0 || c1l == 0);
         if (__any_sync(kFull, can_claim)) {
             if (can_claim) {
+                const u64 key = ((u64)b1 << 32) | b0;
                 u64* slot = reinterpret_cast<u64*>(&sm.sk[set]);
-                if ((u32)c.x == 0) {
+                if (c0l == 0) {
                     const u64 old = atomicCAS(slot, 0ull, key);
                     if (old == 0 || old == key) { way = 0; found = true; }
                 }
@@ -220,13 +252,16 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
                 }
             }
         }
-        if (found) atomicAdd(reinterpret_cast<u32*>(&sm.scnt[set]) + way, 1u);
+        if (found) atomicAdd(reinterpret_cast<u32*>(sm.scnt) + set * 2u + way, 1u);   // ATOMS.POPC.INC
         return found;
     };
 
-    // one pass of phase 2: `count` (<= 32) queued tokens, one per lane
-    auto token_pass = [&](u32 count) {
-        const u32 e = (lane < count) ? queue[(qhead + lane) & (kQueueCap - 1)] : 0u;
+    // one pass of phase 2: `count` (<= 32) queued tokens, one per lane.  general = some
+    // queued token may be longer than 8 bytes (warp-uniform, decided per row).
+    auto token_pass = [&](auto full, u32 count, bool general) {
+        u32 e = q_load(qrd);
+        if (!decltype(full)::value && lane >= count) e = 0;
+        qrd += 2 * count;
         qhead += count;
         const bool live = e != 0;
         const u32* wp = reinterpret_cast<const u32*>(ring + (e & 0xFFCu));
@@ -237,37 +272,31 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
         u32 b1 = __funnelshift_r(w1, w2, sh);
         const uint2 lm = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(sm.lomask) + li);
         b0 &= lm.x; b1 &= lm.y;
-        bool miss = false;
-        u64 mk0 = 0, mk1 = 0;
-        if (!__any_sync(kFull, e >= 0x8000u)) {
+        if (!general) {
             // every token of this pass fits 8 bytes
-            const u64 key = ((u64)b1 << 32) | b0;
-            u32 h = b0 * 0x9E3779B1u + b1 * 0x85EBCA77u;
-            h ^= h >> 16;
-            h *= 0x2C1B3C6Du;
-            if (!short_add(key, h, live) && live) { miss = true; mk0 = le_to_be(key); }
-            my_tokens += live;
+            const u32 h = b0 * 0x9E3779B1u + b1 * 0x85EBCA77u;
+            const bool ok = short_add(b0, b1, h, live);
+            push_misses(live && !ok, b0, b1, 0u, 0u);
         } else {
             const u32 w3 = wp[3], w4 = wp[4];
             u32 b2 = __funnelshift_r(w2, w3, sh);
             u32 b3 = __funnelshift_r(w3, w4, sh);
             const uint2 hm = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(sm.himask) + li);
             b2 &= hm.x; b3 &= hm.y;
-            const u64 lo = ((u64)b1 << 32) | b0, hi = ((u64)b3 << 32) | b2;
-            u32 h = b0 * 0x9E3779B1u + b1 * 0x85EBCA77u;
-            h += b2 * 0xC2B2AE3Du + b3 * 0x27D4EB2Fu;
-            h ^= h >> 16;
-            h *= 0x2C1B3C6Du;
             const bool is_medium = e >= 0x8000u;
-            bool ok = short_add(lo, h, live && !is_medium);      // votes across the warp: every lane calls it
-            if (is_medium) ok = medium_add(sm.mk0, sm.mk1, sm.mcnt, MSLOTS - 1, lo, hi, h);
-            if (live) {
-                if (!ok) { miss = true; mk0 = le_to_be(lo); mk1 = le_to_be(hi); }
-                ++my_tokens;
+            u32 h = b0 * 0x9E3779B1u + b1 * 0x85EBCA77u;
+            bool ok = short_add(b0, b1, h, live && !is_medium);      // votes across the warp: every lane calls it
+            if (is_medium) {
+                h += b2 * 0xC2B2AE3Du + b3 * 0x27D4EB2Fu;
+                h ^= h >> 16;
+                h *= 0x2C1B3C6Du;
+                ok = medium_add(sm.mk0, sm.mk1, sm.mcnt, MSLOTS - 1, ((u64)b1 << 32) | b0, ((u64)b3 << 32) | b2, h);
             }
+            push_misses(live && !ok, b0, b1, b2, b3);
         }
-        push_misses(miss, mk0, mk1);
     };
+    const std::true_type kFullPass{};
+    const std::false_type kPartialPass{};
 
     if (r_begin < r_end) {
         // lane's two chunks of a row: bytes [16l,16l+16) of each half; zero past n
@@ -299,6 +328,7 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
 
         // masks of the chunk in front of the strip (16 bits): "position -1" is whitespace
         u32 carryS = 0xFFFFu, carryA = 0, carryH = 0;
+        bool general_prev = false;
         if (r_begin > 0) {
             // the 16 bytes in front of the strip: predecessor masks for lane 0, folded bytes for the guard
             const uint4 x = *reinterpret_cast<const uint4*>(text + (u64)r_begin * kRow - 16);
@@ -344,7 +374,7 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
             // predecessor chunks: low half = chunk in front of a, high half = chunk in front of b
             const u32 s31 = __shfl_sync(kFull, S, 31), a31 = __shfl_sync(kFull, A, 31);
             u32 pS = __shfl_up_sync(kFull, S, 1), pA = __shfl_up_sync(kFull, A, 1), pH = 0;
-            if (lane == 0) { pS = carryS | (s31 << 16); pA = carryA | (a31 << 16); }
+            if (lane == 0) { pS = __byte_perm(carryS, s31, 0x5410); pA = __byte_perm(carryA, a31, 0x5410); }
             carryS = s31 >> 16; carryA = a31 >> 16;
             if (!ascii_row) {
                 const u32 h31 = __shfl_sync(kFull, H, 31);
@@ -358,21 +388,22 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
             const u32 VSa = __byte_perm(pS, S, 0x5410), VSb = __byte_perm(pS, S, 0x7632);
             const u32 VAa = __byte_perm(pA, A, 0x5410), VAb = __byte_perm(pA, A, 0x7632);
             const u32 Ta = E << 16, Tb = E & 0xFFFF0000u;           // ends in view coordinates
+            const u32 prev_a = pS & 0xFFFFu, prev_b = pS >> 16;     // whitespace of the 16 bytes in front of each chunk
             const u32 base_a = slotpos + kGuard + lane * 16 - 16;   // ring position of view bit 0
             const u32 base_b = base_a + kHalf;
 
             // A fragment that ends in the chunk but has no whitespace in the 16 bytes in front
             // of the chunk may start out of sight: the careful loop decides end by end.
-            bool careful = !ascii_row ||
-                           __any_sync(kFull, (Ta != 0 && (pS & 0xFFFFu) == 0) || (Tb != 0 && (pS >> 16) == 0));
+            bool careful = !ascii_row || __any_sync(kFull, (Ta != 0 && prev_a == 0) || (Tb != 0 && prev_b == 0));
+            bool general_row = true;
             u32 total;
             for (;;) {
                 u32 Fra = 0, Lra = 0, Frb = 0, Lrb = 0, cnt;
                 if (!careful) {
                     // first / last word character of every fragment that ends in the chunk
                     auto first_last = [](u32 VS, u32 VA, u32 T, u32 prev16, u32& Fr, u32& Lr) {
-                        const u32 mt = T ? ((1u << (31 - __clz(T))) - 1u) : 0u;      // below the highest end
-                        const u32 ml = (2u << (31 - __clz(prev16 | 1u))) - 1u;       // up to the last whitespace in front
+                        const u32 mt = shr_clamp(0x7FFFFFFFu, __clz(T));        // below the highest end (0 if none)
+                        const u32 ml = shr_clamp(0xFFFFFFFFu, __clz(prev16));   // up to the last whitespace in front
                         const u32 K = mt & ~ml;
                         const u32 NK = ~VS & K, AK = VA & K;
                         const u32 F = AK & ~(NK + AK);
@@ -380,39 +411,40 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
                         Lr = Ar & ~(Nr + Ar);
                         Fr = __brev(F);
                     };
-                    first_last(VSa, VAa, Ta, pS & 0xFFFFu, Fra, Lra);
-                    first_last(VSb, VAb, Tb, pS >> 16, Frb, Lrb);
+                    first_last(VSa, VAa, Ta, prev_a, Fra, Lra);
+                    first_last(VSb, VAb, Tb, prev_b, Frb, Lrb);
                     cnt = __popc(Fra) + __popc(Frb);
                 } else {
                     cnt = __popc(E);
                 }
-                u32 incl = cnt;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const u32 v = __shfl_up_sync(kFull, incl, d);
-                    if (lane >= d) incl += v;
-                }
+                const u32 incl = warp_inclusive_sum(cnt);
                 total = __shfl_sync(kFull, incl, 31);
                 if ((qtail - qhead) + total > (u32)kQueueCap) {   // pathological row (tokens of 1-2 bytes): make room first
-                    token_pass(qtail - qhead);
+                    token_pass(kPartialPass, qtail - qhead, true);
                     __syncwarp();
                 }
-                u32 qi = qtail + incl - cnt;
+                u32 qwr = (qtail + incl - cnt) * 2;               // byte offset of this lane's first entry
                 if (!careful) {
                     u32 mx = 0;
                     auto emit_fast = [&](u32 Fr, u32 Lr, u32 base) {
                         while (Fr) {
-                            const u32 fr = 31 - __clz(Fr), lr = 31 - __clz(Lr);
-                            Fr ^= 1u << fr;
-                            Lr ^= 1u << lr;
-                            const u32 tl1 = fr - lr;                  // length - 1
+                            const u32 cf = __clz(Fr), cl = __clz(Lr);      // view positions of the first / last word character
+                            Fr ^= 0x80000000u >> cf;
+                            Lr ^= 0x80000000u >> cl;
+                            const u32 tl1 = cl - cf;                        // length - 1
                             mx = max(mx, tl1);
-                            queue[(qi++) & (kQueueCap - 1)] = (uint16_t)((tl1 << 12) | (base + 31 - fr));
+                            q_store(qwr, (tl1 << 12) | (base + cf));
+                            qwr += 2;
                         }
                     };
                     emit_fast(Fra, Lra, base_a);
                     emit_fast(Frb, Lrb, base_b);
-                    if (!__any_sync(kFull, mx > 15)) break;
+                    const u32 longest = __reduce_max_sync(kFull, mx);
+                    if (longest <= 15) {
+                        general_row = longest > 7;
+                        warp_tokens += total;
+                        break;
+                    }
                     careful = true;      // a token longer than 16 bytes: redo the row end by end
                     continue;
                 }
@@ -432,14 +464,15 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
                             const u32 first = __ffs(a) - 1;
                             const u32 tlen = 32 - __clz(a) - first;
                             if (tlen > 16) defer = true;
-                            else entry = ((tlen - 1) << 12) | (base + first);
+                            else { entry = ((tlen - 1) << 12) | (base + first); ++my_tokens; }
                         }
                         if (defer) {
                             const u64 slot_i = atomicAdd(gt.n_deferred, 1ull);
                             if (slot_i < gt.deferred_cap) gt.deferred[slot_i] = gchunk + j;
                             else atomicOr(gt.status, kStatusDeferredFull);
                         }
-                        queue[(qi++) & (kQueueCap - 1)] = (uint16_t)entry;
+                        q_store(qwr, entry);
+                        qwr += 2;
                     }
                 };
                 const u64 ga = (u64)row * kRow + (u64)lane * 16;
@@ -453,14 +486,16 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
 
             // ------------------------------ phase 2 ------------------------------
             // full 32-token passes; the remainder waits for the next row's tokens ...
+            const bool general = general_row || general_prev;   // leftovers are at most one row old
+            general_prev = general_row;
             u32 consumed = 0;
-            while (qtail - qhead >= 32) { token_pass(32); consumed += 32; }
+            while (qtail - qhead >= 32) { token_pass(kFullPass, 32u, general); consumed += 32; }
             // ... unless it would outlive its bytes in the ring (the next row overwrites the
             // slot of the previous one)
-            if (still_carried > consumed) token_pass(qtail - qhead);
+            if (still_carried > consumed) token_pass(kPartialPass, qtail - qhead, general);
             __syncwarp();
         }
-        if (qtail != qhead) token_pass(qtail - qhead);
+        if (qtail != qhead) token_pass(kPartialPass, qtail - qhead, true);
         __syncwarp();
         while (mtail != mhead) drain_misses(min(mtail - mhead, 32u));
     }
@@ -468,7 +503,7 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
     // token total: one atomic per warp
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) my_tokens += __shfl_xor_sync(kFull, my_tokens, d);
-    if (lane == 0 && my_tokens) atomicAdd(gt.n_tokens, (u64)my_tokens);
+    if (lane == 0 && (my_tokens + warp_tokens)) atomicAdd(gt.n_tokens, (u64)my_tokens + warp_tokens);
 
     // flush the combiners into the global table
     __syncthreads();
