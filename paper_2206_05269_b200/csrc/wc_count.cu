@@ -234,25 +234,21 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
         u32 c0l, c0h, c1l, c1h;   // one LDS.128; a stale value only costs a redundant claim attempt (keys never change once set)
         asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(c0l), "=r"(c0h), "=r"(c1l), "=r"(c1h) : "r"(sk_s + set * 16u));
         const bool hit0 = c0l == b0 && c0h == b1, hit1 = c1l == b0 && c1h == b1;
-        u32 way = hit1 ? 1u : 0u;
-        bool found = (hit0 || hit1) && live;
-        // a valid key never has a zero low word (its first byte is a word character)
+        const bool found = (hit0 || hit1) && live;
+        if (found) atomicAdd(reinterpret_cast<u32*>(sm.scnt) + set * 2u + (hit1 ? 1u : 0u), 1u);   // ATOMS.POPC.INC
+        // Claim an empty slot for FUTURE occurrences (a valid key never has a zero low word:
+        // its first byte is a word character).  This occurrence still goes to the global table,
+        // so nothing flows out of the rare branch and the hit path stays straight-line.
         const bool can_claim = live && !found && (c0l == 0 || c1l == 0);
         if (__any_sync(kFull, can_claim)) {
             if (can_claim) {
                 const u64 key = ((u64)b1 << 32) | b0;
                 u64* slot = reinterpret_cast<u64*>(&sm.sk[set]);
-                if (c0l == 0) {
-                    const u64 old = atomicCAS(slot, 0ull, key);
-                    if (old == 0 || old == key) { way = 0; found = true; }
-                }
-                if (!found) {
-                    const u64 old = atomicCAS(slot + 1, 0ull, key);
-                    if (old == 0 || old == key) { way = 1; found = true; }
-                }
+                u64 old = 1;
+                if (c0l == 0) old = atomicCAS(slot, 0ull, key);
+                if (old != 0 && old != key) atomicCAS(slot + 1, 0ull, key);
             }
         }
-        if (found) atomicAdd(reinterpret_cast<u32*>(sm.scnt) + set * 2u + way, 1u);   // ATOMS.POPC.INC
         return found;
     };
 
@@ -293,6 +289,65 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
                 ok = medium_add(sm.mk0, sm.mk1, sm.mcnt, MSLOTS - 1, ((u64)b1 << 32) | b0, ((u64)b3 << 32) | b2, h);
             }
             push_misses(live && !ok, b0, b1, b2, b3);
+        }
+    };
+    // Two full passes at once (64 queued tokens, two per lane), short tokens only: the two
+    // dependency chains (queue -> ring -> bucket -> atomic) interleave, which is worth more
+    // than occupancy on this latency-bound stretch of the kernel.
+    auto token_pass2 = [&]() {
+        const u32 e0 = q_load(qrd), e1 = q_load(qrd + 64);
+        qrd += 128;
+        qhead += 64;
+        const u32* wp0 = reinterpret_cast<const u32*>(ring + (e0 & 0xFFCu));
+        const u32* wp1 = reinterpret_cast<const u32*>(ring + (e1 & 0xFFCu));
+        const u32 x0 = wp0[0], x1 = wp0[1], x2 = wp0[2];
+        const u32 y0 = wp1[0], y1 = wp1[1], y2 = wp1[2];
+        const uint2 lm0 = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(sm.lomask) + ((e0 >> 9) & 0x78u));
+        const uint2 lm1 = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(sm.lomask) + ((e1 >> 9) & 0x78u));
+        const u32 a0 = __funnelshift_r(x0, x1, e0 << 3) & lm0.x, a1 = __funnelshift_r(x1, x2, e0 << 3) & lm0.y;
+        const u32 b0 = __funnelshift_r(y0, y1, e1 << 3) & lm1.x, b1 = __funnelshift_r(y1, y2, e1 << 3) & lm1.y;
+        const u32 seta = ((a0 * 0x9E3779B1u + a1 * 0x85EBCA77u) >> 20) & (SETS - 1);
+        const u32 setb = ((b0 * 0x9E3779B1u + b1 * 0x85EBCA77u) >> 20) & (SETS - 1);
+        u32 p0, p1, p2, p3, r0, r1, r2, r3;
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(p0), "=r"(p1), "=r"(p2), "=r"(p3) : "r"(sk_s + seta * 16u));
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(sk_s + setb * 16u));
+        const bool ha0 = p0 == a0 && p1 == a1, ha1 = p2 == a0 && p3 == a1;
+        const bool hb0 = r0 == b0 && r1 == b1, hb1 = r2 == b0 && r3 == b1;
+        const bool live0 = e0 != 0, live1 = e1 != 0;
+        const bool fa = (ha0 || ha1) && live0, fb = (hb0 || hb1) && live1;
+        if (fa) atomicAdd(reinterpret_cast<u32*>(sm.scnt) + seta * 2u + (ha1 ? 1u : 0u), 1u);
+        if (fb) atomicAdd(reinterpret_cast<u32*>(sm.scnt) + setb * 2u + (hb1 ? 1u : 0u), 1u);
+        const bool ca = live0 && !fa && (p0 == 0 || p2 == 0), cb = live1 && !fb && (r0 == 0 || r2 == 0);
+        if (__any_sync(kFull, ca || cb)) {
+            if (ca) {
+                const u64 key = ((u64)a1 << 32) | a0;
+                u64* slot = reinterpret_cast<u64*>(&sm.sk[seta]);
+                u64 old = 1;
+                if (p0 == 0) old = atomicCAS(slot, 0ull, key);
+                if (old != 0 && old != key) atomicCAS(slot + 1, 0ull, key);
+            }
+            if (cb) {
+                const u64 key = ((u64)b1 << 32) | b0;
+                u64* slot = reinterpret_cast<u64*>(&sm.sk[setb]);
+                u64 old = 1;
+                if (r0 == 0) old = atomicCAS(slot, 0ull, key);
+                if (old != 0 && old != key) atomicCAS(slot + 1, 0ull, key);
+            }
+        }
+        // both miss lists in one append
+        const bool m0 = live0 && !fa, m1 = live1 && !fb;
+        const u32 mm0 = __ballot_sync(kFull, m0), mm1 = __ballot_sync(kFull, m1);
+        const u32 n0 = __popc(mm0);
+        if ((mtail - mhead) + n0 + __popc(mm1) > (u32)kMissCap) {   // rare: make room for up to 64 new keys
+            __syncwarp();
+            drain_misses(mtail - mhead);
+        }
+        if (m0) missbuf[(mtail + __popc(mm0 & lt_mask)) & (kMissCap - 1)] = make_uint4(a0, a1, 0u, 0u);
+        if (m1) missbuf[(mtail + n0 + __popc(mm1 & lt_mask)) & (kMissCap - 1)] = make_uint4(b0, b1, 0u, 0u);
+        mtail += n0 + __popc(mm1);
+        while (mtail - mhead >= 32) {
+            __syncwarp();
+            drain_misses(32);
         }
     };
     const std::true_type kFullPass{};
@@ -425,20 +480,21 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
                 }
                 u32 qwr = (qtail + incl - cnt) * 2;               // byte offset of this lane's first entry
                 if (!careful) {
+                    // one token of each half per trip: two independent chains, half the branches
                     u32 mx = 0;
-                    auto emit_fast = [&](u32 Fr, u32 Lr, u32 base) {
-                        while (Fr) {
-                            const u32 cf = __clz(Fr), cl = __clz(Lr);      // view positions of the first / last word character
-                            Fr ^= 0x80000000u >> cf;
-                            Lr ^= 0x80000000u >> cl;
-                            const u32 tl1 = cl - cf;                        // length - 1
-                            mx = max(mx, tl1);
-                            q_store(qwr, (tl1 << 12) | (base + cf));
-                            qwr += 2;
-                        }
-                    };
-                    emit_fast(Fra, Lra, base_a);
-                    emit_fast(Frb, Lrb, base_b);
+                    u32 qa = qwr, qb = qwr + 2 * __popc(Fra);
+                    while (Fra | Frb) {
+                        const u32 cfa = __clz(Fra), cla = __clz(Lra);     // view positions of the first / last word character
+                        const u32 cfb = __clz(Frb), clb = __clz(Lrb);     // (32 when the half has run out: every term below is 0)
+                        const u32 ta = cla - cfa, tb = clb - cfb;          // length - 1
+                        if (Fra) { q_store(qa, (ta << 12) | (base_a + cfa)); qa += 2; }
+                        if (Frb) { q_store(qb, (tb << 12) | (base_b + cfb)); qb += 2; }
+                        mx = max(mx, max(ta, tb));
+                        Fra ^= shr_clamp(0x80000000u, cfa);
+                        Lra ^= shr_clamp(0x80000000u, cla);
+                        Frb ^= shr_clamp(0x80000000u, cfb);
+                        Lrb ^= shr_clamp(0x80000000u, clb);
+                    }
                     const u32 longest = __reduce_max_sync(kFull, mx);
                     if (longest <= 15) {
                         general_row = longest > 7;
@@ -489,6 +545,9 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
             const bool general = general_row || general_prev;   // leftovers are at most one row old
             general_prev = general_row;
             u32 consumed = 0;
+            if (!general) {
+                while (qtail - qhead >= 64) { token_pass2(); consumed += 64; }
+            }
             while (qtail - qhead >= 32) { token_pass(kFullPass, 32u, general); consumed += 32; }
             // ... unless it would outlive its bytes in the ring (the next row overwrites the
             // slot of the previous one)
