@@ -1,0 +1,95 @@
+"""GPU parity for the paths specific to the third-generation counting kernel (csrc/wc_count.cu):
+1 KiB rows made of two interleaved 512-byte halves, the 32-byte guard in front of a ring slot,
+the bit-parallel first/last-word-character emission and its end-by-end fallback, the 512-entry
+token queue and the two-token passes.  Oracle: the C restatement of serial_wordcount
+(/root/reference/proj/src/pipeline.cpp:131-139, text.cpp:9-57).  Bit-exact.
+"""
+import random
+
+import pytest
+
+from helpers import gpu_wordcount, random_text, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def check(capi, cuda, port, text, **cfg):
+    got, stats = gpu_wordcount(capi, cuda, [text], **cfg)
+    want = port.wordcount([text])
+    assert got == want
+    assert stats[1] == sum(want.values())
+
+
+@pytest.mark.parametrize("sep", [b" ", b"\n", b" \t"])
+def test_dense_one_byte_tokens_overflow_the_queue(capi, cuda, port, sep):
+    """'a b c ...': up to 512 fragment ends per 1 KiB row, more than the queue holds next to
+    the leftovers of the previous row"""
+    rng = random.Random(5)
+    text = sep.join(bytes([rng.choice(b"abcdefghij0123XYZ")]) for _ in range(40000))
+    check(capi, cuda, port, text)
+    check(capi, cuda, port, b"x" * 700 + b" " + text)     # a deferred fragment in front
+
+
+@pytest.mark.parametrize("shift", [0, 1, 15, 16, 17, 495, 496, 497, 511, 512, 513, 1007, 1008, 1009, 1023, 1024, 1025])
+def test_tokens_across_half_and_row_boundaries(capi, cuda, port, shift):
+    """tokens of length 1..18 (with and without edge punctuation) placed so that they straddle the
+    16-byte chunks, the 512-byte halves and the 1 KiB rows of the kernel at every phase"""
+    rng = random.Random(shift)
+    parts = []
+    for rep in range(6):
+        for ln in range(1, 19):
+            word = bytes(rng.choice(b"abcdefgXYZ0189") for _ in range(ln))
+            parts.append(rng.choice([b"", b"(", b"\"'", b"--"]) + word + rng.choice([b"", b".", b",", b"!?)", b"..."]))
+    rng.shuffle(parts)
+    text = b"q" * shift + b" " + b" ".join(parts)
+    check(capi, cuda, port, text)
+
+
+def test_sixteen_byte_tokens_and_seventeen(capi, cuda, port):
+    """16 bytes is the longest token the fast path keeps; 17 takes the row's end-by-end redo and
+    the slow kernel.  Both next to the guard (row start) and in the middle of a row."""
+    w16 = [b"abcdefghijklmnop", b"ABCDEFGHIJKLMNOP", b"a--------------b", b"0123456789abcdef"]
+    w17 = [b"abcdefghijklmnopq", b"a---------------b"]
+    rng = random.Random(16)
+    for lead in (0, 3, 1008 - 17, 1024 - 16, 1024 - 8, 1024, 2048 - 1):
+        parts = [b"z" * lead] if lead else []
+        for _ in range(300):
+            parts.append(rng.choice(w16 + w17 + [b"the", b"of", b"x"]) + rng.choice([b"", b".", b"--"]))
+        check(capi, cuda, port, b" ".join(parts))
+
+
+def test_fragment_with_one_word_character_at_its_start(capi, cuda, port):
+    """'a---------------' (16 bytes, token 'a'): its ring position is the lowest a token can have"""
+    text = b" ".join([b"a" + b"-" * 15, b"b" + b"." * 14, b"--c", b"d"] * 400)
+    for lead in (0, 1, 15, 16, 1023):
+        check(capi, cuda, port, b"k" * lead + (b" " if lead else b"") + text)
+
+
+@pytest.mark.parametrize("vocab,docs", [(50000, 6), (1000000, 6)])
+def test_synthetic_corpus_many_rows_per_warp(capi, cuda, port, vocab, docs):
+    """6 MiB: every warp of the grid walks several rows, leftovers cross rows, 9-byte words
+    (1M vocabulary) take the general passes"""
+    corpus = capi.synth_corpus(seed=3, doc_begin=0, doc_end=docs, vocab=vocab)
+    dev, n = to_dev(cuda, corpus)
+    counter = capi.Counter(table_slots=1 << 21)
+    counter.count_dev(dev.data_ptr(), n)
+    assert counter.to_dict() == port.wordcount([corpus])
+
+
+@pytest.mark.parametrize("size", [1023, 1024, 1025, 2047, 2048, 2049, 28 * 1024 - 1, 28 * 1024, 28 * 1024 + 1, 300007])
+@pytest.mark.parametrize("flavour", ["ascii", "unicode"])
+def test_sizes_around_row_multiples(capi, cuda, port, size, flavour):
+    rng = random.Random(size ^ 0x55)
+    check(capi, cuda, port, random_text(rng, size, flavour))
+    check(capi, cuda, port, random_text(rng, size - 1, flavour) + b"z")      # last byte is a word character
+
+
+def test_non_ascii_rows_between_ascii_rows(capi, cuda, port):
+    """the carried >=0x80 mask: a non-ASCII byte in the last chunk of a row, the fragment ends in the next"""
+    rng = random.Random(77)
+    base = bytearray(random_text(rng, 8192, "ascii"))
+    for pos in (1023, 1022, 1008, 2047, 511, 512, 3071, 4095):
+        t = bytearray(base)
+        t[pos - 1:pos + 1] = "é".encode()
+        t[pos + 1] = ord("x")
+        check(capi, cuda, port, bytes(t))
