@@ -391,8 +391,8 @@ def run_b200(args) -> None:
                        "parallelism": f"document shard d mod {world}" + (", hash-partitioned all-to-all merge" if world > 1 else ""),
                        "l2": "inputs (1 GB per GPU) larger than the 126 MB L2; no flush needed"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak if peak else None, "traffic": ncu_traffic("wc_fast_kernel", nbytes),
-                         "kernel": "wc_fast_kernel", "kernel_ms": k_ms, "kernel_launches": kernel_launches,
+                         "frac": achieved / peak if peak else None, "traffic": ncu_traffic("wc_count_kernel", nbytes),
+                         "kernel": "wc_count_kernel", "kernel_ms": k_ms, "kernel_launches": kernel_launches,
                          "algorithmic_bytes_per_launch": nbytes, "peak_source": peak_src},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": d2h,
                     "steps": e2e_steps, "api": "wfcu_counter_count_host + wfcu_counter_export"},

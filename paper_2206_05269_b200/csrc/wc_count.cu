@@ -124,6 +124,7 @@ struct __align__(1024) Smem {
     u64 lomask[16];                            // [len-1] -> mask of key bytes 0..7
     u64 himask[16];                            // [len-1] -> mask of key bytes 8..15
     ulonglong2 miss[WARPS][kMissCap];
+    uint4 landing[WARPS][32];                  // where the global slot keys of a drain in flight arrive (cp.async)
     uint4 ring[WARPS][kRingBytes / 16];
     u32 mcnt[MSLOTS];
 };
@@ -205,24 +206,62 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
         return v;
     };
 
-    // 32 buffered keys (little-endian packed) -> global table, one key per lane
-    auto drain_misses = [&](u32 count) {
-        if (lane < count) {
-            const uint4 k = missbuf[(mhead + lane) & (kMissCap - 1)];
-            table_add(gt, ((u64)bswap32(k.x) << 32) | bswap32(k.y), ((u64)bswap32(k.z) << 32) | bswap32(k.w), 1ull);
+    // ---- misses -> global table ------------------------------------------------------
+    // Keys wait in the warp's miss buffer (little-endian packed).  Every lane owns one drain
+    // slot; a round (a) finishes what landed: the slot holds the lane's key -> one RED.ADD.64
+    // on its count; another key -> next slot of the probe sequence, still in flight; an empty
+    // slot (first global occurrence) or a long probe sequence -> table_add from scratch; and
+    // (b) hands buffered keys to the free lanes: key -> registers, slot index from the hash,
+    // cp.async of the slot's 16-byte key into the lane's landing word.  No register waits on
+    // the L2 round trip, which overlaps the passes between two rounds.
+    uint4* landing = sm.landing[warp];
+    u32 dk0 = 0, dk1 = 0, dk2 = 0, dk3 = 0;         // the lane's key in flight (big-endian words)
+    u32 didx = 0, dleft = 0;                        // slot being fetched; probes left (0 = lane free)
+    auto drain_round = [&]() {
+        const u32 dst = (u32)__cvta_generic_to_shared(landing + lane);
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        if (dleft) {
+            const uint4 cur = landing[lane];        // {k0 low, k0 high, k1 low, k1 high}
+            if (cur.x == dk1 && cur.y == dk0 && cur.z == dk3 && cur.w == dk2) {
+                atomicAdd(&gt.slots[didx].count, 1ull);
+                dleft = 0;
+            } else if ((cur.x | cur.y) == 0 || --dleft == 0) {
+                table_add(gt, ((u64)dk0 << 32) | dk1, ((u64)dk2 << 32) | dk3, 1ull);
+                dleft = 0;
+            } else {
+                didx = (didx + 1) & (u32)gt.mask;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gt.slots + didx) : "memory");
+            }
         }
-        mhead += count;
+        __syncwarp();                               // miss-buffer entries were written by other lanes
+        const u32 freem = __ballot_sync(kFull, dleft == 0);
+        const u32 avail = mtail - mhead;
+        const u32 rank = __popc(freem & lt_mask);
+        if (dleft == 0 && rank < avail) {
+            const uint4 k = missbuf[(mhead + rank) & (kMissCap - 1)];
+            dk0 = bswap32(k.x); dk1 = bswap32(k.y); dk2 = bswap32(k.z); dk3 = bswap32(k.w);
+            didx = mix32(((u64)dk0 << 32) | dk1, ((u64)dk2 << 32) | dk3) & (u32)gt.mask;
+            dleft = 3;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gt.slots + didx) : "memory");
+        }
+        mhead += min((u32)__popc(freem), avail);
+        asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    // branch-free append; the drain is the only (warp-uniform) branch
+    // called between passes
+    auto drain_step = [&]() {
+        if (mtail - mhead >= 32) drain_round();
+    };
+    // room for `extra` more keys (rare: more than one miss in two tokens for a while)
+    auto make_room = [&](u32 extra) {
+        while ((mtail - mhead) + extra > (u32)kMissCap) drain_round();
+    };
+    // branch-free append
     auto push_misses = [&](bool miss, u32 k0, u32 k1, u32 k2, u32 k3) {
         const u32 mm = __ballot_sync(kFull, miss);
+        if ((mtail - mhead) + __popc(mm) > (u32)kMissCap) make_room(__popc(mm));
         const u32 at = (mtail + __popc(mm & lt_mask)) & (kMissCap - 1);
         if (miss) missbuf[at] = make_uint4(k0, k1, k2, k3);
         mtail += __popc(mm);
-        if (mtail - mhead >= 32) {
-            __syncwarp();
-            drain_misses(32);
-        }
     };
 
     // Two candidate slots in one 16-byte bucket; straight-line hit path, claims behind a
@@ -230,7 +269,7 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
     // buckets can never hold it, but the global table may) is harmless: the flush adds.
     const u32 sk_s = (u32)__cvta_generic_to_shared(sm.sk);
     auto short_add = [&](u32 b0, u32 b1, u32 h, bool live) -> bool {
-        const u32 set = (h >> 20) & (SETS - 1);   // SETS <= 4096
+        const u32 set = __umulhi(h, (u32)SETS);
         u32 c0l, c0h, c1l, c1h;   // one LDS.128; a stale value only costs a redundant claim attempt (keys never change once set)
         asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(c0l), "=r"(c0h), "=r"(c1l), "=r"(c1h) : "r"(sk_s + set * 16u));
         const bool hit0 = c0l == b0 && c0h == b1, hit1 = c1l == b0 && c1h == b1;
@@ -306,8 +345,8 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
         const uint2 lm1 = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(sm.lomask) + ((e1 >> 9) & 0x78u));
         const u32 a0 = __funnelshift_r(x0, x1, e0 << 3) & lm0.x, a1 = __funnelshift_r(x1, x2, e0 << 3) & lm0.y;
         const u32 b0 = __funnelshift_r(y0, y1, e1 << 3) & lm1.x, b1 = __funnelshift_r(y1, y2, e1 << 3) & lm1.y;
-        const u32 seta = ((a0 * 0x9E3779B1u + a1 * 0x85EBCA77u) >> 20) & (SETS - 1);
-        const u32 setb = ((b0 * 0x9E3779B1u + b1 * 0x85EBCA77u) >> 20) & (SETS - 1);
+        const u32 seta = __umulhi(a0 * 0x9E3779B1u + a1 * 0x85EBCA77u, (u32)SETS);
+        const u32 setb = __umulhi(b0 * 0x9E3779B1u + b1 * 0x85EBCA77u, (u32)SETS);
         u32 p0, p1, p2, p3, r0, r1, r2, r3;
         asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(p0), "=r"(p1), "=r"(p2), "=r"(p3) : "r"(sk_s + seta * 16u));
         asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(sk_s + setb * 16u));
@@ -338,17 +377,10 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
         const bool m0 = live0 && !fa, m1 = live1 && !fb;
         const u32 mm0 = __ballot_sync(kFull, m0), mm1 = __ballot_sync(kFull, m1);
         const u32 n0 = __popc(mm0);
-        if ((mtail - mhead) + n0 + __popc(mm1) > (u32)kMissCap) {   // rare: make room for up to 64 new keys
-            __syncwarp();
-            drain_misses(mtail - mhead);
-        }
+        if ((mtail - mhead) + n0 + __popc(mm1) > (u32)kMissCap) make_room(n0 + __popc(mm1));
         if (m0) missbuf[(mtail + __popc(mm0 & lt_mask)) & (kMissCap - 1)] = make_uint4(a0, a1, 0u, 0u);
         if (m1) missbuf[(mtail + n0 + __popc(mm1 & lt_mask)) & (kMissCap - 1)] = make_uint4(b0, b1, 0u, 0u);
         mtail += n0 + __popc(mm1);
-        while (mtail - mhead >= 32) {
-            __syncwarp();
-            drain_misses(32);
-        }
     };
     const std::true_type kFullPass{};
     const std::false_type kPartialPass{};
@@ -546,9 +578,9 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
             general_prev = general_row;
             u32 consumed = 0;
             if (!general) {
-                while (qtail - qhead >= 64) { token_pass2(); consumed += 64; }
+                while (qtail - qhead >= 64) { token_pass2(); consumed += 64; drain_step(); }
             }
-            while (qtail - qhead >= 32) { token_pass(kFullPass, 32u, general); consumed += 32; }
+            while (qtail - qhead >= 32) { token_pass(kFullPass, 32u, general); consumed += 32; drain_step(); }
             // ... unless it would outlive its bytes in the ring (the next row overwrites the
             // slot of the previous one)
             if (still_carried > consumed) token_pass(kPartialPass, qtail - qhead, general);
@@ -556,7 +588,7 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
         }
         if (qtail != qhead) token_pass(kPartialPass, qtail - qhead, true);
         __syncwarp();
-        while (mtail != mhead) drain_misses(min(mtail - mhead, 32u));
+        while (mtail != mhead || __any_sync(kFull, dleft != 0)) drain_round();
     }
 
     // token total: one atomic per warp
@@ -583,17 +615,16 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
 #define WFCU_COUNT_WARPS 28
 #endif
 #ifndef WFCU_COUNT_SETS
-#define WFCU_COUNT_SETS 4096
+#define WFCU_COUNT_SETS 3840
 #endif
 #ifndef WFCU_COUNT_MED_SLOTS
-#define WFCU_COUNT_MED_SLOTS 512
+#define WFCU_COUNT_MED_SLOTS 256
 #endif
 constexpr int kCountWarps = WFCU_COUNT_WARPS;
 constexpr int kCountSets = WFCU_COUNT_SETS;             // two 8-byte keys + two counts per set (24 bytes)
 constexpr int kCountMedSlots = WFCU_COUNT_MED_SLOTS;    // 20 bytes each
 typedef Smem<kCountWarps, kCountSets, kCountMedSlots> CountSmem;
 static_assert(sizeof(CountSmem) + 1024 <= 227 * 1024, "shared memory budget");
-static_assert(kCountSets <= 4096 && (kCountSets & (kCountSets - 1)) == 0, "set index is taken from 12 hash bits");
 static_assert(2 * kSlotStride + 20 <= 4096, "queue entries keep ring positions in 12 bits");
 
 cudaError_t wc_count_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream) {
