@@ -101,6 +101,11 @@ __device__ __forceinline__ u32 shr_clamp(u32 v, u32 s) {
     asm("shr.b32 %0, %1, %2;" : "=r"(r) : "r"(v), "r"(s));
     return r;
 }
+__device__ __forceinline__ u32 shl_clamp(u32 v, u32 s) {
+    u32 r;
+    asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(v), "r"(s));
+    return r;
+}
 // warp inclusive prefix sum; the shuffle's own predicate replaces the lane compare
 __device__ __forceinline__ u32 warp_inclusive_sum(u32 v) {
 #pragma unroll
@@ -488,15 +493,14 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
                 u32 Fra = 0, Lra = 0, Frb = 0, Lrb = 0, cnt;
                 if (!careful) {
                     // first / last word character of every fragment that ends in the chunk
-                    auto first_last = [](u32 VS, u32 VA, u32 T, u32 prev16, u32& Fr, u32& Lr) {
+                    auto first_last = [](u32 VS, u32 VA, u32 T, u32 prev16, u32& F, u32& Lr) {
                         const u32 mt = shr_clamp(0x7FFFFFFFu, __clz(T));        // below the highest end (0 if none)
                         const u32 ml = shr_clamp(0xFFFFFFFFu, __clz(prev16));   // up to the last whitespace in front
                         const u32 K = mt & ~ml;
                         const u32 NK = ~VS & K, AK = VA & K;
-                        const u32 F = AK & ~(NK + AK);
+                        F = AK & ~(NK + AK);                                    // first word characters, view order
                         const u32 Nr = __brev(NK), Ar = __brev(AK);
-                        Lr = Ar & ~(Nr + Ar);
-                        Fr = __brev(F);
+                        Lr = Ar & ~(Nr + Ar);                                   // last word characters, bit-reversed
                     };
                     first_last(VSa, VAa, Ta, prev_a, Fra, Lra);
                     first_last(VSb, VAb, Tb, prev_b, Frb, Lrb);
@@ -512,20 +516,23 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
                 }
                 u32 qwr = (qtail + incl - cnt) * 2;               // byte offset of this lane's first entry
                 if (!careful) {
-                    // one token of each half per trip: two independent chains, half the branches
+                    // One token of each half per trip (two independent chains, half the branches):
+                    // the k-th lowest bit of F pairs with the k-th highest bit of Lr.
                     u32 mx = 0;
                     u32 qa = qwr, qb = qwr + 2 * __popc(Fra);
                     while (Fra | Frb) {
-                        const u32 cfa = __clz(Fra), cla = __clz(Lra);     // view positions of the first / last word character
-                        const u32 cfb = __clz(Frb), clb = __clz(Lrb);     // (32 when the half has run out: every term below is 0)
-                        const u32 ta = cla - cfa, tb = clb - cfb;          // length - 1
-                        if (Fra) { q_store(qa, (ta << 12) | (base_a + cfa)); qa += 2; }
-                        if (Frb) { q_store(qb, (tb << 12) | (base_b + cfb)); qb += 2; }
+                        const u32 lba = Fra & (0u - Fra), lbb = Frb & (0u - Frb);       // lowest set bits
+                        const u32 fpa = 31 - __clz(lba), fpb = 31 - __clz(lbb);        // view position of the first word character
+                        const u32 hla = 31 - __clz(Lra), hlb = 31 - __clz(Lrb);        // 31 - view position of the last one
+                        const u32 ta = Fra ? 31u - hla - fpa : 0u;                     // length - 1
+                        const u32 tb = Frb ? 31u - hlb - fpb : 0u;
+                        if (Fra) { q_store(qa, ta * 4096u + (base_a + fpa)); qa += 2; }
+                        if (Frb) { q_store(qb, tb * 4096u + (base_a + kHalf + fpb)); qb += 2; }
                         mx = max(mx, max(ta, tb));
-                        Fra ^= shr_clamp(0x80000000u, cfa);
-                        Lra ^= shr_clamp(0x80000000u, cla);
-                        Frb ^= shr_clamp(0x80000000u, cfb);
-                        Lrb ^= shr_clamp(0x80000000u, clb);
+                        Fra ^= lba;
+                        Frb ^= lbb;
+                        Lra ^= shl_clamp(1u, hla);
+                        Lrb ^= shl_clamp(1u, hlb);
                     }
                     const u32 longest = __reduce_max_sync(kFull, mx);
                     if (longest <= 15) {
