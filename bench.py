@@ -351,7 +351,7 @@ def run_b200(args) -> None:
 
     # ---- end to end through the host-buffer call (pinned staging, H2D, count, export D2H) ------
     arr = host.numpy()
-    docs = [arr[i * DOC_BYTES:(i + 1) * DOC_BYTES] for i in range(len(my_docs))]
+    docs = capi.HostDocs([arr[i * DOC_BYTES:(i + 1) * DOC_BYTES] for i in range(len(my_docs))])   # pointer/length arrays, built once
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     d2h = 0
 

@@ -41,6 +41,30 @@ __global__ void tb_lower_bound_pos_kernel(const TokenRec* __restrict__ recs, u64
     *out = lo;
 }
 
+// Export of the ordered table, packed on the device: key length of every record ...
+__device__ __forceinline__ u32 key_len_fast(u64 k0, u64 k1) {
+    // bytes are packed first-byte-most-significant and zero padded; a key never ends in NUL
+    return k1 ? 16u - ((u32)(__ffsll((long long)k1) - 1) >> 3) : 8u - ((u32)(__ffsll((long long)k0) - 1) >> 3);
+}
+__global__ void tb_export_lens_kernel(const TokenRec* __restrict__ recs, u64 n, u64* __restrict__ lens) {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        lens[i] = key_len_fast(recs[i].k0, recs[i].k1);
+}
+// ... then, with the exclusive scan of the lengths, the key bytes back to back, the lengths and the counts
+__global__ void tb_export_pack_kernel(const TokenRec* __restrict__ recs, u64 n, const u64* __restrict__ offs,
+                                      uint8_t* __restrict__ bytes, u32* __restrict__ lens32, u64* __restrict__ counts,
+                                      u64* __restrict__ total_bytes) {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const TokenRec r = recs[i];
+        const u32 len = key_len_fast(r.k0, r.k1);
+        uint8_t* out = bytes + offs[i];
+        for (u32 b = 0; b < len; ++b) out[b] = (uint8_t)((b < 8 ? r.k0 >> (56 - 8 * b) : r.k1 >> (120 - 8 * b)) & 0xFF);
+        lens32[i] = len;
+        counts[i] = r.pos;
+        if (i + 1 == n) *total_bytes = offs[i] + len;
+    }
+}
+
 // sum of key lengths (inline keys + long records) -> *out_bytes
 __global__ void tb_key_bytes_kernel(TableView t, u64* __restrict__ out_bytes) {
     u64 local = 0;
@@ -190,6 +214,21 @@ cudaError_t tb_compact_recs(const TableView& t, TokenRec* out, u64 cap, u64* dev
     cudaError_t e = cudaMemsetAsync(dev_count, 0, sizeof(u64), s);
     if (e != cudaSuccess) return e;
     tb_compact_recs_kernel<<<grid_for(t.mask + 1, sm), 256, 0, s>>>(t, out, cap, dev_count);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+cudaError_t exclusive_scan_u64(const u64* in, u64* out, u64 n, u64* tmp, cudaStream_t s, u64* launches);   // tokens.cu
+
+// recs (ordered) -> packed key bytes, lengths, counts; lens64 is scratch of n u64, tmp of scan_tmp_words(n)
+cudaError_t tb_export_pack(const TokenRec* recs, u64 n, u64* lens64, u64* tmp, uint8_t* bytes, u32* lens32, u64* counts,
+                           u64* dev_total_bytes, int sm, cudaStream_t s, u64* launches) {
+    if (n == 0) return cudaMemsetAsync(dev_total_bytes, 0, sizeof(u64), s);
+    tb_export_lens_kernel<<<grid_for(n, sm), 256, 0, s>>>(recs, n, lens64);
+    *launches += 1;
+    cudaError_t e = exclusive_scan_u64(lens64, lens64, n, tmp, s, launches);
+    if (e != cudaSuccess) return e;
+    tb_export_pack_kernel<<<grid_for(n, sm), 256, 0, s>>>(recs, n, lens64, bytes, lens32, counts, dev_total_bytes);
     *launches += 1;
     return cudaGetLastError();
 }
