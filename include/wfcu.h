@@ -139,12 +139,14 @@ WFCU_API int wfcu_counter_count_dev(wfcu_counter* c, const uint8_t* dev_text, ui
 
 /* Host-buffer form (what wfc::serial_wordcount / run_wordcount call): packs the
  * documents with '\n' separators into pinned staging memory, copies them to the
- * device in chunks overlapped with counting, and waits for completion. */
+ * device in chunks overlapped with counting, and waits for completion.  Documents
+ * that lie back to back in page-locked memory and end in ASCII whitespace are not
+ * packed: the copy engine streams them from the caller's buffer at PCIe speed. */
 WFCU_API int wfcu_counter_count_host(wfcu_counter* c, const uint8_t* const* docs, const uint64_t* doc_lens,
                             uint64_t n_docs);
 
 /* Measurement hook: with timing enabled every wfcu_counter_count_dev brackets its
- * dominant kernel (wc_fast_kernel) with CUDA events on the launching stream;
+ * dominant kernel (wc_count_kernel) with CUDA events on the launching stream;
  * take_kernel_ms waits for them and returns the summed device time and the
  * number of launches since the last call. */
 WFCU_API int wfcu_counter_set_timing(wfcu_counter* c, int enabled);
