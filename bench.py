@@ -269,7 +269,7 @@ def run_b200(args) -> None:
     import torch.distributed as dist
 
     from paper_2206_05269_b200 import capi
-    from paper_2206_05269_b200.exchange import DeviceOps, hash_partition_merge
+    from paper_2206_05269_b200.exchange import AsyncExchange, DeviceOps, ExchangeOverflow, hash_partition_merge
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -301,12 +301,20 @@ def run_b200(args) -> None:
     ops = DeviceOps(torch, device)
     stream = torch.cuda.current_stream(device).cuda_stream
 
+    # N > 1: the merge runs without a host synchronisation per step (fixed-capacity regions, sizes read
+    # on the device); its sticky overflow / long-token flags are read once, inside the timed region,
+    # after the K steps -- if they are raised the run is repeated with the synchronising merge.
+    ax = AsyncExchange(local, ops, dist, entries_hint=w["vocab"]) if world > 1 and not args.sync_exchange else None
+
     def step():
         local.reset(stream)
         local.count_dev(dev.data_ptr(), nbytes, stream)
         if world > 1:
             owned.reset(stream)
-            hash_partition_merge(local, owned, ops, dist)
+            if ax is not None:
+                ax.step(local, owned)
+            else:
+                hash_partition_merge(local, owned, ops, dist)
 
     def barrier():
         torch.cuda.synchronize()
@@ -318,6 +326,15 @@ def run_b200(args) -> None:
         step()
     barrier()
     local.status(stream)
+    if ax is not None:
+        try:
+            ax.finish()
+        except ExchangeOverflow as e:      # collective decision: the flags were all-reduced
+            if rank == 0:
+                print(f"warning: {e}; using the synchronising merge", file=sys.stderr)
+            ax = None
+            step()
+            barrier()
 
     # ---- resident-data timing: exactly K steps, CUDA events, max over ranks --------------------
     launches0 = capi.launch_count()
@@ -329,6 +346,8 @@ def run_b200(args) -> None:
         e0.record()
         for _ in range(args.steps):
             step()
+        if ax is not None:
+            ax.finish()     # raises if a step left anything behind (none did in the warm-up)
         e1.record()
         barrier()
     total_ms = e0.elapsed_time(e1)
@@ -361,7 +380,7 @@ def run_b200(args) -> None:
         local.count_host(docs)
         if world > 1:
             owned.reset(stream)
-            hash_partition_merge(local, owned, ops, dist)
+            hash_partition_merge(local, owned, ops, dist)     # the synchronising form: one-shot use
             torch.cuda.synchronize()
         blob, lens, counts = (owned if world > 1 else local).export()
         d2h = blob.nbytes + lens.nbytes + counts.nbytes
@@ -388,7 +407,7 @@ def run_b200(args) -> None:
             "config": {"workload": w["name"], "vocab": w["vocab"], "zipf_s": ZIPF_S, "doc_bytes": DOC_BYTES,
                        "seed": SEED, "documents": total_docs, "bytes_per_gpu": nbytes, "job_bytes": job_bytes,
                        "tokens": job_tokens, "distinct_words": job_distinct,
-                       "parallelism": f"document shard d mod {world}" + (", hash-partitioned all-to-all merge" if world > 1 else ""),
+                       "parallelism": f"document shard d mod {world}" + (", hash-partitioned all-to-all merge" + (" (no host sync per step)" if ax is not None else "") if world > 1 else ""),
                        "l2": "inputs (1 GB per GPU) larger than the 126 MB L2; no flush needed"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if peak else None, "traffic": ncu_traffic("wc_count_kernel", nbytes),
@@ -443,6 +462,8 @@ def main() -> None:
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3")
     ap.add_argument("--docs", type=int, default=None, help="override document count (per GPU for cfg3, total for cfg4)")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--sync-exchange", action="store_true",
+                    help="N > 1: use the merge that reads the region sizes on the host every step")
     ap.add_argument("--sample-docs", type=int, default=None, help="reference arm: documents per step")
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
                     help="collective backend at N > 1 (gloo only for single-GPU testing of the N > 1 path)")

@@ -208,6 +208,20 @@ WFCU_API int wfcu_counter_partition(wfcu_counter* c, uint32_t n_parts, wfcu_entr
 /* Upper bound of the number of inline entries the table can hold (its load limit). */
 WFCU_API uint64_t wfcu_counter_max_entries(const wfcu_counter* c);
 
+/* Synchronisation-free form of the same exchange step (replaces, like wfcu_counter_partition,
+ * plan_partition + encode_outgoing of proj/src/shuffle.cpp:9-66): partition p owns the fixed
+ * region dev_entries[p * cap_per_part, (p+1) * cap_per_part), so the all-to-all needs no sizes
+ * from the host.  dev_counts has n_parts + 2 words: [p] = entries of partition p (reset by the
+ * call); [n_parts] += long tokens in the table and [n_parts + 1] += entries that did not fit --
+ * sticky flags the caller reads once, after any number of steps.  Asynchronous on `stream`. */
+WFCU_API int wfcu_counter_partition_fixed(wfcu_counter* c, uint32_t n_parts, wfcu_entry* dev_entries,
+                                 uint64_t cap_per_part, uint64_t* dev_counts, void* stream);
+/* The receiving side (replaces merge_sorted + reduce_sorted + merge_counts, proj/src/shuffle.cpp:75-96,
+ * proj/src/reduce.cpp:8-21,83-89): adds the first min(dev_region_counts[p], cap_per_part) entries of
+ * every region; the counts are read on the device.  Asynchronous on `stream`. */
+WFCU_API int wfcu_counter_merge_regions(wfcu_counter* c, const wfcu_entry* dev_entries, uint32_t n_parts,
+                               uint64_t cap_per_part, const uint64_t* dev_region_counts, void* stream);
+
 /* Inserts n received entries (summing counts of equal keys). Asynchronous. */
 WFCU_API int wfcu_counter_merge_entries(wfcu_counter* c, const wfcu_entry* dev_entries, uint64_t n, void* stream);
 

@@ -115,6 +115,41 @@ __global__ void tb_partition_scatter_kernel(TableView t, u32 n_parts, u64* __res
     }
 }
 
+// One-pass form for the synchronisation-free exchange: partition p owns the fixed region
+// out[p * cap, (p+1) * cap); counts[p] = entries written, counts[n_parts] += long tokens in
+// the table, counts[n_parts + 1] += entries that did not fit (both sticky flags for the host).
+__global__ void tb_partition_fixed_kernel(TableView t, u32 n_parts, u64 cap, Slot* __restrict__ out,
+                                          u64* __restrict__ counts) {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= t.mask; i += (u64)gridDim.x * blockDim.x) {
+        const Slot s = t.slots[i];
+        if (s.k0 != 0) {
+            const u32 p = owner_mix32(s.k0, s.k1) % n_parts;
+            const u64 j = atomicAdd(&counts[p], 1ull);
+            if (j < cap) out[(u64)p * cap + j] = Slot{s.k0, s.k1, s.count, 0};
+            else atomicAdd(&counts[n_parts + 1], 1ull);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && *t.n_long) atomicAdd(&counts[n_parts], *t.n_long);
+}
+// counts[key] += count for the first min(region_counts[p], cap) entries of every region
+__global__ void tb_merge_regions_kernel(TableView t, const Slot* __restrict__ in, u32 n_parts, u64 cap,
+                                        const u64* __restrict__ region_counts) {
+    u64 tokens = 0;
+    const u64 total = (u64)n_parts * cap;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (u64)gridDim.x * blockDim.x) {
+        const u64 p = i / cap, j = i - p * cap;
+        if (j < region_counts[p]) {
+            const Slot s = in[i];
+            if (s.k0 != 0 && s.count != 0) {
+                table_add(t, s.k0, s.k1, s.count);
+                tokens += s.count;
+            }
+        }
+    }
+    for (int d = 16; d > 0; d >>= 1) tokens += __shfl_xor_sync(0xFFFFFFFFu, tokens, d);
+    if ((threadIdx.x & 31) == 0 && tokens) atomicAdd(t.n_tokens, tokens);
+}
+
 // counts[key] += count for n received entries; also accounts the tokens
 __global__ void tb_merge_entries_kernel(TableView t, const Slot* __restrict__ in, u64 n) {
     u64 tokens = 0;
@@ -257,6 +292,23 @@ cudaError_t tb_partition(const TableView& t, u32 n_parts, Slot* out, u64 cap, u6
     tb_partition_scan_kernel<<<1, 32, 0, s>>>(dev_part_counts, n_parts, cursors);
     tb_partition_scatter_kernel<<<g, 256, 0, s>>>(t, n_parts, cursors, out, cap);
     *launches += 3;
+    return cudaGetLastError();
+}
+
+cudaError_t tb_partition_fixed(const TableView& t, u32 n_parts, u64 cap, Slot* out, u64* dev_counts, int sm,
+                               cudaStream_t s, u64* launches) {
+    cudaError_t e = cudaMemsetAsync(dev_counts, 0, sizeof(u64) * n_parts, s);   // the two flags stay sticky
+    if (e != cudaSuccess) return e;
+    tb_partition_fixed_kernel<<<grid_for(t.mask + 1, sm), 256, 0, s>>>(t, n_parts, cap, out, dev_counts);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+cudaError_t tb_merge_regions(const TableView& t, const Slot* in, u32 n_parts, u64 cap, const u64* region_counts, int sm,
+                             cudaStream_t s, u64* launches) {
+    if (n_parts == 0 || cap == 0) return cudaSuccess;
+    tb_merge_regions_kernel<<<grid_for((u64)n_parts * cap, sm), 256, 0, s>>>(t, in, n_parts, cap, region_counts);
+    *launches += 1;
     return cudaGetLastError();
 }
 

@@ -61,6 +61,12 @@ class DeviceOps:
         if records.numel():
             counter.merge_long_records(records.data_ptr(), records.numel(), part, n_parts, self.stream())
 
+    def partition_fixed(self, counter, n_parts: int, entries, cap_per_part: int, counts) -> None:
+        counter.partition_fixed(n_parts, entries.data_ptr(), cap_per_part, counts.data_ptr(), self.stream())
+
+    def merge_regions(self, counter, entries, n_parts: int, cap_per_part: int, counts) -> None:
+        counter.merge_regions(entries.data_ptr(), n_parts, cap_per_part, counts.data_ptr(), self.stream())
+
     def empty_entries(self, n: int):
         t = self.torch
         return t.empty((max(n, 1), ENTRY_WORDS), dtype=t.int64, device=self.device)
@@ -128,6 +134,57 @@ def hash_partition_merge(local, owned, ops, dist, group=None, force_collectives:
             if long_sizes[r]:
                 ops.merge_long_records(owned, gathered[r * width:r * width + long_sizes[r]], rank, world)
     return ExchangeStats(n_send, n_recv, n_send * 8 * ENTRY_WORDS, long_total)
+
+
+class ExchangeOverflow(RuntimeError):
+    """A synchronisation-free step could not carry everything: redo it with hash_partition_merge."""
+
+
+class AsyncExchange:
+    """The same merge with NO host synchronisation per step, for pipelines that count and merge
+    repeatedly (bench.py's N>1 step): partition p of the local table is scattered into a region of
+    fixed capacity, so both all-to-alls (region sizes, then the regions themselves) have
+    host-independent shapes and the receiving kernel reads the sizes on the device.  What the
+    fixed shapes cannot carry -- a region that overflows, tokens longer than 16 bytes (their
+    variable-length record stream needs sizes on the host) -- raises sticky device flags that
+    finish() reads ONCE, after any number of steps; the caller then falls back to
+    hash_partition_merge for those steps.
+
+    entries_hint: expected distinct words of a local table (regions hold 2x the uniform share);
+    default = the table's capacity, which can never overflow."""
+
+    def __init__(self, local, ops, dist, group=None, entries_hint: int | None = None):
+        self.ops, self.dist, self.group = ops, dist, group
+        self.world = dist.get_world_size(group)
+        bound = local.max_entries()
+        want = bound if entries_hint is None else min(bound, 2 * ((entries_hint + self.world - 1) // self.world) + 1024)
+        self.cap = max(int(want), 16)
+        t = ops.torch
+        self.send = ops.empty_entries(self.world * self.cap)
+        self.recv = ops.empty_entries(self.world * self.cap)
+        self.counts = t.zeros(self.world + 2, dtype=t.int64, device=self.send.device)
+        self.recv_counts = t.zeros(self.world, dtype=t.int64, device=self.send.device)
+        self.steps = 0
+
+    def step(self, local, owned) -> None:
+        """Collective.  Asynchronous on the current stream: returns before anything has run."""
+        ops, world = self.ops, self.world
+        ops.partition_fixed(local, world, self.send, self.cap, self.counts)
+        self.dist.all_to_all_single(self.recv_counts, self.counts[:world], group=self.group)
+        self.dist.all_to_all_single(self.recv, self.send, group=self.group)
+        ops.merge_regions(owned, self.recv, world, self.cap, self.recv_counts)
+        self.steps += 1
+
+    def finish(self) -> None:
+        """The one host read: raises ExchangeOverflow if any step since the last finish() left
+        something behind (on any rank), and clears the flags."""
+        flags = self.counts[self.world:self.world + 2].clone()
+        self.dist.all_reduce(flags, group=self.group)
+        long_tokens, overflow = (int(v) for v in flags.cpu().tolist())
+        self.counts[self.world:].zero_()
+        if overflow or long_tokens:
+            raise ExchangeOverflow(f"{overflow} entries beyond the region capacity {self.cap}, "
+                                   f"{long_tokens} tokens longer than 16 bytes in {self.steps} steps")
 
 
 def allreduce_scalar(partial, dist, group=None, reproducible: bool = True):

@@ -10,7 +10,8 @@ t0 = time.time()
 corpus = capi.synth_corpus(1, 0, docs, vocab)
 print(f"corpus {corpus.size/1e9:.3f} GB generated in {time.time()-t0:.1f}s", flush=True)
 dev = torch.from_numpy(corpus).cuda()
-counter = capi.Counter(table_slots=(1 << 20) if vocab <= 100000 else (1 << 22))
+slots = int(os.environ.get("SLOTS_LOG2", "0")) or (20 if vocab <= 100000 else 22)
+counter = capi.Counter(table_slots=1 << slots)
 s = torch.cuda.current_stream().cuda_stream
 def step():
     counter.reset(s)

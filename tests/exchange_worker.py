@@ -19,12 +19,16 @@ import torch.distributed as dist
 import oracle
 from helpers import random_text
 from paper_2206_05269_b200 import capi
-from paper_2206_05269_b200.exchange import allreduce_scalar, hash_partition_merge, shard_documents
+from paper_2206_05269_b200.exchange import (AsyncExchange, ExchangeOverflow, allreduce_scalar, hash_partition_merge,
+                                            shard_documents)
 
 
 class DictCounter:
     def __init__(self):
         self.table = {}
+
+    def max_entries(self):
+        return 4096
 
 
 def key_words(word: bytes):
@@ -74,6 +78,24 @@ class OracleOps:
                 counter.table[w] = counter.table.get(w, 0) + c
             off += 16 + ln + (-ln % 8)
 
+    def partition_fixed(self, counter, n_parts, entries, cap, counts):
+        counts[:n_parts] = 0
+        for w, c in counter.table.items():
+            if len(w) > 16:
+                counts[n_parts] += 1
+                continue
+            p = capi.owner_of(w, n_parts)
+            j = int(counts[p])
+            counts[p] += 1
+            if j < cap:
+                entries[p * cap + j] = torch.tensor([*key_words(w), c, 0], dtype=torch.int64)
+            else:
+                counts[n_parts + 1] += 1
+
+    def merge_regions(self, counter, entries, n_parts, cap, counts):
+        for p in range(n_parts):
+            self.merge_entries(counter, entries[p * cap:(p + 1) * cap], min(int(counts[p]), cap))
+
     def empty_entries(self, n):
         return torch.zeros((max(n, 1), 4), dtype=torch.int64)
 
@@ -94,6 +116,28 @@ def main():
     stats = hash_partition_merge(local, owned, OracleOps(), dist)
     gathered = [None] * world
     dist.all_gather_object(gathered, {k.hex(): v for k, v in owned.table.items()})
+    # the synchronisation-free form: two steps on the short-token part of the same tables, one finish()
+    short = DictCounter()
+    short.table = {w: c for w, c in local.table.items() if len(w) <= 16}
+    ax = AsyncExchange(short, OracleOps(), dist, entries_hint=len(port.wordcount(docs)))
+    own_a, own_b = DictCounter(), DictCounter()
+    ax.step(short, own_a)
+    ax.step(short, own_b)
+    ax.finish()
+    async_ok = own_a.table == own_b.table == {w: c for w, c in owned.table.items() if len(w) <= 16}
+    # a long token, or regions that are too small, must be reported by finish() on EVERY rank
+    raised = 0
+    for tables, hint in ((local, None), (short, 1)):
+        bad = AsyncExchange(tables, OracleOps(), dist, entries_hint=hint)
+        if hint == 1:
+            bad.cap = 2
+            bad.send = bad.send[:world * 2]
+            bad.recv = bad.recv[:world * 2]
+        bad.step(tables, DictCounter())
+        try:
+            bad.finish()
+        except ExchangeOverflow:
+            raised += 1
     # scalar reduction: both modes
     part = torch.tensor([0.1 * (rank + 1)], dtype=torch.float64)
     s1 = float(allreduce_scalar(part, dist, reproducible=True))
@@ -108,7 +152,8 @@ def main():
                 merged[w] = v
         want = port.wordcount(docs)
         print(json.dumps({"equal": merged == want, "disjoint": ok_disjoint, "owner": ok_owner, "distinct": len(want),
-                          "sent": stats.sent_entries, "scalar": [s1, s2], "world": world}), flush=True)
+                          "sent": stats.sent_entries, "scalar": [s1, s2], "world": world,
+                          "async_equal": async_ok, "async_raised": raised}), flush=True)
     dist.barrier()
     dist.destroy_process_group()
 

@@ -31,6 +31,7 @@ def test_hash_partition_merge_over_gloo(world):
     res = json.loads(outs[0][0].strip().splitlines()[-1])
     assert res["equal"] and res["disjoint"] and res["owner"] and res["world"] == world
     assert res["distinct"] > 100
+    assert res["async_equal"] and res["async_raised"] == 2     # AsyncExchange: same tables; both failure flags reported
     expect = sum(0.1 * (r + 1) for r in range(world))
     assert abs(res["scalar"][0] - expect) < 1e-12 and abs(res["scalar"][1] - expect) < 1e-12
 

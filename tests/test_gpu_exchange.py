@@ -151,6 +151,36 @@ def test_nccl_collective_path_with_one_rank(capi, cuda, port):
         st = hash_partition_merge(local, owned, DeviceOps(torch, torch.device("cuda", 0)), dist, force_collectives=True)
         torch.cuda.synchronize()
         assert owned.to_dict() == oracle.port().wordcount([text])
+        # the synchronisation-free form: long tokens raise the sticky flag ...
+        from paper_2206_05269_b200.exchange import AsyncExchange, ExchangeOverflow
+        ops = DeviceOps(torch, torch.device("cuda", 0))
+        ax = AsyncExchange(local, ops, dist)
+        own2 = capi.Counter(table_slots=1 << 15)
+        ax.step(local, own2)
+        try:
+            ax.finish(); raise SystemExit("long tokens were not reported")
+        except ExchangeOverflow:
+            pass
+        # ... a corpus without them merges exactly, twice, with one finish() ...
+        text2 = capi.synth_corpus(seed=8, doc_begin=0, doc_end=2, vocab=5000, doc_bytes=1 << 16).tobytes()   # words of <= 8 bytes
+        dev2, n2 = to_dev(torch, text2)
+        loc2 = capi.Counter(table_slots=1 << 15)
+        loc2.count_dev(dev2.data_ptr(), n2)
+        want2 = oracle.port().wordcount([text2])
+        ax2 = AsyncExchange(loc2, ops, dist, entries_hint=len(want2))
+        for _ in range(2):
+            own3 = capi.Counter(table_slots=1 << 15)
+            ax2.step(loc2, own3)
+            assert own3.to_dict() == want2
+        ax2.finish()
+        # ... and regions that are too small are reported, not silently truncated
+        ax3 = AsyncExchange(loc2, ops, dist, entries_hint=1)
+        ax3.cap = 8
+        ax3.step(loc2, capi.Counter(table_slots=1 << 15))
+        try:
+            ax3.finish(); raise SystemExit("overflow was not reported")
+        except ExchangeOverflow:
+            pass
         x = torch.tensor([1.25], dtype=torch.float64, device="cuda")
         assert float(allreduce_scalar(x, dist)) == 1.25 and float(allreduce_scalar(x, dist, reproducible=False)) == 1.25
         dist.destroy_process_group()
