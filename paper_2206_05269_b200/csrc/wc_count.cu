@@ -251,6 +251,7 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
         }
         mhead += min((u32)__popc(freem), avail);
         asm volatile("cp.async.commit_group;" ::: "memory");
+        __syncwarp();                               // the entries just read may be overwritten by the next append
     };
     // called between passes
     auto drain_step = [&]() {
