@@ -423,7 +423,8 @@ def run_b200(args) -> None:
             os.sched_setaffinity(0, all_cpus)      # the CPU baseline gets every core of the box
             line["cpu_baseline"] = cpu_baseline(capi, w["vocab"], total_docs)
         if not args.no_mapreduce:
-            line["extra"] = {"mapreduce": mapreduce_line(capi, torch, device, stream, peak)}
+            line["extra"] = {"mapreduce": mapreduce_line(capi, torch, device, stream, peak),
+                             "sanitize": sanitize_line(capi, torch, dev, nbytes, peak)}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -451,6 +452,33 @@ def mapreduce_line(capi, torch, device, stream, peak) -> dict:
         res[name] = {"ms": ms, "GBps": 4 * n / ms / 1e6, "frac_of_hbm_peak": 4 * n / ms / 1e6 / peak,
                      "rel_err_vs_torch_fp64": abs(float(out.item()) - ref) / max(1.0, abs(ref))}
     return {"config": "sum f(x) over 2^28 fp32 (torch.rand), 1 GiB, 1 GPU", **res}
+
+
+def sanitize_line(capi, torch, dev, nbytes, peak) -> dict:
+    """The ingest step in front of the path (utf8_sanitize) on the resident shard:
+    the valid corpus as it is, and with 0xFF planted every 1000 bytes.  Algorithmic bytes = input read
+    once + output written once; the call includes its one host read (the output length)."""
+    out = torch.empty(nbytes + nbytes // 400 + 64, dtype=torch.uint8, device=dev.device)
+    res = {}
+    for name in ("valid", "1_in_1000_invalid"):
+        src = dev
+        if name != "valid":
+            src = dev.clone()
+            src[500::1000] = 0xFF
+        m = 0
+        for _ in range(3):
+            m = capi.utf8_sanitize_dev(src.data_ptr(), nbytes, out.data_ptr(), out.numel())
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            capi.utf8_sanitize_dev(src.data_ptr(), nbytes, out.data_ptr(), out.numel())
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 5
+        res[name] = {"ms": ms, "input_GBps": nbytes / ms / 1e6, "algorithmic_GBps": (nbytes + m) / ms / 1e6,
+                     "frac_of_hbm_peak": (nbytes + m) / ms / 1e6 / peak, "out_bytes": m}
+    return {"config": "utf8_sanitize of the resident 1 GB shard, 1 GPU", **res}
 
 
 def main() -> None:

@@ -242,6 +242,15 @@ WFCU_API int wfcu_counter_merge_long_records(wfcu_counter* c, const uint8_t* dev
 
 typedef struct wfcu_tokens wfcu_tokens; /* device-resident token list in text order */
 
+/* utf8_sanitize (proj/src/unicode.cpp:56-70; the ingest step, proj/src/analysis.cpp:53): every byte
+ * that strict UTF-8 decoding (unicode.cpp:11-44) rejects becomes U+FFFD (EF BF BD), one replacement
+ * per byte; valid sequences are copied.  The output is at most 3*n bytes; *out_len receives its
+ * length (also when WFCU_ERR_BUFFER_TOO_SMALL reports that out_cap was not enough).  The device form
+ * needs a 16-byte aligned dev_text, runs on `stream` and waits for it. */
+WFCU_API int wfcu_utf8_sanitize_dev(const uint8_t* dev_text, uint64_t n, uint8_t* dev_out, uint64_t out_cap,
+                           uint64_t* out_len, void* stream);
+WFCU_API int wfcu_utf8_sanitize_host(const uint8_t* text, uint64_t n, uint8_t* out, uint64_t out_cap, uint64_t* out_len);
+
 /* normalize_word (proj/src/text.cpp:9-30) over a batch of whitespace-free fragments:
  * case fold, strip non-word characters from both ends, U+FFFD for invalid bytes.
  * Fragment f is bytes[sum(lens[0..f)) ..]; the normalised words are written back to

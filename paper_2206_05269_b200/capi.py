@@ -88,6 +88,8 @@ SIGNATURES = {
     "wfcu_counter_merge_entries": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "wfcu_counter_long_records": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, u64p, C.c_void_p]),
     "wfcu_counter_merge_long_records": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p]),
+    "wfcu_utf8_sanitize_dev": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, u64p, C.c_void_p]),
+    "wfcu_utf8_sanitize_host": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, u64p]),
     "wfcu_normalize_words_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p]),
     "wfcu_tokenize_dev": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.POINTER(C.c_void_p)]),
     "wfcu_tokenize_host": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p)]),
@@ -218,6 +220,22 @@ def map_reduce_blocked_dev(ptr: int, dtype: int, n: int, kind: int, block_size: 
 
 
 # ---- counter ----------------------------------------------------------------------------
+def utf8_sanitize_host(data) -> bytes:
+    """wfc::utf8_sanitize on the device, host buffers in and out."""
+    a = np.frombuffer(data, dtype=np.uint8) if isinstance(data, (bytes, bytearray, memoryview)) else np.ascontiguousarray(data)
+    out = np.zeros(3 * a.size + 16, np.uint8)
+    n = C.c_uint64(0)
+    check(lib.wfcu_utf8_sanitize_host(_ptr(a), a.size, _ptr(out), out.size, C.byref(n)))
+    return out[:n.value].tobytes()
+
+
+def utf8_sanitize_dev(in_ptr: int, n: int, out_ptr: int, out_cap: int, stream: int = 0) -> int:
+    """Device buffers; returns the output length (waits for the stream)."""
+    m = C.c_uint64(0)
+    check(lib.wfcu_utf8_sanitize_dev(C.c_void_p(in_ptr), n, C.c_void_p(out_ptr), out_cap, C.byref(m), C.c_void_p(stream)))
+    return m.value
+
+
 class HostDocs:
     """The (pointer, length) arrays of wfcu_counter_count_host for a list of host documents.
     Keeps the buffers alive; reusable across calls."""

@@ -64,6 +64,10 @@ cudaError_t tokens_rle_flags(const TokenRec* recs, u64 n, const uint8_t* arena, 
                              cudaStream_t s, u64* launches);
 cudaError_t tokens_rle_insert(const TokenRec* recs, u64 n, const uint8_t* arena, u64* flags, u64* run_start, u64* tmp,
                               const TableView& t, int sm, cudaStream_t s, u64* launches);
+// sanitize.cu
+u64 sanitize_scratch_bytes(u64 n);
+cudaError_t sanitize_launch(const uint8_t* text, u64 n, uint8_t* out, u64 out_cap, void* scratch, u64* dev_total,
+                            int sm_count, cudaStream_t s, u64* launches);
 // analysis.cpp
 uint64_t analysis_top_k(const uint8_t* bytes, const uint32_t* lens, const uint64_t* counts, uint64_t n, uint64_t k,
                         uint64_t* out_idx, double* out_rel, uint64_t* total);
@@ -112,6 +116,8 @@ struct DeviceState {
     double* mr_partials = nullptr;   // kMrGridMax doubles
     double* mr_out = nullptr;        // device result
     u64* scratch = nullptr;          // 64 u64 of device scratch (counts, cursors)
+    void* sn_scratch = nullptr;      // grow-only scratch of utf8_sanitize
+    u64 sn_cap = 0;
 };
 static constexpr int kMaxDevices = 64;
 static DeviceState g_dev[kMaxDevices];
@@ -1322,6 +1328,55 @@ extern "C" int wfcu_counter_count_dev_sorted(wfcu_counter* c, const uint8_t* dev
 
 // normalize_word over a batch of fragments (host buffers).  Fragment f is
 // bytes[sum(lens[0..f)) ...]; out_lens[f] = 0 means "nothing remains" (nullopt).
+// ---- ingest: utf8_sanitize ---------------------------------------------------------------
+extern "C" int wfcu_utf8_sanitize_dev(const uint8_t* dev_text, uint64_t n, uint8_t* dev_out, uint64_t out_cap,
+                                      uint64_t* out_len, void* stream) {
+    DeviceState* d;
+    if (int rc = current_device_state(&d)) return rc;
+    if (!out_len) return fail(WFCU_ERR_INVALID_ARGUMENT, "out_len is null");
+    *out_len = 0;
+    if (n == 0) return WFCU_OK;
+    if (!dev_text || !dev_out) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
+    if (reinterpret_cast<uintptr_t>(dev_text) & 15u)
+        return fail(WFCU_ERR_INVALID_ARGUMENT, "device text must be 16-byte aligned");
+    cudaStream_t s = (cudaStream_t)stream;
+    const u64 need = sanitize_scratch_bytes(n);
+    if (d->sn_cap < need) {
+        CUDA_TRY(cudaDeviceSynchronize());
+        if (d->sn_scratch) cudaFree(d->sn_scratch);
+        d->sn_scratch = nullptr;
+        d->sn_cap = 0;
+        CUDA_TRY(cudaMalloc(&d->sn_scratch, need + need / 4));
+        d->sn_cap = need + need / 4;
+    }
+    LaunchTally tally;
+    CUDA_TRY(sanitize_launch(dev_text, n, dev_out, out_cap, d->sn_scratch, d->scratch + 32, d->sm_count, s, &tally.n));
+    u64 total = 0;
+    CUDA_TRY(cudaMemcpyAsync(&total, d->scratch + 32, sizeof(u64), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    *out_len = total;
+    if (total > out_cap)
+        return fail(WFCU_ERR_BUFFER_TOO_SMALL, "utf8_sanitize needs %llu bytes of output", (unsigned long long)total);
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_utf8_sanitize_host(const uint8_t* text, uint64_t n, uint8_t* out, uint64_t out_cap, uint64_t* out_len) {
+    DeviceState* d;
+    if (int rc = current_device_state(&d)) return rc;
+    if (!out_len) return fail(WFCU_ERR_INVALID_ARGUMENT, "out_len is null");
+    *out_len = 0;
+    if (n == 0) return WFCU_OK;
+    if (!text || !out) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
+    DevBuf din, dout;
+    const u64 cap = std::min<u64>(out_cap, 3 * n);
+    CUDA_TRY(din.alloc(n));
+    CUDA_TRY(dout.alloc(cap));
+    CUDA_TRY(cudaMemcpy(din.p, text, n, cudaMemcpyHostToDevice));
+    if (int rc = wfcu_utf8_sanitize_dev(din.as<uint8_t>(), n, dout.as<uint8_t>(), cap, out_len, nullptr)) return rc;
+    CUDA_TRY(cudaMemcpy(out, dout.p, *out_len, cudaMemcpyDeviceToHost));
+    return WFCU_OK;
+}
+
 extern "C" int wfcu_normalize_words_host(const uint8_t* bytes, const uint32_t* lens, uint64_t n_frag,
                                          uint8_t* out_bytes, uint64_t out_cap, uint32_t* out_lens) {
     DeviceState* d;

@@ -44,6 +44,10 @@ struct WordList {
     bool sorted = false;
 };
 
+// ---- unicode (reference: wfc/unicode.hpp, the ingest step) ----------------------------
+std::string utf8_sanitize(std::string_view text);
+bool utf8_valid(std::string_view text);     // no byte needs replacing (same device pass)
+
 std::optional<Word> normalize_word(std::string_view fragment);
 std::vector<std::optional<Word>> normalize_words(std::span<const std::string> fragments);  // batch form (one launch)
 WordList tokenize(const RawDocument& doc);

@@ -146,6 +146,20 @@ std::uint64_t since(Clock::time_point t0) {
 
 }  // namespace
 
+// ---- unicode --------------------------------------------------------------------------------
+std::string utf8_sanitize(std::string_view text) {   // proj/src/unicode.cpp:56-70
+    std::string out(3 * text.size() + 16, '\0');
+    std::uint64_t n = 0;
+    ok(wfcu_utf8_sanitize_host(reinterpret_cast<const std::uint8_t*>(text.data()), text.size(),
+                               reinterpret_cast<std::uint8_t*>(out.data()), out.size(), &n));
+    out.resize(n);
+    return out;
+}
+
+bool utf8_valid(std::string_view text) {   // proj/src/unicode.cpp:46-54: every replacement adds two bytes
+    return utf8_sanitize(text).size() == text.size();
+}
+
 // ---- text ---------------------------------------------------------------------------------
 std::vector<std::optional<Word>> normalize_words(std::span<const std::string> fragments) {
     const Packed p = pack(fragments);

@@ -155,6 +155,28 @@ static void text_cases() {
     }
 }
 
+static void unicode_cases() {
+    // text_test.cpp:171-187: invalid bytes are replaced, valid tokens stay countable
+    const std::string bytes = std::string("good ") + char(0xFF) + " word";
+    const std::string clean = utf8_sanitize(bytes);
+    CHECK(clean == "good \xEF\xBF\xBD word");
+    CHECK(utf8_valid(clean));
+    // text_test.cpp:180-187
+    CHECK(utf8_valid("plain ascii"));
+    CHECK(utf8_valid("caf\xC3\xA9 \xE3\x81\x82"));
+    CHECK(!utf8_valid(std::string("\xC0\xAF")));
+    CHECK(!utf8_valid(std::string("\xED\xA0\x80")));
+    CHECK(!utf8_valid(std::string("\xF5\x80\x80\x80")));
+    CHECK(!utf8_valid(std::string("\x80")));
+    CHECK((tokenize(RawDocument{"d", clean}).words == std::vector<std::string>{"good", "word"}));
+    CHECK(utf8_sanitize("") == "");
+    CHECK(utf8_sanitize("caf\xC3\xA9 \xE2\x80\x9Cq\xE2\x80\x9D") == "caf\xC3\xA9 \xE2\x80\x9Cq\xE2\x80\x9D");   // valid text is unchanged
+    CHECK(utf8_sanitize("\xC0\xAF") == "\xEF\xBF\xBD\xEF\xBF\xBD");                 // overlong: one replacement per byte
+    CHECK(utf8_sanitize("\xED\xA0\x80") == "\xEF\xBF\xBD\xEF\xBF\xBD\xEF\xBF\xBD");   // surrogate
+    CHECK(utf8_sanitize("a\xE2\x82") == "a\xEF\xBF\xBD\xEF\xBF\xBD");                 // truncated at the end
+    CHECK(utf8_sanitize(clean) == clean);                                               // idempotent
+}
+
 static void reduce_cases() {
     // reduce_test.cpp:28-58
     CHECK(reduce_sorted(WordList{{"a", "algorithm", "cool", "i", "is", "mapreduce"}, true}) ==
@@ -377,6 +399,7 @@ static void analysis_cases() {
 int main() {
     try {
         text_cases();
+        unicode_cases();
         reduce_cases();
         pipeline_cases();
         range_partition_cases();
