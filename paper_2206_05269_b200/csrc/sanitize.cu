@@ -9,12 +9,12 @@
 // consumed by an earlier sequence, so every lead is a decode position and its validity
 // depends on the next three bytes only; a continuation byte is kept iff the closest lead in
 // front of it starts a valid sequence that reaches it.  So:
-//   pass A  one thread per 16 bytes (plus a 3-byte halo on both sides): 16-bit keep mask and
-//           the output size of the chunk (16 + 2 per replaced byte);
-//   scan    exclusive prefix sum of the sizes (tokens.cu);
-//   pass B  every thread writes its chunk at its offset: one 16-byte store when nothing was
-//           replaced in or before it (the offset is then 16-byte aligned), bytes otherwise.
-// HBM traffic: 2 reads + 1 write of the text (3 bytes per input byte) + 12 bytes per 16-byte chunk.
+//   pass A  one thread per 16 bytes (plus a 3-byte halo on both sides): 16-bit keep mask; the
+//           output size (16 + 2 per replaced byte) is summed per CTA (4 KiB of input);
+//   scan    exclusive prefix sum of the CTA sizes (tokens.cu);
+//   pass B  every CTA rebuilds its output in shared memory, placed so that shared and global
+//           addresses agree modulo 16, and writes it with 16-byte stores whatever the offset.
+// HBM traffic: 2 reads + 1 write of the text + 2 bytes per 16-byte chunk: ~3.25 bytes per input byte.
 #include "wfcu_dev.cuh"
 
 namespace wfcu {
@@ -85,42 +85,114 @@ __device__ __forceinline__ u32 keep_mask(const Window& win) {
     return keep & 0xFFFFu;
 }
 
-__global__ void sn_sizes_kernel(const uint8_t* __restrict__ text, u64 n, u64 n_chunks, u32* __restrict__ masks,
-                                u64* __restrict__ sizes) {
-    for (u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x; c < n_chunks; c += (u64)gridDim.x * blockDim.x) {
-        const Window win = load_window(text, n, c);
+constexpr int kSnThreads = 256;
+constexpr int kSnBlockBytes = kSnThreads * 16;        // input bytes per CTA
+constexpr int kSnStageBytes = 3 * kSnBlockBytes + 32; // worst case output of a CTA + alignment slack
+
+// pass A: keep masks (16 bits per 16-byte chunk) and the output size of every 4 KiB block
+__global__ void __launch_bounds__(kSnThreads)
+sn_sizes_kernel(const uint8_t* __restrict__ text, u64 n, u64 n_blocks, uint16_t* __restrict__ masks,
+                u64* __restrict__ block_sizes) {
+    __shared__ u32 warp_sums[kSnThreads / 32];
+    for (u64 b = blockIdx.x; b < n_blocks; b += gridDim.x) {
+        const u64 c = b * kSnThreads + threadIdx.x;
         const u64 g = c * 16;
-        const u32 valid = n - g >= 16 ? 16u : (u32)(n - g);           // bytes of the chunk inside the text
-        const u32 in_text = valid == 16 ? 0xFFFFu : ((1u << valid) - 1u);
-        const u32 keep = keep_mask(win) & in_text;
-        masks[c] = keep;
-        sizes[c] = valid + 2 * (valid - __popc(keep));
+        u32 size = 0;
+        if (g < n) {
+            const Window win = load_window(text, n, c);
+            const u32 valid = n - g >= 16 ? 16u : (u32)(n - g);       // bytes of the chunk inside the text
+            const u32 in_text = valid == 16 ? 0xFFFFu : ((1u << valid) - 1u);
+            const u32 keep = keep_mask(win) & in_text;
+            masks[c] = (uint16_t)keep;
+            size = valid + 2 * (valid - __popc(keep));
+        }
+        for (int d = 16; d > 0; d >>= 1) size += __shfl_xor_sync(0xFFFFFFFFu, size, d);
+        if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = size;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            u32 total = 0;
+            for (int w = 0; w < kSnThreads / 32; ++w) total += warp_sums[w];
+            block_sizes[b] = total;
+        }
+        __syncthreads();
     }
 }
 
-__global__ void sn_write_kernel(const uint8_t* __restrict__ text, u64 n, u64 n_chunks, const u32* __restrict__ masks,
-                                const u64* __restrict__ offs, uint8_t* __restrict__ out, u64 out_cap,
-                                u64* __restrict__ total) {
-    for (u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x; c < n_chunks; c += (u64)gridDim.x * blockDim.x) {
-        const u64 g = c * 16, at = offs[c];
-        const u32 valid = n - g >= 16 ? 16u : (u32)(n - g);
-        const u32 keep = masks[c];
-        const u64 size = valid + 2 * (valid - __popc(keep));
-        if (c + 1 == n_chunks) *total = at + size;
-        if (at + size > out_cap) continue;                            // reported through *total
-        if (valid == 16 && keep == 0xFFFFu && (at & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
-            *reinterpret_cast<uint4*>(out + at) = *reinterpret_cast<const uint4*>(text + g);
-            continue;
-        }
-        uint8_t* o = out + at;
-        for (u32 i = 0; i < valid; ++i) {
-            if ((keep >> i) & 1u) {
-                *o++ = text[g + i];
-            } else {
-                o[0] = 0xEF; o[1] = 0xBF; o[2] = 0xBD;
-                o += 3;
+// pass B: every CTA builds the output of its 4 KiB in shared memory -- placed so that shared and
+// global addresses agree modulo 16 -- and writes it with 16-byte stores (bytes at the two ends)
+__global__ void __launch_bounds__(kSnThreads)
+sn_write_kernel(const uint8_t* __restrict__ text, u64 n, u64 n_blocks, const uint16_t* __restrict__ masks,
+                const u64* __restrict__ block_offs, uint8_t* __restrict__ out, u64 out_cap, u64* __restrict__ total) {
+    __shared__ __align__(16) uint8_t stage[kSnStageBytes];
+    __shared__ u32 warp_sums[kSnThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (u64 b = blockIdx.x; b < n_blocks; b += gridDim.x) {
+        const u64 c = b * kSnThreads + threadIdx.x;
+        const u64 g = c * 16;
+        const u64 boff = block_offs[b];
+        u32 valid = 0, keep = 0;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (g < n) {
+            valid = n - g >= 16 ? 16u : (u32)(n - g);
+            keep = masks[c];
+            if (valid == 16) v = *reinterpret_cast<const uint4*>(text + g);
+            else {
+                u32 w[4];
+                for (u32 k = 0; k < 4; ++k) w[k] = load_word(text, n, g + 4 * k);
+                v = make_uint4(w[0], w[1], w[2], w[3]);
             }
         }
+        const u32 size = valid + 2 * (valid - __popc(keep));
+        // exclusive scan of the chunk sizes inside the CTA
+        u32 incl = size;
+        for (int d = 1; d < 32; d <<= 1) {
+            const u32 t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+            if (lane >= d) incl += t;
+        }
+        if (lane == 31) warp_sums[warp] = incl;
+        __syncthreads();
+        u32 base = 0, bsize = 0;
+        for (int w = 0; w < kSnThreads / 32; ++w) {
+            if (w < warp) base += warp_sums[w];
+            bsize += warp_sums[w];
+        }
+        const u32 shift = (u32)((reinterpret_cast<uintptr_t>(out) + boff) & 15);   // stage[shift + j] = output byte j
+        uint8_t* o = stage + shift + base + incl - size;
+        const u32 words[4] = {v.x, v.y, v.z, v.w};
+        const u32 ofs = shift + base + incl - size;
+        if (keep == 0xFFFFu && (ofs & 3) == 0) {
+            u32* o4 = reinterpret_cast<u32*>(o);
+            o4[0] = v.x; o4[1] = v.y; o4[2] = v.z; o4[3] = v.w;
+        } else if (keep == 0xFFFFu && (ofs & 1) == 0) {       // every replacement shifts the output by 2
+            uint16_t* o2 = reinterpret_cast<uint16_t*>(o);
+#pragma unroll
+            for (u32 i = 0; i < 8; ++i) o2[i] = (uint16_t)(words[i >> 1] >> (16 * (i & 1)));
+        } else {
+#pragma unroll
+            for (u32 i = 0; i < 16; ++i) {
+                if (i < valid) {
+                    if ((keep >> i) & 1u) {
+                        *o++ = (uint8_t)(words[i >> 2] >> (8 * (i & 3)));
+                    } else {
+                        o[0] = 0xEF; o[1] = 0xBF; o[2] = 0xBD;
+                        o += 3;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (b + 1 == n_blocks && threadIdx.x == 0) *total = boff + bsize;
+        if (boff + bsize <= out_cap) {
+            // [shift, shift + bsize) of the stage -> out[boff, boff + bsize)
+            const u32 begin = shift, end = shift + bsize;
+            const u32 mid_begin = min((begin + 15u) & ~15u, end), mid_end = max(end & ~15u, mid_begin);
+            uint8_t* gout = out + boff - shift;                        // gout + s is the global address of stage[s]
+            for (u32 s2 = begin + threadIdx.x; s2 < mid_begin; s2 += kSnThreads) gout[s2] = stage[s2];
+            for (u32 s2 = mid_begin + 16 * threadIdx.x; s2 < mid_end; s2 += 16 * kSnThreads)
+                *reinterpret_cast<uint4*>(gout + s2) = *reinterpret_cast<const uint4*>(stage + s2);
+            for (u32 s2 = mid_end + threadIdx.x; s2 < end; s2 += kSnThreads) gout[s2] = stage[s2];
+        }
+        __syncthreads();
     }
 }
 
@@ -129,26 +201,26 @@ __global__ void sn_write_kernel(const uint8_t* __restrict__ text, u64 n, u64 n_c
 u64 sanitize_scratch_bytes(u64 n);
 u64 scan_tmp_words(u64 n);
 
-// scratch layout: sizes/offs u64[n_chunks] | scan tmp | masks u32[n_chunks]
+// scratch layout: block sizes/offsets u64[n_blocks] | scan tmp | masks u16[n_chunks]
 u64 sanitize_scratch_bytes(u64 n) {
-    const u64 chunks = (n + 15) / 16;
-    return sizeof(u64) * chunks + sizeof(u64) * scan_tmp_words(chunks) + sizeof(u32) * chunks + 64;
+    const u64 blocks = (n + kSnBlockBytes - 1) / kSnBlockBytes;
+    return sizeof(u64) * blocks + sizeof(u64) * scan_tmp_words(blocks) + sizeof(uint16_t) * blocks * kSnThreads + 64;
 }
 
 cudaError_t sanitize_launch(const uint8_t* text, u64 n, uint8_t* out, u64 out_cap, void* scratch, u64* dev_total,
                             int sm_count, cudaStream_t s, u64* launches) {
     if (n == 0) return cudaMemsetAsync(dev_total, 0, sizeof(u64), s);
-    const u64 chunks = (n + 15) / 16;
+    const u64 blocks = (n + kSnBlockBytes - 1) / kSnBlockBytes;
     u64* sizes = static_cast<u64*>(scratch);
-    u64* tmp = sizes + chunks;
-    u32* masks = reinterpret_cast<u32*>(tmp + scan_tmp_words(chunks));
-    u64 g = (chunks + 255) / 256;
-    if (g > (u64)sm_count * 16) g = (u64)sm_count * 16;
-    sn_sizes_kernel<<<(unsigned)g, 256, 0, s>>>(text, n, chunks, masks, sizes);
+    u64* tmp = sizes + blocks;
+    uint16_t* masks = reinterpret_cast<uint16_t*>(tmp + scan_tmp_words(blocks));
+    u64 g = blocks;
+    if (g > (u64)sm_count * 8) g = (u64)sm_count * 8;
+    sn_sizes_kernel<<<(unsigned)g, kSnThreads, 0, s>>>(text, n, blocks, masks, sizes);
     *launches += 1;
-    cudaError_t e = exclusive_scan_u64(sizes, sizes, chunks, tmp, s, launches);
+    cudaError_t e = exclusive_scan_u64(sizes, sizes, blocks, tmp, s, launches);
     if (e != cudaSuccess) return e;
-    sn_write_kernel<<<(unsigned)g, 256, 0, s>>>(text, n, chunks, masks, sizes, out, out_cap, dev_total);
+    sn_write_kernel<<<(unsigned)g, kSnThreads, 0, s>>>(text, n, blocks, masks, sizes, out, out_cap, dev_total);
     *launches += 1;
     return cudaGetLastError();
 }
