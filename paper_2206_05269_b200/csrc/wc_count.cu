@@ -28,6 +28,7 @@
 //     a fragment whose start is out of sight, a token longer than 16 bytes -- is appended
 //     to the deferred list and handled by wc_slow_kernel (wordcount.cu), an exact
 //     restatement of the reference's UTF-8 rules.
+#include <cstdlib>
 #include <type_traits>
 
 #include "wfcu_dev.cuh"
@@ -85,6 +86,63 @@ __device__ __forceinline__ Masks classify16(const uint4& x, uint4& f) {
     }
     return m;
 }
+// Chunks with bytes >= 0x80.  Two-byte sequences C3..DF 80..BF (U+00C0..U+07FF: Latin-1 letters,
+// Latin Extended, Greek, Cyrillic, ...) stay on the fast path: every such code point is a word
+// character except U+00D7 and U+00F7, none is whitespace, and the only case fold in the range
+// (U+00C0..U+00DE -> +0x20, proj/src/unicode.cpp:117-121) is "second byte | 0x20 after C3", which
+// keeps the length.  This function produces the per-byte flags; pairing leads with continuation
+// bytes is done on the gathered masks (hi_masks_finish).  prev_c3: 0x80000000 if the byte in front
+// of the chunk is 0xC3.
+struct HiMasks { u32 s7, a7, h7, c7, l7, x7; };   // whitespace, ASCII alnum, >= 0x80, continuation, lead C3..DF, x / division sign
+__device__ __forceinline__ HiMasks classify16_hi(const uint4& x, u32 prev_c3, uint4& f) {
+    const u32 M = 0x80808080u;
+    const u32 xs[4] = {x.x, x.y, x.z, x.w};
+    u32 fs[4], s[4], al[4], hi[4], co[4], ld[4], xd[4];
+    u32 c3_prev = prev_c3;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        const u32 xw = xs[w], v = xw & 0x7F7F7F7Fu, y = v | 0x20202020u, nx = ~xw;
+        const u32 t = (y + 0x1F1F1F1Fu) & ~(y + 0x05050505u) & M & nx;          // ASCII letters
+        const u32 u = (v + 0x50505050u) & ~(v + 0x46464646u) & M & nx;          // ASCII digits
+        const u32 z = (v ^ 0x20202020u) + 0x7F7F7F7Fu;
+        s[w] = (~z | ((v + 0x77777777u) & ~(v + 0x72727272u))) & M & nx;
+        al[w] = t | u;
+        hi[w] = xw & M;
+        co[w] = xw & ~(xw << 1) & M;                                              // 10xxxxxx
+        ld[w] = xw & (v + 0x3D3D3D3Du) & ~(v + 0x20202020u) & M;                 // C3..DF
+        const u32 c3 = xw & ~((v ^ 0x43434343u) + 0x7F7F7F7Fu) & M;              // == 0xC3
+        const u32 after_c3 = __funnelshift_l(c3_prev, c3, 8);                     // the byte in front is 0xC3
+        c3_prev = c3;
+        const u32 lat = co[w] & after_c3;                                         // second byte of U+00C0..U+00FF
+        const u32 fold_hi = lat & ~(v + 0x61616161u);                             // 80..9E -> A0..BE (97 is deferred anyway)
+        xd[w] = lat & ~(((v & 0x5F5F5F5Fu) ^ 0x17171717u) + 0x7F7F7F7Fu);         // C3 97 (x) and C3 B7 (division sign)
+        fs[w] = xw | ((t | fold_hi) >> 2);
+    }
+    f = make_uint4(fs[0], fs[1], fs[2], fs[3]);
+    HiMasks m;
+    m.s7 = gather8(s[2], s[3], 0) * 256u + gather8(s[0], s[1], 0);
+    m.a7 = gather8(al[2], al[3], 0) * 256u + gather8(al[0], al[1], 0);
+    m.h7 = gather8(hi[2], hi[3], 0) * 256u + gather8(hi[0], hi[1], 0);
+    m.c7 = gather8(co[2], co[3], 0) * 256u + gather8(co[0], co[1], 0);
+    m.l7 = gather8(ld[2], ld[3], 0) * 256u + gather8(ld[0], ld[1], 0);
+    m.x7 = gather8(xd[2], xd[3], 0) * 256u + gather8(xd[0], xd[1], 0);
+    return m;
+}
+// Pairs leads with continuation bytes on packed masks (low 16 bits = half a, high = half b).
+// lead_before: bit 0 / bit 16 set if the byte in front of half a / b is a lead C3..DF.
+// Out: A gains the bytes of valid two-byte letters; H = bytes the fast path must not touch
+// (anything else >= 0x80, x / division sign, a lead without its continuation byte -- that lead
+// itself when it lies in the same chunk; bad_first tells the caller to flag the LAST byte of the
+// chunk in front when the unmatched lead is there).
+__device__ __forceinline__ void hi_masks_finish(u32 Hi, u32 C, u32 L, u32 X, u32 lead_before, u32& A, u32& H, u32& bad_first) {
+    const u32 Lsh = ((L << 1) & 0xFFFEFFFEu) | (lead_before & 0x00010001u);     // the byte in front is a lead
+    const u32 validC = C & Lsh;
+    const u32 badnext = Lsh & ~C;                                                 // successor of an unmatched lead
+    bad_first = badnext & 0x00010001u;
+    H = (Hi & ~(validC | L)) | X | badnext | ((badnext >> 1) & 0x7FFF7FFFu);
+    A |= (validC | L) & ~H;
+}
+
 // pack the masks of the lane's two chunks: low 16 bits = half a, high 16 bits = half b
 __device__ __forceinline__ u32 pack7(u32 a7, u32 b7) { return (b7 << 9) | (a7 >> 7); }
 
@@ -167,9 +225,13 @@ using namespace cnt3;
 
 // text[0..n): documents concatenated with whitespace between them by the caller.
 // Position n acts as a whitespace byte, so does "position -1".
-template <int WARPS, int SETS, int MSLOTS>
-__global__ void __launch_bounds__(WARPS * 32, 1)
-wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, TableView gt) {
+// Two variants of the body, both exact: HI = false treats every fragment with a byte >= 0x80 as
+// the slow kernel's business (the ASCII corpora of the benchmarks never pay for anything else);
+// HI = true keeps two-byte letters (accented Latin, Greek, Cyrillic ...) on the fast path.  Every
+// CTA picks its variant from a sample of its own part of the text (wc_count_kernel below): the
+// choice affects speed only.
+template <int WARPS, int SETS, int MSLOTS, bool HI>
+__device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, const TableView& gt) {
     extern __shared__ uint8_t smem_raw[];
     typedef Smem<WARPS, SETS, MSLOTS> SM;
     const u32 sbase = (u32)__cvta_generic_to_shared(smem_raw);
@@ -421,13 +483,23 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
 
         // masks of the chunk in front of the strip (16 bits): "position -1" is whitespace
         u32 carryS = 0xFFFFu, carryA = 0, carryH = 0;
+        u32 carryL = 0, carryC3 = 0;   // HI: lead mask of that chunk; 0x80000000 if it ends in 0xC3
         bool general_prev = false;
         if (r_begin > 0) {
             // the 16 bytes in front of the strip: predecessor masks for lane 0, folded bytes for the guard
             const uint4 x = *reinterpret_cast<const uint4*>(text + (u64)r_begin * kRow - 16);
             uint4 f;
-            const Masks m = classify16<false>(x, f);
-            carryS = m.s7 >> 7; carryA = m.a7 >> 7; carryH = m.h7 >> 7;
+            if constexpr (HI) {
+                // what lies in front of THEM is unknown: a leading continuation byte is flagged (conservative)
+                const HiMasks m = classify16_hi(x, 0u, f);
+                u32 A = m.a7 >> 7, H, bad_first;
+                hi_masks_finish(m.h7 >> 7, m.c7 >> 7, m.l7 >> 7, m.x7 >> 7, 0u, A, H, bad_first);
+                carryS = m.s7 >> 7; carryA = A & 0xFFFFu; carryH = H & 0xFFFFu; carryL = (m.l7 >> 7) & 0xFFFFu;
+                carryC3 = (x.w >> 24) == 0xC3u ? 0x80000000u : 0u;
+            } else {
+                const Masks m = classify16<false>(x, f);
+                carryS = m.s7 >> 7; carryA = m.a7 >> 7; carryH = m.h7 >> 7;
+            }
             if (lane == 0) *reinterpret_cast<uint4*>(ring + (r_begin & 1u) * kSlotStride + 16) = f;
         }
         uint4 nxa, nxb;
@@ -442,11 +514,34 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
             u32 S, A, H = 0;
             uint4 fa, fb;
             const u32 anyhi = (xa.x | xa.y | xa.z | xa.w | xb.x | xb.y | xb.z | xb.w) & 0x80808080u;
-            const bool ascii_row = !__any_sync(kFull, anyhi != 0) && carryH == 0;
+            const bool ascii_row = !__any_sync(kFull, anyhi != 0) && (carryH | carryL) == 0;
+            u32 pH_fix = 0;
             if (ascii_row) {
                 const Masks ma = classify16<true>(xa, fa), mb = classify16<true>(xb, fb);
                 S = pack7(ma.s7, mb.s7);
                 A = pack7(ma.a7, mb.a7);
+                carryC3 = 0;
+            } else if constexpr (HI) {
+                // is the byte in front of each chunk 0xC3 (chunk a: lane-1's a, lane 0: the previous row's
+                // last chunk; chunk b: lane-1's b, lane 0: this row's a of lane 31)
+                const u32 last_c3 = ((xa.w >> 24) == 0xC3u ? 1u : 0u) | ((xb.w >> 24) == 0xC3u ? 2u : 0u);
+                const u32 l31 = __shfl_sync(kFull, last_c3, 31);
+                u32 pc3 = __shfl_up_sync(kFull, last_c3, 1);
+                if (lane == 0) pc3 = (carryC3 ? 1u : 0u) | ((l31 & 1u) << 1);
+                carryC3 = (l31 & 2u) ? 0x80000000u : 0u;
+                const HiMasks ma = classify16_hi(xa, (pc3 & 1u) ? 0x80000000u : 0u, fa);
+                const HiMasks mb = classify16_hi(xb, (pc3 & 2u) ? 0x80000000u : 0u, fb);
+                S = pack7(ma.s7, mb.s7);
+                A = pack7(ma.a7, mb.a7);
+                const u32 L = pack7(ma.l7, mb.l7);
+                // is the byte in front of each chunk a lead C3..DF
+                const u32 L31 = __shfl_sync(kFull, L, 31);
+                u32 pL = __shfl_up_sync(kFull, L, 1);
+                if (lane == 0) pL = __byte_perm(carryL, L31, 0x5410);
+                carryL = L31 >> 16;
+                u32 bad_first;
+                hi_masks_finish(pack7(ma.h7, mb.h7), pack7(ma.c7, mb.c7), L, pack7(ma.x7, mb.x7), pL >> 15, A, H, bad_first);
+                pH_fix = bad_first << 15;     // an unmatched lead at the end of the chunk in front
             } else {
                 const Masks ma = classify16<false>(xa, fa), mb = classify16<false>(xb, fb);
                 S = pack7(ma.s7, mb.s7);
@@ -473,6 +568,7 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
                 const u32 h31 = __shfl_sync(kFull, H, 31);
                 pH = __shfl_up_sync(kFull, H, 1);
                 if (lane == 0) pH = carryH | (h31 << 16);
+                pH |= pH_fix;
                 carryH = h31 >> 16;
             }
             // fragment ends: whitespace byte whose predecessor is not whitespace
@@ -487,7 +583,9 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
 
             // A fragment that ends in the chunk but has no whitespace in the 16 bytes in front
             // of the chunk may start out of sight: the careful loop decides end by end.
-            bool careful = !ascii_row || __any_sync(kFull, (Ta != 0 && prev_a == 0) || (Tb != 0 && prev_b == 0));
+            // (HI: rows whose bytes >= 0x80 are all two-byte letters stay on the bit-parallel emission)
+            bool careful = (HI ? __any_sync(kFull, (H | pH) != 0) : !ascii_row) ||
+                           __any_sync(kFull, (Ta != 0 && prev_a == 0) || (Tb != 0 && prev_b == 0));
             bool general_row = true;
             u32 total;
             for (;;) {
@@ -618,6 +716,30 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, Tabl
     }
 }
 
+// One kernel per variant (a kernel holding both bodies compiles the ASCII one measurably worse);
+// both are launched, and every CTA runs in exactly one of them: it samples one 16-byte chunk per
+// thread, spread evenly over its own rows, and takes HI if more than one in 64 holds a byte >= 0x80
+// (then most 1 KiB rows do).  The CTA of the other variant sees the same sample and returns.
+// force: 0 / 1 = variant for every CTA (tests), anything else = sample.
+template <int WARPS, int SETS, int MSLOTS, bool HI>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, int force, TableView gt) {
+    bool hi = force == 1;
+    if (force != 0 && force != 1) {
+        const u64 first = (u64)blockIdx.x * WARPS * rows_per_warp * kRow;
+        const u64 span = (u64)WARPS * rows_per_warp * kRow;
+        const u64 at = (first + (u64)((unsigned __int128)threadIdx.x * span / (WARPS * 32))) & ~15ull;
+        bool hit = false;
+        if (at + 16 <= n) {
+            const uint4 v = *reinterpret_cast<const uint4*>(text + at);
+            hit = ((v.x | v.y | v.z | v.w) & 0x80808080u) != 0;
+        }
+        hi = __syncthreads_count(hit) * 64 > WARPS * 32;
+    }
+    if (hi != HI) return;
+    wc_count_body<WARPS, SETS, MSLOTS, HI>(text, n, rows_per_warp, gt);
+}
+
 // ---- host-side launcher (called from wordcount.cu) ---------------------------------
 #ifndef WFCU_COUNT_WARPS
 #define WFCU_COUNT_WARPS 28
@@ -635,17 +757,23 @@ typedef Smem<kCountWarps, kCountSets, kCountMedSlots> CountSmem;
 static_assert(sizeof(CountSmem) + 1024 <= 227 * 1024, "shared memory budget");
 static_assert(2 * kSlotStride + 20 <= 4096, "queue entries keep ring positions in 12 bits");
 
-cudaError_t wc_count_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream) {
+cudaError_t wc_count_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream, u64* launches) {
     const size_t smem = sizeof(CountSmem) + 1024;   // + slack for the 1 KiB alignment
-    auto kernel = wc_count_kernel<kCountWarps, kCountSets, kCountMedSlots>;
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto k_ascii = wc_count_kernel<kCountWarps, kCountSets, kCountMedSlots, false>;
+    auto k_hi = wc_count_kernel<kCountWarps, kCountSets, kCountMedSlots, true>;
+    cudaError_t e = cudaFuncSetAttribute(k_ascii, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_hi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const u64 n_rows = n / kRow + 1;
     u64 grid = (u64)sm_count;
     if (grid * kCountWarps > n_rows) grid = (n_rows + kCountWarps - 1) / kCountWarps;   // at least one row per warp
     if (grid == 0) grid = 1;
     const u64 rows_per_warp = (n_rows + grid * kCountWarps - 1) / (grid * kCountWarps);
-    kernel<<<(unsigned)grid, kCountWarps * 32, smem, stream>>>(text, n, (u32)rows_per_warp, gt);
+    static const int force = [] { const char* v = getenv("WFCU_COUNT_VARIANT"); return v ? atoi(v) : -1; }();   // tests: 0 / 1
+    if (force != 1) k_ascii<<<(unsigned)grid, kCountWarps * 32, smem, stream>>>(text, n, (u32)rows_per_warp, force, gt);
+    if (force != 0) k_hi<<<(unsigned)grid, kCountWarps * 32, smem, stream>>>(text, n, (u32)rows_per_warp, force, gt);
+    *launches += (force == 0 || force == 1) ? 1 : 2;
     return cudaGetLastError();
 }
 

@@ -658,7 +658,7 @@ size_t wc_fast_smem_bytes() { return sizeof(FastSmem<kFastWarps, kFastSlots, kFa
 
 // wc_count.cu: the counting kernel (third generation).  wc_fast_kernel<.., EMIT = false> stays
 // selectable (WFCU_COUNT_KERNEL=2 in the environment) for A/B runs on the same box.
-cudaError_t wc_count_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream);
+cudaError_t wc_count_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream, u64* launches);
 static bool use_gen2_count_kernel() {
     static const bool v = [] { const char* e = getenv("WFCU_COUNT_KERNEL"); return e && e[0] == '2'; }();
     return v;
@@ -682,15 +682,16 @@ static cudaError_t wc_launch_impl(const uint8_t* text, u64 n, const TableView& g
     const u64 rows_per_warp = (n_rows + grid * kFastWarps - 1) / (grid * kFastWarps);
     if (ev_before_fast) cudaEventRecord(*ev_before_fast, stream);
     if (!EMIT && !use_gen2_count_kernel()) {
-        cudaError_t e = wc_count_launch(text, n, gt, sm_count, stream);
+        cudaError_t e = wc_count_launch(text, n, gt, sm_count, stream, launches);
         if (e != cudaSuccess) return e;
     } else {
         kernel<<<(unsigned)grid, kFastWarps * 32, smem, stream>>>(text, n, rows_per_warp, gt, em);
+        *launches += 1;
     }
     if (ev_after_fast) cudaEventRecord(*ev_after_fast, stream);
     wc_slow_kernel<<<sm_count * 2, 128, 0, stream>>>(text, n, gt, em, EMIT ? 1 : 0);
     wc_reset_deferred_kernel<<<1, 1, 0, stream>>>(gt);
-    *launches += 3;
+    *launches += 2;
     return cudaGetLastError();
 }
 

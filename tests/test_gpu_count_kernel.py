@@ -93,3 +93,66 @@ def test_non_ascii_rows_between_ascii_rows(capi, cuda, port):
         t[pos - 1:pos + 1] = "é".encode()
         t[pos + 1] = ord("x")
         check(capi, cuda, port, bytes(t))
+
+
+# ---- two-byte letters on the fast path (the HI variant of the kernel) ---------------------------
+LATIN = ["é", "É", "à", "À", "ü", "Ü", "ß", "ÿ", "Þ", "þ", "ñ", "Ñ", "ç", "Ç", "ø", "Ø", "×", "÷", "µ", "ª", "¿",
+         " ", "ō", "Ł", "ł", "Ω", "ω", "я", "Я", "ж", "Ж", "א", "߿", "€", "“", "”", "あ"]
+
+
+def latin_text(rng, n):
+    """dense in two-byte characters: words of ASCII letters and LATIN characters, some upper case, with
+    edge punctuation; a few invalid bytes (a lead without its continuation byte, a stray continuation)"""
+    out = bytearray()
+    while len(out) < n:
+        r = rng.random()
+        if r < 0.17:
+            out += rng.choice([b" ", b"\n", b"  ", b"\t"])
+        elif r < 0.24:
+            out += bytes([rng.choice(b".,;!?-'\"()")])
+        elif r < 0.50:
+            out += rng.choice(LATIN).encode()
+        elif r < 0.52:
+            out += bytes([rng.choice([0xC3, 0xC4, 0xD0, 0xDF, 0x80, 0xA9, 0xBF, 0xC2, 0xC0, 0xE0, 0xFF])])
+        else:
+            out += bytes([rng.choice(b"abcdefghijklmnopqrstuvwxyzABCDEFGHIJKLMNOPQRSTUVWXYZ0123456789")])
+    return bytes(out[:n])
+
+
+@pytest.mark.parametrize("size", [1, 2, 15, 16, 17, 33, 511, 513, 1023, 1024, 1025, 2049, 30011, 400003])
+def test_two_byte_letters_match_oracle(capi, cuda, port, size):
+    rng = random.Random(size * 7 + 1)
+    for rep in range(3):
+        check(capi, cuda, port, latin_text(rng, size))
+
+
+def test_two_byte_case_fold_and_edges(capi, cuda, port):
+    """golden-style cases (proj/src/unicode.cpp:117-121: U+00C0..U+00DE except U+00D7 fold by +0x20, nothing
+    else above ASCII folds; U+00D7 / U+00F7 are not word characters) repeated so that the CTA sampler
+    picks the two-byte variant"""
+    unit = ("École ÉCOLE école Ærø ÆRØ STRASSE straße Ÿ ÿ ÞORN þorn 3×4 ×× a÷b ÷ "
+            "Ωμέγα ΩΜΈΓΑ Жук жук ŁÓDŹ łódź don't’ “quoted” naïve. (café) —señor— ").encode()
+    text = unit * 300
+    got, _ = gpu_wordcount(capi, cuda, [text])
+    assert got == port.wordcount([text])
+    assert got["école".encode()] == 900 and got["strasse".encode()] == 300 and got["straße".encode()] == 300
+    assert got["3×4".encode()] == 300 and got["a÷b".encode()] == 300          # interior x / division sign stay
+    assert "××".encode() not in got and "÷".encode() not in got
+    assert got["ærø".encode()] == 600 and got["þorn".encode()] == 600 and got["ÿ".encode()] == 300 and got["Ÿ".encode()] == 300
+    assert got["Ωμέγα".encode()] == 300 and got["ΩΜΈΓΑ".encode()] == 300    # Greek does not fold
+    assert got["łódź".encode()] == 300 and got["ŁódŹ".encode()] == 300       # only the Latin-1 letters fold
+    assert got["don't".encode()] == 300 and got["quoted".encode()] == 300 and got["señor".encode()] == 300
+
+
+@pytest.mark.parametrize("shift", [0, 1, 14, 15, 16, 17, 510, 511, 512, 513, 1022, 1023, 1024, 1025])
+def test_two_byte_sequences_across_chunk_half_and_row_boundaries(capi, cuda, port, shift):
+    """a lead byte as the last byte of a 16-byte chunk / a half / a row, with and without its continuation
+    byte behind the boundary; also the end of the text right after a lead"""
+    rng = random.Random(shift + 99)
+    body = " ".join("".join(rng.choice(["é", "É", "a", "B", "ü", "Ж", "ß", "x"]) for _ in range(rng.randint(1, 7)))
+                    for _ in range(400)).encode()
+    for tail in (b"", b"\xc3", b"\xc3 z", b" \xd0", b"\xa9", b"\xc3\xc3\xa9"):
+        text = b"q" * shift + b" " + body + tail
+        check(capi, cuda, port, text)
+        for cut in (1, 2, 3):
+            check(capi, cuda, port, text[:len(text) - cut])

@@ -164,9 +164,10 @@ def test_count_host_zero_copy_path(capi, cuda, port):
 
 
 def test_deferred_list_overflow_is_reported(capi, cuda, port):
-    """a corpus of non-ASCII words overflows a tiny slow-path list: loud error, and the same
-    text counts exactly once the capacity is raised (what the C++ drop-in's retry does)"""
-    text = (" ".join("héllo%d" % (i % 50) for i in range(20000))).encode()
+    """a corpus of words the fast path defers (three-byte characters) overflows a tiny slow-path list:
+    loud error, and the same text counts exactly once the capacity is raised (what the C++ drop-in's
+    retry does)"""
+    text = (" ".join("h€llo%d" % (i % 50) for i in range(20000))).encode()
     dev, n = to_dev(cuda, text)
     small = capi.Counter(table_slots=1 << 12, deferred_slots=1024)
     small.count_dev(dev.data_ptr(), n)
