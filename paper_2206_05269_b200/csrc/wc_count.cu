@@ -93,11 +93,17 @@ __device__ __forceinline__ Masks classify16(const uint4& x, uint4& f) {
 // keeps the length.  This function produces the per-byte flags; pairing leads with continuation
 // bytes is done on the gathered masks (hi_masks_finish).  prev_c3: 0x80000000 if the byte in front
 // of the chunk is 0xC3.
-struct HiMasks { u32 s7, a7, h7, c7, l7, x7; };   // whitespace, ASCII alnum, >= 0x80, continuation, lead C3..DF, x / division sign
+//
+// The same for the General Punctuation block's E2 80 90..A7 / B0..BF (U+2010..U+2027, U+2030..U+203F:
+// typographic apostrophes and quotes, dashes, ellipsis ...): valid, never word characters, never
+// whitespace, so their three bytes behave like ASCII punctuation (kept inside a token, trimmed at
+// its edges) and need not defer the fragment.
+struct HiMasks { u32 s7, a7, h7, c7, l7, x7, e7, z7, k7; };   // whitespace, ASCII alnum, >= 0x80, continuation, lead C3..DF,
+                                                              // x / division sign, == E2, == 80, third byte of the punctuation above
 __device__ __forceinline__ HiMasks classify16_hi(const uint4& x, u32 prev_c3, uint4& f) {
     const u32 M = 0x80808080u;
     const u32 xs[4] = {x.x, x.y, x.z, x.w};
-    u32 fs[4], s[4], al[4], hi[4], co[4], ld[4], xd[4];
+    u32 fs[4], s[4], al[4], hi[4], co[4], ld[4], xd[4], e2[4], z8[4], k3[4];
     u32 c3_prev = prev_c3;
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
@@ -117,6 +123,9 @@ __device__ __forceinline__ HiMasks classify16_hi(const uint4& x, u32 prev_c3, ui
         const u32 fold_hi = lat & ~(v + 0x61616161u);                             // 80..9E -> A0..BE (97 is deferred anyway)
         xd[w] = lat & ~(((v & 0x5F5F5F5Fu) ^ 0x17171717u) + 0x7F7F7F7Fu);         // C3 97 (x) and C3 B7 (division sign)
         fs[w] = xw | ((t | fold_hi) >> 2);
+        e2[w] = xw & ~((v ^ 0x62626262u) + 0x7F7F7F7Fu) & M;                      // == 0xE2
+        z8[w] = xw & ~(v + 0x7F7F7F7Fu) & M;                                      // == 0x80
+        k3[w] = co[w] & (((v + 0x70707070u) & ~(v + 0x58585858u)) | (v + 0x50505050u));   // 90..A7 or B0..BF
     }
     f = make_uint4(fs[0], fs[1], fs[2], fs[3]);
     HiMasks m;
@@ -126,21 +135,36 @@ __device__ __forceinline__ HiMasks classify16_hi(const uint4& x, u32 prev_c3, ui
     m.c7 = gather8(co[2], co[3], 0) * 256u + gather8(co[0], co[1], 0);
     m.l7 = gather8(ld[2], ld[3], 0) * 256u + gather8(ld[0], ld[1], 0);
     m.x7 = gather8(xd[2], xd[3], 0) * 256u + gather8(xd[0], xd[1], 0);
+    m.e7 = gather8(e2[2], e2[3], 0) * 256u + gather8(e2[0], e2[1], 0);
+    m.z7 = gather8(z8[2], z8[3], 0) * 256u + gather8(z8[0], z8[1], 0);
+    m.k7 = gather8(k3[2], k3[3], 0) * 256u + gather8(k3[0], k3[1], 0);
     return m;
 }
 // Pairs leads with continuation bytes on packed masks (low 16 bits = half a, high = half b).
 // lead_before: bit 0 / bit 16 set if the byte in front of half a / b is a lead C3..DF.
+// tails_before: per half, bits 0,1 = "the byte two / one in front of the chunk is E2", bit 2 = "the
+// byte in front is 80" (hi_tails of the chunk in front).
 // Out: A gains the bytes of valid two-byte letters; H = bytes the fast path must not touch
 // (anything else >= 0x80, x / division sign, a lead without its continuation byte -- that lead
 // itself when it lies in the same chunk; bad_first tells the caller to flag the LAST byte of the
-// chunk in front when the unmatched lead is there).
-__device__ __forceinline__ void hi_masks_finish(u32 Hi, u32 C, u32 L, u32 X, u32 lead_before, u32& A, u32& H, u32& bad_first) {
-    const u32 Lsh = ((L << 1) & 0xFFFEFFFEu) | (lead_before & 0x00010001u);     // the byte in front is a lead
-    const u32 validC = C & Lsh;
-    const u32 badnext = Lsh & ~C;                                                 // successor of an unmatched lead
+// chunk in front when the unmatched lead is there).  A chunk cannot know whether an E2 (80) at its
+// end will be completed, so it flags them; clear_before tells the caller which of the last two
+// bytes of the chunk in front the sequences completed HERE clear again.
+struct HiIn { u32 Hi, C, L, X, E2, Z, K; };
+__device__ __forceinline__ u32 hi_tails(u32 E2, u32 Z) { return ((E2 >> 14) & 0x00030003u) | ((Z >> 13) & 0x00040004u); }
+__device__ __forceinline__ void hi_masks_finish(const HiIn& in, u32 lead_before, u32 tails_before, u32& A, u32& H,
+                                                u32& bad_first, u32& clear_before) {
+    const u32 Lsh = ((in.L << 1) & 0xFFFEFFFEu) | (lead_before & 0x00010001u);  // the byte in front is a lead
+    const u32 validC = in.C & Lsh;
+    const u32 badnext = Lsh & ~in.C;                                              // successor of an unmatched lead
     bad_first = badnext & 0x00010001u;
-    H = (Hi & ~(validC | L)) | X | badnext | ((badnext >> 1) & 0x7FFF7FFFu);
-    A |= (validC | L) & ~H;
+    const u32 Zsh = ((in.Z << 1) & 0xFFFEFFFEu) | ((tails_before >> 2) & 0x00010001u);   // the byte in front is 80
+    const u32 Esh = ((in.E2 << 2) & 0xFFFCFFFCu) | (tails_before & 0x00030003u);          // the byte two in front is E2
+    const u32 T3 = in.K & Zsh & Esh;                                              // third byte of a punctuation sequence
+    const u32 P3 = T3 | ((T3 >> 1) & 0x7FFF7FFFu) | ((T3 >> 2) & 0x3FFF3FFFu);    // its bytes inside the chunk
+    clear_before = ((T3 & 0x00010001u) << 15) | ((T3 & 0x00010001u) << 14) | ((T3 & 0x00020002u) << 14);
+    H = (in.Hi & ~(validC | in.L | P3)) | in.X | badnext | ((badnext >> 1) & 0x7FFF7FFFu);
+    A |= (validC | in.L) & ~H;
 }
 
 // pack the masks of the lane's two chunks: low 16 bits = half a, high 16 bits = half b
@@ -484,6 +508,7 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
         // masks of the chunk in front of the strip (16 bits): "position -1" is whitespace
         u32 carryS = 0xFFFFu, carryA = 0, carryH = 0;
         u32 carryL = 0, carryC3 = 0;   // HI: lead mask of that chunk; 0x80000000 if it ends in 0xC3
+        u32 carryT = 0;                // HI: hi_tails of that chunk (E2 / 80 in its last two bytes)
         bool general_prev = false;
         if (r_begin > 0) {
             // the 16 bytes in front of the strip: predecessor masks for lane 0, folded bytes for the guard
@@ -492,9 +517,11 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
             if constexpr (HI) {
                 // what lies in front of THEM is unknown: a leading continuation byte is flagged (conservative)
                 const HiMasks m = classify16_hi(x, 0u, f);
-                u32 A = m.a7 >> 7, H, bad_first;
-                hi_masks_finish(m.h7 >> 7, m.c7 >> 7, m.l7 >> 7, m.x7 >> 7, 0u, A, H, bad_first);
+                u32 A = m.a7 >> 7, H, bad_first, clear_before;
+                const HiIn in{m.h7 >> 7, m.c7 >> 7, m.l7 >> 7, m.x7 >> 7, m.e7 >> 7, m.z7 >> 7, m.k7 >> 7};
+                hi_masks_finish(in, 0u, 0u, A, H, bad_first, clear_before);
                 carryS = m.s7 >> 7; carryA = A & 0xFFFFu; carryH = H & 0xFFFFu; carryL = (m.l7 >> 7) & 0xFFFFu;
+                carryT = hi_tails(in.E2, in.Z) & 0xFFFFu;
                 carryC3 = (x.w >> 24) == 0xC3u ? 0x80000000u : 0u;
             } else {
                 const Masks m = classify16<false>(x, f);
@@ -515,7 +542,7 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
             uint4 fa, fb;
             const u32 anyhi = (xa.x | xa.y | xa.z | xa.w | xb.x | xb.y | xb.z | xb.w) & 0x80808080u;
             const bool ascii_row = !__any_sync(kFull, anyhi != 0) && (carryH | carryL) == 0;
-            u32 pH_fix = 0;
+            u32 pH_fix = 0, pH_clear = 0;
             if (ascii_row) {
                 const Masks ma = classify16<true>(xa, fa), mb = classify16<true>(xb, fb);
                 S = pack7(ma.s7, mb.s7);
@@ -539,8 +566,16 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
                 u32 pL = __shfl_up_sync(kFull, L, 1);
                 if (lane == 0) pL = __byte_perm(carryL, L31, 0x5410);
                 carryL = L31 >> 16;
+                const HiIn in{pack7(ma.h7, mb.h7), pack7(ma.c7, mb.c7), L, pack7(ma.x7, mb.x7),
+                              pack7(ma.e7, mb.e7), pack7(ma.z7, mb.z7), pack7(ma.k7, mb.k7)};
+                // E2 / 80 in the last two bytes of the chunk in front
+                const u32 tails = hi_tails(in.E2, in.Z);
+                const u32 t31 = __shfl_sync(kFull, tails, 31);
+                u32 pT = __shfl_up_sync(kFull, tails, 1);
+                if (lane == 0) pT = __byte_perm(carryT, t31, 0x5410);
+                carryT = t31 >> 16;
                 u32 bad_first;
-                hi_masks_finish(pack7(ma.h7, mb.h7), pack7(ma.c7, mb.c7), L, pack7(ma.x7, mb.x7), pL >> 15, A, H, bad_first);
+                hi_masks_finish(in, pL >> 15, pT, A, H, bad_first, pH_clear);
                 pH_fix = bad_first << 15;     // an unmatched lead at the end of the chunk in front
             } else {
                 const Masks ma = classify16<false>(xa, fa), mb = classify16<false>(xb, fb);
@@ -568,7 +603,7 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
                 const u32 h31 = __shfl_sync(kFull, H, 31);
                 pH = __shfl_up_sync(kFull, H, 1);
                 if (lane == 0) pH = carryH | (h31 << 16);
-                pH |= pH_fix;
+                pH = (pH & ~pH_clear) | pH_fix;
                 carryH = h31 >> 16;
             }
             // fragment ends: whitespace byte whose predecessor is not whitespace

@@ -524,7 +524,8 @@ __device__ __forceinline__ u32 enc_byte(u32 cp, u32 n, u32 i) {
 
 // Counts (or, when em != nullptr, emits) the token of one whitespace-free piece
 // [a,b) of the text (normalize_word).
-__device__ void slow_count_piece(const uint8_t* text, u64 a, u64 b, const TableView& gt, const EmitView* em) {
+// Returns 1 if the piece yields a token (the caller accounts the tokens: one atomic per warp, not per token).
+__device__ u32 slow_count_piece(const uint8_t* text, u64 a, u64 b, const TableView& gt, const EmitView* em) {
     // pass 1: normalised offsets of the first / last word character
     u64 noff = 0, nfirst = 0, nlast_end = 0, first_b = b, last_e = a;
     for (u64 pos = a; pos < b;) {
@@ -539,9 +540,8 @@ __device__ void slow_count_piece(const uint8_t* text, u64 a, u64 b, const TableV
         noff += el;
         pos += d.len;
     }
-    if (first_b == b) return;
+    if (first_b == b) return 0;
     const u64 nlen = nlast_end - nfirst;
-    atomicAdd(gt.n_tokens, 1ull);
     if (nlen <= 16) {
         u64 k0 = 0, k1 = 0;
         u32 i = 0;
@@ -562,11 +562,11 @@ __device__ void slow_count_piece(const uint8_t* text, u64 a, u64 b, const TableV
         } else {
             table_add(gt, k0, k1, 1ull);
         }
-        return;
+        return 1;
     }
-    if (nlen > 0xFFFFFFFFull) { atomicOr(gt.status, kStatusArenaFull); return; }
+    if (nlen > 0xFFFFFFFFull) { atomicOr(gt.status, kStatusArenaFull); return 1; }
     const u64 rec = arena_alloc(gt, (u32)nlen);
-    if (!rec) return;
+    if (!rec) return 1;
     uint8_t* out = gt.arena + rec + 8;
     u32 h = 2166136261u;
     u64 i = 0, p0 = 0, p1 = 0;
@@ -588,10 +588,11 @@ __device__ void slow_count_piece(const uint8_t* text, u64 a, u64 b, const TableV
     if (em) {
         const u64 at = atomicAdd(em->n_out, 1ull);
         if (at < em->cap) em->out[at] = TokenRec{p0, p1, rec, first_b};
-        return;
+        return 1;
     }
     __threadfence();
     long_add(gt, rec, 1ull);
+    return 1;
 }
 
 __device__ __forceinline__ bool ascii_space(u32 b) { return b == 0x20 || (b >= 0x09 && b <= 0x0D); }
@@ -601,6 +602,7 @@ __device__ __forceinline__ bool ascii_space(u32 b) { return b == 0x20 || (b >= 0
 __global__ void wc_slow_kernel(const uint8_t* __restrict__ text, u64 n, TableView gt, EmitView em, int emit) {
     u64 count = *gt.n_deferred;
     if (count > gt.deferred_cap) count = gt.deferred_cap;
+    u32 tokens = 0;
     for (u64 idx = (u64)blockIdx.x * blockDim.x + threadIdx.x; idx < count; idx += (u64)gridDim.x * blockDim.x) {
         const u64 e = gt.deferred[idx];
         u64 s = e;
@@ -616,7 +618,7 @@ __global__ void wc_slow_kernel(const uint8_t* __restrict__ text, u64 n, TableVie
                 boundary = d.valid && uni_space(d.cp);
             }
             if (boundary) {
-                if (in_piece) slow_count_piece(text, piece, pos, gt, emit ? &em : nullptr);
+                if (in_piece) tokens += slow_count_piece(text, piece, pos, gt, emit ? &em : nullptr);
                 in_piece = false;
             } else if (!in_piece) {
                 piece = pos;
@@ -625,6 +627,9 @@ __global__ void wc_slow_kernel(const uint8_t* __restrict__ text, u64 n, TableVie
             pos += d.len;
         }
     }
+    // token total: one atomic per warp (a per-token atomic on one address was most of this kernel's time)
+    for (int d = 16; d > 0; d >>= 1) tokens += __shfl_xor_sync(0xFFFFFFFFu, tokens, d);
+    if ((threadIdx.x & 31) == 0 && tokens) atomicAdd(gt.n_tokens, (u64)tokens);
 }
 
 __global__ void wc_reset_deferred_kernel(TableView gt) { *gt.n_deferred = 0; }
@@ -635,7 +640,7 @@ __global__ void wc_reset_deferred_kernel(TableView gt) { *gt.n_deferred = 0; }
 __global__ void wc_normalize_kernel(const uint8_t* __restrict__ text, const u64* __restrict__ offsets, u64 n_frag,
                                     TableView gt, EmitView em) {
     for (u64 f = (u64)blockIdx.x * blockDim.x + threadIdx.x; f < n_frag; f += (u64)gridDim.x * blockDim.x)
-        slow_count_piece(text, offsets[f], offsets[f + 1], gt, &em);
+        if (slow_count_piece(text, offsets[f], offsets[f + 1], gt, &em)) atomicAdd(gt.n_tokens, 1ull);
 }
 
 // ---- host-side launchers (called from capi.cu) -----------------------------------
@@ -689,7 +694,7 @@ static cudaError_t wc_launch_impl(const uint8_t* text, u64 n, const TableView& g
         *launches += 1;
     }
     if (ev_after_fast) cudaEventRecord(*ev_after_fast, stream);
-    wc_slow_kernel<<<sm_count * 2, 128, 0, stream>>>(text, n, gt, em, EMIT ? 1 : 0);
+    wc_slow_kernel<<<sm_count * 16, 128, 0, stream>>>(text, n, gt, em, EMIT ? 1 : 0);
     wc_reset_deferred_kernel<<<1, 1, 0, stream>>>(gt);
     *launches += 2;
     return cudaGetLastError();

@@ -156,3 +156,28 @@ def test_two_byte_sequences_across_chunk_half_and_row_boundaries(capi, cuda, por
         check(capi, cuda, port, text)
         for cut in (1, 2, 3):
             check(capi, cuda, port, text[:len(text) - cut])
+
+
+def test_typographic_punctuation_stays_inside_tokens(capi, cuda, port):
+    """U+2010..U+2027 / U+2030..U+203F (E2 80 xx) are punctuation: kept inside a token, trimmed at its edges,
+    never whitespace; their neighbours in the block that ARE whitespace (U+2009, U+2028, U+202F) split"""
+    unit = ("don’t “quoted” well—known… it’s ‘single’ a‐b x†y 5‰ rock’n’roll ’tis end’ "
+            "thin space para sep nnbsp zero​width bidi‪x €5 ").encode()
+    text = unit * 400
+    got, _ = gpu_wordcount(capi, cuda, [text])
+    assert got == port.wordcount([text])
+    assert got["don’t".encode()] == 400 and got["quoted".encode()] == 400 and got["well—known".encode()] == 400
+    assert got["rock’n’roll".encode()] == 400 and got["tis".encode()] == 400 and got["end".encode()] == 400
+    assert got["thin".encode()] == 400 and got["space".encode()] == 400 and got["nnbsp".encode()] == 400
+
+
+@pytest.mark.parametrize("shift", [0, 13, 14, 15, 16, 509, 510, 511, 512, 1021, 1022, 1023, 1024])
+def test_three_byte_punctuation_across_boundaries(capi, cuda, port, shift):
+    """E2 | 80 | xx split over 16-byte chunks, halves and rows in every way, complete and truncated"""
+    rng = random.Random(shift + 5)
+    body = " ".join("".join(rng.choice(["a", "B", "’", "—", "…", "é", "x", "“"]) for _ in range(rng.randint(1, 6)))
+                    for _ in range(500)).encode()
+    for tail in (b"", b"\xe2", b"\xe2\x80", b"\xe2\x80\x99", b"\xe2\x80 z", b"\xe2\x80\x80", b"\xe2\x81\x99", b"\x80\x99"):
+        text = b"q" * shift + b" " + body + tail
+        check(capi, cuda, port, text)
+        check(capi, cuda, port, text[:len(text) - 1])
