@@ -103,41 +103,50 @@ struct HiMasks { u32 s7, a7, h7, c7, l7, x7, e7, z7, k7; };   // whitespace, ASC
 __device__ __forceinline__ HiMasks classify16_hi(const uint4& x, u32 prev_c3, uint4& f) {
     const u32 M = 0x80808080u;
     const u32 xs[4] = {x.x, x.y, x.z, x.w};
-    u32 fs[4], s[4], al[4], hi[4], co[4], ld[4], xd[4], e2[4], z8[4], k3[4];
+    u32 fs[4];
+    u32 acc[9][2];        // 128 * (8-bit mask) of words {0,1} and {2,3}, per class
     u32 c3_prev = prev_c3;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-        const u32 xw = xs[w], v = xw & 0x7F7F7F7Fu, y = v | 0x20202020u, nx = ~xw;
-        const u32 t = (y + 0x1F1F1F1Fu) & ~(y + 0x05050505u) & M & nx;          // ASCII letters
-        const u32 u = (v + 0x50505050u) & ~(v + 0x46464646u) & M & nx;          // ASCII digits
-        const u32 z = (v ^ 0x20202020u) + 0x7F7F7F7Fu;
-        s[w] = (~z | ((v + 0x77777777u) & ~(v + 0x72727272u))) & M & nx;
-        al[w] = t | u;
-        hi[w] = xw & M;
-        co[w] = xw & ~(xw << 1) & M;                                              // 10xxxxxx
-        ld[w] = xw & (v + 0x3D3D3D3Du) & ~(v + 0x20202020u) & M;                 // C3..DF
-        const u32 c3 = xw & ~((v ^ 0x43434343u) + 0x7F7F7F7Fu) & M;              // == 0xC3
-        const u32 after_c3 = __funnelshift_l(c3_prev, c3, 8);                     // the byte in front is 0xC3
-        c3_prev = c3;
-        const u32 lat = co[w] & after_c3;                                         // second byte of U+00C0..U+00FF
-        const u32 fold_hi = lat & ~(v + 0x61616161u);                             // 80..9E -> A0..BE (97 is deferred anyway)
-        xd[w] = lat & ~(((v & 0x5F5F5F5Fu) ^ 0x17171717u) + 0x7F7F7F7Fu);         // C3 97 (x) and C3 B7 (division sign)
-        fs[w] = xw | ((t | fold_hi) >> 2);
-        e2[w] = xw & ~((v ^ 0x62626262u) + 0x7F7F7F7Fu) & M;                      // == 0xE2
-        z8[w] = xw & ~(v + 0x7F7F7F7Fu) & M;                                      // == 0x80
-        k3[w] = co[w] & (((v + 0x70707070u) & ~(v + 0x58585858u)) | (v + 0x50505050u));   // 90..A7 or B0..BF
+    for (int pair = 0; pair < 2; ++pair) {       // two words at a time keeps the live flag words few
+        u32 fl[9][2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int w = 2 * pair + k;
+            const u32 xw = xs[w], v = xw & 0x7F7F7F7Fu, y = v | 0x20202020u, nx = ~xw;
+            const u32 t = (y + 0x1F1F1F1Fu) & ~(y + 0x05050505u) & M & nx;          // ASCII letters
+            const u32 u = (v + 0x50505050u) & ~(v + 0x46464646u) & M & nx;          // ASCII digits
+            const u32 z = (v ^ 0x20202020u) + 0x7F7F7F7Fu;
+            fl[0][k] = (~z | ((v + 0x77777777u) & ~(v + 0x72727272u))) & M & nx;    // whitespace
+            fl[1][k] = t | u;                                                         // ASCII alnum
+            fl[2][k] = xw & M;                                                        // >= 0x80
+            const u32 co = xw & ~(xw << 1) & M;                                       // 10xxxxxx
+            fl[3][k] = co;
+            fl[4][k] = xw & (v + 0x3D3D3D3Du) & ~(v + 0x20202020u) & M;              // C3..DF
+            const u32 c3 = xw & ~((v ^ 0x43434343u) + 0x7F7F7F7Fu) & M;              // == 0xC3
+            const u32 after_c3 = __funnelshift_l(c3_prev, c3, 8);                     // the byte in front is 0xC3
+            c3_prev = c3;
+            const u32 lat = co & after_c3;                                            // second byte of U+00C0..U+00FF
+            const u32 fold_hi = lat & ~(v + 0x61616161u);                             // 80..9E -> A0..BE (97 is deferred anyway)
+            fl[5][k] = lat & ~(((v & 0x5F5F5F5Fu) ^ 0x17171717u) + 0x7F7F7F7Fu);      // C3 97 (x) and C3 B7 (division sign)
+            fs[w] = xw | ((t | fold_hi) >> 2);
+            fl[6][k] = xw & ~((v ^ 0x62626262u) + 0x7F7F7F7Fu) & M;                   // == 0xE2
+            fl[7][k] = xw & ~(v + 0x7F7F7F7Fu) & M;                                   // == 0x80
+            fl[8][k] = co & (((v + 0x70707070u) & ~(v + 0x58585858u)) | (v + 0x50505050u));   // 90..A7 or B0..BF
+        }
+#pragma unroll
+        for (int c = 0; c < 9; ++c) acc[c][pair] = gather8(fl[c][0], fl[c][1], 0);
     }
     f = make_uint4(fs[0], fs[1], fs[2], fs[3]);
     HiMasks m;
-    m.s7 = gather8(s[2], s[3], 0) * 256u + gather8(s[0], s[1], 0);
-    m.a7 = gather8(al[2], al[3], 0) * 256u + gather8(al[0], al[1], 0);
-    m.h7 = gather8(hi[2], hi[3], 0) * 256u + gather8(hi[0], hi[1], 0);
-    m.c7 = gather8(co[2], co[3], 0) * 256u + gather8(co[0], co[1], 0);
-    m.l7 = gather8(ld[2], ld[3], 0) * 256u + gather8(ld[0], ld[1], 0);
-    m.x7 = gather8(xd[2], xd[3], 0) * 256u + gather8(xd[0], xd[1], 0);
-    m.e7 = gather8(e2[2], e2[3], 0) * 256u + gather8(e2[0], e2[1], 0);
-    m.z7 = gather8(z8[2], z8[3], 0) * 256u + gather8(z8[0], z8[1], 0);
-    m.k7 = gather8(k3[2], k3[3], 0) * 256u + gather8(k3[0], k3[1], 0);
+    m.s7 = acc[0][1] * 256u + acc[0][0];
+    m.a7 = acc[1][1] * 256u + acc[1][0];
+    m.h7 = acc[2][1] * 256u + acc[2][0];
+    m.c7 = acc[3][1] * 256u + acc[3][0];
+    m.l7 = acc[4][1] * 256u + acc[4][0];
+    m.x7 = acc[5][1] * 256u + acc[5][0];
+    m.e7 = acc[6][1] * 256u + acc[6][0];
+    m.z7 = acc[7][1] * 256u + acc[7][0];
+    m.k7 = acc[8][1] * 256u + acc[8][0];
     return m;
 }
 // Pairs leads with continuation bytes on packed masks (low 16 bits = half a, high = half b).
@@ -557,6 +566,7 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
                 if (lane == 0) pc3 = (carryC3 ? 1u : 0u) | ((l31 & 1u) << 1);
                 carryC3 = (l31 & 2u) ? 0x80000000u : 0u;
                 const HiMasks ma = classify16_hi(xa, (pc3 & 1u) ? 0x80000000u : 0u, fa);
+                asm volatile("" ::: "memory");     // one chunk after the other: fewer live flag words
                 const HiMasks mb = classify16_hi(xb, (pc3 & 2u) ? 0x80000000u : 0u, fb);
                 S = pack7(ma.s7, mb.s7);
                 A = pack7(ma.a7, mb.a7);
