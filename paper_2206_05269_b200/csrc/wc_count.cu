@@ -4,8 +4,9 @@
 // loop (/root/reference/proj/src/text.cpp:9-57, proj/src/unicode.cpp:90-121,
 // proj/src/pipeline.cpp:131-139).  Bytes are read from HBM once; tokens never reach HBM.
 //
-// The kernel is bound by instruction issue, not by HBM, so every
-// choice below is about warp-instructions per corpus byte:
+// The kernel is bound by instruction issue and by the shared-memory pipe, not by HBM (DESIGN.md
+// section 4.1), so every choice below is about warp-instructions and shared-memory wavefronts
+// per corpus byte:
 //   * a ROW is 1 KiB = two interleaved 512-byte halves; lane l owns bytes [16l,16l+16) of
 //     each half, so both 16-byte global loads of a warp are fully coalesced and both
 //     16-byte shared stores are conflict free, while the per-row bookkeeping (shuffles,
@@ -22,12 +23,14 @@
 //     (everything is resolved backwards from the whitespace byte that ends the fragment);
 //   * phase 2 takes one queued token per lane: unaligned fetch of the folded bytes from
 //     the ring, length mask from a table, multiply hash, one 16-byte load of a two-key
-//     bucket of the CTA-wide combiner, shared-memory atomic count.  Misses are buffered
-//     per warp and go to the global table (ATOMG.CAS.128 / RED.ADD.64) 32 at a time;
-//   * whatever byte-class logic cannot decide exactly -- a byte >= 0x80 in the fragment,
-//     a fragment whose start is out of sight, a token longer than 16 bytes -- is appended
-//     to the deferred list and handled by wc_slow_kernel (wordcount.cu), an exact
-//     restatement of the reference's UTF-8 rules.
+//     bucket of the CTA-wide combiner, shared-memory atomic count; two tokens per lane per
+//     trip.  Misses are buffered per warp; every lane owns a drain slot whose global slot key
+//     arrives by cp.async while the passes go on, then one RED.ADD.64 (table_add --
+//     ATOMG.CAS.128 -- only for a first occurrence or a long probe sequence);
+//   * whatever byte-class logic cannot decide exactly -- a byte >= 0x80 in the fragment (the HI
+//     variant keeps two-byte letters and the E2 80 xx punctuation), a fragment whose start is
+//     out of sight, a token longer than 16 bytes -- is appended to the deferred list and handled
+//     by wc_slow_kernel (wordcount.cu), an exact restatement of the reference's UTF-8 rules.
 #include <cstdlib>
 #include <type_traits>
 

@@ -7,7 +7,7 @@ docs = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 vocab = int(sys.argv[2]) if len(sys.argv) > 2 else 50000
 corpus = capi.synth_corpus(1, 0, docs, vocab)
 dev = torch.from_numpy(corpus).cuda()
-counter = capi.Counter(table_slots=1 << 20)
+counter = capi.Counter(table_slots=(1 << 20) if vocab <= 100000 else (1 << 22))
 for _ in range(4):
     counter.reset(); counter.count_dev(dev.data_ptr(), dev.numel())
 torch.cuda.synchronize()
