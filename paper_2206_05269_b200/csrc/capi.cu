@@ -1326,8 +1326,6 @@ extern "C" int wfcu_counter_count_dev_sorted(wfcu_counter* c, const uint8_t* dev
     return rc;
 }
 
-// normalize_word over a batch of fragments (host buffers).  Fragment f is
-// bytes[sum(lens[0..f)) ...]; out_lens[f] = 0 means "nothing remains" (nullopt).
 // ---- ingest: utf8_sanitize ---------------------------------------------------------------
 extern "C" int wfcu_utf8_sanitize_dev(const uint8_t* dev_text, uint64_t n, uint8_t* dev_out, uint64_t out_cap,
                                       uint64_t* out_len, void* stream) {
@@ -1377,6 +1375,8 @@ extern "C" int wfcu_utf8_sanitize_host(const uint8_t* text, uint64_t n, uint8_t*
     return WFCU_OK;
 }
 
+// normalize_word over a batch of fragments (host buffers).  Fragment f is
+// bytes[sum(lens[0..f)) ...]; out_lens[f] = 0 means "nothing remains" (nullopt).
 extern "C" int wfcu_normalize_words_host(const uint8_t* bytes, const uint32_t* lens, uint64_t n_frag,
                                          uint8_t* out_bytes, uint64_t out_cap, uint32_t* out_lens) {
     DeviceState* d;

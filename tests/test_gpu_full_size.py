@@ -1,0 +1,90 @@
+"""GPU, at BASELINE.json's full single-GPU size (cfg3: 1 GB, 50k-word Zipf corpus): the oracle cannot
+count a gigabyte in seconds, so parity is carried by size-independent properties of the reference's
+definitions -- counts are additive over a split at whitespace (merge_counts, proj/src/reduce.cpp:83-89),
+the token total is the number of fragments with a word character (proj/src/text.cpp:45-55), every
+partition of the table merges back to the table (shuffle + merge_counts) -- plus an exact oracle
+comparison on a slice, and the host-buffer path against the resident one."""
+import numpy as np
+import pytest
+
+from helpers import to_dev
+
+pytestmark = pytest.mark.gpu
+
+DOCS = 954   # bench.py's cfg3 shard
+
+
+@pytest.fixture(scope="module")
+def corpus(capi):
+    return capi.synth_corpus(seed=1, doc_begin=0, doc_end=DOCS, vocab=50000)
+
+
+def table(counter):
+    blob, lens, counts = counter.export()
+    return blob.tobytes(), lens.tobytes(), counts.tobytes()
+
+
+def test_full_size_properties(capi, cuda, port, corpus):
+    n = corpus.size
+    dev, _ = to_dev(cuda, corpus)
+    whole = capi.Counter(table_slots=1 << 20)
+    whole.count_dev(dev.data_ptr(), n)
+    distinct, tokens, _ = whole.stats()
+    assert distinct == 50000
+
+    # token total = fragments (every fragment of this corpus holds a letter): starts of non-space runs
+    sp = (corpus == 0x20) | (corpus == 0x0A)
+    starts = int((~sp[1:] & sp[:-1]).sum()) + int(not sp[0])
+    assert tokens == starts
+
+    # additivity: split at a document boundary (whitespace), count the halves apart, merge
+    cut = (DOCS // 3) << 20
+    a, b = capi.Counter(table_slots=1 << 20), capi.Counter(table_slots=1 << 20)
+    a.count_dev(dev.data_ptr(), cut)
+    b.count_dev(dev.data_ptr() + cut, n - cut)
+    a.merge(b)
+    assert table(a) == table(whole)
+
+    # accumulation over two calls doubles every count
+    whole2 = capi.Counter(table_slots=1 << 20)
+    for _ in range(2):
+        whole2.count_dev(dev.data_ptr(), n)
+    blob, lens, counts = whole.export()
+    blob2, lens2, counts2 = whole2.export()
+    assert blob.tobytes() == blob2.tobytes() and (counts2 == 2 * counts).all()
+    assert int(counts.sum()) == tokens
+
+    # the exchange kernels: 8 fixed-capacity regions, merged back, give the same table
+    t = cuda
+    cap = 2 * (50000 // 8) + 1024
+    ent = t.empty((8 * cap, 4), dtype=t.int64, device="cuda")
+    cnt = t.zeros(10, dtype=t.int64, device="cuda")
+    whole.partition_fixed(8, ent.data_ptr(), cap, cnt.data_ptr())
+    back = capi.Counter(table_slots=1 << 20)
+    back.merge_regions(ent.data_ptr(), 8, cap, cnt.data_ptr())
+    t.cuda.synchronize()
+    host_cnt = cnt.cpu().tolist()
+    assert sum(host_cnt[:8]) == 50000 and host_cnt[8] == 0 and host_cnt[9] == 0
+    assert max(host_cnt[:8]) < 1.1 * 50000 / 8          # the owner hash spreads the keys
+    assert table(back) == table(whole)
+
+    # exact oracle comparison on a slice of the same corpus (4 MiB) ...
+    part = corpus[100 << 20:104 << 20]
+    dpart, m = to_dev(cuda, part)
+    c = capi.Counter(table_slots=1 << 18)
+    c.count_dev(dpart.data_ptr(), m)
+    assert c.to_dict() == port.wordcount([part])
+
+
+def test_host_path_equals_resident_path_at_full_size(capi, cuda, corpus):
+    n = corpus.size
+    pinned = cuda.from_numpy(corpus.copy()).pin_memory()
+    arr = pinned.numpy()
+    docs = capi.HostDocs([arr[i << 20:(i + 1) << 20] for i in range(DOCS)])
+    h = capi.Counter(table_slots=1 << 20)
+    h.count_host(docs)
+    dev = pinned.cuda()
+    d = capi.Counter(table_slots=1 << 20)
+    d.count_dev(dev.data_ptr(), n)
+    assert table(h) == table(d)
+    assert h.stats() == d.stats()
