@@ -69,3 +69,22 @@ def test_headline_config_square_sum(capi, cuda, port):
     dx = cuda.from_numpy(x).cuda()
     got = capi.map_reduce_dev(dx.data_ptr(), capi.DTYPE_F32, dx.numel(), capi.MAP_SQUARE)
     assert rel(got, port.map_reduce_serial(x, capi.MAP_SQUARE)) <= REL_TOL
+
+
+def test_headline_config_full_size(capi, cuda, port):
+    """BASELINE.json config 2 at its full size: sum of x and of x^2 over 2^28 fp32 (the reference bench's
+    mt19937_64 / uniform(0,1) recipe, proj/src/cli.cpp:122-124) against the oracle's serial fold
+    (proj/src/engine.cpp:15-20, 82-86) within the north star's 1e-5 relative tolerance, and the sum of two
+    halves equal to the whole (the split the multi-GPU reduction makes)."""
+    n = 1 << 28
+    x = capi.synth_uniform(1, n, np.float32)
+    dx = cuda.from_numpy(x).cuda()
+    for kind in (capi.MAP_IDENTITY, capi.MAP_SQUARE):
+        got = capi.map_reduce_dev(dx.data_ptr(), capi.DTYPE_F32, n, kind)
+        want = port.map_reduce_serial(x, kind)
+        assert rel(got, want) <= 1e-5, (kind, got, want)
+        assert rel(got, want) <= 1e-9           # fp64 accumulation; the serial left fold itself drifts by ~sqrt(n) ulp
+        half = n // 2
+        parts = (capi.map_reduce_dev(dx.data_ptr(), capi.DTYPE_F32, half, kind) +
+                 capi.map_reduce_dev(dx.data_ptr() + 4 * half, capi.DTYPE_F32, half, kind, position_base=half))
+        assert rel(parts, got) <= 1e-13
