@@ -27,6 +27,7 @@
 #include <stdexcept>
 #include <string>
 #include <string_view>
+#include <ostream>
 #include <vector>
 
 namespace wfc {
@@ -167,5 +168,11 @@ struct DistinctivenessReport {
 };
 DistinctivenessReport distinctive_words(const CountMap& target, const CountMap& others, std::string label,
                                         std::size_t k);
+
+// ---- report (reference: wfc/report.hpp, the text writers; the JSON ones need the vendored json.hpp) ----
+std::string format_double(double v);                                                    // "%.12g"
+void write_frequency_tsv(std::ostream& out, const FrequencyTable& table);               // word<TAB>count<TAB>relfreq
+void write_compare_tsv(std::ostream& out, const FrequencyTable& table, const DistinctivenessReport& report);
+void write_timings_tsv(std::ostream& out, const StageTimings& timings);                 // timing<TAB>stage<TAB>ns
 
 }  // namespace wfc

@@ -560,3 +560,32 @@ DistinctivenessReport distinctive_words(const CountMap& target, const CountMap& 
 }
 
 }  // namespace wfc
+
+// ---- report (proj/src/report.cpp:7-55): host formatting of what the device path produced -----------
+namespace wfc {
+
+std::string format_double(double v) {
+    char buf[64];
+    std::snprintf(buf, sizeof(buf), "%.12g", v);
+    return buf;
+}
+
+void write_frequency_tsv(std::ostream& out, const FrequencyTable& table) {
+    for (const auto& row : table.rows) out << row.word << '\t' << row.count << '\t' << format_double(row.rel_freq) << '\n';
+}
+
+void write_compare_tsv(std::ostream& out, const FrequencyTable& table, const DistinctivenessReport& report) {
+    for (const auto& row : table.rows)
+        out << table.label << "\ttop\t" << row.word << '\t' << row.count << '\t' << format_double(row.rel_freq) << '\n';
+    for (const auto& row : report.rows)
+        out << report.label << "\tdistinct\t" << row.word << '\t' << format_double(row.score) << '\n';
+}
+
+void write_timings_tsv(std::ostream& out, const StageTimings& t) {
+    out << "timing\tmap\t" << t.map_ns << '\n' << "timing\tsort\t" << t.sort_ns << '\n'
+        << "timing\tencode\t" << t.encode_ns << '\n' << "timing\texchange\t" << t.exchange_ns << '\n'
+        << "timing\treduce\t" << t.reduce_ns << '\n' << "timing\trepair\t" << t.repair_ns << '\n'
+        << "timing\ttotal\t" << t.total_ns << '\n';
+}
+
+}  // namespace wfc

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <map>
 #include <random>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -396,6 +397,34 @@ static void analysis_cases() {
     CHECK(top.total_words == 12);
 }
 
+static void report_cases() {
+    // cli_test.cpp:45-63: the byte-exact table of `wfc wordcount --input two-docs --workers 2 --format tsv`
+    // (counts_for_directory -> run_wordcount -> top_k(.., 25) -> write_frequency_tsv, cli.cpp:79-104)
+    const RunResult r = run_wordcount(kTwoDocs, 2);
+    std::ostringstream out;
+    write_frequency_tsv(out, top_k(r.counts, "two-docs", 25));
+    CHECK(out.str() ==
+          "mapreduce\t2\t0.166666666667\n"
+          "test\t2\t0.166666666667\n"
+          "to\t2\t0.166666666667\n"
+          "a\t1\t0.0833333333333\n"
+          "algorithm\t1\t0.0833333333333\n"
+          "cool\t1\t0.0833333333333\n"
+          "i\t1\t0.0833333333333\n"
+          "is\t1\t0.0833333333333\n"
+          "want\t1\t0.0833333333333\n");
+    CHECK(format_double(1.0986122886681098) == "1.09861228867");
+    const FrequencyTable t = top_k(CountMap{{"war", 2}, {"peace", 1}}, "A", 1);
+    const DistinctivenessReport d = distinctive_words(CountMap{{"war", 2}, {"peace", 1}}, CountMap{{"peace", 2}, {"love", 1}}, "A", 1);
+    std::ostringstream cmp;
+    write_compare_tsv(cmp, t, d);
+    CHECK(cmp.str() == "A\ttop\twar\t2\t0.666666666667\nA\tdistinct\twar\t1.09861228867\n");
+    std::ostringstream tim;
+    write_timings_tsv(tim, r.timings);
+    CHECK(tim.str().rfind("timing\tmap\t", 0) == 0);
+    CHECK(tim.str().find("timing\ttotal\t") != std::string::npos);
+}
+
 int main() {
     try {
         text_cases();
@@ -405,6 +434,7 @@ int main() {
         range_partition_cases();
         engine_cases();
         analysis_cases();
+        report_cases();
     } catch (const std::exception& e) {
         std::printf("FAILED with exception: %s\n", e.what());
         return 2;
