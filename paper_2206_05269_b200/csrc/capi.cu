@@ -498,10 +498,74 @@ extern "C" int wfcu_counter_stats(wfcu_counter* c, void* stream, uint64_t* disti
 }
 
 namespace {
-struct DevBuf {   // RAII device allocation
+// Scratch cache: the token / export paths need gigabyte-sized scratch per call, and cudaMalloc + cudaFree
+// of such buffers cost more host time than their kernels.  Freed blocks are kept (per device, up to
+// kScratchKeepBytes) and handed out again to requests they fit within a factor of two.  scratch_free
+// waits for the device like cudaFree does, so callers keep cudaFree's ordering guarantees.
+constexpr size_t kScratchKeepBytes = size_t(24) << 30;
+struct ScratchBlock { void* p; size_t bytes; int device; };
+std::mutex g_scratch_mu;
+std::vector<ScratchBlock> g_scratch_free;
+std::vector<ScratchBlock> g_scratch_live;
+
+cudaError_t scratch_alloc(void** out, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lock(g_scratch_mu);
+        size_t best = g_scratch_free.size();
+        for (size_t i = 0; i < g_scratch_free.size(); ++i) {
+            const ScratchBlock& b = g_scratch_free[i];
+            if (b.device == dev && b.bytes >= bytes && b.bytes <= 2 * bytes + 4096 &&
+                (best == g_scratch_free.size() || b.bytes < g_scratch_free[best].bytes))
+                best = i;
+        }
+        if (best != g_scratch_free.size()) {
+            *out = g_scratch_free[best].p;
+            g_scratch_live.push_back(g_scratch_free[best]);
+            g_scratch_free.erase(g_scratch_free.begin() + best);
+            return cudaSuccess;
+        }
+    }
+    cudaError_t e = cudaMalloc(out, bytes);
+    if (e != cudaSuccess) {   // give the cached blocks back and try once more
+        cudaGetLastError();
+        std::lock_guard<std::mutex> lock(g_scratch_mu);
+        for (const ScratchBlock& b : g_scratch_free) cudaFree(b.p);
+        g_scratch_free.clear();
+        e = cudaMalloc(out, bytes);
+        if (e != cudaSuccess) return e;
+    }
+    std::lock_guard<std::mutex> lock(g_scratch_mu);
+    g_scratch_live.push_back({*out, bytes, dev});
+    return cudaSuccess;
+}
+
+void scratch_free(void* p) {
+    if (!p) return;
+    cudaDeviceSynchronize();          // what cudaFree would have done
+    std::lock_guard<std::mutex> lock(g_scratch_mu);
+    for (size_t i = 0; i < g_scratch_live.size(); ++i) {
+        if (g_scratch_live[i].p != p) continue;
+        g_scratch_free.push_back(g_scratch_live[i]);
+        g_scratch_live.erase(g_scratch_live.begin() + i);
+        size_t kept = 0;
+        for (const ScratchBlock& b : g_scratch_free) kept += b.bytes;
+        while (kept > kScratchKeepBytes && !g_scratch_free.empty()) {   // oldest first
+            kept -= g_scratch_free.front().bytes;
+            cudaFree(g_scratch_free.front().p);
+            g_scratch_free.erase(g_scratch_free.begin());
+        }
+        return;
+    }
+    cudaFree(p);                      // not ours
+}
+
+struct DevBuf {   // RAII device scratch
     void* p = nullptr;
-    cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes ? bytes : 16); }
-    ~DevBuf() { cudaFree(p); }
+    cudaError_t alloc(size_t bytes) { return scratch_alloc(&p, bytes); }
+    ~DevBuf() { scratch_free(p); }
     template <typename T> T* as() { return static_cast<T*>(p); }
 };
 }  // namespace
@@ -1070,8 +1134,8 @@ struct wfcu_tokens {
 
 static void tokens_free(wfcu_tokens* t) {
     if (!t) return;
-    cudaFree(t->recs);
-    cudaFree(t->arena);
+    scratch_free(t->recs);
+    scratch_free(t->arena);
     delete t;
 }
 
