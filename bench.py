@@ -395,6 +395,15 @@ def run_b200(args) -> None:
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_value = job_bytes / float(t.item()) / 1e9
+    # context for the end-to-end number: a bare pinned host -> device copy of the same shard
+    dev.copy_(host, non_blocking=True)
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record()
+    dev.copy_(host, non_blocking=True)
+    c1.record()
+    torch.cuda.synchronize()
+    h2d_gbps = nbytes / (c0.elapsed_time(c1) * 1e-3) / 1e9 if nbytes else 0.0
 
     if rank == 0:
         peak, peak_src = measured_peak_gbs()
@@ -414,7 +423,8 @@ def run_b200(args) -> None:
                          "kernel": "wc_count_kernel", "kernel_ms": k_ms, "kernel_launches": kernel_launches,
                          "algorithmic_bytes_per_launch": nbytes, "peak_source": peak_src},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": d2h,
-                    "steps": e2e_steps, "api": "wfcu_counter_count_host + wfcu_counter_export"},
+                    "steps": e2e_steps, "api": "wfcu_counter_count_host + wfcu_counter_export",
+                    "bare_pinned_h2d_copy_GBps_per_gpu": h2d_gbps},
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
         }
