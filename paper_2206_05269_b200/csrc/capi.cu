@@ -68,6 +68,10 @@ cudaError_t tokens_rle_insert(const TokenRec* recs, u64 n, const uint8_t* arena,
 u64 sanitize_scratch_bytes(u64 n);
 cudaError_t sanitize_launch(const uint8_t* text, u64 n, uint8_t* out, u64 out_cap, void* scratch, u64* dev_total,
                             int sm_count, cudaStream_t s, u64* launches);
+cudaError_t tokens_compact_split(const TokenRec* recs, u64 n, u64* keys_a, TokenRec* rest, u64 rest_cap, u64* dev_counts,
+                                 int sm, cudaStream_t s, u64* launches);
+cudaError_t tokens_compact_count(u64* keys_a, u64* keys_b, u64 nk, u64 vary, u64* hist, u64* tmp, u64* flags, u64* run_start,
+                                 const TableView& t, int sm, cudaStream_t s, u64* launches);
 // analysis.cpp
 uint64_t analysis_top_k(const uint8_t* bytes, const uint32_t* lens, const uint64_t* counts, uint64_t n, uint64_t k,
                         uint64_t* out_idx, double* out_rel, uint64_t* total);
@@ -1383,9 +1387,59 @@ extern "C" int wfcu_counter_count_dev_sorted(wfcu_counter* c, const uint8_t* dev
     if (!c) return fail(WFCU_ERR_INVALID_ARGUMENT, "counter is null");
     if (n == 0) return WFCU_OK;
     wfcu_tokens* t = nullptr;
-    if (int rc = tokenize_unordered(dev_text, n, (cudaStream_t)stream, &t)) return rc;
-    int rc = wfcu_tokens_sort(t, stream);
-    if (rc == WFCU_OK) rc = wfcu_tokens_reduce_sorted(t, c, stream);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (int rc = tokenize_unordered(dev_text, n, s, &t)) return rc;
+    // Tokens of at most 8 bytes (the bulk) are sorted and run-length encoded as 64-bit keys; the others keep
+    // the 32-byte record path.  Counting does not care about text order, so nothing is sorted by position.
+    int rc = WFCU_OK;
+    if (t->n) {
+        const u64 nt = t->n, rest_cap = nt / 4 + 1024;
+        DevBuf keys_a, keys_b, rest, counts;
+        cudaError_t e = keys_a.alloc(sizeof(u64) * nt);
+        if (e == cudaSuccess) e = keys_b.alloc(sizeof(u64) * nt);
+        if (e == cudaSuccess) e = rest.alloc(sizeof(TokenRec) * rest_cap);
+        if (e == cudaSuccess) e = counts.alloc(sizeof(u64) * 4);
+        LaunchTally tally;
+        u64 h[4] = {0, 0, 0, 0};
+        if (e == cudaSuccess) e = tokens_compact_split(t->recs, nt, keys_a.as<u64>(), rest.as<TokenRec>(), rest_cap, counts.as<u64>(),
+                                                        c->sm_count, s, &tally.n);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h, counts.p, sizeof(h), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) {
+            tokens_free(t);
+            return fail(WFCU_ERR_CUDA, "count_dev_sorted: %s", cudaGetErrorString(e));
+        }
+        const u64 nk = h[0], nr = h[1];
+        if (nr > rest_cap) {
+            // many long tokens: the record path for everything
+            rc = wfcu_tokens_sort(t, stream);
+            if (rc == WFCU_OK) rc = wfcu_tokens_reduce_sorted(t, c, stream);
+        } else {
+            if (nk) {
+                const u64 hw = sort_hist_words(nk);
+                DevBuf hist, tmp, flags, starts;
+                e = hist.alloc(sizeof(u64) * hw);
+                if (e == cudaSuccess) e = tmp.alloc(sizeof(u64) * std::max(scan_tmp_words(hw), scan_tmp_words(nk)));
+                if (e == cudaSuccess) e = flags.alloc(sizeof(u64) * nk);
+                if (e == cudaSuccess) e = starts.alloc(sizeof(u64) * nk);
+                if (e == cudaSuccess) e = tokens_compact_count(keys_a.as<u64>(), keys_b.as<u64>(), nk, h[2] ^ h[3], hist.as<u64>(),
+                                                                tmp.as<u64>(), flags.as<u64>(), starts.as<u64>(), c->v, c->sm_count, s,
+                                                                &tally.n);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+                if (e != cudaSuccess) {
+                    tokens_free(t);
+                    return fail(WFCU_ERR_CUDA, "count_dev_sorted: %s", cudaGetErrorString(e));
+                }
+            }
+            if (nr) {   // the longer tokens: records, in a token list of their own (it borrows the arena)
+                wfcu_tokens sub = *t;
+                sub.recs = rest.as<TokenRec>();
+                sub.n = nr;
+                rc = sort_device_tokens(&sub, /*by_position=*/false, s);
+                if (rc == WFCU_OK) rc = wfcu_tokens_reduce_sorted(&sub, c, stream);
+            }
+        }
+    }
     tokens_free(t);
     return rc;
 }
