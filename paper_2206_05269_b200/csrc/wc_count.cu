@@ -546,7 +546,6 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
 
         for (u32 row = r_begin; row < r_end; ++row) {
             const uint4 xa = nxa, xb = nxb;
-            load_row(row + 1, nxa, nxb);
             const u32 slotpos = (row & 1u) * kSlotStride;
 
             // ------------------------------ phase 1 ------------------------------
@@ -725,6 +724,10 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
             const u32 still_carried = qtail - qhead;    // 0 if room had to be made
             qtail += total;
             __syncwarp();
+
+            // the next row's bytes are requested here, not at the top of the loop: phase 2 (thousands of
+            // cycles) covers the latency, and phase 1 -- the register peak -- does not carry them
+            load_row(row + 1, nxa, nxb);
 
             // ------------------------------ phase 2 ------------------------------
             // full 32-token passes; the remainder waits for the next row's tokens ...
