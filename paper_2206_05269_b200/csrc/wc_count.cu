@@ -769,8 +769,10 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
 
 // One kernel per variant (a kernel holding both bodies compiles the ASCII one measurably worse);
 // both are launched, and every CTA runs in exactly one of them: it samples one 16-byte chunk per
-// thread, spread evenly over its own rows, and takes HI if more than one in 64 holds a byte >= 0x80
-// (then most 1 KiB rows do).  The CTA of the other variant sees the same sample and returns.
+// thread, spread evenly over its own rows, and takes HI as soon as two of them hold a byte >= 0x80
+// (HI costs 4 % on pure ASCII; the ASCII body on text with one such fragment in a few hundred
+// already loses more than that to the slow kernel).  The CTA of the other variant sees the same
+// sample and returns.
 // force: 0 / 1 = variant for every CTA (tests), anything else = sample.
 template <int WARPS, int SETS, int MSLOTS, bool HI>
 __global__ void __launch_bounds__(WARPS * 32, 1)
@@ -785,7 +787,7 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, int 
             const uint4 v = *reinterpret_cast<const uint4*>(text + at);
             hit = ((v.x | v.y | v.z | v.w) & 0x80808080u) != 0;
         }
-        hi = __syncthreads_count(hit) * 64 > WARPS * 32;
+        hi = __syncthreads_count(hit) >= 2;
     }
     if (hi != HI) return;
     wc_count_body<WARPS, SETS, MSLOTS, HI>(text, n, rows_per_warp, gt);
