@@ -77,3 +77,46 @@ def test_pack_unpack_roundtrip(capi):
     words = [b"a", b"", b"hello", bytes(range(256))]
     blob, lens = capi.pack_words(words)
     assert capi.unpack_words(blob, lens) == words
+
+
+def test_host_docs_marshals_pointers_and_lengths(capi):
+    """HostDocs is the (pointer, length) pair of arrays wfcu_counter_count_host takes; built once, reusable"""
+    blob = np.frombuffer(b"alpha beta\ngamma\n\ndelta ", dtype=np.uint8).copy()
+    views = [blob[0:11], blob[11:17], blob[17:18], blob[18:24], blob[24:24]]
+    hd = capi.HostDocs(views + [b"tail bytes"])
+    assert hd.n == 6
+    base = blob.ctypes.data
+    assert [hd.ptrs[i] for i in range(5)] == [base, base + 11, base + 17, base + 18, None]    # empty document: NULL
+    assert [hd.lens[i] for i in range(6)] == [11, 6, 1, 6, 0, 10]
+    assert ctypes.string_at(hd.ptrs[5], 10) == b"tail bytes"
+
+
+def test_async_exchange_region_capacity():
+    """the fixed region capacity: 2 x the uniform share of the hint (+ slack), never above what the table can hold"""
+    from paper_2206_05269_b200.exchange import AsyncExchange
+
+    class Table:
+        def max_entries(self): return 524288
+
+    class Torch:
+        int64 = "i64"
+        @staticmethod
+        def zeros(n, dtype=None, device=None): return [0] * n
+
+    class Ops:
+        torch = Torch
+        def empty_entries(self, n):
+            class E:
+                device = "cpu"
+                rows = n
+            return E()
+
+    class Dist:
+        def __init__(self, w): self.w = w
+        def get_world_size(self, group=None): return self.w
+
+    assert AsyncExchange(Table(), Ops(), Dist(8), entries_hint=50000).cap == 2 * 6250 + 1024
+    assert AsyncExchange(Table(), Ops(), Dist(2), entries_hint=50000).cap == 2 * 25000 + 1024
+    assert AsyncExchange(Table(), Ops(), Dist(4)).cap == 524288                     # no hint: cannot overflow
+    assert AsyncExchange(Table(), Ops(), Dist(1), entries_hint=10 ** 9).cap == 524288
+    assert AsyncExchange(Table(), Ops(), Dist(8), entries_hint=50000).send.rows == 8 * (2 * 6250 + 1024)
