@@ -163,6 +163,30 @@ def test_count_host_zero_copy_path(capi, cuda, port):
     assert c.to_dict() == want
 
 
+def test_count_host_packing_slices(capi, cuda, port, monkeypatch):
+    """pageable documents are packed into pinned staging by a pool of host threads in 256 KiB slices of the
+    packed image: documents shorter, equal to and much longer than a slice, empty documents at slice edges,
+    several staging chunks (the last word of a document must not join the first of the next)"""
+    rng = random.Random(256)
+    lens = [0, 1, (256 << 10) - 1, 0, 0, 256 << 10, 1, 0, (256 << 10) + 1, 700001, 5, 0, 2_500_000, 0, 3, 1 << 20, 0]
+    docs = []
+    for ln in lens:
+        base = random_text(rng, min(ln, 70001), "ascii")
+        t = bytearray((base * (ln // max(len(base), 1) + 1))[:ln])
+        if ln:
+            t[0] = ord("a")
+            t[-1] = ord("z")          # word characters at both edges of every document
+        docs.append(bytes(t))
+    want = port.wordcount(docs)
+    counter = capi.Counter(table_slots=1 << 18)
+    counter.count_host(docs)
+    got = counter.to_dict()
+    assert got == want
+    counter.reset()
+    counter.count_host(capi.HostDocs(docs))
+    assert counter.to_dict() == want
+
+
 def test_deferred_list_overflow_is_reported(capi, cuda, port):
     """a corpus of words the fast path defers (three-byte characters) overflows a tiny slow-path list:
     loud error, and the same text counts exactly once the capacity is raised (what the C++ drop-in's
