@@ -52,15 +52,26 @@ constexpr u64 kSlotLocked = 1ull;
 
 // ---- SWAR byte classes: bit 7 of each byte lane is the answer ----------------------
 // ASCII = true: caller guarantees no byte has bit 7 set.
+// The range-test additions can run on the FMA pipe as v * one + K (IMAD R, R, Rone, imm) with a 1 the
+// compiler cannot see through (a kernel argument): the integer ALU pipe is the busiest unit of the kernel.
+// WFCU_FMA_ADDS: bit i = addition i of classify4 goes to the FMA pipe.
+#ifndef WFCU_FMA_ADDS
+#define WFCU_FMA_ADDS 0
+#endif
+template <u32 K, int BIT>
+__device__ __forceinline__ u32 add_k(u32 v, u32 one) {
+    if ((WFCU_FMA_ADDS >> BIT) & 1) return v * one + K;
+    return v + K;
+}
 template <bool ASCII>
-__device__ __forceinline__ void classify4(u32 x, u32& s, u32& t, u32& u, u32& f) {
+__device__ __forceinline__ void classify4(u32 x, u32 one, u32& s, u32& t, u32& u, u32& f) {
     const u32 M = 0x80808080u;
     const u32 v = ASCII ? x : (x & 0x7F7F7F7Fu);
     const u32 y = v | 0x20202020u;
-    t = (y + 0x1F1F1F1Fu) & ~(y + 0x05050505u) & M;          // 'a'..'z' after folding
-    u = (v + 0x50505050u) & ~(v + 0x46464646u) & M;          // '0'..'9'
-    const u32 z = (v ^ 0x20202020u) + 0x7F7F7F7Fu;           // bit 7 clear <=> byte == 0x20
-    s = (~z | ((v + 0x77777777u) & ~(v + 0x72727272u))) & M; // 0x20 or 0x09..0x0D
+    t = add_k<0x1F1F1F1Fu, 0>(y, one) & ~add_k<0x05050505u, 1>(y, one) & M;          // 'a'..'z' after folding
+    u = add_k<0x50505050u, 2>(v, one) & ~add_k<0x46464646u, 3>(v, one) & M;          // '0'..'9'
+    const u32 z = add_k<0x7F7F7F7Fu, 4>(v ^ 0x20202020u, one);                       // bit 7 clear <=> byte == 0x20
+    s = (~z | (add_k<0x77777777u, 5>(v, one) & ~add_k<0x72727272u, 6>(v, one))) & M; // 0x20 or 0x09..0x0D
     if (!ASCII) { t &= ~x; u &= ~x; s &= ~x; }
     f = x | (t >> 2);                                        // A-Z -> a-z (a-z unchanged)
 }
@@ -73,12 +84,12 @@ __device__ __forceinline__ u32 gather8(u32 f0, u32 f1, u32 acc) {
 struct Masks { u32 s7, a7, h7; };   // 16-bit masks of one 16-byte chunk, scaled by 128
 
 template <bool ASCII>
-__device__ __forceinline__ Masks classify16(const uint4& x, uint4& f) {
+__device__ __forceinline__ Masks classify16(const uint4& x, u32 one, uint4& f) {
     u32 s0, s1, s2, s3, t0, t1, t2, t3, u0, u1, u2, u3;
-    classify4<ASCII>(x.x, s0, t0, u0, f.x);
-    classify4<ASCII>(x.y, s1, t1, u1, f.y);
-    classify4<ASCII>(x.z, s2, t2, u2, f.z);
-    classify4<ASCII>(x.w, s3, t3, u3, f.w);
+    classify4<ASCII>(x.x, one, s0, t0, u0, f.x);
+    classify4<ASCII>(x.y, one, s1, t1, u1, f.y);
+    classify4<ASCII>(x.z, one, s2, t2, u2, f.z);
+    classify4<ASCII>(x.w, one, s3, t3, u3, f.w);
     Masks m;
     m.s7 = gather8(s2, s3, 0) * 256u + gather8(s0, s1, 0);
     m.a7 = gather8(t2, t3, gather8(u2, u3, 0)) * 256u + gather8(t0, t1, gather8(u0, u1, 0));
@@ -267,7 +278,7 @@ using namespace cnt3;
 // CTA picks its variant from a sample of its own part of the text (wc_count_kernel below): the
 // choice affects speed only.
 template <int WARPS, int SETS, int MSLOTS, bool HI>
-__device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, const TableView& gt) {
+__device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, u32 one, const TableView& gt) {
     extern __shared__ uint8_t smem_raw[];
     typedef Smem<WARPS, SETS, MSLOTS> SM;
     const u32 sbase = (u32)__cvta_generic_to_shared(smem_raw);
@@ -536,7 +547,7 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
                 carryT = hi_tails(in.E2, in.Z) & 0xFFFFu;
                 carryC3 = (x.w >> 24) == 0xC3u ? 0x80000000u : 0u;
             } else {
-                const Masks m = classify16<false>(x, f);
+                const Masks m = classify16<false>(x, one, f);
                 carryS = m.s7 >> 7; carryA = m.a7 >> 7; carryH = m.h7 >> 7;
             }
             if (lane == 0) *reinterpret_cast<uint4*>(ring + (r_begin & 1u) * kSlotStride + 16) = f;
@@ -555,7 +566,7 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
             const bool ascii_row = !__any_sync(kFull, anyhi != 0) && (carryH | carryL) == 0;
             u32 pH_fix = 0, pH_clear = 0;
             if (ascii_row) {
-                const Masks ma = classify16<true>(xa, fa), mb = classify16<true>(xb, fb);
+                const Masks ma = classify16<true>(xa, one, fa), mb = classify16<true>(xb, one, fb);
                 S = pack7(ma.s7, mb.s7);
                 A = pack7(ma.a7, mb.a7);
                 carryC3 = 0;
@@ -590,7 +601,7 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
                 hi_masks_finish(in, pL >> 15, pT, A, H, bad_first, pH_clear);
                 pH_fix = bad_first << 15;     // an unmatched lead at the end of the chunk in front
             } else {
-                const Masks ma = classify16<false>(xa, fa), mb = classify16<false>(xb, fb);
+                const Masks ma = classify16<false>(xa, one, fa), mb = classify16<false>(xb, one, fb);
                 S = pack7(ma.s7, mb.s7);
                 A = pack7(ma.a7, mb.a7);
                 H = pack7(ma.h7, mb.h7);
@@ -776,7 +787,7 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
 // force: 0 / 1 = variant for every CTA (tests), anything else = sample.
 template <int WARPS, int SETS, int MSLOTS, bool HI>
 __global__ void __launch_bounds__(WARPS * 32, 1)
-wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, int force, TableView gt) {
+wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, int force, u32 one, TableView gt) {
     bool hi = force == 1;
     if (force != 0 && force != 1) {
         const u64 first = (u64)blockIdx.x * WARPS * rows_per_warp * kRow;
@@ -790,7 +801,7 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, int 
         hi = __syncthreads_count(hit) >= 2;
     }
     if (hi != HI) return;
-    wc_count_body<WARPS, SETS, MSLOTS, HI>(text, n, rows_per_warp, gt);
+    wc_count_body<WARPS, SETS, MSLOTS, HI>(text, n, rows_per_warp, one, gt);
 }
 
 // ---- host-side launcher (called from wordcount.cu) ---------------------------------
@@ -824,8 +835,8 @@ cudaError_t wc_count_launch(const uint8_t* text, u64 n, const TableView& gt, int
     if (grid == 0) grid = 1;
     const u64 rows_per_warp = (n_rows + grid * kCountWarps - 1) / (grid * kCountWarps);
     static const int force = [] { const char* v = getenv("WFCU_COUNT_VARIANT"); return v ? atoi(v) : -1; }();   // tests: 0 / 1
-    if (force != 1) k_ascii<<<(unsigned)grid, kCountWarps * 32, smem, stream>>>(text, n, (u32)rows_per_warp, force, gt);
-    if (force != 0) k_hi<<<(unsigned)grid, kCountWarps * 32, smem, stream>>>(text, n, (u32)rows_per_warp, force, gt);
+    if (force != 1) k_ascii<<<(unsigned)grid, kCountWarps * 32, smem, stream>>>(text, n, (u32)rows_per_warp, force, 1u, gt);
+    if (force != 0) k_hi<<<(unsigned)grid, kCountWarps * 32, smem, stream>>>(text, n, (u32)rows_per_warp, force, 1u, gt);
     *launches += (force == 0 || force == 1) ? 1 : 2;
     return cudaGetLastError();
 }
