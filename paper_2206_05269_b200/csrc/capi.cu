@@ -58,6 +58,7 @@ struct SortScratch {
     int* flag;
 };
 u64 sort_hist_words(u64 n);
+u64 sort_n_tiles(u64 n);
 u64 scan_tmp_words(u64 n);
 cudaError_t tokens_sort(TokenRec* recs, u64 n, bool by_position, const uint8_t* arena, const SortScratch& sc, int sm,
                         cudaStream_t s, u64* launches);
@@ -69,10 +70,9 @@ cudaError_t tokens_rle_insert(const TokenRec* recs, u64 n, const uint8_t* arena,
 u64 sanitize_scratch_bytes(u64 n);
 cudaError_t sanitize_launch(const uint8_t* text, u64 n, uint8_t* out, u64 out_cap, void* scratch, u64* dev_total,
                             int sm_count, cudaStream_t s, u64* launches);
-cudaError_t tokens_compact_split(const TokenRec* recs, u64 n, u64* keys_a, TokenRec* rest, u64 rest_cap, u64* dev_counts,
-                                 int sm, cudaStream_t s, u64* launches);
 cudaError_t tokens_compact_count(u64* keys_a, u64* keys_b, u64 nk, u64 vary, u64* hist, u64* tmp, u64* flags, u64* run_start,
-                                 const TableView& t, int sm, cudaStream_t s, u64* launches);
+                                 const TableView& t, int sm, cudaStream_t s, u64* launches, const u32* tile_counts,
+                                 u64 tiled_tiles);
 // analysis.cpp
 uint64_t analysis_top_k(const uint8_t* bytes, const uint32_t* lens, const uint64_t* counts, uint64_t n, uint64_t k,
                         uint64_t* out_idx, double* out_rel, uint64_t* total);
@@ -1231,7 +1231,16 @@ static int sort_device_tokens(wfcu_tokens* t, bool by_position, cudaStream_t s) 
 }
 
 // Runs the tokenizer kernels; the records come out in no particular order.
-static int tokenize_unordered(const uint8_t* dev_text, uint64_t n, cudaStream_t s, wfcu_tokens** out) {
+// Compact mode of tokenize_unordered (counting by sort + RLE): tokens of at most 8 bytes come back as 64-bit
+// keys in the tokenizer's tiled layout, only the others as records.
+struct CompactKeys {
+    DevBuf keys, tile_counts;
+    u64 tiles = 0;     // tiles handed out (kKeyTile keys each, tile t holds tile_counts[t])
+    u64 n_keys = 0;
+    u64 vary = 0;      // bits that differ between keys
+};
+
+static int tokenize_unordered(const uint8_t* dev_text, uint64_t n, cudaStream_t s, wfcu_tokens** out, CompactKeys* ck = nullptr) {
     *out = nullptr;
     DeviceState* d;
     if (int rc = current_device_state(&d)) return rc;
@@ -1244,7 +1253,8 @@ static int tokenize_unordered(const uint8_t* dev_text, uint64_t n, cudaStream_t 
         *out = t;
         return WFCU_OK;
     }
-    u64 cap = n / 5 + 1024;                 // records; grown to the exact count on overflow
+    u64 cap = ck ? n / 16 + 1024 : n / 5 + 1024;   // records; grown to the exact count on overflow
+    u64 key_tiles = ck ? (n / 4) / (kKeyTile - 32) + (u64)d->sm_count * 32 + 64 : 0;   // a warp leaves < 32 slots of a tile unused
     u64 deferred_cap = n / 16 + 1024;       // grown on overflow
     u64 arena_cap = std::max<u64>(1 << 20, n / 4);
     for (int attempt = 0; attempt < 4; ++attempt) {
@@ -1257,6 +1267,14 @@ static int tokenize_unordered(const uint8_t* dev_text, uint64_t n, cudaStream_t 
         const u64 arena_start = 8;
         u64* cnt = counters.as<u64>();
         if (e == cudaSuccess) e = cudaMemcpyAsync(cnt + 4, &arena_start, sizeof(u64), cudaMemcpyHostToDevice, s);
+        DevBuf keys, tile_counts;
+        const u64 all_ones = ~0ull;
+        if (ck) {
+            if (e == cudaSuccess) e = keys.alloc(sizeof(u64) * kKeyTile * key_tiles);
+            if (e == cudaSuccess) e = tile_counts.alloc(sizeof(u32) * key_tiles);
+            if (e == cudaSuccess) e = cudaMemsetAsync(tile_counts.p, 0, sizeof(u32) * key_tiles, s);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(cnt + 11, &all_ones, sizeof(u64), cudaMemcpyHostToDevice, s);   // AND of the keys
+        }
         if (e != cudaSuccess) {
             tokens_free(t);
             return fail(WFCU_ERR_CUDA, "tokenize allocation: %s", cudaGetErrorString(e));
@@ -1267,9 +1285,15 @@ static int tokenize_unordered(const uint8_t* dev_text, uint64_t n, cudaStream_t 
         v.deferred = deferred.as<u64>(); v.deferred_cap = deferred_cap;
         v.arena = arena.as<uint8_t>(); v.arena_cap = arena_cap;
         EmitView em{recs.as<TokenRec>(), cap, cnt + 6};
+        if (ck) {
+            em.keys = keys.as<u64>();
+            em.key_tiles = key_tiles;
+            em.tile_counts = tile_counts.as<u32>();
+            em.kc = cnt + 8;
+        }
         LaunchTally tally;
         e = wc_tokenize_launch(dev_text, n, v, em, d->sm_count, s, &tally.n);
-        u64 h[8];
+        u64 h[12];
         if (e == cudaSuccess) e = cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) {
@@ -1278,6 +1302,11 @@ static int tokenize_unordered(const uint8_t* dev_text, uint64_t n, cudaStream_t 
         }
         const int st = (int)(h[5] & 0xFFFFFFFFu);
         const u64 produced = h[6];
+        if (ck && h[8] > key_tiles) {             // the count of tiles asked for is exact
+            key_tiles = h[8] + 64;
+            if (produced > cap) cap = produced + 1024;
+            continue;
+        }
         if (produced > cap || (st & (kStatusDeferredFull | kStatusArenaFull))) {
             // grow what overflowed and run again (n_out keeps counting past cap, so it is exact
             // unless the deferred list or the arena cut the run short)
@@ -1293,6 +1322,13 @@ static int tokenize_unordered(const uint8_t* dev_text, uint64_t n, cudaStream_t 
         t->n = produced;
         t->arena_used = h[4];
         t->arena_cap = arena_cap;
+        if (ck) {
+            ck->keys.p = keys.p; keys.p = nullptr;
+            ck->tile_counts.p = tile_counts.p; tile_counts.p = nullptr;
+            ck->tiles = h[8];
+            ck->n_keys = h[9];
+            ck->vary = h[9] ? (h[10] ^ h[11]) : 0;
+        }
         *out = t;
         return WFCU_OK;
     }
@@ -1455,57 +1491,34 @@ extern "C" int wfcu_counter_count_dev_sorted(wfcu_counter* c, const uint8_t* dev
     if (n == 0) return WFCU_OK;
     wfcu_tokens* t = nullptr;
     cudaStream_t s = (cudaStream_t)stream;
-    if (int rc = tokenize_unordered(dev_text, n, s, &t)) return rc;
-    // Tokens of at most 8 bytes (the bulk) are sorted and run-length encoded as 64-bit keys; the others keep
-    // the 32-byte record path.  Counting does not care about text order, so nothing is sorted by position.
+    // Tokens of at most 8 bytes (the bulk) leave the tokenizer as 64-bit keys and are sorted and run-length
+    // encoded as such; the others keep the 32-byte record path.  Counting does not care about text order, so
+    // nothing is sorted by position.
+    CompactKeys ck;
+    if (int rc = tokenize_unordered(dev_text, n, s, &t, &ck)) return rc;
     int rc = WFCU_OK;
-    if (t->n) {
-        const u64 nt = t->n, rest_cap = nt / 4 + 1024;
-        DevBuf keys_a, keys_b, rest, counts;
-        cudaError_t e = keys_a.alloc(sizeof(u64) * nt);
-        if (e == cudaSuccess) e = keys_b.alloc(sizeof(u64) * nt);
-        if (e == cudaSuccess) e = rest.alloc(sizeof(TokenRec) * rest_cap);
-        if (e == cudaSuccess) e = counts.alloc(sizeof(u64) * 4);
+    if (ck.n_keys) {
+        const u64 nk = ck.n_keys;
+        const u64 hw = 256 * std::max(ck.tiles, sort_n_tiles(nk));
+        DevBuf keys_b, hist, tmp, flags, starts;
         LaunchTally tally;
-        u64 h[4] = {0, 0, 0, 0};
-        if (e == cudaSuccess) e = tokens_compact_split(t->recs, nt, keys_a.as<u64>(), rest.as<TokenRec>(), rest_cap, counts.as<u64>(),
-                                                        c->sm_count, s, &tally.n);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(h, counts.p, sizeof(h), cudaMemcpyDeviceToHost, s);
+        cudaError_t e = keys_b.alloc(sizeof(u64) * nk);
+        if (e == cudaSuccess) e = hist.alloc(sizeof(u64) * hw);
+        if (e == cudaSuccess) e = tmp.alloc(sizeof(u64) * std::max(scan_tmp_words(hw), scan_tmp_words(nk)));
+        if (e == cudaSuccess) e = flags.alloc(sizeof(u64) * nk);
+        if (e == cudaSuccess) e = starts.alloc(sizeof(u64) * nk);
+        if (e == cudaSuccess) e = tokens_compact_count(ck.keys.as<u64>(), keys_b.as<u64>(), nk, ck.vary, hist.as<u64>(), tmp.as<u64>(),
+                                                        flags.as<u64>(), starts.as<u64>(), c->v, c->sm_count, s, &tally.n,
+                                                        ck.tile_counts.as<u32>(), ck.tiles);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) {
             tokens_free(t);
             return fail(WFCU_ERR_CUDA, "count_dev_sorted: %s", cudaGetErrorString(e));
         }
-        const u64 nk = h[0], nr = h[1];
-        if (nr > rest_cap) {
-            // many long tokens: the record path for everything
-            rc = wfcu_tokens_sort(t, stream);
-            if (rc == WFCU_OK) rc = wfcu_tokens_reduce_sorted(t, c, stream);
-        } else {
-            if (nk) {
-                const u64 hw = sort_hist_words(nk);
-                DevBuf hist, tmp, flags, starts;
-                e = hist.alloc(sizeof(u64) * hw);
-                if (e == cudaSuccess) e = tmp.alloc(sizeof(u64) * std::max(scan_tmp_words(hw), scan_tmp_words(nk)));
-                if (e == cudaSuccess) e = flags.alloc(sizeof(u64) * nk);
-                if (e == cudaSuccess) e = starts.alloc(sizeof(u64) * nk);
-                if (e == cudaSuccess) e = tokens_compact_count(keys_a.as<u64>(), keys_b.as<u64>(), nk, h[2] ^ h[3], hist.as<u64>(),
-                                                                tmp.as<u64>(), flags.as<u64>(), starts.as<u64>(), c->v, c->sm_count, s,
-                                                                &tally.n);
-                if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-                if (e != cudaSuccess) {
-                    tokens_free(t);
-                    return fail(WFCU_ERR_CUDA, "count_dev_sorted: %s", cudaGetErrorString(e));
-                }
-            }
-            if (nr) {   // the longer tokens: records, in a token list of their own (it borrows the arena)
-                wfcu_tokens sub = *t;
-                sub.recs = rest.as<TokenRec>();
-                sub.n = nr;
-                rc = sort_device_tokens(&sub, /*by_position=*/false, s);
-                if (rc == WFCU_OK) rc = wfcu_tokens_reduce_sorted(&sub, c, stream);
-            }
-        }
+    }
+    if (t->n) {   // the longer tokens: records
+        rc = sort_device_tokens(t, /*by_position=*/false, s);
+        if (rc == WFCU_OK) rc = wfcu_tokens_reduce_sorted(t, c, stream);
     }
     tokens_free(t);
     return rc;

@@ -383,41 +383,10 @@ cudaError_t tokens_rle_insert(const TokenRec* recs, u64 n, const uint8_t* arena,
 // bulk of the tokens is sorted as 8-byte keys instead of 32-byte records (a quarter of the traffic
 // per radix pass); the few longer tokens keep the record path above.
 // ---------------------------------------------------------------------------------
-__global__ void ck_split_kernel(const TokenRec* __restrict__ recs, u64 n, u64* __restrict__ keys, TokenRec* __restrict__ rest,
-                                u64 rest_cap, u64* __restrict__ counts /* [0] keys, [1] rest, [2] OR of keys, [3] AND of keys */) {
-    const u32 lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
-    u64 o = 0, a = ~0ull;
-    const u64 stride = (u64)gridDim.x * blockDim.x;
-    for (u64 base = (u64)blockIdx.x * blockDim.x + threadIdx.x - lane; base < n; base += stride) {
-        const u64 i = base + lane;
-        TokenRec r{};
-        const bool live = i < n;
-        if (live) r = recs[i];
-        const bool is_key = live && r.k1 == 0 && r.ext == 0;
-        const u32 mk = __ballot_sync(0xFFFFFFFFu, is_key), mr = __ballot_sync(0xFFFFFFFFu, live && !is_key);
-        u64 bk = 0, br = 0;
-        if (lane == 0) {
-            if (mk) bk = atomicAdd(counts + 0, (u64)__popc(mk));
-            if (mr) br = atomicAdd(counts + 1, (u64)__popc(mr));
-        }
-        bk = __shfl_sync(0xFFFFFFFFu, bk, 0);
-        br = __shfl_sync(0xFFFFFFFFu, br, 0);
-        if (is_key) {
-            keys[bk + __popc(mk & lt)] = r.k0;
-            o |= r.k0; a &= r.k0;
-        } else if (live) {
-            const u64 at = br + __popc(mr & lt);
-            if (at < rest_cap) rest[at] = r;
-        }
-    }
-    for (int d = 16; d > 0; d >>= 1) {
-        o |= __shfl_xor_sync(0xFFFFFFFFu, o, d);
-        a &= __shfl_xor_sync(0xFFFFFFFFu, a, d);
-    }
-    if (lane == 0) { atomicOr(counts + 2, o); atomicAnd(counts + 3, a); }
-}
-
-__global__ void ck_hist_kernel(const u64* __restrict__ in, u64 n, u64 n_tiles, int shift, u64* __restrict__ hist) {
+// tile_counts != nullptr: `in` is the tokenizer's tiled layout (EmitView::keys), tile t holds tile_counts[t] keys
+static_assert(kTileItems == (int)kKeyTile, "the tokenizer's key tiles are the sort's tiles");
+__global__ void ck_hist_kernel(const u64* __restrict__ in, u64 n, u64 n_tiles, int shift, u64* __restrict__ hist,
+                               const u32* __restrict__ tile_counts) {
     __shared__ u32 sh[kSortWarps][256];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const u64 tile = (u64)blockIdx.x * kSortWarps + warp;
@@ -425,7 +394,7 @@ __global__ void ck_hist_kernel(const u64* __restrict__ in, u64 n, u64 n_tiles, i
     __syncwarp();
     if (tile < n_tiles) {
         const u64 lo = tile * kTileItems;
-        const u64 hi = min(lo + (u64)kTileItems, n);
+        const u64 hi = tile_counts ? lo + tile_counts[tile] : min(lo + (u64)kTileItems, n);
         for (u64 i = lo + lane; i < hi; i += 32) atomicAdd(&sh[warp][(u32)(in[i] >> shift) & 0xFF], 1u);
     }
     __syncwarp();
@@ -434,7 +403,7 @@ __global__ void ck_hist_kernel(const u64* __restrict__ in, u64 n, u64 n_tiles, i
 }
 
 __global__ void ck_scatter_kernel(const u64* __restrict__ in, u64* __restrict__ out, u64 n, u64 n_tiles, int shift,
-                                  const u64* __restrict__ offs) {
+                                  const u64* __restrict__ offs, const u32* __restrict__ tile_counts) {
     __shared__ u64 sh[kSortWarps][256];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const u64 tile = (u64)blockIdx.x * kSortWarps + warp;
@@ -442,7 +411,7 @@ __global__ void ck_scatter_kernel(const u64* __restrict__ in, u64* __restrict__ 
     for (int d = lane; d < 256; d += 32) sh[warp][d] = offs[(u64)d * n_tiles + tile];
     __syncwarp();
     const u64 lo = tile * kTileItems;
-    const u64 hi = min(lo + (u64)kTileItems, n);
+    const u64 hi = tile_counts ? lo + tile_counts[tile] : min(lo + (u64)kTileItems, n);
     const u32 lt = (1u << lane) - 1u;
     for (u64 base = lo; base < hi; base += 32) {
         const u64 i = base + lane;
@@ -486,37 +455,33 @@ __global__ void ck_insert_kernel(const u64* __restrict__ keys, u64 n, const u64*
     if ((threadIdx.x & 31) == 0 && tokens) atomicAdd(t.n_tokens, tokens);
 }
 
-// Step 1 (asynchronous): split recs into keys_a (count -> dev_counts[0]) and rest (count -> dev_counts[1]),
-// with the OR / AND of the keys in dev_counts[2..3].
-cudaError_t tokens_compact_split(const TokenRec* recs, u64 n, u64* keys_a, TokenRec* rest, u64 rest_cap, u64* dev_counts,
-                                 int sm, cudaStream_t s, u64* launches) {
-    const u64 init[4] = {0, 0, 0, ~0ull};
-    cudaError_t e = cudaMemcpyAsync(dev_counts, init, sizeof(init), cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return e;
-    ck_split_kernel<<<blocks_for(n, 256, sm), 256, 0, s>>>(recs, n, keys_a, rest, rest_cap, dev_counts);
-    *launches += 1;
-    return cudaGetLastError();
-}
-
-// Step 2: radix sort of the nk keys on the byte positions that vary, run-length encode, add to the table.
+// Radix sort of the nk keys on the byte positions that vary, run-length encode, add to the table.
 // keys_a / keys_b: nk u64 each; hist: sort_hist_words(nk); tmp: max(scan_tmp_words(hist words), scan_tmp_words(nk));
-// flags / run_start: nk u64 each.
+// flags / run_start: nk u64 each.  tile_counts / tiled_tiles: keys_a is the tokenizer's tiled layout (hist and tmp
+// sized for max(tiled_tiles, sort_n_tiles(nk)) tiles), keys_b holds nk keys.
 cudaError_t tokens_compact_count(u64* keys_a, u64* keys_b, u64 nk, u64 vary, u64* hist, u64* tmp, u64* flags, u64* run_start,
-                                 const TableView& t, int sm, cudaStream_t s, u64* launches) {
+                                 const TableView& t, int sm, cudaStream_t s, u64* launches, const u32* tile_counts,
+                                 u64 tiled_tiles) {
     if (nk == 0) return cudaSuccess;
-    const u64 n_tiles = sort_n_tiles(nk);
-    const unsigned grid = (unsigned)((n_tiles + kSortWarps - 1) / kSortWarps);
     u64* a = keys_a;
     u64* b = keys_b;
+    // tiled input (straight from the tokenizer): the first pass reads the tiles and writes nk dense keys; if no
+    // byte position varies it still runs, on position 0, to make the keys dense
+    bool tiled = tile_counts != nullptr;
+    if (tiled && !vary) vary = 0xFF;
     for (int p = 0; p < 8; ++p) {
         if (!((vary >> (8 * p)) & 0xFF)) continue;
-        ck_hist_kernel<<<grid, kSortWarps * 32, 0, s>>>(a, nk, n_tiles, 8 * p, hist);
+        const u64 n_tiles = tiled ? tiled_tiles : sort_n_tiles(nk);
+        const unsigned grid = (unsigned)((n_tiles + kSortWarps - 1) / kSortWarps);
+        const u32* tc = tiled ? tile_counts : nullptr;
+        ck_hist_kernel<<<grid, kSortWarps * 32, 0, s>>>(a, nk, n_tiles, 8 * p, hist, tc);
         *launches += 1;
         cudaError_t e = exclusive_scan_u64(hist, hist, 256 * n_tiles, tmp, s, launches);
         if (e != cudaSuccess) return e;
-        ck_scatter_kernel<<<grid, kSortWarps * 32, 0, s>>>(a, b, nk, n_tiles, 8 * p, hist);
+        ck_scatter_kernel<<<grid, kSortWarps * 32, 0, s>>>(a, b, nk, n_tiles, 8 * p, hist, tc);
         *launches += 1;
         u64* x = a; a = b; b = x;
+        tiled = false;
     }
     const unsigned g = blocks_for(nk, 256, sm);
     ck_heads_kernel<<<g, 256, 0, s>>>(a, nk, flags);

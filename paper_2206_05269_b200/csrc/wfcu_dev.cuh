@@ -66,7 +66,15 @@ struct EmitView {
     TokenRec* out;
     u64 cap;
     u64* n_out;
+    // Compact mode (counting by sort + RLE, where text order does not matter): a token of at most 8 bytes
+    // is written as its 64-bit key into a tile of kKeyTile keys that its warp owns (one atomic per tile
+    // instead of one per 32 tokens); only the longer tokens become records.  keys == nullptr: off.
+    u64* keys = nullptr;
+    u64 key_tiles = 0;           // capacity in tiles
+    u32* tile_counts = nullptr;  // keys written to each tile
+    u64* kc = nullptr;           // [0] tiles handed out, [1] keys written, [2] OR of the keys, [3] AND of the keys
 };
+constexpr u32 kKeyTile = 2048;   // == the radix sort's tile (tokens.cu)
 
 // ---- hashing -----------------------------------------------------------------
 // 32-bit mix of the 128-bit key.  Only used to pick a slot / an owner, never as

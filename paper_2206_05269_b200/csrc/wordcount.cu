@@ -185,6 +185,10 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
     u32 my_tokens = 0;
     u32 qhead = 0, qtail = 0;     // token queue (warp-uniform)
     u32 mhead = 0, mtail = 0;     // miss buffer (warp-uniform)
+    // compact emission (EmitView::keys): the warp's current key tile
+    u64 ktile = ~0ull;            // warp-uniform; ~0 = none yet
+    u32 kused = 0, ktotal = 0;    // keys in the tile / written by this warp (warp-uniform)
+    u64 kor = 0, kand = ~0ull;    // per lane
 
     // 32 buffered keys -> global table, one key per lane
     auto drain_misses = [&](u32 count) {
@@ -222,11 +226,35 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
             u64 lo = ((u64)b1 << 32) | b0, hi = ((u64)b3 << 32) | b2;
             if (tlen <= 8) { lo &= ~0ull >> ((64u - 8u * tlen) & 63u); hi = 0; }
             else hi &= ~0ull >> ((128u - 8u * tlen) & 63u);
-            const u32 live = __ballot_sync(0xFFFFFFFFu, tlen != 0);
+            bool as_record = tlen != 0;
+            if (em.keys) {
+                const bool is_key = tlen != 0 && tlen <= 8;
+                const u32 mk = __ballot_sync(0xFFFFFFFFu, is_key), cnt = __popc(mk);
+                if (cnt) {
+                    if (ktile == ~0ull || kused + cnt > kKeyTile) {       // next tile (the old one keeps its gap)
+                        if (ktile != ~0ull && ktile < em.key_tiles && lane == 0) em.tile_counts[ktile] = kused;
+                        u64 t = 0;
+                        if (lane == 0) t = atomicAdd(em.kc + 0, 1ull);
+                        ktile = __shfl_sync(0xFFFFFFFFu, t, 0);
+                        kused = 0;
+                    }
+                    if (is_key) {
+                        const u64 key = le_to_be(lo);
+                        if (ktile < em.key_tiles) em.keys[ktile * kKeyTile + kused + __popc(mk & lt_mask)] = key;
+                        kor |= key;
+                        kand &= key;
+                        ++my_tokens;
+                    }
+                    kused += cnt;
+                    ktotal += cnt;
+                }
+                as_record = tlen > 8;
+            }
+            const u32 live = __ballot_sync(0xFFFFFFFFu, as_record);
             u64 base = 0;
             if (lane == 0 && live) base = atomicAdd(em.n_out, (u64)__popc(live));
             base = __shfl_sync(0xFFFFFFFFu, base, 0);
-            if (tlen) {
+            if (as_record) {
                 const u64 at = base + __popc(live & lt_mask);
                 // token start: within one ring length before the end of the current row
                 const u32 back = ((u32)row_end_off - sp) & (kRingBytes - 1);
@@ -439,6 +467,22 @@ wc_fast_kernel(const uint8_t* __restrict__ text, u64 n, u64 rows_per_warp, Table
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) my_tokens += __shfl_xor_sync(0xFFFFFFFFu, my_tokens, d);
     if (lane == 0 && my_tokens) atomicAdd(gt.n_tokens, (u64)my_tokens);
+
+    if constexpr (EMIT) {
+        if (em.keys) {                                         // close the warp's key tile, publish its totals
+            if (ktile != ~0ull && ktile < em.key_tiles && lane == 0) em.tile_counts[ktile] = kused;
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) {
+                kor |= __shfl_xor_sync(0xFFFFFFFFu, kor, d);
+                kand &= __shfl_xor_sync(0xFFFFFFFFu, kand, d);
+            }
+            if (lane == 0 && ktotal) {
+                atomicAdd(em.kc + 1, (u64)ktotal);
+                atomicOr(em.kc + 2, kor);
+                atomicAnd(em.kc + 3, kand);
+            }
+        }
+    }
 
     // flush the combiners into the global table
     __syncthreads();
@@ -703,7 +747,7 @@ static cudaError_t wc_launch_impl(const uint8_t* text, u64 n, const TableView& g
 // count text[0..n) into the tables of gt
 cudaError_t wc_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream,
                       u64* launches, cudaEvent_t* ev_before_fast, cudaEvent_t* ev_after_fast) {
-    return wc_launch_impl<false>(text, n, gt, EmitView{nullptr, 0, nullptr}, sm_count, stream, launches,
+    return wc_launch_impl<false>(text, n, gt, EmitView{}, sm_count, stream, launches,
                                  ev_before_fast, ev_after_fast);
 }
 
