@@ -305,6 +305,7 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
     uint8_t* ring = reinterpret_cast<uint8_t*>(sm.ring[warp]);
     uint4* missbuf = reinterpret_cast<uint4*>(sm.miss[warp]);
     const u32 q_s = (u32)__cvta_generic_to_shared(sm.queue[warp]);   // 1 KiB aligned: index wrap is an OR
+    u32 inserted = 0;             // global slots this lane claimed (first occurrences)
     u32 my_tokens = 0;            // per lane (careful rows)
     u32 warp_tokens = 0;          // warp-uniform (fast rows)
     u32 qhead = 0, qtail = 0;     // token queue (warp-uniform, free running, in entries)
@@ -340,7 +341,7 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
                 atomicAdd(&gt.slots[didx].count, 1ull);
                 dleft = 0;
             } else if ((cur.x | cur.y) == 0 || --dleft == 0) {
-                table_add(gt, ((u64)dk0 << 32) | dk1, ((u64)dk2 << 32) | dk3, 1ull);
+                table_add(gt, ((u64)dk0 << 32) | dk1, ((u64)dk2 << 32) | dk3, 1ull, &inserted);
                 dleft = 0;
             } else {
                 didx = (didx + 1) & (u32)gt.mask;
@@ -769,13 +770,16 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
     for (int i = tid; i < 2 * SETS; i += WARPS * 32) {
         const u64 k = reinterpret_cast<const u64*>(sm.sk)[i];
         const u32 c = reinterpret_cast<const u32*>(sm.scnt)[i];
-        if (k != 0 && c) table_add(gt, le_to_be(k), 0ull, (u64)c);
+        if (k != 0 && c) table_add(gt, le_to_be(k), 0ull, (u64)c, &inserted);
     }
     for (int i = tid; i < MSLOTS; i += WARPS * 32) {
         const u64 k = sm.mk0[i];
         const u32 c = sm.mcnt[i];
-        if (k > kSlotLocked && c) table_add(gt, le_to_be(k), le_to_be(sm.mk1[i]), (u64)c);
+        if (k > kSlotLocked && c) table_add(gt, le_to_be(k), le_to_be(sm.mk1[i]), (u64)c, &inserted);
     }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) inserted += __shfl_xor_sync(kFull, inserted, d);
+    if (lane == 0) table_note_inserted(gt, inserted);
 }
 
 // One kernel per variant (a kernel holding both bodies compiles the ASCII one measurably worse);

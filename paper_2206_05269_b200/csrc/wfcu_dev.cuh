@@ -131,7 +131,9 @@ __device__ __forceinline__ ulonglong2 ld_key(const Slot* s) {
 // counts[key] += add in the global table.  Exact: a slot is claimed with one
 // 128-bit CAS, and a plain (possibly torn) read that matches k0 but not k1 is
 // re-read through the CAS before the probe moves on.
-__device__ __forceinline__ void table_add(const TableView& t, u64 k0, u64 k1, u64 add) {
+// inserted != nullptr: a newly claimed slot is counted there instead of in t.n_used; the caller adds its total
+// with table_note_inserted (a million first occurrences are a million atomics on ONE address otherwise).
+__device__ __forceinline__ void table_add(const TableView& t, u64 k0, u64 k1, u64 add, u32* inserted = nullptr) {
     u64 i = mix32(k0, k1) & t.mask;
     for (u64 probes = 0; probes <= t.mask; ++probes) {
         Slot* s = t.slots + i;
@@ -139,8 +141,12 @@ __device__ __forceinline__ void table_add(const TableView& t, u64 k0, u64 k1, u6
         if (cur.x == 0 || (cur.x == k0 && cur.y != k1)) {
             cur = cas128(s, k0, k1);
             if (cur.x == 0 && cur.y == 0) {
-                const u64 used = atomicAdd(t.n_used, 1ull) + 1;
-                if (used > t.max_used) atomicOr(t.status, kStatusTableFull);
+                if (inserted) {
+                    ++*inserted;
+                } else {
+                    const u64 used = atomicAdd(t.n_used, 1ull) + 1;
+                    if (used > t.max_used) atomicOr(t.status, kStatusTableFull);
+                }
                 cur.x = k0; cur.y = k1;
             }
         }
@@ -151,6 +157,14 @@ __device__ __forceinline__ void table_add(const TableView& t, u64 k0, u64 k1, u6
         i = (i + 1) & t.mask;
     }
     atomicOr(t.status, kStatusTableFull);
+}
+
+// n slots were claimed through table_add(..., &inserted): one atomic for all of them.  An over-full table is
+// noticed here instead of at the insertion that crossed the limit (probing terminates either way).
+__device__ __forceinline__ void table_note_inserted(const TableView& t, u64 n) {
+    if (n == 0) return;
+    const u64 used = atomicAdd(t.n_used, n) + n;
+    if (used > t.max_used) atomicOr(t.status, kStatusTableFull);
 }
 
 // Long tokens: `rec` is the arena offset of a complete record of this token
