@@ -102,16 +102,29 @@ __global__ void tb_partition_scan_kernel(const u64* __restrict__ part_counts, u3
         for (u32 p = 0; p < n_parts; ++p) { cursors[p] = acc; acc += part_counts[p]; }
     }
 }
+// A cursor per partition is a handful of addresses for up to millions of entries: the lanes of a warp that
+// go to the same partition take their places with ONE atomic (match_any), not one each.
+__device__ __forceinline__ u64 warp_claim(u64* __restrict__ cursors, u32 p, bool live) {
+    const u32 lane = threadIdx.x & 31;
+    const u32 peers = __match_any_sync(0xFFFFFFFFu, live ? p : 0xFFFFFFFFu);
+    const u32 leader = __ffs(peers) - 1;
+    u64 base = 0;
+    if (live && lane == leader) base = atomicAdd(&cursors[p], (u64)__popc(peers));
+    base = __shfl_sync(0xFFFFFFFFu, base, leader);
+    return base + __popc(peers & ((1u << lane) - 1u));
+}
 // pass 2: scatter entries into their partition's region
 __global__ void tb_partition_scatter_kernel(TableView t, u32 n_parts, u64* __restrict__ cursors,
                                             Slot* __restrict__ out, u64 out_cap) {
-    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= t.mask; i += (u64)gridDim.x * blockDim.x) {
-        const Slot s = t.slots[i];
-        if (s.k0 != 0) {
-            const u32 p = owner_mix32(s.k0, s.k1) % n_parts;
-            const u64 j = atomicAdd(&cursors[p], 1ull);
-            if (j < out_cap) out[j] = Slot{s.k0, s.k1, s.count, 0};
-        }
+    const u32 lane = threadIdx.x & 31;
+    for (u64 i0 = (u64)blockIdx.x * blockDim.x + threadIdx.x - lane; i0 <= t.mask; i0 += (u64)gridDim.x * blockDim.x) {
+        const u64 i = i0 + lane;
+        Slot s{};
+        if (i <= t.mask) s = t.slots[i];
+        const bool live = s.k0 != 0;
+        const u32 p = live ? owner_mix32(s.k0, s.k1) % n_parts : 0u;
+        const u64 j = warp_claim(cursors, p, live);
+        if (live && j < out_cap) out[j] = Slot{s.k0, s.k1, s.count, 0};
     }
 }
 
@@ -120,11 +133,15 @@ __global__ void tb_partition_scatter_kernel(TableView t, u32 n_parts, u64* __res
 // the table, counts[n_parts + 1] += entries that did not fit (both sticky flags for the host).
 __global__ void tb_partition_fixed_kernel(TableView t, u32 n_parts, u64 cap, Slot* __restrict__ out,
                                           u64* __restrict__ counts) {
-    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= t.mask; i += (u64)gridDim.x * blockDim.x) {
-        const Slot s = t.slots[i];
-        if (s.k0 != 0) {
-            const u32 p = owner_mix32(s.k0, s.k1) % n_parts;
-            const u64 j = atomicAdd(&counts[p], 1ull);
+    const u32 lane = threadIdx.x & 31;
+    for (u64 i0 = (u64)blockIdx.x * blockDim.x + threadIdx.x - lane; i0 <= t.mask; i0 += (u64)gridDim.x * blockDim.x) {
+        const u64 i = i0 + lane;
+        Slot s{};
+        if (i <= t.mask) s = t.slots[i];
+        const bool live = s.k0 != 0;
+        const u32 p = live ? owner_mix32(s.k0, s.k1) % n_parts : 0u;
+        const u64 j = warp_claim(counts, p, live);
+        if (live) {
             if (j < cap) out[(u64)p * cap + j] = Slot{s.k0, s.k1, s.count, 0};
             else atomicAdd(&counts[n_parts + 1], 1ull);
         }
@@ -135,46 +152,61 @@ __global__ void tb_partition_fixed_kernel(TableView t, u32 n_parts, u64 cap, Slo
 __global__ void tb_merge_regions_kernel(TableView t, const Slot* __restrict__ in, u32 n_parts, u64 cap,
                                         const u64* __restrict__ region_counts) {
     u64 tokens = 0;
+    u32 inserted = 0;
     const u64 total = (u64)n_parts * cap;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (u64)gridDim.x * blockDim.x) {
         const u64 p = i / cap, j = i - p * cap;
         if (j < region_counts[p]) {
             const Slot s = in[i];
             if (s.k0 != 0 && s.count != 0) {
-                table_add(t, s.k0, s.k1, s.count);
+                table_add(t, s.k0, s.k1, s.count, &inserted);
                 tokens += s.count;
             }
         }
     }
-    for (int d = 16; d > 0; d >>= 1) tokens += __shfl_xor_sync(0xFFFFFFFFu, tokens, d);
+    for (int d = 16; d > 0; d >>= 1) {
+        tokens += __shfl_xor_sync(0xFFFFFFFFu, tokens, d);
+        inserted += __shfl_xor_sync(0xFFFFFFFFu, inserted, d);
+    }
+    if ((threadIdx.x & 31) == 0) table_note_inserted(t, inserted);
     if ((threadIdx.x & 31) == 0 && tokens) atomicAdd(t.n_tokens, tokens);
 }
 
 // counts[key] += count for n received entries; also accounts the tokens
 __global__ void tb_merge_entries_kernel(TableView t, const Slot* __restrict__ in, u64 n) {
     u64 tokens = 0;
+    u32 inserted = 0;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
         const Slot s = in[i];
         if (s.k0 != 0 && s.count != 0) {
-            table_add(t, s.k0, s.k1, s.count);
+            table_add(t, s.k0, s.k1, s.count, &inserted);
             tokens += s.count;
         }
     }
-    for (int d = 16; d > 0; d >>= 1) tokens += __shfl_xor_sync(0xFFFFFFFFu, tokens, d);
+    for (int d = 16; d > 0; d >>= 1) {
+        tokens += __shfl_xor_sync(0xFFFFFFFFu, tokens, d);
+        inserted += __shfl_xor_sync(0xFFFFFFFFu, inserted, d);
+    }
+    if ((threadIdx.x & 31) == 0) table_note_inserted(t, inserted);
     if ((threadIdx.x & 31) == 0 && tokens) atomicAdd(t.n_tokens, tokens);
 }
 
 // dst += src for whole tables (inline part)
 __global__ void tb_merge_table_kernel(TableView dst, TableView src) {
     u64 tokens = 0;
+    u32 inserted = 0;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= src.mask; i += (u64)gridDim.x * blockDim.x) {
         const Slot s = src.slots[i];
         if (s.k0 != 0 && s.count != 0) {
-            table_add(dst, s.k0, s.k1, s.count);
+            table_add(dst, s.k0, s.k1, s.count, &inserted);
             tokens += s.count;
         }
     }
-    for (int d = 16; d > 0; d >>= 1) tokens += __shfl_xor_sync(0xFFFFFFFFu, tokens, d);
+    for (int d = 16; d > 0; d >>= 1) {
+        tokens += __shfl_xor_sync(0xFFFFFFFFu, tokens, d);
+        inserted += __shfl_xor_sync(0xFFFFFFFFu, inserted, d);
+    }
+    if ((threadIdx.x & 31) == 0) table_note_inserted(dst, inserted);
     if ((threadIdx.x & 31) == 0 && tokens) atomicAdd(dst.n_tokens, tokens);
 }
 

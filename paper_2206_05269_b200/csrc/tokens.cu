@@ -247,6 +247,7 @@ __global__ void rle_insert_kernel(const TokenRec* __restrict__ recs, u64 n, cons
     const bool last_is_head = (n == 1) || rec_compare(recs[n - 2], recs[n - 1], arena) != 0;
     const u64 n_runs = flags_scan[n - 1] + (last_is_head ? 1 : 0);
     u64 tokens = 0;
+    u32 inserted = 0;
     for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < n_runs; r += (u64)gridDim.x * blockDim.x) {
         const u64 lo = run_start[r];
         const u64 hi = (r + 1 < n_runs) ? run_start[r + 1] : n;
@@ -254,7 +255,7 @@ __global__ void rle_insert_kernel(const TokenRec* __restrict__ recs, u64 n, cons
         const u64 len = hi - lo;
         tokens += len;
         if (!rec.ext) {
-            table_add(t, rec.k0, rec.k1, len);
+            table_add(t, rec.k0, rec.k1, len, &inserted);
         } else {
             const u32 blen = *reinterpret_cast<const u32*>(arena + rec.ext);
             const u64 dst = arena_alloc(t, blen);
@@ -267,7 +268,11 @@ __global__ void rle_insert_kernel(const TokenRec* __restrict__ recs, u64 n, cons
             }
         }
     }
-    for (int d = 16; d > 0; d >>= 1) tokens += __shfl_xor_sync(0xFFFFFFFFu, tokens, d);
+    for (int d = 16; d > 0; d >>= 1) {
+        tokens += __shfl_xor_sync(0xFFFFFFFFu, tokens, d);
+        inserted += __shfl_xor_sync(0xFFFFFFFFu, inserted, d);
+    }
+    if ((threadIdx.x & 31) == 0) table_note_inserted(t, inserted);
     if ((threadIdx.x & 31) == 0 && tokens) atomicAdd(t.n_tokens, tokens);
 }
 
@@ -449,13 +454,18 @@ __global__ void ck_insert_kernel(const u64* __restrict__ keys, u64 n, const u64*
     const bool last_is_head = (n == 1) || keys[n - 2] != keys[n - 1];
     const u64 n_runs = flags_scan[n - 1] + (last_is_head ? 1 : 0);
     u64 tokens = 0;
+    u32 inserted = 0;
     for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < n_runs; r += (u64)gridDim.x * blockDim.x) {
         const u64 lo = run_start[r];
         const u64 hi = (r + 1 < n_runs) ? run_start[r + 1] : n;
-        table_add(t, keys[lo], 0ull, hi - lo);
+        table_add(t, keys[lo], 0ull, hi - lo, &inserted);
         tokens += hi - lo;
     }
-    for (int d = 16; d > 0; d >>= 1) tokens += __shfl_xor_sync(0xFFFFFFFFu, tokens, d);
+    for (int d = 16; d > 0; d >>= 1) {
+        tokens += __shfl_xor_sync(0xFFFFFFFFu, tokens, d);
+        inserted += __shfl_xor_sync(0xFFFFFFFFu, inserted, d);
+    }
+    if ((threadIdx.x & 31) == 0) table_note_inserted(t, inserted);
     if ((threadIdx.x & 31) == 0 && tokens) atomicAdd(t.n_tokens, tokens);
 }
 

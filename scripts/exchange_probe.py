@@ -11,8 +11,10 @@ torch.cuda.set_device(0)
 dev = torch.device("cuda", 0)
 dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
 docs = int(sys.argv[1]) if len(sys.argv) > 1 else 954
-corpus = torch.from_numpy(capi.synth_corpus(1, 0, docs, 50000)).cuda()
-local, owned = capi.Counter(table_slots=1 << 20), capi.Counter(table_slots=1 << 20)
+vocab = int(os.environ.get("VOCAB", "50000"))
+corpus = torch.from_numpy(capi.synth_corpus(1, 0, docs, vocab)).cuda()
+slots = 1 << 20 if vocab <= 100000 else 1 << 22
+local, owned = capi.Counter(table_slots=slots), capi.Counter(table_slots=slots)
 ops = DeviceOps(torch, dev)
 s = torch.cuda.current_stream().cuda_stream
 mode = sys.argv[2] if len(sys.argv) > 2 else "sync"
