@@ -9,24 +9,36 @@ namespace wfcu {
 
 // Dense list of the non-empty inline slots (order unspecified).
 __global__ void tb_compact_kernel(TableView t, Slot* __restrict__ out, u64 out_cap, u64* __restrict__ out_count) {
-    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= t.mask; i += (u64)gridDim.x * blockDim.x) {
-        const Slot s = t.slots[i];
-        if (s.k0 != 0) {
-            const u64 j = atomicAdd(out_count, 1ull);
-            if (j < out_cap) out[j] = Slot{s.k0, s.k1, s.count, 0};
-        }
+    const u32 lane = threadIdx.x & 31;                    // one atomic per warp, not per entry
+    for (u64 i0 = (u64)blockIdx.x * blockDim.x + threadIdx.x - lane; i0 <= t.mask; i0 += (u64)gridDim.x * blockDim.x) {
+        const u64 i = i0 + lane;
+        Slot s{};
+        if (i <= t.mask) s = t.slots[i];
+        const bool live = s.k0 != 0;
+        const u32 m = __ballot_sync(0xFFFFFFFFu, live);
+        u64 base = 0;
+        if (lane == 0 && m) base = atomicAdd(out_count, (u64)__popc(m));
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        const u64 j = base + __popc(m & ((1u << lane) - 1u));
+        if (live && j < out_cap) out[j] = Slot{s.k0, s.k1, s.count, 0};
     }
 }
 
 // Same, as TokenRec {k0,k1,ext=0,pos=count}: the radix sort of tokens.cu then orders the
 // table by key on the device and carries the count along.
 __global__ void tb_compact_recs_kernel(TableView t, TokenRec* __restrict__ out, u64 out_cap, u64* __restrict__ out_count) {
-    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= t.mask; i += (u64)gridDim.x * blockDim.x) {
-        const Slot s = t.slots[i];
-        if (s.k0 != 0) {
-            const u64 j = atomicAdd(out_count, 1ull);
-            if (j < out_cap) out[j] = TokenRec{s.k0, s.k1, 0ull, s.count};
-        }
+    const u32 lane = threadIdx.x & 31;                    // one atomic per warp, not per entry
+    for (u64 i0 = (u64)blockIdx.x * blockDim.x + threadIdx.x - lane; i0 <= t.mask; i0 += (u64)gridDim.x * blockDim.x) {
+        const u64 i = i0 + lane;
+        Slot s{};
+        if (i <= t.mask) s = t.slots[i];
+        const bool live = s.k0 != 0;
+        const u32 m = __ballot_sync(0xFFFFFFFFu, live);
+        u64 base = 0;
+        if (lane == 0 && m) base = atomicAdd(out_count, (u64)__popc(m));
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        const u64 j = base + __popc(m & ((1u << lane) - 1u));
+        if (live && j < out_cap) out[j] = TokenRec{s.k0, s.k1, 0ull, s.count};
     }
 }
 
