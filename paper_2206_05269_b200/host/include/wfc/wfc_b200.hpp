@@ -15,19 +15,27 @@
 //   * run_wordcount partitions by key hash, not by alphabetical range (BASELINE.json;
 //     SURVEY.md D2): RunResult::counts is identical, the shards are pairwise disjoint,
 //     pre_repair_shards == shards and boundary_repair has nothing left to do;
-//   * the Transport overload is accepted and ignored: the exchange runs over device
-//     memory / NCCL, not over host frames.
+//   * run_wordcount(corpus, n, Transport&) runs the paper's own range-partitioned exchange over
+//     the caller's transport, WCX1 frames included (tokenize / sort / run-length encode on the
+//     device, frames on the host, like the reference); run_wordcount(corpus, n) is the fast
+//     path and exchanges table entries in device memory / over NCCL instead.
 #pragma once
 
+#include <array>
+#include <condition_variable>
 #include <cstddef>
 #include <cstdint>
+#include <deque>
 #include <map>
+#include <memory>
+#include <mutex>
 #include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
 #include <string_view>
 #include <ostream>
+#include <utility>
 #include <vector>
 
 namespace wfc {
@@ -49,6 +57,21 @@ struct WordList {
 std::string utf8_sanitize(std::string_view text);
 bool utf8_valid(std::string_view text);     // no byte needs replacing (same device pass)
 
+// Per-code-point accessors of the same header, for source compatibility: plain host arithmetic on ONE
+// code point.  Nothing in this library calls them on a data path -- tokenize, normalize_word,
+// utf8_sanitize and the counting kernels classify bytes on the device.
+inline constexpr char32_t kReplacementChar = 0xFFFD;
+struct DecodedChar {
+    char32_t cp = kReplacementChar;
+    unsigned length = 1;   // bytes consumed
+    bool valid = false;
+};
+DecodedChar utf8_decode(std::string_view text, std::size_t pos);
+void utf8_append(std::string& out, char32_t cp);
+bool is_unicode_space(char32_t cp);
+bool is_word_char(char32_t cp);
+char32_t simple_lower(char32_t cp);
+
 std::optional<Word> normalize_word(std::string_view fragment);
 std::vector<std::optional<Word>> normalize_words(std::span<const std::string> fragments);  // batch form (one launch)
 WordList tokenize(const RawDocument& doc);
@@ -63,13 +86,55 @@ ShardedCounts boundary_repair(ShardedCounts sharded);
 CountMap merge_counts(std::span<const CountMap> maps);
 std::size_t count_unreduced_words(const ShardedCounts& sharded);
 
-// ---- transport seam (reference: wfc/transport.hpp, wfc/wire.hpp) ------------------------
+// ---- wire format and transport seam (reference: wfc/wire.hpp, wfc/transport.hpp) -----------
+// Frame of one word batch: "WCX1", u32-LE word count, u32-LE byte length of each word, then the
+// word payloads; nothing may follow.
 using WireMessage = std::vector<std::uint8_t>;
+inline constexpr std::array<std::uint8_t, 4> kFrameMagic = {0x57, 0x43, 0x58, 0x31};
+
+class WireError : public std::runtime_error {
+public:
+    enum class Kind { BadMagic, Truncated, TrailingBytes, BadEncoding };
+    WireError(Kind kind, const std::string& what) : std::runtime_error(what), kind_(kind) {}
+    Kind kind() const { return kind_; }
+
+private:
+    Kind kind_;
+};
+
+WireMessage encode_message(std::span<const std::string> words);             // std::length_error beyond 2^32-1
+std::vector<std::string> decode_message(std::span<const std::uint8_t> frame);   // exact inverse; throws WireError
+
+class TransportError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+
+// Ordered, reliable, point-to-point frame channel between worker pairs; recv blocks.
 class Transport {
 public:
     virtual ~Transport() = default;
     virtual void send(std::size_t from, std::size_t to, WireMessage frame) = 0;
     virtual WireMessage recv(std::size_t at, std::size_t from) = 0;
+};
+
+// One unbounded FIFO per ordered worker pair, in this process.
+class InProcessTransport final : public Transport {
+public:
+    explicit InProcessTransport(std::size_t n_workers);
+    void send(std::size_t from, std::size_t to, WireMessage frame) override;
+    WireMessage recv(std::size_t at, std::size_t from) override;
+    std::size_t n_workers() const { return n_; }
+
+private:
+    struct Channel {
+        std::mutex mu;
+        std::condition_variable cv;
+        std::deque<WireMessage> queue;
+    };
+    Channel& channel(std::size_t from, std::size_t to);
+    std::size_t n_;
+    std::vector<std::unique_ptr<Channel>> channels_;
 };
 
 // ---- pipeline (reference: wfc/pipeline.hpp) --------------------------------------------
@@ -120,8 +185,33 @@ struct ShardPlan {
     std::size_t n_workers = 1;
     std::size_t local_count = 0;
     std::vector<std::size_t> boundaries;   // n+1 cut indices
+    std::size_t chunk_begin(std::size_t c) const { return boundaries[c]; }
+    std::size_t chunk_end(std::size_t c) const { return boundaries[c + 1]; }
+    std::size_t chunk_size(std::size_t c) const { return boundaries[c + 1] - boundaries[c]; }
 };
 ShardPlan plan_partition(const WordList& sorted, std::size_t worker_id, std::size_t n_workers);
+
+// The shuffle of wfc/shuffle.hpp: every worker keeps chunk `worker_id` of its sorted list and frames
+// chunk c for worker c; exchange_encoded runs n concurrent workers over the transport and merges what
+// each receives (ties: lowest source first), so the result does not depend on arrival order.
+struct WorkerShard {
+    ShardPlan plan;
+    WordList words;
+};
+struct EncodedShard {
+    std::size_t worker_id = 0;
+    std::size_t n_workers = 1;
+    std::vector<Word> kept;
+    std::vector<std::pair<std::size_t, WireMessage>> outgoing;   // (peer, frame)
+};
+class ExchangeError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+EncodedShard encode_outgoing(const ShardPlan& plan, const WordList& sorted);
+std::vector<WordList> exchange_encoded(std::vector<EncodedShard> shards, Transport& transport);
+std::vector<WordList> exchange(const std::vector<WorkerShard>& inputs, Transport& transport);
+std::vector<WordList> exchange(const std::vector<WorkerShard>& inputs);
 RunResult run_wordcount_range_partitioned(std::span<const RawDocument> corpus, std::size_t n_workers);
 CountMap serial_wordcount(std::span<const RawDocument> corpus);
 

@@ -286,6 +286,8 @@ CountMap serial_wordcount(std::span<const RawDocument> corpus) {
     return result;
 }
 
+static RunResult run_range_partitioned(std::span<const RawDocument> corpus, std::size_t n_workers, Transport& transport);
+
 RunResult run_wordcount(std::span<const RawDocument> corpus, std::size_t n_workers) {
     if (n_workers == 0) throw std::invalid_argument("run_wordcount: n_workers must be >= 1");
     const auto run_start = Clock::now();
@@ -380,8 +382,10 @@ RunResult run_wordcount(std::span<const RawDocument> corpus, std::size_t n_worke
     return result;
 }
 
-RunResult run_wordcount(std::span<const RawDocument> corpus, std::size_t n_workers, Transport&) {
-    return run_wordcount(corpus, n_workers);
+// The caller's transport carries the reference's own exchange: the paper's range-partitioned pipeline
+// (pipeline.cpp:61-123) with WCX1 frames between the logical workers.
+RunResult run_wordcount(std::span<const RawDocument> corpus, std::size_t n_workers, Transport& transport) {
+    return run_range_partitioned(corpus, n_workers, transport);
 }
 
 // Chunk sizes: the kept chunk gets floor(k/n); the rest is spread over the other chunks,
@@ -409,6 +413,12 @@ ShardPlan plan_partition(const WordList& sorted, std::size_t worker_id, std::siz
 }
 
 RunResult run_wordcount_range_partitioned(std::span<const RawDocument> corpus, std::size_t n_workers) {
+    if (n_workers == 0) throw std::invalid_argument("run_wordcount: n_workers must be >= 1");
+    InProcessTransport transport(n_workers);
+    return run_range_partitioned(corpus, n_workers, transport);
+}
+
+static RunResult run_range_partitioned(std::span<const RawDocument> corpus, std::size_t n_workers, Transport& transport) {
     if (n_workers == 0) throw std::invalid_argument("run_wordcount: n_workers must be >= 1");
     const auto run_start = Clock::now();
     RunResult result;
@@ -444,17 +454,13 @@ RunResult run_wordcount_range_partitioned(std::span<const RawDocument> corpus, s
     stage("sort", t.sort_ns, [&] {        // device radix sort
         for (auto& l : local) l = sort_words(std::move(l));
     });
-    std::vector<WordList> exchanged(n);
-    stage("encode", t.encode_ns, [&] {    // range partition by position
-        for (std::size_t j = 0; j < n; ++j) {
-            const ShardPlan plan = plan_partition(local[j], j, n);
-            for (std::size_t c = 0; c < n; ++c)
-                exchanged[c].words.insert(exchanged[c].words.end(), local[j].words.begin() + plan.boundaries[c],
-                                          local[j].words.begin() + plan.boundaries[c + 1]);
-        }
+    std::vector<EncodedShard> shards(n);
+    stage("encode", t.encode_ns, [&] {    // range partition by position, one WCX1 frame per peer
+        for (std::size_t j = 0; j < n; ++j) shards[j] = encode_outgoing(plan_partition(local[j], j, n), local[j]);
     });
-    stage("exchange", t.exchange_ns, [&] {   // the n-way merge of sorted chunks == a stable sort of their concatenation
-        for (auto& e : exchanged) e = sort_words(std::move(e));
+    std::vector<WordList> exchanged;
+    stage("exchange", t.exchange_ns, [&] {   // n concurrent workers over the transport, n-way merge
+        exchanged = exchange_encoded(std::move(shards), transport);
     });
     result.pre_repair_shards.assign(n, CountMap{});
     stage("reduce", t.reduce_ns, [&] {    // device run-length encode

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <map>
+#include <mutex>
 #include <random>
 #include <sstream>
 #include <string>
@@ -15,7 +16,11 @@
 #include "wfc/engine.hpp"
 #include "wfc/pipeline.hpp"
 #include "wfc/reduce.hpp"
+#include "wfc/shuffle.hpp"
 #include "wfc/text.hpp"
+#include "wfc/transport.hpp"
+#include "wfc/unicode.hpp"
+#include "wfc/wire.hpp"
 
 using namespace wfc;
 
@@ -425,6 +430,250 @@ static void report_cases() {
     CHECK(tim.str().find("timing\ttotal\t") != std::string::npos);
 }
 
+
+// ---- the paper's own exchange: WCX1 frames, transports, shuffle ---------------------------------
+static std::vector<std::string> batch(std::initializer_list<const char*> words) { return {words.begin(), words.end()}; }
+template <typename Fn>
+static bool wire_error_kind(Fn&& fn, WireError::Kind kind) {
+    try {
+        fn();
+    } catch (const WireError& e) {
+        return e.kind() == kind;
+    } catch (...) {
+    }
+    return false;
+}
+template <typename Ex, typename Fn>
+static bool throws_with(Fn&& fn, const char* needle) {
+    try {
+        fn();
+    } catch (const Ex& e) {
+        return std::string(e.what()).find(needle) != std::string::npos;
+    } catch (...) {
+    }
+    return false;
+}
+
+static void wire_cases() {
+    // wire_test.cpp:38-50 -- golden bytes
+    CHECK((encode_message(batch({})) == WireMessage{0x57, 0x43, 0x58, 0x31, 0x00, 0x00, 0x00, 0x00}));
+    CHECK((encode_message(batch({"a"})) == WireMessage{0x57, 0x43, 0x58, 0x31, 0x01, 0x00, 0x00, 0x00, 0x01, 0x00, 0x00, 0x00, 0x61}));
+    CHECK((encode_message(batch({"to", "a"})) == WireMessage{0x57, 0x43, 0x58, 0x31, 0x02, 0x00, 0x00, 0x00, 0x02, 0x00, 0x00, 0x00,
+                                                           0x01, 0x00, 0x00, 0x00, 0x74, 0x6F, 0x61}));
+    // wire_test.cpp:52-70 -- round trips
+    CHECK(decode_message(WireMessage{0x57, 0x43, 0x58, 0x31, 0x00, 0x00, 0x00, 0x00}).empty());
+    for (const auto& words : {batch({"test", "to", "want"}), batch({"", "a", ""}), batch({"caf\xc3\xa9", "\xe6\xbc\xa2\xe5\xad\x97", "x"})})
+        CHECK(decode_message(encode_message(words)) == words);
+    Rng rng(9);
+    for (int round = 0; round < 20; ++round) {
+        std::vector<std::string> words(std::uniform_int_distribution<int>(0, 40)(rng));
+        std::size_t payload = 0;
+        for (auto& w : words) {
+            const int len = std::uniform_int_distribution<int>(0, 12)(rng);
+            for (int i = 0; i < len; ++i) utf8_append(w, std::uniform_int_distribution<int>(0, 3)(rng) ? U'a' + (rng() % 26) : char32_t(0xC0 + rng() % 0x2F00));
+            payload += w.size();
+        }
+        const WireMessage frame = encode_message(words);
+        CHECK(frame.size() == 8 + 4 * words.size() + payload);       // wire_test.cpp:120-131
+        CHECK(decode_message(frame) == words);
+    }
+    // wire_test.cpp:72-118 -- every way a frame can be wrong
+    {
+        WireMessage frame = encode_message(batch({"a"}));
+        frame[0] = 0x58;
+        CHECK(wire_error_kind([&] { decode_message(frame); }, WireError::Kind::BadMagic));
+        CHECK(throws_with<WireError>([&] { decode_message(frame); }, "magic"));
+        CHECK_THROWS_AS(decode_message(WireMessage{0x57, 0x43}), WireError);
+        const WireMessage two = encode_message(batch({"test", "to"}));
+        for (std::size_t cut : {std::size_t(5), std::size_t(9), two.size() - 1}) {
+            const WireMessage shorter(two.begin(), two.begin() + cut);
+            CHECK(wire_error_kind([&] { decode_message(shorter); }, WireError::Kind::Truncated));
+        }
+        WireMessage longer = encode_message(batch({"a", "b"}));
+        longer.push_back(0x00);
+        CHECK(wire_error_kind([&] { decode_message(longer); }, WireError::Kind::TrailingBytes));
+        const WireMessage not_utf8{0x57, 0x43, 0x58, 0x31, 0x01, 0x00, 0x00, 0x00, 0x01, 0x00, 0x00, 0x00, 0xFF};
+        CHECK(wire_error_kind([&] { decode_message(not_utf8); }, WireError::Kind::BadEncoding));
+    }
+}
+
+namespace {
+class RecordingTransport final : public Transport {        // shuffle_test.cpp:37-60
+public:
+    explicit RecordingTransport(std::size_t n) : inner_(n) {}
+    void send(std::size_t from, std::size_t to, WireMessage frame) override {
+        {
+            std::lock_guard<std::mutex> lock(mu_);
+            frames.push_back(frame);
+        }
+        inner_.send(from, to, std::move(frame));
+    }
+    WireMessage recv(std::size_t at, std::size_t from) override { return inner_.recv(at, from); }
+    std::vector<WireMessage> frames;
+
+private:
+    InProcessTransport inner_;
+    std::mutex mu_;
+};
+class FailingTransport final : public Transport {          // shuffle_test.cpp:62-68
+public:
+    void send(std::size_t, std::size_t, WireMessage) override { throw TransportError("link down"); }
+    WireMessage recv(std::size_t, std::size_t) override { throw TransportError("link down"); }
+};
+class CorruptingTransport final : public Transport {       // shuffle_test.cpp:70-86, pipeline_test.cpp:146-160
+public:
+    CorruptingTransport(std::size_t n, std::size_t victim) : inner_(n), victim_(victim) {}
+    void send(std::size_t from, std::size_t to, WireMessage frame) override { inner_.send(from, to, std::move(frame)); }
+    WireMessage recv(std::size_t at, std::size_t from) override {
+        WireMessage frame = inner_.recv(at, from);
+        if ((victim_ == ~std::size_t(0) || at == victim_) && !frame.empty()) frame[0] = 0x00;
+        return frame;
+    }
+
+private:
+    InProcessTransport inner_;
+    std::size_t victim_;
+};
+}  // namespace
+
+static WordList sorted_list(std::vector<std::string> words) { return sort_words(WordList{std::move(words), false}); }
+static std::vector<WorkerShard> make_shards(std::vector<WordList> lists) {
+    std::vector<WorkerShard> shards;
+    for (std::size_t j = 0; j < lists.size(); ++j) shards.push_back({plan_partition(lists[j], j, lists.size()), lists[j]});
+    return shards;
+}
+
+static void shuffle_cases() {
+    // shuffle_test.cpp:154-162
+    {
+        const WordList doc1 = sorted_list({"i", "want", "to", "test", "mapreduce"});
+        const EncodedShard shard = encode_outgoing(plan_partition(doc1, 0, 2), doc1);
+        CHECK((shard.kept == std::vector<std::string>{"i", "mapreduce"}));
+        CHECK(shard.outgoing.size() == 1 && shard.outgoing[0].first == 1);
+        CHECK((decode_message(shard.outgoing[0].second) == std::vector<std::string>{"test", "to", "want"}));
+        CHECK_THROWS_AS(encode_outgoing(plan_partition(doc1, 0, 2), WordList{{"b", "a"}, false}), std::invalid_argument);
+    }
+    // shuffle_test.cpp:164-182
+    {
+        const auto out = wfc::exchange(make_shards({sorted_list({"i", "want", "to", "test", "mapreduce"}),
+                                               sorted_list({"mapreduce", "is", "a", "cool", "algorithm", "to", "test"})}));
+        CHECK(out.size() == 2);
+        CHECK((out[0].words == std::vector<std::string>{"a", "algorithm", "cool", "i", "is", "mapreduce"}));
+        CHECK((out[1].words == std::vector<std::string>{"mapreduce", "test", "test", "to", "to", "want"}));
+        CHECK(out[0].sorted && out[1].sorted);
+        const auto one = wfc::exchange(make_shards({sorted_list({"b", "a", "c", "a"})}));
+        CHECK((one.size() == 1 && one[0].words == std::vector<std::string>{"a", "a", "b", "c"}));
+    }
+    // shuffle_test.cpp:184-230 -- conservation, sortedness, determinism; :232-255 -- every frame is a valid message
+    {
+        Rng rng(31);
+        for (std::size_t n : {2, 4, 8}) {
+            std::vector<WordList> lists;
+            std::map<std::string, int> before, after;
+            for (std::size_t j = 0; j < n; ++j) {
+                std::vector<std::string> words(std::uniform_int_distribution<std::size_t>(0, 400)(rng));
+                for (auto& w : words) w = vocab_word(rng() % 50);
+                for (const auto& w : words) ++before[w];
+                lists.push_back(sorted_list(std::move(words)));
+            }
+            const auto shards = make_shards(lists);
+            std::size_t sent = 0;
+            for (const auto& sh : shards) sent += sh.plan.local_count - sh.plan.chunk_size(sh.plan.worker_id);
+            RecordingTransport transport(n);
+            const auto out = wfc::exchange(shards, transport);
+            for (const auto& o : out) {
+                CHECK(o.sorted && std::is_sorted(o.words.begin(), o.words.end()));
+                for (const auto& w : o.words) ++after[w];
+            }
+            CHECK(before == after);
+            CHECK(transport.frames.size() == n * (n - 1));
+            std::size_t decoded = 0;
+            for (const auto& f : transport.frames) decoded += decode_message(f).size();
+            CHECK(decoded == sent);
+            const auto again = wfc::exchange(shards);
+            for (std::size_t j = 0; j < n; ++j) CHECK(again[j].words == out[j].words);
+        }
+    }
+    // shuffle_test.cpp:257-279 -- failures name the pair / the worker; layout validation
+    {
+        const auto shards = make_shards({sorted_list({"a", "b"}), sorted_list({"c", "d"})});
+        FailingTransport failing;
+        CHECK(throws_with<ExchangeError>([&] { wfc::exchange(shards, failing); }, "worker 0 -> worker 1"));
+        CorruptingTransport corrupting(2, 0);
+        CHECK(throws_with<ExchangeError>([&] { wfc::exchange(shards, corrupting); }, "worker 0 got an invalid frame from worker 1"));
+        const WordList list = sorted_list({"a"});
+        std::vector<WorkerShard> bad;
+        bad.push_back({plan_partition(list, 0, 3), list});
+        CHECK_THROWS_AS(wfc::exchange(bad), std::invalid_argument);
+        CHECK_THROWS_AS(wfc::exchange(std::vector<WorkerShard>{}), std::invalid_argument);
+        CHECK_THROWS_AS(InProcessTransport(0), TransportError);
+    }
+    // pipeline_test.cpp:106-127, 162-175 -- the transport overload: same counts, the reference's pre-repair shards,
+    // and a failure inside the exchange is attributed to its stage
+    {
+        InProcessTransport transport(2);
+        const RunResult r = run_wordcount(kTwoDocs, 2, transport);
+        CHECK(r.counts == serial_wordcount(kTwoDocs));
+        CHECK(r.pre_repair_shards.size() == 2 && r.pre_repair_shards[0].count("mapreduce") && r.pre_repair_shards[1].count("mapreduce"));
+        CHECK(count_unreduced_words(r.pre_repair_shards) == 1 && count_unreduced_words(r.shards) == 0);
+        Rng rng(303);
+        const auto corpus = iid_corpus(rng, 20, 200, 80);
+        for (std::size_t n : {1, 3, 8}) {
+            RecordingTransport rec(n);
+            const RunResult rr = run_wordcount(corpus, n, rec);
+            CHECK(rr.counts == serial_wordcount(corpus));
+            CHECK(rec.frames.size() == n * (n - 1));
+        }
+        CorruptingTransport broken(2, ~std::size_t(0));
+        bool attributed = false;
+        try {
+            run_wordcount(kTwoDocs, 2, broken);
+        } catch (const PipelineError& e) {
+            const std::string what = e.what();
+            attributed = e.stage() == "exchange" && what.find("exchange stage") != std::string::npos &&
+                         what.find("invalid frame") != std::string::npos;
+        }
+        CHECK(attributed);
+    }
+}
+
+static void code_point_cases() {
+    // text_test.cpp:171-187 and unicode.cpp's pinned classes, through the per-code-point accessors
+    CHECK(utf8_decode("a", 0).valid && utf8_decode("a", 0).cp == U'a' && utf8_decode("a", 0).length == 1);
+    const std::string e_acute = "\xc3\xa9", kanji = "\xe6\xbc\xa2", emoji = "\xf0\x9f\x98\x80";
+    CHECK(utf8_decode(e_acute, 0).cp == 0xE9 && utf8_decode(e_acute, 0).length == 2);
+    CHECK(utf8_decode(kanji, 0).cp == 0x6F22 && utf8_decode(kanji, 0).length == 3);
+    CHECK(utf8_decode(emoji, 0).cp == 0x1F600 && utf8_decode(emoji, 0).length == 4);
+    for (const std::string bad : {"\xff", "\xc0\x80", "\xe0\x80\x80", "\xed\xa0\x80", "\xf4\x90\x80\x80", "\xc3", "\xe6\xbc", "\x80"}) {
+        const DecodedChar d = utf8_decode(bad, 0);
+        CHECK(!d.valid && d.length == 1 && d.cp == kReplacementChar);
+    }
+    for (char32_t cp : {char32_t(0x24), char32_t(0xE9), char32_t(0x6F22), char32_t(0x1F600), char32_t(0x7FF), char32_t(0x800), char32_t(0xFFFF), char32_t(0x10FFFF)}) {
+        std::string s;
+        utf8_append(s, cp);
+        const DecodedChar d = utf8_decode(s, 0);
+        CHECK(d.valid && d.cp == cp && d.length == s.size());
+        CHECK(utf8_valid(s));                                        // the device validator agrees
+    }
+    for (char32_t cp : {0x09, 0x0D, 0x20, 0x85, 0xA0, 0x1680, 0x2000, 0x200A, 0x2028, 0x2029, 0x202F, 0x205F, 0x3000}) CHECK(is_unicode_space(cp));
+    for (char32_t cp : {0x08, 0x0E, 0x1F, 0x21, 0x84, 0x200B, 0x2060, 0x3001, 0xFEFF}) CHECK(!is_unicode_space(cp));
+    for (char32_t cp : {U'0', U'9', U'a', U'Z', char32_t(0xAA), char32_t(0xB5), char32_t(0xBA), char32_t(0xC0), char32_t(0x80), char32_t(0x3B1), char32_t(0x6F22), char32_t(0x2070), char32_t(0x3040), char32_t(0xFF10), char32_t(0xFF21), char32_t(0xFF66), char32_t(0x1F600)})
+        CHECK(is_word_char(cp));
+    for (char32_t cp : {U'_', U'-', U'\'', U' ', char32_t(0x7F), char32_t(0x85), char32_t(0xA0), char32_t(0xA1), char32_t(0xBF), char32_t(0xD7), char32_t(0xF7), char32_t(0x2019), char32_t(0x206F), char32_t(0x3000), char32_t(0x303F), char32_t(0xFF01), char32_t(0xFF0F), char32_t(0xFF1A), char32_t(0xFF20), char32_t(0xFF3B), char32_t(0xFF40), char32_t(0xFF5B), char32_t(0xFF65), char32_t(0xFFFD), char32_t(0x1680)})
+        CHECK(!is_word_char(cp));
+    CHECK(simple_lower(U'A') == U'a' && simple_lower(U'Z') == U'z' && simple_lower(U'a') == U'a' && simple_lower(U'0') == U'0');
+    CHECK(simple_lower(0xC0) == 0xE0 && simple_lower(0xDE) == 0xFE && simple_lower(0xD7) == 0xD7 && simple_lower(0xDF) == 0xDF);
+    CHECK(simple_lower(0x391) == 0x391 && simple_lower(0x178) == 0x178);
+    // the accessors and the device tokenizer agree: a word character survives normalize_word, anything else is trimmed
+    for (char32_t cp : {char32_t(0xAA), char32_t(0xD7), char32_t(0x2019), char32_t(0x6F22), char32_t(0xFF0F), char32_t(0xFF10), char32_t(0x80), char32_t(0x3B1)}) {
+        std::string s;
+        utf8_append(s, cp);
+        if (is_unicode_space(cp)) continue;
+        const auto w = normalize_word(s);
+        CHECK(w.has_value() == is_word_char(cp));
+    }
+}
+
 int main() {
     try {
         text_cases();
@@ -432,6 +681,9 @@ int main() {
         reduce_cases();
         pipeline_cases();
         range_partition_cases();
+        wire_cases();
+        shuffle_cases();
+        code_point_cases();
         engine_cases();
         analysis_cases();
         report_cases();

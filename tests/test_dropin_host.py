@@ -12,7 +12,10 @@ def test_dropin_exports_reference_api(capi):
     import re
     for name in ("tokenize", "normalize_word", "sort_words", "reduce_sorted", "boundary_repair", "merge_counts",
                  "count_unreduced_words", "run_wordcount", "serial_wordcount", "map_reduce_serial", "map_reduce_blocked",
-                 "alternating_harmonic", "top_k", "distinctive_words"):
+                 "alternating_harmonic", "top_k", "distinctive_words",
+                 # the paper's own exchange and the code-point accessors (wfc/{wire,shuffle,transport,unicode}.hpp)
+                 "encode_message", "decode_message", "plan_partition", "encode_outgoing", "exchange_encoded", "exchange",
+                 "utf8_decode", "utf8_append", "utf8_sanitize", "utf8_valid", "is_unicode_space", "is_word_char", "simple_lower"):
         assert re.search(r"\bwfc::%s(\[abi:cxx11\])?\(" % name, syms), name
 
 
