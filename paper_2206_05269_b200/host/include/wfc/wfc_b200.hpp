@@ -4,9 +4,11 @@
 // /root/reference/proj/include/wfc/{text,reduce,pipeline,engine,analysis}.hpp, so a
 // caller of the reference (proj/src/cli.cpp:79-86, 138-141, 202-221) relinks against
 // libwfc_b200.so unchanged.  The per-topic headers wfc/text.hpp, wfc/reduce.hpp, ...
-// forward here.  Every function below runs its arithmetic on the GPU through the C ABI
-// of include/wfcu.h; there is no CPU implementation to fall back to -- without a device
-// the calls throw wfc::DeviceError.
+// forward here.  Every data path below (tokenize, normalize, sort, count, reduce, merge, map-reduce,
+// top-k, sanitize) runs its arithmetic on the GPU through the C ABI of include/wfcu.h; there is no CPU
+// implementation to fall back to -- without a device the calls throw wfc::DeviceError.  Host code is
+// what is host code in the reference too: containers, the WCX1 frames / transports / threads of the
+// paper's exchange, index arithmetic (plan_partition) and the single-code-point accessors.
 //
 // Differences a caller can observe (all additive):
 //   * MapKind gains `square` (value 3) for f(x) = x^2; map_reduce_fast() is the
