@@ -569,7 +569,8 @@ __device__ __forceinline__ u32 enc_byte(u32 cp, u32 n, u32 i) {
 // Counts (or, when em != nullptr, emits) the token of one whitespace-free piece
 // [a,b) of the text (normalize_word).
 // Returns 1 if the piece yields a token (the caller accounts the tokens: one atomic per warp, not per token).
-__device__ u32 slow_count_piece(const uint8_t* text, u64 a, u64 b, const TableView& gt, const EmitView* em) {
+__device__ u32 slow_count_piece(const uint8_t* text, u64 a, u64 b, const TableView& gt, const EmitView* em,
+                                u32* inserted = nullptr) {
     // pass 1: normalised offsets of the first / last word character
     u64 noff = 0, nfirst = 0, nlast_end = 0, first_b = b, last_e = a;
     for (u64 pos = a; pos < b;) {
@@ -604,7 +605,7 @@ __device__ u32 slow_count_piece(const uint8_t* text, u64 a, u64 b, const TableVi
             const u64 at = atomicAdd(em->n_out, 1ull);
             if (at < em->cap) em->out[at] = TokenRec{k0, k1, 0ull, first_b};
         } else {
-            table_add(gt, k0, k1, 1ull);
+            table_add(gt, k0, k1, 1ull, inserted);
         }
         return 1;
     }
@@ -646,7 +647,8 @@ __device__ __forceinline__ bool ascii_space(u32 b) { return b == 0x20 || (b >= 0
 __global__ void wc_slow_kernel(const uint8_t* __restrict__ text, u64 n, TableView gt, EmitView em, int emit) {
     u64 count = *gt.n_deferred;
     if (count > gt.deferred_cap) count = gt.deferred_cap;
-    u32 tokens = 0;
+    if (count == 0) return;
+    u32 tokens = 0, inserted = 0;
     for (u64 idx = (u64)blockIdx.x * blockDim.x + threadIdx.x; idx < count; idx += (u64)gridDim.x * blockDim.x) {
         const u64 e = gt.deferred[idx];
         u64 s = e;
@@ -662,7 +664,7 @@ __global__ void wc_slow_kernel(const uint8_t* __restrict__ text, u64 n, TableVie
                 boundary = d.valid && uni_space(d.cp);
             }
             if (boundary) {
-                if (in_piece) tokens += slow_count_piece(text, piece, pos, gt, emit ? &em : nullptr);
+                if (in_piece) tokens += slow_count_piece(text, piece, pos, gt, emit ? &em : nullptr, &inserted);
                 in_piece = false;
             } else if (!in_piece) {
                 piece = pos;
@@ -671,8 +673,12 @@ __global__ void wc_slow_kernel(const uint8_t* __restrict__ text, u64 n, TableVie
             pos += d.len;
         }
     }
-    // token total: one atomic per warp (a per-token atomic on one address was most of this kernel's time)
-    for (int d = 16; d > 0; d >>= 1) tokens += __shfl_xor_sync(0xFFFFFFFFu, tokens, d);
+    // token and claimed-slot totals: one atomic per warp (a per-token atomic on one address was most of this kernel's time)
+    for (int d = 16; d > 0; d >>= 1) {
+        tokens += __shfl_xor_sync(0xFFFFFFFFu, tokens, d);
+        inserted += __shfl_xor_sync(0xFFFFFFFFu, inserted, d);
+    }
+    if ((threadIdx.x & 31) == 0) table_note_inserted(gt, inserted);
     if ((threadIdx.x & 31) == 0 && tokens) atomicAdd(gt.n_tokens, (u64)tokens);
 }
 
