@@ -302,12 +302,22 @@ class Counter:
         check(lib.wfcu_counter_stats(self._h, C.c_void_p(stream), C.byref(d), C.byref(t), C.byref(b)))
         return d.value, t.value, b.value
 
-    def export(self, stream: int = 0) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
-        """(key_bytes, key_lens, counts) in std::map order."""
+    def export(self, stream: int = 0, out=None) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+        """(key_bytes, key_lens, counts) in std::map order.
+        out: optional (uint8, uint32, uint64) arrays to fill instead of new ones -- e.g. views of page-locked
+        memory reused from call to call, which the copy engine fills several times faster than fresh pageable
+        arrays; they must be large enough (WfcuError ERR_BUFFER_TOO_SMALL otherwise)."""
         distinct, _, key_bytes = self.stats(stream)
-        blob = np.zeros(max(key_bytes, 1), np.uint8)
-        lens = np.zeros(max(distinct, 1), np.uint32)
-        counts = np.zeros(max(distinct, 1), np.uint64)
+        if out is None:
+            blob = np.empty(max(key_bytes, 1), np.uint8)
+            lens = np.empty(max(distinct, 1), np.uint32)
+            counts = np.empty(max(distinct, 1), np.uint64)
+        else:
+            blob, lens, counts = out
+            if blob.dtype != np.uint8 or lens.dtype != np.uint32 or counts.dtype != np.uint64:
+                raise TypeError("export(out=...) wants (uint8, uint32, uint64) arrays")
+            if blob.size < key_bytes or lens.size < distinct or counts.size < distinct:
+                raise WfcuError(ERR_BUFFER_TOO_SMALL, f"export needs {key_bytes} key bytes and {distinct} rows")
         check(lib.wfcu_counter_export(self._h, C.c_void_p(stream), _ptr(blob), key_bytes, _ptr(lens), _ptr(counts), distinct))
         return blob[:key_bytes], lens[:distinct], counts[:distinct]
 

@@ -187,6 +187,27 @@ def test_count_host_packing_slices(capi, cuda, port, monkeypatch):
     assert counter.to_dict() == want
 
 
+def test_export_into_caller_buffers(capi, cuda, port):
+    """export(out=...) fills caller-owned (here page-locked, reused) arrays with the same three arrays"""
+    import numpy as np
+    text = random_text(random.Random(61), 60000, "ascii") + b" " + random_text(random.Random(62), 20000, "unicode")
+    dev, n = to_dev(cuda, text)
+    counter = capi.Counter(table_slots=1 << 15)
+    counter.count_dev(dev.data_ptr(), n)
+    blob, lens, counts = counter.export()
+    rows, _, key_bytes = counter.stats()
+    pinned = lambda dt, k: cuda.empty(k * np.dtype(dt).itemsize, dtype=cuda.uint8).pin_memory().numpy().view(dt)
+    out = (pinned(np.uint8, key_bytes + 100), pinned(np.uint32, rows + 10), pinned(np.uint64, rows + 10))
+    for _ in range(2):
+        b2, l2, c2 = counter.export(out=out)
+        assert bytes(b2) == bytes(blob) and (l2 == lens).all() and (c2 == counts).all()
+    with pytest.raises(capi.WfcuError) as e:
+        counter.export(out=(out[0][:key_bytes - 1], out[1], out[2]))
+    assert e.value.code == capi.ERR_BUFFER_TOO_SMALL
+    with pytest.raises(TypeError):
+        counter.export(out=(out[0], out[1].view(np.int32), out[2]))
+
+
 def test_deferred_list_overflow_is_reported(capi, cuda, port):
     """a corpus of words the fast path defers (three-byte characters) overflows a tiny slow-path list:
     loud error, and the same text counts exactly once the capacity is raised (what the C++ drop-in's
