@@ -105,3 +105,22 @@ def test_sorted_count_on_zipf_corpus(capi, cuda, port):
     c = capi.Counter(table_slots=1 << 18)
     c.count_dev_sorted(dev.data_ptr(), n)
     assert c.to_dict() == port.wordcount([corpus])
+
+
+def test_sorted_count_key_tiles(capi, cuda, port):
+    """the counting form of the sort + RLE path takes short tokens straight from the tokenizer as 64-bit keys in
+    tiles of 2048 that a warp owns: token-dense text overflows the first tile estimate (one retry), a single
+    repeated word makes no byte position vary (the densifying pass still runs), empty and tiny inputs use no or
+    one tile, and 9..16-byte / non-ASCII tokens keep the record path next to it"""
+    rng = random.Random(77)
+    dense = b" ".join(bytes([rng.choice(b"abcdefghijklmnopqrstuvwxyz0123456789")]) for _ in range(3_000_000))   # n/2 tokens
+    same = b"word " * 700_000
+    mixed = b" ".join(rng.choice([b"the", b"of", b"internationalisation", b"caf\xc3\xa9", b"x", b"encyclopaedia", b"Zebra"])
+                      for _ in range(400_000))
+    for text in (dense, same, mixed, b"", b"a", b"  ", b"abcdefgh abcdefghi"):
+        dev, n = to_dev(cuda, text)
+        c = capi.Counter(table_slots=1 << 14)
+        c.count_dev_sorted(dev.data_ptr(), n)
+        want = port.wordcount([text])
+        assert c.to_dict() == want
+        assert c.stats()[1] == sum(want.values())
