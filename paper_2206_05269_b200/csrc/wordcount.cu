@@ -571,8 +571,10 @@ __device__ __forceinline__ u32 enc_byte(u32 cp, u32 n, u32 i) {
 // Returns 1 if the piece yields a token (the caller accounts the tokens: one atomic per warp, not per token).
 __device__ u32 slow_count_piece(const uint8_t* text, u64 a, u64 b, const TableView& gt, const EmitView* em,
                                 u32* inserted = nullptr) {
-    // pass 1: normalised offsets of the first / last word character
+    // one pass: normalised offsets of the first / last word character, and the first 16 normalised bytes from
+    // the first word character on (what lies behind the last word character is masked off afterwards)
     u64 noff = 0, nfirst = 0, nlast_end = 0, first_b = b, last_e = a;
+    u64 k0 = 0, k1 = 0;
     for (u64 pos = a; pos < b;) {
         const Dec d = utf8_dec(text, pos, b);
         const u32 cp = lower_cp(d.cp);
@@ -582,25 +584,22 @@ __device__ u32 slow_count_piece(const uint8_t* text, u64 a, u64 b, const TableVi
             last_e = pos + d.len;
             nlast_end = noff + el;
         }
+        if (first_b != b) {
+            const u64 at = noff - nfirst;
+            for (u32 k = 0; k < el && at + k < 16; ++k) {
+                const u64 byte = enc_byte(cp, el, k), i = at + k;
+                if (i < 8) k0 |= byte << (56 - 8 * i);
+                else k1 |= byte << (56 - 8 * (i - 8));
+            }
+        }
         noff += el;
         pos += d.len;
     }
     if (first_b == b) return 0;
     const u64 nlen = nlast_end - nfirst;
     if (nlen <= 16) {
-        u64 k0 = 0, k1 = 0;
-        u32 i = 0;
-        for (u64 pos = first_b; pos < last_e;) {
-            const Dec d = utf8_dec(text, pos, b);
-            const u32 cp = lower_cp(d.cp);
-            const u32 el = enc_len(cp);
-            for (u32 k = 0; k < el; ++k, ++i) {
-                const u64 byte = enc_byte(cp, el, k);
-                if (i < 8) k0 |= byte << (56 - 8 * i);
-                else k1 |= byte << (56 - 8 * (i - 8));
-            }
-            pos += d.len;
-        }
+        if (nlen <= 8) { k0 &= ~0ull << (64 - 8 * nlen); k1 = 0; }
+        else if (nlen < 16) k1 &= ~0ull << (128 - 8 * nlen);
         if (em) {
             const u64 at = atomicAdd(em->n_out, 1ull);
             if (at < em->cap) em->out[at] = TokenRec{k0, k1, 0ull, first_b};
