@@ -566,43 +566,48 @@ __device__ __forceinline__ u32 enc_byte(u32 cp, u32 n, u32 i) {
     return 0x80 | ((cp >> shift) & 0x3F);
 }
 
-// Counts (or, when em != nullptr, emits) the token of one whitespace-free piece
-// [a,b) of the text (normalize_word).
-// Returns 1 if the piece yields a token (the caller accounts the tokens: one atomic per warp, not per token).
-__device__ u32 slow_count_piece(const uint8_t* text, u64 a, u64 b, const TableView& gt, const EmitView* em,
-                                u32* inserted = nullptr) {
-    // one pass: normalised offsets of the first / last word character, and the first 16 normalised bytes from
-    // the first word character on (what lies behind the last word character is masked off afterwards)
-    u64 noff = 0, nfirst = 0, nlast_end = 0, first_b = b, last_e = a;
-    u64 k0 = 0, k1 = 0;
-    for (u64 pos = a; pos < b;) {
-        const Dec d = utf8_dec(text, pos, b);
-        const u32 cp = lower_cp(d.cp);
-        const u32 el = enc_len(cp);
-        if (word_char(cp)) {
-            if (first_b == b) { first_b = pos; nfirst = noff; }
-            last_e = pos + d.len;
-            nlast_end = noff + el;
-        }
-        if (first_b != b) {
-            const u64 at = noff - nfirst;
-            for (u32 k = 0; k < el && at + k < 16; ++k) {
-                const u64 byte = enc_byte(cp, el, k), i = at + k;
-                if (i < 8) k0 |= byte << (56 - 8 * i);
-                else k1 |= byte << (56 - 8 * (i - 8));
-            }
-        }
-        noff += el;
-        pos += d.len;
+// normalize_word over one whitespace-free piece of the text, fed one decoded character at a time so that the
+// caller's own walk over the fragment (which looks for Unicode whitespace) is the only one: normalised offsets of
+// the first / last word character, and the first 16 normalised bytes from the first word character on (what lies
+// behind the last word character is masked off at the end).
+struct Piece {
+    u64 noff, nfirst, nlast_end, first_b, last_e, k0, k1;
+    bool any;      // a word character was seen
+};
+__device__ __forceinline__ void piece_reset(Piece& p) {
+    p.noff = p.nfirst = p.nlast_end = p.first_b = p.last_e = p.k0 = p.k1 = 0;
+    p.any = false;
+}
+__device__ __forceinline__ void piece_feed(Piece& p, u64 pos, const Dec& d) {
+    const u32 cp = lower_cp(d.cp);
+    const u32 el = enc_len(cp);
+    if (word_char(cp)) {
+        if (!p.any) { p.any = true; p.first_b = pos; p.nfirst = p.noff; }
+        p.last_e = pos + d.len;
+        p.nlast_end = p.noff + el;
     }
-    if (first_b == b) return 0;
-    const u64 nlen = nlast_end - nfirst;
+    if (p.any) {
+        const u64 at = p.noff - p.nfirst;
+        for (u32 k = 0; k < el && at + k < 16; ++k) {
+            const u64 byte = enc_byte(cp, el, k), i = at + k;
+            if (i < 8) p.k0 |= byte << (56 - 8 * i);
+            else p.k1 |= byte << (56 - 8 * (i - 8));
+        }
+    }
+    p.noff += el;
+}
+// Counts (or, when em != nullptr, emits) the token of the piece.  Returns 1 if there is one (the caller
+// accounts the tokens: one atomic per warp, not per token).
+__device__ u32 piece_finish(const uint8_t* text, const Piece& p, const TableView& gt, const EmitView* em, u32* inserted) {
+    if (!p.any) return 0;
+    const u64 nlen = p.nlast_end - p.nfirst;
     if (nlen <= 16) {
+        u64 k0 = p.k0, k1 = p.k1;
         if (nlen <= 8) { k0 &= ~0ull << (64 - 8 * nlen); k1 = 0; }
         else if (nlen < 16) k1 &= ~0ull << (128 - 8 * nlen);
         if (em) {
             const u64 at = atomicAdd(em->n_out, 1ull);
-            if (at < em->cap) em->out[at] = TokenRec{k0, k1, 0ull, first_b};
+            if (at < em->cap) em->out[at] = TokenRec{k0, k1, 0ull, p.first_b};
         } else {
             table_add(gt, k0, k1, 1ull, inserted);
         }
@@ -614,8 +619,8 @@ __device__ u32 slow_count_piece(const uint8_t* text, u64 a, u64 b, const TableVi
     uint8_t* out = gt.arena + rec + 8;
     u32 h = 2166136261u;
     u64 i = 0, p0 = 0, p1 = 0;
-    for (u64 pos = first_b; pos < last_e;) {
-        const Dec d = utf8_dec(text, pos, b);
+    for (u64 pos = p.first_b; pos < p.last_e;) {      // every sequence in [first_b, last_e) is complete
+        const Dec d = utf8_dec(text, pos, p.last_e);
         const u32 cp = lower_cp(d.cp);
         const u32 el = enc_len(cp);
         for (u32 k = 0; k < el; ++k, ++i) {
@@ -631,12 +636,25 @@ __device__ u32 slow_count_piece(const uint8_t* text, u64 a, u64 b, const TableVi
     *reinterpret_cast<u32*>(gt.arena + rec + 4) = h;
     if (em) {
         const u64 at = atomicAdd(em->n_out, 1ull);
-        if (at < em->cap) em->out[at] = TokenRec{p0, p1, rec, first_b};
+        if (at < em->cap) em->out[at] = TokenRec{p0, p1, rec, p.first_b};
         return 1;
     }
     __threadfence();
     long_add(gt, rec, 1ull);
     return 1;
+}
+
+// the piece [a,b) on its own (normalize_word of a caller-supplied fragment)
+__device__ u32 slow_count_piece(const uint8_t* text, u64 a, u64 b, const TableView& gt, const EmitView* em,
+                                u32* inserted = nullptr) {
+    Piece p;
+    piece_reset(p);
+    for (u64 pos = a; pos < b;) {
+        const Dec d = utf8_dec(text, pos, b);
+        piece_feed(p, pos, d);
+        pos += d.len;
+    }
+    return piece_finish(text, p, gt, em, inserted);
 }
 
 __device__ __forceinline__ bool ascii_space(u32 b) { return b == 0x20 || (b >= 0x09 && b <= 0x0D); }
@@ -652,25 +670,24 @@ __global__ void wc_slow_kernel(const uint8_t* __restrict__ text, u64 n, TableVie
         const u64 e = gt.deferred[idx];
         u64 s = e;
         while (s > 0 && !ascii_space(text[s - 1])) --s;
-        // split [s,e) on valid non-ASCII whitespace code points (text.cpp:45-55)
-        u64 piece = s;
-        bool in_piece = false;
-        for (u64 pos = s; pos <= e;) {
-            Dec d{0, 1, false};
-            bool boundary = (pos == e);
-            if (!boundary) {
-                d = utf8_dec(text, pos, e);
-                boundary = d.valid && uni_space(d.cp);
-            }
-            if (boundary) {
-                if (in_piece) tokens += slow_count_piece(text, piece, pos, gt, emit ? &em : nullptr, &inserted);
-                in_piece = false;
-            } else if (!in_piece) {
-                piece = pos;
-                in_piece = true;
+        // one forward walk: a valid non-ASCII whitespace code point ends a piece (text.cpp:45-55), anything else
+        // feeds the piece's normalisation.  Decoding against the end of the fragment instead of the end of the
+        // piece changes nothing: the byte that follows a piece is the lead of the whitespace character, which no
+        // sequence accepts as a continuation byte.
+        const EmitView* emp = emit ? &em : nullptr;
+        Piece p;
+        piece_reset(p);
+        for (u64 pos = s; pos < e;) {
+            const Dec d = utf8_dec(text, pos, e);
+            if (d.valid && uni_space(d.cp)) {
+                tokens += piece_finish(text, p, gt, emp, &inserted);
+                piece_reset(p);
+            } else {
+                piece_feed(p, pos, d);
             }
             pos += d.len;
         }
+        tokens += piece_finish(text, p, gt, emp, &inserted);
     }
     // token and claimed-slot totals: one atomic per warp (a per-token atomic on one address was most of this kernel's time)
     for (int d = 16; d > 0; d >>= 1) {
