@@ -34,11 +34,12 @@
 #include <cstdlib>
 #include <type_traits>
 
-#include "wfcu_dev.cuh"
+#include "wc_count_common.cuh"
 
 namespace wfcu {
 
 namespace cnt3 {
+using namespace cntc;
 
 constexpr int kHalf = 512;                         // 32 lanes x 16 bytes
 constexpr int kRow = 2 * kHalf;
@@ -47,59 +48,7 @@ constexpr int kSlotStride = kGuard + kRow;         // 1056
 constexpr int kRingBytes = 2 * kSlotStride + 32;   // two slots + slack for the unaligned fetch
 constexpr int kQueueCap = 512;                     // u16 entries per warp: (len-1) << 12 | ring position, 0 = dead
 constexpr int kMissCap = 64;
-constexpr u32 kFull = 0xFFFFFFFFu;
-constexpr u64 kSlotLocked = 1ull;
 
-// ---- SWAR byte classes: bit 7 of each byte lane is the answer ----------------------
-// ASCII = true: caller guarantees no byte has bit 7 set.
-// The range-test additions can run on the FMA pipe as v * one + K (IMAD R, R, Rone, imm) with a 1 the
-// compiler cannot see through (a kernel argument): the integer ALU pipe is the busiest unit of the kernel.
-// WFCU_FMA_ADDS: bit i = addition i of classify4 goes to the FMA pipe.
-#ifndef WFCU_FMA_ADDS
-#define WFCU_FMA_ADDS 0
-#endif
-template <u32 K, int BIT>
-__device__ __forceinline__ u32 add_k(u32 v, u32 one) {
-    if ((WFCU_FMA_ADDS >> BIT) & 1) return v * one + K;
-    return v + K;
-}
-template <bool ASCII>
-__device__ __forceinline__ void classify4(u32 x, u32 one, u32& s, u32& t, u32& u, u32& f) {
-    const u32 M = 0x80808080u;
-    const u32 v = ASCII ? x : (x & 0x7F7F7F7Fu);
-    const u32 y = v | 0x20202020u;
-    t = add_k<0x1F1F1F1Fu, 0>(y, one) & ~add_k<0x05050505u, 1>(y, one) & M;          // 'a'..'z' after folding
-    u = add_k<0x50505050u, 2>(v, one) & ~add_k<0x46464646u, 3>(v, one) & M;          // '0'..'9'
-    const u32 z = add_k<0x7F7F7F7Fu, 4>(v ^ 0x20202020u, one);                       // bit 7 clear <=> byte == 0x20
-    s = (~z | (add_k<0x77777777u, 5>(v, one) & ~add_k<0x72727272u, 6>(v, one))) & M; // 0x20 or 0x09..0x0D
-    if (!ASCII) { t &= ~x; u &= ~x; s &= ~x; }
-    f = x | (t >> 2);                                        // A-Z -> a-z (a-z unchanged)
-}
-
-// flags (0x80 per byte) of two words -> 128 * (8-bit mask), accumulated on the FMA pipe
-__device__ __forceinline__ u32 gather8(u32 f0, u32 f1, u32 acc) {
-    return __dp4a(f0, 0x08040201u, __dp4a(f1, 0x80402010u, acc));
-}
-
-struct Masks { u32 s7, a7, h7; };   // 16-bit masks of one 16-byte chunk, scaled by 128
-
-template <bool ASCII>
-__device__ __forceinline__ Masks classify16(const uint4& x, u32 one, uint4& f) {
-    u32 s0, s1, s2, s3, t0, t1, t2, t3, u0, u1, u2, u3;
-    classify4<ASCII>(x.x, one, s0, t0, u0, f.x);
-    classify4<ASCII>(x.y, one, s1, t1, u1, f.y);
-    classify4<ASCII>(x.z, one, s2, t2, u2, f.z);
-    classify4<ASCII>(x.w, one, s3, t3, u3, f.w);
-    Masks m;
-    m.s7 = gather8(s2, s3, 0) * 256u + gather8(s0, s1, 0);
-    m.a7 = gather8(t2, t3, gather8(u2, u3, 0)) * 256u + gather8(t0, t1, gather8(u0, u1, 0));
-    m.h7 = 0;
-    if (!ASCII) {
-        const u32 M = 0x80808080u;
-        m.h7 = gather8(x.z & M, x.w & M, 0) * 256u + gather8(x.x & M, x.y & M, 0);
-    }
-    return m;
-}
 // Chunks with bytes >= 0x80.  Two-byte sequences C3..DF 80..BF (U+00C0..U+07FF: Latin-1 letters,
 // Latin Extended, Greek, Cyrillic, ...) stay on the fast path: every such code point is a word
 // character except U+00D7 and U+00F7, none is whitespace, and the only case fold in the range
@@ -190,40 +139,6 @@ __device__ __forceinline__ void hi_masks_finish(const HiIn& in, u32 lead_before,
     A |= (validC | in.L) & ~H;
 }
 
-// pack the masks of the lane's two chunks: low 16 bits = half a, high 16 bits = half b
-__device__ __forceinline__ u32 pack7(u32 a7, u32 b7) { return (b7 << 9) | (a7 >> 7); }
-
-__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
-    uint4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-    return v;
-}
-
-// PTX shifts clamp: a shift amount >= 32 gives 0 (C++ leaves it undefined)
-__device__ __forceinline__ u32 shr_clamp(u32 v, u32 s) {
-    u32 r;
-    asm("shr.b32 %0, %1, %2;" : "=r"(r) : "r"(v), "r"(s));
-    return r;
-}
-__device__ __forceinline__ u32 shl_clamp(u32 v, u32 s) {
-    u32 r;
-    asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(v), "r"(s));
-    return r;
-}
-// warp inclusive prefix sum; the shuffle's own predicate replaces the lane compare
-__device__ __forceinline__ u32 warp_inclusive_sum(u32 v) {
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        asm volatile("{ .reg .pred p; .reg .u32 t; shfl.sync.up.b32 t|p, %0, %1, 0, 0xffffffff; @p add.u32 %0, %0, t; }"
-                     : "+r"(v) : "r"(d));
-    }
-    return v;
-}
-
-__device__ __forceinline__ u32 bswap32(u32 v) { return __byte_perm(v, 0, 0x0123); }
-__device__ __forceinline__ u64 le_to_be(u64 v) { return ((u64)bswap32((u32)v) << 32) | bswap32((u32)(v >> 32)); }
-
 template <int WARPS, int SETS, int MSLOTS>
 struct __align__(1024) Smem {
     uint16_t queue[WARPS][kQueueCap];          // 1 KiB per warp, 1 KiB aligned (index wrap by OR)
@@ -238,33 +153,6 @@ struct __align__(1024) Smem {
     uint4 ring[WARPS][kRingBytes / 16];
     u32 mcnt[MSLOTS];
 };
-
-// Medium tokens (9..16 bytes): 2-way, k1 is written before k0 is published.
-__device__ __forceinline__ bool medium_add(u64* __restrict__ k0s, u64* __restrict__ k1s, u32* __restrict__ cnt,
-                                           u32 mask, u64 k0, u64 k1, u32 h) {
-    u32 i = h & mask;
-#pragma unroll 1
-    for (int way = 0; way < 2; ++way) {
-        u64 c0 = *reinterpret_cast<volatile u64*>(k0s + i);
-        if (c0 == 0) {
-            c0 = atomicCAS(k0s + i, 0ull, kSlotLocked);
-            if (c0 == 0) {
-                *reinterpret_cast<volatile u64*>(k1s + i) = k1;
-                __threadfence_block();
-                atomicExch(k0s + i, k0);
-                atomicAdd(cnt + i, 1u);
-                return true;
-            }
-        }
-        if (c0 == kSlotLocked) return false;
-        if (c0 == k0 && *reinterpret_cast<volatile u64*>(k1s + i) == k1) {
-            atomicAdd(cnt + i, 1u);
-            return true;
-        }
-        i = (h >> 16) & mask;
-    }
-    return false;
-}
 
 }  // namespace cnt3
 
@@ -792,38 +680,30 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
 template <int WARPS, int SETS, int MSLOTS, bool HI>
 __global__ void __launch_bounds__(WARPS * 32, 1)
 wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, int force, u32 one, TableView gt) {
-    bool hi = force == 1;
-    if (force != 0 && force != 1) {
-        const u64 first = (u64)blockIdx.x * WARPS * rows_per_warp * kRow;
-        const u64 span = (u64)WARPS * rows_per_warp * kRow;
-        const u64 at = (first + (u64)((unsigned __int128)threadIdx.x * span / (WARPS * 32))) & ~15ull;
-        bool hit = false;
-        if (at + 16 <= n) {
-            const uint4 v = *reinterpret_cast<const uint4*>(text + at);
-            hit = ((v.x | v.y | v.z | v.w) & 0x80808080u) != 0;
-        }
-        hi = __syncthreads_count(hit) >= 2;
-    }
+    const bool hi = variant_is_hi(text, n, (u64)blockIdx.x * WARPS * rows_per_warp * kRow, (u64)WARPS * rows_per_warp * kRow, force);
     if (hi != HI) return;
     wc_count_body<WARPS, SETS, MSLOTS, HI>(text, n, rows_per_warp, one, gt);
 }
 
 // ---- host-side launcher (called from wordcount.cu) ---------------------------------
-#ifndef WFCU_COUNT_WARPS
-#define WFCU_COUNT_WARPS 28
-#endif
 #ifndef WFCU_COUNT_SETS
 #define WFCU_COUNT_SETS 3840
 #endif
 #ifndef WFCU_COUNT_MED_SLOTS
 #define WFCU_COUNT_MED_SLOTS 256
 #endif
-constexpr int kCountWarps = WFCU_COUNT_WARPS;
+constexpr int kCountWarps = kCountVariantWarps;
 constexpr int kCountSets = WFCU_COUNT_SETS;             // two 8-byte keys + two counts per set (24 bytes)
 constexpr int kCountMedSlots = WFCU_COUNT_MED_SLOTS;    // 20 bytes each
 typedef Smem<kCountWarps, kCountSets, kCountMedSlots> CountSmem;
 static_assert(sizeof(CountSmem) + 1024 <= 227 * 1024, "shared memory budget");
 static_assert(2 * kSlotStride + 20 <= 4096, "queue entries keep ring positions in 12 bits");
+
+// wc_count4.cu: the fourth-generation ASCII body (bulk-TMA rows, tokens counted straight from the masks).  Exact, but
+// measured slower than this file's on every corpus (cfg3 934 against 1014 GB/s), so it only
+// runs when WFCU_COUNT_KERNEL=4 is set in the environment (A/B runs, tests).
+cudaError_t wc_count4_launch(const uint8_t* text, u64 n, u32 rows_per_warp, unsigned grid, int force, const TableView& gt,
+                             cudaStream_t stream);
 
 cudaError_t wc_count_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream, u64* launches) {
     const size_t smem = sizeof(CountSmem) + 1024;   // + slack for the 1 KiB alignment
@@ -839,7 +719,15 @@ cudaError_t wc_count_launch(const uint8_t* text, u64 n, const TableView& gt, int
     if (grid == 0) grid = 1;
     const u64 rows_per_warp = (n_rows + grid * kCountWarps - 1) / (grid * kCountWarps);
     static const int force = [] { const char* v = getenv("WFCU_COUNT_VARIANT"); return v ? atoi(v) : -1; }();   // tests: 0 / 1
-    if (force != 1) k_ascii<<<(unsigned)grid, kCountWarps * 32, smem, stream>>>(text, n, (u32)rows_per_warp, force, 1u, gt);
+    static const bool gen4_ascii = [] { const char* v = getenv("WFCU_COUNT_KERNEL"); return v && v[0] == '4'; }();
+    if (force != 1) {
+        if (!gen4_ascii) {
+            k_ascii<<<(unsigned)grid, kCountWarps * 32, smem, stream>>>(text, n, (u32)rows_per_warp, force, 1u, gt);
+        } else {
+            e = wc_count4_launch(text, n, (u32)rows_per_warp, (unsigned)grid, force, gt, stream);
+            if (e != cudaSuccess) return e;
+        }
+    }
     if (force != 0) k_hi<<<(unsigned)grid, kCountWarps * 32, smem, stream>>>(text, n, (u32)rows_per_warp, force, 1u, gt);
     *launches += (force == 0 || force == 1) ? 1 : 2;
     return cudaGetLastError();
