@@ -183,23 +183,37 @@ def build_corpus(capi, np, torch, vocab: int, docs: list[int], stride: int):
 
 
 def run_reference(args) -> None:
+    """The reference's own CPU implementation (wfc::run_wordcount, unmodified sources compiled into oracle/_ref) on
+    this box's host cores, on the b200 arm's config: every step counts the WHOLE shard of one GPU.  The corpus comes
+    from the stand-alone generator (oracle/libwfsynth.so): the CUDA library is never mapped into this process."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import numpy as np
     import oracle
-    from paper_2206_05269_b200 import capi
     oracle.build()
     cores = os.cpu_count() or 1
-    w, total, _ = plan(args.workload, max(args.gpus, 1), 0, args.docs)
+    w, total, my_docs = plan(args.workload, max(args.gpus, 1), 0, args.docs)
     use_ref = oracle.ref_available()
     cpu = oracle.ref() if use_ref else oracle.port()
+    k = len(my_docs)
+    same_config = True
+    if args.sample_docs:
+        k, same_config = min(k, args.sample_docs), args.sample_docs >= k
+    else:
+        # run_wordcount keeps every token as a std::string (about 100 bytes of host memory per corpus byte at its
+        # peak): bound the shard by what the box has, and say so
+        try:
+            import psutil
+            fit = int(psutil.virtual_memory().available * 0.6 / (100 * DOC_BYTES))
+            if fit < k:
+                k, same_config = max(8, fit), False
+        except Exception:
+            pass
+    blob = oracle.synth_corpus(SEED, my_docs[0], k, w["vocab"], ZIPF_S, 0, DOC_BYTES, doc_stride=max(args.gpus, 1))
+    docs = [blob[i * DOC_BYTES:(i + 1) * DOC_BYTES] for i in range(k)]
 
-    def docs_of(k):
-        blob = capi.synth_corpus(SEED, 0, k, w["vocab"], ZIPF_S, 0, DOC_BYTES)
-        return [blob[i * DOC_BYTES:(i + 1) * DOC_BYTES] for i in range(k)]
-
-    def one(docs):
+    def one():
         t0 = time.perf_counter()
         if use_ref:
             table, _ = cpu.run_wordcount(docs, cores)
@@ -207,29 +221,24 @@ def run_reference(args) -> None:
             table = cpu.wordcount(docs)
         return time.perf_counter() - t0, len(table)
 
-    # calibrate the bounded sample: ~4 s of CPU work per step, 8..256 documents
-    t_probe, _ = one(docs_of(8))
-    k = int(min(256, max(8, 8 * 4.0 / max(t_probe, 1e-3))))
-    if args.sample_docs:
-        k = args.sample_docs
-    docs = docs_of(k)
     for _ in range(args.warmup):
-        one(docs)
+        one()
     t0 = time.perf_counter()
     distinct = 0
     for _ in range(args.steps):
-        _, distinct = one(docs)
+        _, distinct = one()
     dt = time.perf_counter() - t0
     nbytes = k * DOC_BYTES
     value = nbytes * args.steps / dt / 1e9
-    sample = (f"{k} of {total} one-MiB documents ({nbytes / 1e6:.0f} MB) per step, "
+    sample = (f"{k} of the {len(my_docs)} one-MiB documents of one GPU's shard ({nbytes / 1e6:.0f} MB) per step, "
               f"{'wfc::run_wordcount(corpus, n_workers=%d)' % cores if use_ref else 'oracle port, serial'}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": w["scaling"],
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": w["name"], "vocab": w["vocab"], "zipf_s": ZIPF_S, "doc_bytes": DOC_BYTES, "seed": SEED,
-                   "sample": sample, "distinct_words_in_sample": distinct},
+                   "documents": total, "bytes_per_step": nbytes, "same_config": same_config,
+                   "sample": sample, "distinct_words": distinct},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores if use_ref else 1,
                          "kind": "reference" if use_ref else "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -238,8 +247,9 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(capi, vocab: int, total_docs: int) -> dict:
-    """The reference CPU path on this box's host cores, bounded sample (rank 0, N=1 only)."""
+def cpu_baseline(capi, vocab: int, total_docs: int):
+    """The reference CPU path on this box's host cores, bounded sample (rank 0, N=1 only).
+    Returns (the JSON object, documents in the sample, the reference's table of the sample)."""
     import oracle
     cores = os.cpu_count() or 1
     use_ref = oracle.ref_available()
@@ -250,17 +260,30 @@ def cpu_baseline(capi, vocab: int, total_docs: int) -> dict:
 
     def one(d):
         t0 = time.perf_counter()
-        cpu.run_wordcount(d, cores) if use_ref else cpu.wordcount(d)
-        return time.perf_counter() - t0
-    t = one(docs[:k])
+        table = cpu.run_wordcount(d, cores)[0] if use_ref else cpu.wordcount(d)
+        return time.perf_counter() - t0, table
+    t, table = one(docs[:k])
     if t < 5.0:      # grow the sample towards ~10-20 s of CPU work, at most 256 documents
         k = int(min(cap, max(k, k * 12.0 / max(t, 1e-3))))
-        t = one(docs[:k])
+        t, table = one(docs[:k])
     nbytes = k * DOC_BYTES
     return {"value": nbytes / t / 1e9, "unit": UNIT, "cores": cores if use_ref else 1,
             "kind": "reference" if use_ref else "port",
             "sample": f"first {k} of {total_docs} one-MiB documents ({nbytes / 1e6:.0f} MB), one run of "
-                      f"{'wfc::run_wordcount with n_workers=%d' % cores if use_ref else 'the serial oracle port'}, {t:.1f} s"}
+                      f"{'wfc::run_wordcount with n_workers=%d' % cores if use_ref else 'the serial oracle port'}, {t:.1f} s"}, k, table
+
+
+def parity_check(capi, dev_ptr: int, k: int, slots: int, ref_table: dict) -> dict:
+    """The table the timed kernels build, checked against the reference's: the first k documents of the resident
+    shard are counted once more into a fresh counter and the exported (ordered) table is compared entry by entry."""
+    c = capi.Counter(table_slots=slots)
+    c.count_dev(dev_ptr, k * DOC_BYTES)
+    blob, lens, counts = c.export()
+    words = capi.unpack_words(blob, lens)
+    want = sorted(ref_table.items())
+    equal = len(words) == len(want) and all(a == b[0] and int(n) == b[1] for a, n, b in zip(words, counts.tolist(), want))
+    return {"checked": True, "docs": k, "bytes": k * DOC_BYTES, "distinct": len(words), "equal": bool(equal),
+            "against": "reference run_wordcount table of the same documents (std::map order, exact counts)"}
 
 
 def run_b200(args) -> None:
@@ -286,8 +309,8 @@ def run_b200(args) -> None:
             dist.init_process_group("nccl", device_id=device)
         else:   # gloo carries CUDA tensors through the host: lets 2 ranks share one GPU in tests
             dist.init_process_group("gloo")
-    if world != max(args.gpus, 1) and rank == 0:
-        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    if world != max(args.gpus, 1):
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     all_cpus = os.sched_getaffinity(0)
     numa = bind_to_gpu_numa_node(torch, local_rank)
@@ -432,6 +455,7 @@ def run_b200(args) -> None:
                        "l2": "inputs (1 GB per GPU) larger than the 126 MB L2; no flush needed"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if peak else None, "traffic": ncu_traffic("wc_count_kernel", nbytes),
+                         "traffic_source": "static: ncu --set full capture of this kernel on this config (profiles/traffic.json), not re-measured in this run",
                          "kernel": "wc_count_kernel", "kernel_ms": k_ms, "kernel_launches": kernel_launches,
                          "algorithmic_bytes_per_launch": nbytes, "peak_source": peak_src},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": d2h,
@@ -443,9 +467,12 @@ def run_b200(args) -> None:
         line["host_numa"] = numa
         if world == 1 and not args.no_cpu:
             os.sched_setaffinity(0, all_cpus)      # the CPU baseline gets every core of the box
-            line["cpu_baseline"] = cpu_baseline(capi, w["vocab"], total_docs)
+            line["cpu_baseline"], k_docs, ref_table = cpu_baseline(capi, w["vocab"], total_docs)
+            line["parity"] = parity_check(capi, dev.data_ptr(), min(k_docs, len(my_docs)), slots, ref_table)
+            if not line["parity"]["equal"]:
+                print("PARITY FAILURE: the device table differs from the reference's", file=sys.stderr)
         if not args.no_mapreduce:
-            line["extra"] = {"mapreduce": mapreduce_line(capi, torch, device, stream, peak),
+            line["extra"] = {"mapreduce": mapreduce_line(capi, torch, device, stream, peak, world == 1 and not args.no_cpu),
                              "sanitize": sanitize_line(capi, torch, dev, nbytes, peak)}
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -453,10 +480,20 @@ def run_b200(args) -> None:
         dist.destroy_process_group()
 
 
-def mapreduce_line(capi, torch, device, stream, peak) -> dict:
-    """BASELINE.json config 2: sum of x^2 over 2^28 fp32 (1 GiB), resident, event timed."""
+def mapreduce_line(capi, torch, device, stream, peak, with_cpu: bool) -> dict:
+    """BASELINE.json config 2: sum of f(x) over 2^28 fp32 (1 GiB), f = identity and x^2.
+    Input = the reference bench's recipe (proj/src/cli.cpp:122-124: mt19937_64(seed 1), uniform(0,1)), rounded to
+    fp32.  Per map: resident + CUDA-event timed (GBps), checked against the oracle's serial fold
+    (engine.cpp:82-86 on the widened values; 1e-5 relative is the bar), end to end through wfcu_map_reduce_host from
+    pinned host memory (e2e_GBps, H2D inside), and the reference's own map_reduce_serial / map_reduce_blocked{256,
+    all cores} on this box's host cores (MapKind has no x^2: the CPU figures are the identity map's)."""
+    import numpy as np
+    import oracle
     n = 1 << 28
-    x = torch.rand(n, device=device, dtype=torch.float32)
+    host = torch.empty(n, dtype=torch.float32).pin_memory()
+    xh = host.numpy()
+    xh[:] = capi.synth_uniform(SEED, n, np.float32)
+    x = host.to(device, non_blocking=True)
     out = torch.zeros(1, device=device, dtype=torch.float64)
     res = {}
     for name, kind in (("identity", capi.MAP_IDENTITY), ("square", capi.MAP_SQUARE)):
@@ -470,10 +507,32 @@ def mapreduce_line(capi, torch, device, stream, peak) -> dict:
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 10
-        ref = float((x.double() if kind == capi.MAP_IDENTITY else x.double() ** 2).sum().item())
+        got = float(out.item())
+        ref = oracle.port().map_reduce_serial(xh, kind)
+        capi.map_reduce_host(xh, kind)
+        t0 = time.perf_counter()
+        e2e_got = 0.0
+        for _ in range(3):
+            e2e_got = capi.map_reduce_host(xh, kind)
+        e2e_s = (time.perf_counter() - t0) / 3
         res[name] = {"ms": ms, "GBps": 4 * n / ms / 1e6, "frac_of_hbm_peak": 4 * n / ms / 1e6 / peak,
-                     "rel_err_vs_torch_fp64": abs(float(out.item()) - ref) / max(1.0, abs(ref))}
-    return {"config": "sum f(x) over 2^28 fp32 (torch.rand), 1 GiB, 1 GPU", **res}
+                     "value": got, "oracle_serial_fold": ref, "rel_err_vs_oracle": abs(got - ref) / max(1.0, abs(ref)),
+                     "e2e_GBps": 4 * n / e2e_s / 1e9, "e2e_rel_err_vs_oracle": abs(e2e_got - ref) / max(1.0, abs(ref)),
+                     "e2e_api": "wfcu_map_reduce_host (pinned host fp32 -> H2D -> reduce -> scalar)"}
+    line = {"config": "sum f(x) over 2^28 fp32, mt19937_64(1) uniform(0,1) (reference bench recipe), 1 GiB, 1 GPU", **res}
+    if with_cpu and oracle.ref_available():
+        cores = os.cpu_count() or 1
+        m = 1 << 26      # bounded sample: 2^26 doubles (the reference's spans are fp64)
+        xd = xh[:m].astype(np.float64)
+        t0 = time.perf_counter()
+        v1 = oracle.ref().map_reduce_serial(xd, capi.MAP_IDENTITY)
+        t1 = time.perf_counter()
+        v2 = oracle.ref().map_reduce_blocked(xd, capi.MAP_IDENTITY, 256, cores)
+        t2 = time.perf_counter()
+        line["cpu_baseline"] = {"kind": "reference", "sample": f"first 2^26 of the 2^28 values, widened to fp64 ({8 * m >> 20} MiB)",
+                                "map_reduce_serial": {"GBps_of_fp64": 8 * m / (t1 - t0) / 1e9, "cores": 1, "value": v1},
+                                "map_reduce_blocked_256": {"GBps_of_fp64": 8 * m / (t2 - t1) / 1e9, "cores": cores, "value": v2}}
+    return line
 
 
 def sanitize_line(capi, torch, dev, nbytes, peak) -> dict:
@@ -503,6 +562,17 @@ def sanitize_line(capi, torch, dev, nbytes, peak) -> dict:
     return {"config": "utf8_sanitize of the resident 1 GB shard, 1 GPU", **res}
 
 
+def self_launch_cmd(gpus: int, argv: list[str], port: int | None = None) -> list[str]:
+    """`python bench.py --gpus N` outside torchrun: the command that runs it as one rank per GPU."""
+    if port is None:
+        import socket
+        with socket.socket() as sock:
+            sock.bind(("127.0.0.1", 0))
+            port = sock.getsockname()[1]
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *argv]
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -520,6 +590,12 @@ def main() -> None:
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-mapreduce", action="store_true", help="skip the config-2 map-reduce extra")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "b200":
+        # one rank per GPU: re-run under torch.distributed.run (NCCL's init lines stay on: they name every rank)
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        raise SystemExit(subprocess.call(self_launch_cmd(args.gpus, sys.argv[1:]), env=env))
     # the native libraries are built in-tree; make sure they exist and are current (rank 0 builds, a no-op when fresh)
     from paper_2206_05269_b200 import build as native
     if int(os.environ.get("LOCAL_RANK", "0")) == 0:

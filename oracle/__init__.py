@@ -279,6 +279,38 @@ class CpuLib:
 
 
 _cache: dict[str, CpuLib] = {}
+SYNTH_LIB = HERE / "libwfsynth.so"
+
+
+def _synth():
+    if "synth" not in _cache:
+        if not SYNTH_LIB.exists():
+            build()
+        lib = C.CDLL(str(SYNTH_LIB))
+        lib.wfs_corpus_strided.restype = C.c_int
+        lib.wfs_corpus_strided.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, C.c_double,
+                                           C.c_uint32, C.c_uint64, C.c_void_p, C.c_int]
+        lib.wfs_uniform.restype = C.c_int
+        lib.wfs_uniform.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_void_p]
+        _cache["synth"] = lib
+    return _cache["synth"]
+
+
+def synth_corpus(seed: int, doc_begin: int, n_docs: int, vocab: int, zipf_s: float = 1.1, speaker: int = 0,
+                 doc_bytes: int = 1 << 20, doc_stride: int = 1) -> np.ndarray:
+    """The bench corpus (documents doc_begin, doc_begin + stride, ...) without the CUDA library in the process."""
+    out = np.empty(n_docs * doc_bytes, np.uint8)
+    rc = _synth().wfs_corpus_strided(seed, doc_begin, doc_stride, n_docs, vocab, zipf_s, speaker, doc_bytes, _ptr(out), 0)
+    assert rc == 0
+    return out
+
+
+def synth_uniform(seed: int, n: int, dtype=np.float64) -> np.ndarray:
+    """mt19937_64(seed) + uniform(0,1), the reference bench's input recipe (proj/src/cli.cpp:120-125)."""
+    out = np.empty(n, dtype)
+    rc = _synth().wfs_uniform(seed, n, 1 if out.dtype == np.float64 else 0, _ptr(out))
+    assert rc == 0
+    return out
 
 
 def port() -> CpuLib:
