@@ -201,11 +201,11 @@ def run_reference(args) -> None:
     if args.sample_docs:
         k, same_config = min(k, args.sample_docs), args.sample_docs >= k
     else:
-        # run_wordcount keeps every token as a std::string (about 100 bytes of host memory per corpus byte at its
+        # run_wordcount keeps every token as a std::string (a few tens of bytes of host memory per corpus byte at its
         # peak): bound the shard by what the box has, and say so
         try:
             import psutil
-            fit = int(psutil.virtual_memory().available * 0.6 / (100 * DOC_BYTES))
+            fit = int(psutil.virtual_memory().available * 0.6 / (40 * DOC_BYTES))
             if fit < k:
                 k, same_config = max(8, fit), False
         except Exception:

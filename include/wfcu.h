@@ -172,6 +172,16 @@ WFCU_API int wfcu_counter_top_k(wfcu_counter* c, uint64_t k, void* stream, uint8
                                 uint32_t* key_lens, uint64_t* counts, double* rel_freq, uint64_t rows_cap,
                                 uint64_t* n_rows, uint64_t* total_words);
 
+/* distinctive_words (proj/src/analysis.cpp:77-132; the per-speaker report of cli.cpp:213-221) on two device-resident
+ * tables, without exporting either: score = log((c_t+1)/(T_t+V)) - log((c_o+1)/(T_o+V)), V = size of the union
+ * vocabulary, rows by score descending (exact double compare), ties by word ascending, at most k.  The tables are
+ * joined and scored on the device; only the rows that can make the cut are downloaded and ranked with the
+ * reference's expression in host doubles, so words and scores are bit-identical to the reference's.  Both
+ * counters must live on the same device.  key_bytes_cap >= 16 * k covers tables without long tokens. */
+WFCU_API int wfcu_counter_distinctive(wfcu_counter* target, wfcu_counter* others, uint64_t k, void* stream,
+                                      uint8_t* key_bytes, uint64_t key_bytes_cap, uint32_t* key_lens, double* scores,
+                                      uint64_t rows_cap, uint64_t* n_rows);
+
 /* dst[word] += src[word]  (merge_counts, proj/src/reduce.cpp:83-89), on device. */
 WFCU_API int wfcu_counter_merge(wfcu_counter* dst, const wfcu_counter* src, void* stream);
 

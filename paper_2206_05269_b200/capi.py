@@ -78,6 +78,8 @@ SIGNATURES = {
     "wfcu_counter_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64]),
     "wfcu_counter_top_k": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.c_uint64, u64p, u64p]),
+    "wfcu_counter_distinctive": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64,
+                                           C.c_void_p, C.c_void_p, C.c_uint64, u64p]),
     "wfcu_counter_merge": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "wfcu_counter_add_words": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64]),
     "wfcu_owner_of": (C.c_uint32, [C.c_void_p, C.c_uint32, C.c_uint32]),
@@ -342,6 +344,18 @@ class Counter:
         n = rows.value
         words = unpack_words(blob, lens[:n])
         return [(words[r], int(counts[r]), float(rel[r])) for r in range(n)], total.value
+
+    def distinctive(self, others: "Counter", k: int, stream: int = 0) -> list[tuple[bytes, float]]:
+        """distinctive_words(self, others) on the device tables: [(word, score)], at most k rows."""
+        cap = max(k, 1)
+        kb = np.zeros(64 * cap + 1024, np.uint8)
+        kl = np.zeros(cap, np.uint32)
+        sc = np.zeros(cap, np.float64)
+        n = C.c_uint64()
+        check(lib.wfcu_counter_distinctive(self._h, others._h, k, C.c_void_p(stream), _ptr(kb), kb.size, _ptr(kl),
+                                           _ptr(sc), cap, C.byref(n)))
+        words = unpack_words(kb, kl[:n.value])
+        return [(w, float(sc[i])) for i, w in enumerate(words)]
 
     def merge(self, other: "Counter", stream: int = 0) -> None:
         check(lib.wfcu_counter_merge(self._h, other._h, C.c_void_p(stream)))

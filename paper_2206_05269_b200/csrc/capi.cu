@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <map>
 #include <string>
 #include <thread>
 #include <utility>
@@ -31,6 +32,12 @@ cudaError_t mr_blocked_launch(const void* values, int is_f64, u64 n, u64 base, i
 cudaError_t tb_compact(const TableView& t, Slot* out, u64 cap, u64* dev_count, int sm, cudaStream_t s, u64* launches);
 cudaError_t tb_compact_recs(const TableView& t, TokenRec* out, u64 cap, u64* dev_count, int sm, cudaStream_t s, u64* launches);
 cudaError_t tb_lower_bound_pos(const TokenRec* recs, u64 n, u64 value, u64* dev_out, cudaStream_t s, u64* launches);
+cudaError_t tb_union_rows(const TableView& target, const TableView& others, TokenRec* recs, u64* ct, u64* co, u64 cap,
+                          u64* dev_cursor, int sm, cudaStream_t s, u64* launches);
+cudaError_t tb_score_rows(TokenRec* recs, const u64* ct, const u64* co, const u64* dev_n_rows, u64 max_rows, u64 extra_vocab,
+                          u64 t_total, u64 o_total, int sm, cudaStream_t s, u64* launches);
+cudaError_t tb_gather_counts(const TokenRec* recs, u64 first, u64 n, const u64* ct, const u64* co, u64* out_ct, u64* out_co,
+                             int sm, cudaStream_t s, u64* launches);
 cudaError_t tb_export_pack(const TokenRec* recs, u64 n, u64* lens64, u64* tmp, uint8_t* bytes, u32* lens32, u64* counts,
                            u64* dev_total_bytes, int sm, cudaStream_t s, u64* launches);
 cudaError_t tb_key_bytes(const TableView& t, u64* dev_bytes, int sm, cudaStream_t s, u64* launches);
@@ -79,6 +86,13 @@ uint64_t analysis_top_k(const uint8_t* bytes, const uint32_t* lens, const uint64
 uint64_t analysis_distinctive(const uint8_t* t_bytes, const uint32_t* t_lens, const uint64_t* t_counts, uint64_t nt,
                               const uint8_t* o_bytes, const uint32_t* o_lens, const uint64_t* o_counts, uint64_t no,
                               uint64_t k, int32_t* out_src, uint64_t* out_idx, double* out_score);
+struct ScoredRow {
+    const uint8_t* key;
+    uint32_t len;
+    uint64_t in_target, in_others, tag;
+    double score;
+};
+uint64_t analysis_rank_rows(std::vector<ScoredRow>& rows, uint64_t vocab, uint64_t t_total, uint64_t o_total, uint64_t k);
 // synth.cpp
 int synth_document(uint64_t seed, uint64_t doc, uint32_t vocab, double s, uint32_t speaker, uint8_t* out, uint64_t doc_bytes);
 int synth_corpus(uint64_t seed, uint64_t doc_begin, uint64_t doc_end, uint32_t vocab, double s, uint32_t speaker,
@@ -783,6 +797,136 @@ extern "C" int wfcu_counter_top_k(wfcu_counter* c, uint64_t k, void* stream, uin
         key_lens[r] = (u32)cand[r].key.size();
         counts[r] = cand[r].count;
         rel_freq[r] = double(cand[r].count) / double(*total_words);
+    }
+    *n_rows = keep;
+    return WFCU_OK;
+}
+
+// the long-token table of a counter (rare) as host strings
+static int counter_pull_long(wfcu_counter* c, u64 arena_used, cudaStream_t s, std::vector<HostEntry>* out) {
+    std::vector<u64> refs(c->long_slots), cnts(c->long_slots);
+    std::vector<uint8_t> arena(arena_used);
+    CUDA_TRY(cudaMemcpyAsync(refs.data(), c->v.long_ref, sizeof(u64) * c->long_slots, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(cnts.data(), c->v.long_count, sizeof(u64) * c->long_slots, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(arena.data(), c->v.arena, arena_used, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    for (u64 i = 0; i < c->long_slots; ++i) {
+        if (!refs[i]) continue;
+        u32 len;
+        std::memcpy(&len, arena.data() + refs[i], 4);
+        out->push_back({std::string(reinterpret_cast<const char*>(arena.data() + refs[i] + 8), len), cnts[i]});
+    }
+    return WFCU_OK;
+}
+
+static inline double sort_key_to_double(u64 key) {
+    const u64 b = (key >> 63) ? (key ^ 0x8000000000000000ull) : ~key;
+    double v;
+    std::memcpy(&v, &b, 8);
+    return v;
+}
+static inline u64 double_to_sort_key(double v) {
+    u64 b;
+    std::memcpy(&b, &v, 8);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// distinctive_words (proj/src/analysis.cpp:77-132; cli.cpp:213-221) on two device-resident tables.
+//   1. the union of the two tables as dense rows {word, count in target, count in others}: every slot of one table
+//      probes the other (tb_union_rows), which also gives the size V of the union vocabulary;
+//   2. a score per row on the device and a radix sort by it;
+//   3. only the rows whose device score is within 1e-9 of the k-th best are downloaded (the device's log may differ
+//      from the host's in the last bits; ties are exact, they share both counts) and ranked by
+//      analysis_rank_rows: the reference's expression in host doubles, score descending by exact compare, word
+//      ascending.  Tokens longer than 16 bytes (rare) are joined and scored on the host.
+extern "C" int wfcu_counter_distinctive(wfcu_counter* target, wfcu_counter* others, uint64_t k, void* stream,
+                                        uint8_t* key_bytes, uint64_t key_bytes_cap, uint32_t* key_lens, double* scores,
+                                        uint64_t rows_cap, uint64_t* n_rows) {
+    if (!target || !others || !n_rows) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
+    if (target->device != others->device) return fail(WFCU_ERR_INVALID_ARGUMENT, "the two tables live on different devices");
+    cudaStream_t s = (cudaStream_t)stream;
+    u64 ht[8], ho[8];
+    CUDA_TRY(cudaMemcpyAsync(ht, target->counters, sizeof(ht), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(ho, others->counters, sizeof(ho), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (int rc = status_to_rc((int)(ht[5] & 0xFFFFFFFFu))) return rc;
+    if (int rc = status_to_rc((int)(ho[5] & 0xFFFFFFFFu))) return rc;
+    *n_rows = 0;
+    const u64 t_total = ht[1], o_total = ho[1];
+    // long tokens: joined here
+    std::vector<HostEntry> lt, lo;
+    if (ht[3]) { if (int rc = counter_pull_long(target, ht[4], s, &lt)) return rc; }
+    if (ho[3]) { if (int rc = counter_pull_long(others, ho[4], s, &lo)) return rc; }
+    std::map<std::string, std::pair<u64, u64>> longs;
+    for (const auto& e : lt) longs[e.key].first += e.count;
+    for (const auto& e : lo) longs[e.key].second += e.count;
+
+    const u64 cap = ht[0] + ho[0];
+    std::vector<TokenRec> cand;
+    std::vector<u64> cand_ct, cand_co;
+    u64 n_union = 0;
+    LaunchTally tally;
+    if (cap) {
+        DevBuf recs, alt, ct, co, hist, tmp, flag, oct, oco;
+        const u64 hw = sort_hist_words(cap);
+        CUDA_TRY(recs.alloc(sizeof(TokenRec) * cap));
+        CUDA_TRY(alt.alloc(sizeof(TokenRec) * cap));
+        CUDA_TRY(ct.alloc(sizeof(u64) * cap));
+        CUDA_TRY(co.alloc(sizeof(u64) * cap));
+        CUDA_TRY(hist.alloc(sizeof(u64) * hw));
+        CUDA_TRY(tmp.alloc(sizeof(u64) * scan_tmp_words(hw)));
+        CUDA_TRY(flag.alloc(sizeof(int)));
+        u64* cursor = target->counters + 10;     // [10] rows of the union, [11] words in both tables
+        CUDA_TRY(tb_union_rows(target->v, others->v, recs.as<TokenRec>(), ct.as<u64>(), co.as<u64>(), cap, cursor,
+                               target->sm_count, s, &tally.n));
+        CUDA_TRY(tb_score_rows(recs.as<TokenRec>(), ct.as<u64>(), co.as<u64>(), cursor, cap, longs.size(), t_total, o_total,
+                               target->sm_count, s, &tally.n));
+        CUDA_TRY(cudaMemcpyAsync(&n_union, cursor, sizeof(u64), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (n_union && k) {
+            SortScratch sc{alt.as<TokenRec>(), hist.as<u64>(), tmp.as<u64>(), flag.as<int>()};
+            CUDA_TRY(tokens_sort(recs.as<TokenRec>(), n_union, /*by_position=*/true, nullptr, sc, target->sm_count, s, &tally.n));
+            const u64 kth = n_union > k ? n_union - k : 0;
+            TokenRec pivot;
+            CUDA_TRY(cudaMemcpyAsync(&pivot, recs.as<TokenRec>() + kth, sizeof(TokenRec), cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            const double thr = sort_key_to_double(pivot.pos);
+            const double low = thr - 1e-9 * std::max(1.0, std::fabs(thr));
+            CUDA_TRY(tb_lower_bound_pos(recs.as<TokenRec>(), n_union, double_to_sort_key(low), target->counters + 9, s, &tally.n));
+            u64 first = 0;
+            CUDA_TRY(cudaMemcpyAsync(&first, target->counters + 9, sizeof(u64), cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            const u64 m = n_union - first;
+            CUDA_TRY(oct.alloc(sizeof(u64) * m));
+            CUDA_TRY(oco.alloc(sizeof(u64) * m));
+            CUDA_TRY(tb_gather_counts(recs.as<TokenRec>(), first, n_union, ct.as<u64>(), co.as<u64>(), oct.as<u64>(), oco.as<u64>(),
+                                      target->sm_count, s, &tally.n));
+            cand.resize(m); cand_ct.resize(m); cand_co.resize(m);
+            CUDA_TRY(cudaMemcpyAsync(cand.data(), recs.as<TokenRec>() + first, sizeof(TokenRec) * m, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaMemcpyAsync(cand_ct.data(), oct.p, sizeof(u64) * m, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaMemcpyAsync(cand_co.data(), oco.p, sizeof(u64) * m, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+        }
+    }
+    // exact ranking on the host: the candidates and every long row
+    std::vector<uint8_t> keybuf(16 * cand.size());
+    std::vector<ScoredRow> rows;
+    rows.reserve(cand.size() + longs.size());
+    for (size_t i = 0; i < cand.size(); ++i) {
+        key_to_bytes(cand[i].k0, cand[i].k1, keybuf.data() + 16 * i);
+        rows.push_back({keybuf.data() + 16 * i, key_len(cand[i].k0, cand[i].k1), cand_ct[i], cand_co[i], 0, 0.0});
+    }
+    for (const auto& kv : longs)
+        rows.push_back({reinterpret_cast<const uint8_t*>(kv.first.data()), (uint32_t)kv.first.size(), kv.second.first, kv.second.second, 1, 0.0});
+    const u64 keep = analysis_rank_rows(rows, n_union + longs.size(), t_total, o_total, k);
+    if (keep > rows_cap) return fail(WFCU_ERR_BUFFER_TOO_SMALL, "distinctive needs %llu rows", (unsigned long long)keep);
+    u64 off = 0;
+    for (u64 r = 0; r < keep; ++r) {
+        if (off + rows[r].len > key_bytes_cap) return fail(WFCU_ERR_BUFFER_TOO_SMALL, "distinctive key buffer too small");
+        std::memcpy(key_bytes + off, rows[r].key, rows[r].len);
+        off += rows[r].len;
+        key_lens[r] = rows[r].len;
+        scores[r] = rows[r].score;
     }
     *n_rows = keep;
     return WFCU_OK;

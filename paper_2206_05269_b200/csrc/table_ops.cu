@@ -272,6 +272,78 @@ __global__ void tb_long_merge_kernel(TableView t, const uint8_t* __restrict__ re
     }
 }
 
+
+// ---- distinctive_words on the device (proj/src/analysis.cpp:77-132) ---------------------------------------
+// counts[key] of the table, 0 if the key is absent (read only: the table is not being written)
+__device__ __forceinline__ bool table_find(const TableView& t, u64 k0, u64 k1, u64* count) {
+    u64 i = mix32(k0, k1) & t.mask;
+    for (u64 probes = 0; probes <= t.mask; ++probes) {
+        const Slot s = t.slots[i];
+        if (s.k0 == 0) return false;
+        if (s.k0 == k0 && s.k1 == k1) { *count = s.count; return true; }
+        i = (i + 1) & t.mask;
+    }
+    return false;
+}
+// Union of two tables as dense rows: every word of `a` (with its count in `b`), and -- second launch, swapped,
+// only_missing -- every word of `b` that `a` does not hold.  recs[i] = {k0,k1,ext=i,pos=0}, ca[i] / cb[i] = the two
+// counts; cursor[0] = rows written, cursor[1] += words found in both tables (first launch only).
+__global__ void tb_union_rows_kernel(TableView a, TableView b, bool only_missing, TokenRec* __restrict__ recs,
+                                     u64* __restrict__ ca, u64* __restrict__ cb, u64 cap, u64* __restrict__ cursor) {
+    const u32 lane = threadIdx.x & 31;
+    u32 both = 0;
+    for (u64 i0 = (u64)blockIdx.x * blockDim.x + threadIdx.x - lane; i0 <= a.mask; i0 += (u64)gridDim.x * blockDim.x) {
+        const u64 i = i0 + lane;
+        Slot s{};
+        if (i <= a.mask) s = a.slots[i];
+        bool live = s.k0 != 0;
+        u64 other = 0;
+        if (live) {
+            const bool found = table_find(b, s.k0, s.k1, &other);
+            if (found && !only_missing) ++both;
+            if (found && only_missing) live = false;
+        }
+        const u32 m = __ballot_sync(0xFFFFFFFFu, live);
+        u64 base = 0;
+        if (lane == 0 && m) base = atomicAdd(cursor, (u64)__popc(m));
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        const u64 j = base + __popc(m & ((1u << lane) - 1u));
+        if (live && j < cap) {
+            recs[j] = TokenRec{s.k0, s.k1, j, 0ull};
+            ca[j] = only_missing ? 0ull : s.count;
+            cb[j] = only_missing ? s.count : other;
+        }
+    }
+    for (int d = 16; d > 0; d >>= 1) both += __shfl_xor_sync(0xFFFFFFFFu, both, d);
+    if (lane == 0 && both) atomicAdd(cursor + 1, (u64)both);
+}
+// ascending order of the key = ascending order of the double
+__device__ __forceinline__ u64 double_sort_key(double v) {
+    const u64 b = (u64)__double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+// recs[i].pos = sort key of the score  log((ct+1)/(Tt+V)) - log((co+1)/(To+V)),  V = rows + extra_vocab.  The device's
+// log is within a few ulp of the host's: the caller only uses these scores to find which rows CAN make the cut
+// (with a margin), the reported scores are computed on the host with the reference's expression.
+__global__ void tb_score_rows_kernel(TokenRec* __restrict__ recs, const u64* __restrict__ ct, const u64* __restrict__ co,
+                                     const u64* __restrict__ n_rows, u64 extra_vocab, u64 t_total, u64 o_total) {
+    const u64 n = *n_rows;
+    const double v = (double)(n + extra_vocab);
+    const double t_den = (double)t_total + v, o_den = (double)o_total + v;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const double sc = log(((double)ct[i] + 1.0) / t_den) - log(((double)co[i] + 1.0) / o_den);
+        recs[i].pos = double_sort_key(sc);
+    }
+}
+// the two counts of the candidate rows recs[first, n), in that order
+__global__ void tb_gather_counts_kernel(const TokenRec* __restrict__ recs, u64 first, u64 n, const u64* __restrict__ ct,
+                                        const u64* __restrict__ co, u64* __restrict__ out_ct, u64* __restrict__ out_co) {
+    for (u64 i = first + (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        out_ct[i - first] = ct[recs[i].ext];
+        out_co[i - first] = co[recs[i].ext];
+    }
+}
+
 // ---- launchers ----------------------------------------------------------------------
 static inline unsigned grid_for(u64 items, int sm_count) {
     u64 g = (items + 255) / 256;
@@ -382,6 +454,31 @@ cudaError_t tb_long_merge(const TableView& t, const uint8_t* recs, u64 n_bytes, 
                           u64* launches) {
     if (n_bytes == 0) return cudaSuccess;
     tb_long_merge_kernel<<<1, 32, 0, s>>>(t, recs, n_bytes, part, n_parts);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+// rows of the union of target and others; dev_cursor[0] = rows, dev_cursor[1] = words in both
+cudaError_t tb_union_rows(const TableView& target, const TableView& others, TokenRec* recs, u64* ct, u64* co, u64 cap,
+                          u64* dev_cursor, int sm, cudaStream_t s, u64* launches) {
+    cudaError_t e = cudaMemsetAsync(dev_cursor, 0, 2 * sizeof(u64), s);
+    if (e != cudaSuccess) return e;
+    tb_union_rows_kernel<<<grid_for(target.mask + 1, sm), 256, 0, s>>>(target, others, false, recs, ct, co, cap, dev_cursor);
+    // words only the others hold: written as (a = others, b = target), so the count lands in cb = `co`
+    tb_union_rows_kernel<<<grid_for(others.mask + 1, sm), 256, 0, s>>>(others, target, true, recs, ct, co, cap, dev_cursor);
+    *launches += 2;
+    return cudaGetLastError();
+}
+cudaError_t tb_score_rows(TokenRec* recs, const u64* ct, const u64* co, const u64* dev_n_rows, u64 max_rows, u64 extra_vocab,
+                          u64 t_total, u64 o_total, int sm, cudaStream_t s, u64* launches) {
+    tb_score_rows_kernel<<<grid_for(max_rows, sm), 256, 0, s>>>(recs, ct, co, dev_n_rows, extra_vocab, t_total, o_total);
+    *launches += 1;
+    return cudaGetLastError();
+}
+cudaError_t tb_gather_counts(const TokenRec* recs, u64 first, u64 n, const u64* ct, const u64* co, u64* out_ct, u64* out_co,
+                             int sm, cudaStream_t s, u64* launches) {
+    if (first >= n) return cudaSuccess;
+    tb_gather_counts_kernel<<<grid_for(n - first, sm), 256, 0, s>>>(recs, first, n, ct, co, out_ct, out_co);
     *launches += 1;
     return cudaGetLastError();
 }
