@@ -280,6 +280,11 @@ WFCU_API int wfcu_tokens_export(const wfcu_tokens* t, uint8_t* bytes, uint64_t b
 /* Builds a device token list from packed host words (WordList -> device). */
 WFCU_API int wfcu_tokens_from_words(const uint8_t* bytes, const uint32_t* lens, uint64_t n_tokens,
                            wfcu_tokens** out);
+/* The exchange of the paper's range-partitioned pipeline in device memory (proj/src/shuffle.cpp:98-130: chunk c of
+ * every worker's sorted list goes to worker c): a new list made of the slices [begin[i], end[i]) of n_src lists, in
+ * that order.  Device-to-device copies (peer copies between GPUs); no frame, no host string. */
+WFCU_API int wfcu_tokens_concat_slices(const wfcu_tokens* const* src, const uint64_t* begin, const uint64_t* end,
+                                       uint32_t n_src, wfcu_tokens** out);
 /* sort_words (proj/src/text.cpp:59-63): stable byte-wise sort, in place. */
 WFCU_API int wfcu_tokens_sort(wfcu_tokens* t, void* stream);
 /* reduce_sorted (proj/src/reduce.cpp:8-21): run-length encodes a sorted list
@@ -288,6 +293,31 @@ WFCU_API int wfcu_tokens_reduce_sorted(const wfcu_tokens* t, wfcu_counter* into,
 /* The sort + RLE alternative end to end on a device buffer: tokenize, sort,
  * run-length encode, add the runs to the counter. */
 WFCU_API int wfcu_counter_count_dev_sorted(wfcu_counter* c, const uint8_t* dev_text, uint64_t n, void* stream);
+
+/* ------------------------------------------------------------------------- */
+/* run_wordcount over n workers on the GPUs of one box                         */
+/* (proj/src/pipeline.cpp:61-123, proj/include/wfc/pipeline.hpp:15-51)         */
+/* ------------------------------------------------------------------------- */
+
+/* StageTimings (proj/include/wfc/pipeline.hpp:15-23), filled from CUDA events: maximum over the workers. */
+typedef struct wfcu_stage_ns {
+    uint64_t map_ns;       /* H2D + fused tokenize / count kernels */
+    uint64_t sort_ns;      /* 0: the hash-count path does not sort */
+    uint64_t encode_ns;    /* partition of the local table by owner */
+    uint64_t exchange_ns;  /* device-to-device delivery of the regions + merge-insert */
+    uint64_t reduce_ns;    /* 0 here: the caller exports the owner tables */
+    uint64_t repair_ns;    /* 0: every key has exactly one owner */
+    uint64_t total_ns;     /* host wall clock of the call */
+} wfcu_stage_ns;
+
+/* Worker j (0 <= j < n_workers) lives on device j mod wfcu_device_count(), counts the documents d = j (mod n_workers)
+ * (the reference's rule, pipeline.cpp:83) and ends up owning the keys whose owner hash is j: out_shards[j] is that
+ * table, resident on its device (the caller destroys it).  One host thread per worker; regions travel device to
+ * device (cudaMemcpyPeerAsync: NVLink between GPUs).  The union of the shards is serial_wordcount's map and no key
+ * has two holders (count_unreduced_words == 0).  cfg sizes every table (NULL: defaults).  On failure nothing is
+ * returned and the message names the lowest-indexed worker that failed. */
+WFCU_API int wfcu_wordcount_multi(const uint8_t* const* docs, const uint64_t* lens, uint64_t n_docs, uint32_t n_workers,
+                                  const wfcu_counter_config* cfg, wfcu_counter** out_shards, wfcu_stage_ns* timings);
 
 /* ------------------------------------------------------------------------- */
 /* top_k / distinctive_words over exported tables                            */

@@ -78,6 +78,8 @@ SIGNATURES = {
     "wfcu_counter_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64]),
     "wfcu_counter_top_k": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.c_uint64, u64p, u64p]),
+    "wfcu_wordcount_multi": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "wfcu_tokens_concat_slices": (C.c_int, [C.c_void_p, u64p, u64p, C.c_uint32, C.POINTER(C.c_void_p)]),
     "wfcu_counter_distinctive": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64,
                                            C.c_void_p, C.c_void_p, C.c_uint64, u64p]),
     "wfcu_counter_merge": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -250,8 +252,18 @@ class HostDocs:
         self.lens = (C.c_uint64 * max(self.n, 1))(*[a.size for a in self._keep])
 
 
+class StageNs(C.Structure):
+    _fields_ = [(k, C.c_uint64) for k in ("map_ns", "sort_ns", "encode_ns", "exchange_ns", "reduce_ns", "repair_ns", "total_ns")]
+
+
 class Counter:
     """Device-resident word -> count table (wfcu_counter)."""
+
+    @classmethod
+    def _adopt(cls, handle) -> "Counter":
+        c = cls.__new__(cls)
+        c._h = C.c_void_p(handle)
+        return c
 
     def __init__(self, table_slots: int = 0, deferred_slots: int = 0, arena_bytes: int = 0, long_slots: int = 0):
         self._h = C.c_void_p()
@@ -393,6 +405,17 @@ class Counter:
         check(lib.wfcu_counter_merge_long_records(self._h, C.c_void_p(ptr), n_bytes, part, n_parts, C.c_void_p(stream)))
 
 
+def wordcount_multi(docs, n_workers: int, table_slots: int = 0) -> "tuple[list[Counter], dict[str, int]]":
+    """run_wordcount over n_workers workers on this box's GPUs (worker j on device j mod device_count, documents
+    d = j mod n): the owner tables, one per worker, and the CUDA-event stage times."""
+    hd = docs if isinstance(docs, HostDocs) else HostDocs(docs)
+    shards = (C.c_void_p * n_workers)()
+    cfg = CounterConfig(table_slots, 0, 0, 0)
+    t = StageNs()
+    check(lib.wfcu_wordcount_multi(hd.ptrs, hd.lens, hd.n, n_workers, C.byref(cfg), shards, C.byref(t)))
+    return [Counter._adopt(h) for h in shards], {k: int(getattr(t, k)) for k, _ in StageNs._fields_}
+
+
 def owner_of(word: bytes, n_parts: int) -> int:
     buf = np.frombuffer(word, dtype=np.uint8)
     return int(lib.wfcu_owner_of(_ptr(buf), len(word), n_parts))
@@ -423,6 +446,17 @@ class Tokens:
         blob, lens = pack_words(words)
         h = C.c_void_p()
         check(lib.wfcu_tokens_from_words(_ptr(blob), _ptr(lens), len(words), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def concat_slices(cls, srcs: "list[Tokens]", begins: list[int], ends: list[int]) -> "Tokens":
+        """A new device list: the slices [begin, end) of the source lists, in order (device-to-device)."""
+        n = len(srcs)
+        hs = (C.c_void_p * max(n, 1))(*[t._h for t in srcs])
+        b = (C.c_uint64 * max(n, 1))(*begins)
+        e = (C.c_uint64 * max(n, 1))(*ends)
+        h = C.c_void_p()
+        check(lib.wfcu_tokens_concat_slices(hs, b, e, n, C.byref(h)))
         return cls(h)
 
     def close(self) -> None:

@@ -4,6 +4,7 @@
 // tokens.cu; there is no CPU implementation of the path behind any entry point.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
@@ -36,6 +37,7 @@ cudaError_t tb_union_rows(const TableView& target, const TableView& others, Toke
                           u64* dev_cursor, int sm, cudaStream_t s, u64* launches);
 cudaError_t tb_score_rows(TokenRec* recs, const u64* ct, const u64* co, const u64* dev_n_rows, u64 max_rows, u64 extra_vocab,
                           u64 t_total, u64 o_total, int sm, cudaStream_t s, u64* launches);
+cudaError_t tk_rebase_ext(TokenRec* recs, u64 n, u64 delta, int sm, cudaStream_t s, u64* launches);
 cudaError_t tb_gather_counts(const TokenRec* recs, u64 first, u64 n, const u64* ct, const u64* co, u64* out_ct, u64* out_co,
                              int sm, cudaStream_t s, u64* launches);
 cudaError_t tb_export_pack(const TokenRec* recs, u64 n, u64* lens64, u64* tmp, uint8_t* bytes, u32* lens32, u64* counts,
@@ -1310,6 +1312,170 @@ extern "C" int wfcu_counter_merge_long_records(wfcu_counter* c, const uint8_t* d
     return WFCU_OK;
 }
 
+// ---- run_wordcount over n workers on the GPUs of this box ---------------------------------------------------
+// (proj/src/pipeline.cpp:61-123 with the hash-partitioned merge of BASELINE.json in place of the range shuffle.)
+// One host thread per worker; worker j lives on device j mod wfcu_device_count(), counts the documents
+// d = j (mod n) into a local table, partitions it by owner (tb_partition_*), then -- after a barrier -- pulls region j
+// of every worker's partition straight from that worker's device memory (cudaMemcpyPeerAsync: NVLink between GPUs,
+// a plain device copy when two workers share one) and merge-inserts it into the table it owns.  Long tokens (rare)
+// travel as the record stream.  Stage times are CUDA-event times on each worker's device, maximum over workers.
+namespace {
+struct SpinBarrier {      // n threads, reusable
+    explicit SpinBarrier(unsigned n) : n_(n) {}
+    void wait() {
+        std::unique_lock<std::mutex> lock(mu_);
+        const unsigned gen = gen_;
+        if (++arrived_ == n_) { arrived_ = 0; ++gen_; cv_.notify_all(); }
+        else cv_.wait(lock, [&] { return gen_ != gen; });
+    }
+    std::mutex mu_;
+    std::condition_variable cv_;
+    unsigned n_, arrived_ = 0, gen_ = 0;
+};
+struct MultiWorker {
+    int device = 0;
+    wfcu_counter* local = nullptr;
+    wfcu_counter* owned = nullptr;
+    Slot* entries = nullptr;             // the local table partitioned by owner (on `device`)
+    std::vector<u64> part_counts;        // entries per owner
+    std::vector<uint8_t> long_records;   // host copy of the long-token record stream
+    float map_ms = 0, encode_ms = 0, exchange_ms = 0;
+    int rc = WFCU_OK;
+    std::string error;
+};
+}  // namespace
+
+extern "C" int wfcu_wordcount_multi(const uint8_t* const* docs, const uint64_t* lens, uint64_t n_docs, uint32_t n_workers,
+                                    const wfcu_counter_config* cfg, wfcu_counter** out_shards, wfcu_stage_ns* timings) {
+    if (n_workers == 0 || n_workers > 4096) return fail(WFCU_ERR_INVALID_ARGUMENT, "n_workers must be in 1..4096");
+    if (!out_shards) return fail(WFCU_ERR_INVALID_ARGUMENT, "out_shards is null");
+    if (n_docs && (!docs || !lens)) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
+    for (u32 j = 0; j < n_workers; ++j) out_shards[j] = nullptr;
+    int n_dev = 0;
+    if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev <= 0) {
+        cudaGetLastError();
+        return fail(WFCU_ERR_NO_DEVICE, "no CUDA device available; libwfcu has no CPU path");
+    }
+    int caller_dev = 0;
+    cudaGetDevice(&caller_dev);
+    const auto t_start = std::chrono::steady_clock::now();
+    const u32 n = n_workers;
+    std::vector<MultiWorker> w(n);
+    SpinBarrier barrier(n);
+    auto body = [&](u32 j) {
+        MultiWorker& me = w[j];
+        me.device = int(j % u32(n_dev));
+        auto failed = [&](int rc) { me.rc = rc; me.error = g_last_error; return rc; };
+        auto cuda = [&](cudaError_t e, const char* what) {
+            if (e == cudaSuccess) return WFCU_OK;
+            me.rc = WFCU_ERR_CUDA;
+            me.error = std::string(what) + ": " + cudaGetErrorString(e);
+            return WFCU_ERR_CUDA;
+        };
+        cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+        u64* dev_counts = nullptr;
+        Slot* recv = nullptr;
+        do {   // phase 1: map + encode
+            if (cuda(cudaSetDevice(me.device), "cudaSetDevice")) break;
+            for (auto& e : ev) if (cuda(cudaEventCreate(&e), "cudaEventCreate")) break;
+            if (me.rc) break;
+            if (failed(wfcu_counter_create(&me.local, cfg))) break;
+            if (failed(wfcu_counter_create(&me.owned, cfg))) break;
+            std::vector<const uint8_t*> my_docs;
+            std::vector<uint64_t> my_lens;
+            for (u64 d = j; d < n_docs; d += n) { my_docs.push_back(docs[d]); my_lens.push_back(lens[d]); }
+            cudaEventRecord(ev[0], nullptr);
+            if (failed(wfcu_counter_count_host(me.local, my_docs.data(), my_lens.data(), my_docs.size()))) break;
+            cudaEventRecord(ev[1], nullptr);
+            uint64_t distinct = 0;
+            if (failed(wfcu_counter_stats(me.local, nullptr, &distinct, nullptr, nullptr))) break;
+            if (cuda(cudaMalloc((void**)&me.entries, sizeof(Slot) * std::max<u64>(distinct, 1)), "cudaMalloc entries")) break;
+            if (cuda(cudaMalloc((void**)&dev_counts, sizeof(u64) * (n + 1)), "cudaMalloc counts")) break;
+            if (failed(wfcu_counter_partition(me.local, n, reinterpret_cast<wfcu_entry*>(me.entries), std::max<u64>(distinct, 1),
+                                              reinterpret_cast<uint64_t*>(dev_counts), nullptr))) break;
+            me.part_counts.assign(n + 1, 0);
+            if (cuda(cudaMemcpy(me.part_counts.data(), dev_counts, sizeof(u64) * (n + 1), cudaMemcpyDeviceToHost), "D2H counts")) break;
+            if (me.part_counts[n]) {   // long-token records: serialise, keep a host copy for the owners
+                uint8_t* dev_recs = nullptr;
+                uint64_t bytes = me.part_counts[n];
+                if (cuda(cudaMalloc((void**)&dev_recs, bytes), "cudaMalloc records")) break;
+                int rc = wfcu_counter_long_records(me.local, dev_recs, bytes, &bytes, nullptr);
+                me.long_records.resize(bytes);
+                if (rc == WFCU_OK && cudaMemcpy(me.long_records.data(), dev_recs, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) rc = WFCU_ERR_CUDA;
+                cudaFree(dev_recs);
+                if (rc) { failed(rc); break; }
+            }
+            cudaEventRecord(ev[2], nullptr);
+        } while (false);
+        barrier.wait();     // every partition is complete (or its worker has failed)
+        bool any_failed = false;
+        for (const MultiWorker& o : w) any_failed |= o.rc != WFCU_OK;
+        if (!any_failed) {
+            do {   // phase 2: exchange + merge-insert of what this worker owns
+                u64 most = 1;
+                for (const MultiWorker& o : w) most = std::max(most, o.part_counts[j]);
+                if (cuda(cudaMalloc((void**)&recv, sizeof(Slot) * most), "cudaMalloc receive buffer")) break;
+                for (u32 k = 0; k < n && me.rc == WFCU_OK; ++k) {
+                    const MultiWorker& o = w[(j + k) % n];        // start with the own region: spreads the peers
+                    const u64 cnt = o.part_counts[j];
+                    if (cnt) {
+                        u64 off = 0;
+                        for (u32 p = 0; p < j; ++p) off += o.part_counts[p];
+                        if (cuda(cudaMemcpyPeerAsync(recv, me.device, o.entries + off, o.device, sizeof(Slot) * cnt, nullptr), "peer copy")) break;
+                        if (failed(wfcu_counter_merge_entries(me.owned, reinterpret_cast<const wfcu_entry*>(recv), cnt, nullptr))) break;
+                        if (cuda(cudaStreamSynchronize(nullptr), "exchange")) break;     // recv is reused
+                    }
+                    if (!o.long_records.empty()) {
+                        uint8_t* dev_recs = nullptr;
+                        if (cuda(cudaMalloc((void**)&dev_recs, o.long_records.size()), "cudaMalloc records")) break;
+                        int rc = cudaMemcpy(dev_recs, o.long_records.data(), o.long_records.size(), cudaMemcpyHostToDevice) == cudaSuccess ? WFCU_OK : WFCU_ERR_CUDA;
+                        if (rc == WFCU_OK) rc = wfcu_counter_merge_long_records(me.owned, dev_recs, o.long_records.size(), j, n, nullptr);
+                        cudaDeviceSynchronize();
+                        cudaFree(dev_recs);
+                        if (rc) { failed(rc); break; }
+                    }
+                }
+                if (me.rc) break;
+                if (failed(wfcu_counter_status(me.owned, nullptr))) break;
+                cudaEventRecord(ev[3], nullptr);
+                if (cuda(cudaEventSynchronize(ev[3]), "exchange")) break;
+                cudaEventElapsedTime(&me.map_ms, ev[0], ev[1]);
+                cudaEventElapsedTime(&me.encode_ms, ev[1], ev[2]);
+                cudaEventElapsedTime(&me.exchange_ms, ev[2], ev[3]);
+            } while (false);
+        }
+        barrier.wait();     // nobody frees a partition a peer may still be reading
+        cudaFree(recv);
+        cudaFree(dev_counts);
+        cudaFree(me.entries);
+        me.entries = nullptr;
+        wfcu_counter_destroy(me.local);
+        me.local = nullptr;
+        for (auto& e : ev) if (e) cudaEventDestroy(e);
+    };
+    std::vector<std::thread> threads;
+    for (u32 j = 1; j < n; ++j) threads.emplace_back(body, j);
+    body(0);
+    for (auto& t : threads) t.join();
+    cudaSetDevice(caller_dev);
+    for (u32 j = 0; j < n; ++j) {     // the lowest-indexed failure is the one reported (pipeline.cpp:30-45)
+        if (w[j].rc == WFCU_OK) continue;
+        for (MultiWorker& o : w) { wfcu_counter_destroy(o.owned); o.owned = nullptr; }
+        cudaSetDevice(caller_dev);
+        return fail(w[j].rc, "worker %u: %s", j, w[j].error.c_str());
+    }
+    wfcu_stage_ns t{};
+    for (u32 j = 0; j < n; ++j) {
+        out_shards[j] = w[j].owned;
+        t.map_ns = std::max<uint64_t>(t.map_ns, uint64_t(w[j].map_ms * 1e6));
+        t.encode_ns = std::max<uint64_t>(t.encode_ns, uint64_t(w[j].encode_ms * 1e6));
+        t.exchange_ns = std::max<uint64_t>(t.exchange_ns, uint64_t(w[j].exchange_ms * 1e6));
+    }
+    t.total_ns = uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_start).count());
+    if (timings) *timings = t;
+    return WFCU_OK;
+}
+
 // ---- synthetic corpora ------------------------------------------------------------------
 extern "C" int wfcu_synth_document(uint64_t seed, uint64_t doc, uint32_t vocab, double zipf_s, uint32_t speaker,
                                    uint8_t* out, uint64_t doc_bytes) {
@@ -1596,6 +1762,57 @@ extern "C" int wfcu_tokens_from_words(const uint8_t* bytes, const uint32_t* lens
     t->recs = static_cast<TokenRec*>(p);
     if (int rc = upload(arena.data(), arena.size(), &p)) { tokens_free(t); return rc; }
     t->arena = static_cast<uint8_t*>(p);
+    *out = t;
+    return WFCU_OK;
+}
+
+// The exchange of the paper's range-partitioned pipeline without leaving device memory (proj/src/shuffle.cpp:98-130:
+// chunk c of every worker's sorted list goes to worker c): a new list made of the slices [begin[i], end[i]) of
+// n_src lists, in that order.  Records move device to device (peer copies between GPUs); the long-token arenas of
+// the sources are appended and the records' references rebased.
+extern "C" int wfcu_tokens_concat_slices(const wfcu_tokens* const* src, const uint64_t* begin, const uint64_t* end,
+                                         uint32_t n_src, wfcu_tokens** out) {
+    if (!out) return fail(WFCU_ERR_INVALID_ARGUMENT, "out is null");
+    *out = nullptr;
+    DeviceState* d;
+    if (int rc = current_device_state(&d)) return rc;
+    if (n_src && (!src || !begin || !end)) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
+    u64 total = 0, arena_total = 8;
+    for (u32 i = 0; i < n_src; ++i) {
+        if (!src[i] || begin[i] > end[i] || end[i] > src[i]->n)
+            return fail(WFCU_ERR_INVALID_ARGUMENT, "slice %u is out of range", i);
+        total += end[i] - begin[i];
+        if (src[i]->arena_used > 8 && end[i] > begin[i]) arena_total += src[i]->arena_used - 8;
+    }
+    auto* t = new wfcu_tokens;
+    cudaGetDevice(&t->device);
+    t->sm_count = d->sm_count;
+    t->n = total;
+    t->arena_used = arena_total;
+    t->arena_cap = arena_total;
+    void* p = nullptr;
+    cudaError_t e = scratch_alloc(&p, sizeof(TokenRec) * std::max<u64>(total, 1));
+    if (e == cudaSuccess) { t->recs = static_cast<TokenRec*>(p); e = scratch_alloc(&p, arena_total); }
+    if (e == cudaSuccess) { t->arena = static_cast<uint8_t*>(p); e = cudaMemsetAsync(t->arena, 0, 8, nullptr); }
+    LaunchTally tally;
+    u64 at = 0, arena_at = 8;
+    for (u32 i = 0; i < n_src && e == cudaSuccess; ++i) {
+        const u64 m = end[i] - begin[i];
+        if (m == 0) continue;
+        e = cudaMemcpyPeerAsync(t->recs + at, t->device, src[i]->recs + begin[i], src[i]->device, sizeof(TokenRec) * m, nullptr);
+        if (e == cudaSuccess && src[i]->arena_used > 8) {
+            const u64 bytes = src[i]->arena_used - 8;
+            e = cudaMemcpyPeerAsync(t->arena + arena_at, t->device, src[i]->arena + 8, src[i]->device, bytes, nullptr);
+            if (e == cudaSuccess) e = tk_rebase_ext(t->recs + at, m, arena_at - 8, t->sm_count, nullptr, &tally.n);
+            arena_at += bytes;
+        }
+        at += m;
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
+    if (e != cudaSuccess) {
+        tokens_free(t);
+        return fail(WFCU_ERR_CUDA, "concat of token slices: %s", cudaGetErrorString(e));
+    }
     *out = t;
     return WFCU_OK;
 }

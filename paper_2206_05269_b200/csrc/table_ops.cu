@@ -344,6 +344,12 @@ __global__ void tb_gather_counts_kernel(const TokenRec* __restrict__ recs, u64 f
     }
 }
 
+// records moved into a list whose arena holds the source arena `delta` bytes further on
+__global__ void tk_rebase_ext_kernel(TokenRec* __restrict__ recs, u64 n, u64 delta) {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        if (recs[i].ext) recs[i].ext += delta;
+}
+
 // ---- launchers ----------------------------------------------------------------------
 static inline unsigned grid_for(u64 items, int sm_count) {
     u64 g = (items + 255) / 256;
@@ -479,6 +485,13 @@ cudaError_t tb_gather_counts(const TokenRec* recs, u64 first, u64 n, const u64* 
                              int sm, cudaStream_t s, u64* launches) {
     if (first >= n) return cudaSuccess;
     tb_gather_counts_kernel<<<grid_for(n - first, sm), 256, 0, s>>>(recs, first, n, ct, co, out_ct, out_co);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+cudaError_t tk_rebase_ext(TokenRec* recs, u64 n, u64 delta, int sm, cudaStream_t s, u64* launches) {
+    if (n == 0 || delta == 0) return cudaSuccess;
+    tk_rebase_ext_kernel<<<grid_for(n, sm), 256, 0, s>>>(recs, n, delta);
     *launches += 1;
     return cudaGetLastError();
 }

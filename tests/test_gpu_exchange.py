@@ -189,3 +189,37 @@ def test_nccl_collective_path_with_one_rank(capi, cuda, port):
     env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29544")
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env)
     assert out.returncode == 0 and "nccl path ok" in out.stdout, out.stderr[-3000:]
+
+
+@pytest.mark.parametrize("n_workers", [1, 2, 3, 8])
+def test_wordcount_multi_entry(capi, cuda, port, n_workers):
+    """wfcu_wordcount_multi: n workers (threads) mapped round-robin onto the visible GPUs, documents d mod n, regions
+    delivered device to device; the union of the owner tables == serial_wordcount, no key has two holders, and every
+    key sits on the worker its owner hash names."""
+    import random
+    from helpers import random_text
+    rng = random.Random(n_workers)
+    docs = [capi.synth_corpus(seed=4, doc_begin=d, doc_end=d + 1, vocab=50000, doc_bytes=1 << 17).tobytes() for d in range(5)]
+    docs.append(random_text(rng, 40000, "unicode") + b" " + b"Z" * 70 + b" zz")
+    docs.append(b"")
+    docs.append((b"y" * 33 + b" ") * 9)
+    shards, ns = capi.wordcount_multi(docs, n_workers, table_slots=1 << 16)
+    assert len(shards) == n_workers
+    tables = [s.to_dict() for s in shards]
+    union = {}
+    for j, t in enumerate(tables):
+        for w, c in t.items():
+            assert w not in union
+            union[w] = c
+            if len(w) <= 16:
+                assert capi.owner_of(w, n_workers) == j
+    assert union == port.wordcount(docs)
+    assert ns["map_ns"] > 0 and ns["total_ns"] >= ns["map_ns"] and ns["sort_ns"] == 0 and ns["repair_ns"] == 0
+    assert sum(s.stats()[1] for s in shards) == sum(union.values())
+
+
+def test_wordcount_multi_rejects_bad_arguments(capi, cuda):
+    with pytest.raises(capi.InvalidArgument):
+        capi.wordcount_multi([b"a b"], 0)
+    shards, _ = capi.wordcount_multi([], 3)
+    assert [s.to_dict() for s in shards] == [{}, {}, {}]

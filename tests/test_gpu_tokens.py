@@ -124,3 +124,27 @@ def test_sorted_count_key_tiles(capi, cuda, port):
         want = port.wordcount([text])
         assert c.to_dict() == want
         assert c.stats()[1] == sum(want.values())
+
+
+def test_concat_slices_is_the_range_exchange(capi, cuda, port):
+    """wfcu_tokens_concat_slices: chunk c of every worker's sorted list, gathered on the device, equals the
+    reference's exchange output (proj/src/shuffle.cpp:98-130) once sorted; long tokens travel with their records."""
+    import random
+    rng = random.Random(3)
+    n = 3
+    vocab = [b"w%03d" % i for i in range(40)] + [b"L" * 20 + b"%d" % i for i in range(3)]
+    lists = [sorted(rng.choice(vocab) for _ in range(rng.randrange(0, 90))) for _ in range(n)]
+    handles = [capi.Tokens.from_words(l) for l in lists]
+    for h in handles:
+        h.sort()
+    plans = [port.plan_partition(len(lists[j]), j, n) for j in range(n)]
+    for c in range(n):
+        got = capi.Tokens.concat_slices(handles, [plans[j][c] for j in range(n)], [plans[j][c + 1] for j in range(n)])
+        want = [w for j in range(n) for w in lists[j][plans[j][c]:plans[j][c + 1]]]
+        assert got.words() == want
+        got.sort()
+        assert got.words() == sorted(want)
+    empty = capi.Tokens.concat_slices(handles, [0] * n, [0] * n)
+    assert empty.words() == []
+    with pytest.raises(capi.InvalidArgument):
+        capi.Tokens.concat_slices(handles, [0] * n, [10 ** 6] * n)
