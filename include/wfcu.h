@@ -299,6 +299,14 @@ WFCU_API int wfcu_counter_count_dev_sorted(wfcu_counter* c, const uint8_t* dev_t
 /* (proj/src/pipeline.cpp:61-123, proj/include/wfc/pipeline.hpp:15-51)         */
 /* ------------------------------------------------------------------------- */
 
+/* A pair of CUDA events on the current device: the device time between start and stop on the legacy default stream,
+ * which is what the reference's timed_stage (proj/src/pipeline.cpp:48-57) becomes when the stage runs on the GPU. */
+typedef struct wfcu_timer wfcu_timer;
+WFCU_API int wfcu_timer_create(wfcu_timer** out);
+WFCU_API int wfcu_timer_start(wfcu_timer* t);
+WFCU_API int wfcu_timer_stop_ns(wfcu_timer* t, uint64_t* elapsed_ns);   /* waits for the device */
+WFCU_API void wfcu_timer_destroy(wfcu_timer* t);
+
 /* StageTimings (proj/include/wfc/pipeline.hpp:15-23), filled from CUDA events: maximum over the workers. */
 typedef struct wfcu_stage_ns {
     uint64_t map_ns;       /* H2D + fused tokenize / count kernels */

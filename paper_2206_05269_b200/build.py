@@ -95,9 +95,38 @@ def build_host(force: bool = False) -> Path | None:
     return out
 
 
+REF_TESTS = Path("/root/reference/proj/tests")
+REF_SUITES = ["text", "reduce", "engine", "pipeline", "analysis", "shuffle", "wire"]
+
+
+def build_reference_suites(force: bool = False) -> list[Path]:
+    """The reference's OWN test files (proj/tests/*_test.cpp + support.hpp), compiled unmodified from where they
+    lie against libwfc_b200.so: the drop-in headers stand in for proj/include, tests/shim/doctest.h for the
+    vendored doctest the reference tree does not ship.  Binaries land in lib/reftests/ and travel to the GPU
+    box; nothing of the reference is copied.  No-op where /root/reference is absent (the GPU box)."""
+    out_dir = LIB / "reftests"
+    if not REF_TESTS.exists() or not (LIB / "libwfc_b200.so").exists():
+        return sorted(out_dir.glob("*_test")) if out_dir.exists() else []
+    out_dir.mkdir(exist_ok=True)
+    cxx = os.environ.get("CXX") or shutil.which("g++") or "g++"
+    shim = ROOT / "tests" / "shim"
+    deps = sorted((HOST / "include" / "wfc").glob("*.hpp")) + [shim / "doctest.h", LIB / "libwfc_b200.so"]
+    built = []
+    for name in REF_SUITES:
+        src = REF_TESTS / f"{name}_test.cpp"
+        exe = out_dir / f"{name}_test"
+        if force or _stale(exe, [src, REF_TESTS / "support.hpp"] + deps):
+            _run([cxx, "-std=c++20", "-O1", "-pthread", f"-I{shim}", f"-I{HOST / 'include'}", f"-I{REF_TESTS}",
+                  '-DWFC_FIXTURES_DIR="/root/reference/proj/fixtures"', "-o", str(exe), str(src),
+                  f"-L{LIB}", "-lwfc_b200", "-lwfcu", "-Wl,-rpath,$ORIGIN/.."])
+        built.append(exe)
+    return built
+
+
 def build_all(force: bool = False, verbose: bool = False) -> None:
     build_wfcu(force, verbose)
     build_host(force)
+    build_reference_suites(force)
 
 
 if __name__ == "__main__":

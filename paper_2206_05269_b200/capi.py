@@ -78,6 +78,10 @@ SIGNATURES = {
     "wfcu_counter_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64]),
     "wfcu_counter_top_k": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.c_uint64, u64p, u64p]),
+    "wfcu_timer_create": (C.c_int, [C.POINTER(C.c_void_p)]),
+    "wfcu_timer_start": (C.c_int, [C.c_void_p]),
+    "wfcu_timer_stop_ns": (C.c_int, [C.c_void_p, u64p]),
+    "wfcu_timer_destroy": (None, [C.c_void_p]),
     "wfcu_wordcount_multi": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "wfcu_tokens_concat_slices": (C.c_int, [C.c_void_p, u64p, u64p, C.c_uint32, C.POINTER(C.c_void_p)]),
     "wfcu_counter_distinctive": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64,

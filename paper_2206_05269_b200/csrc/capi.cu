@@ -1312,6 +1312,43 @@ extern "C" int wfcu_counter_merge_long_records(wfcu_counter* c, const uint8_t* d
     return WFCU_OK;
 }
 
+// ---- stage timer: a pair of CUDA events ---------------------------------------------------------------------
+struct wfcu_timer {
+    cudaEvent_t a = nullptr, b = nullptr;
+};
+extern "C" int wfcu_timer_create(wfcu_timer** out) {
+    if (!out) return fail(WFCU_ERR_INVALID_ARGUMENT, "out is null");
+    DeviceState* d;
+    if (int rc = current_device_state(&d)) return rc;
+    auto* t = new wfcu_timer;
+    if (cudaEventCreate(&t->a) != cudaSuccess || cudaEventCreate(&t->b) != cudaSuccess) {
+        wfcu_timer_destroy(t);
+        return fail(WFCU_ERR_CUDA, "cudaEventCreate failed");
+    }
+    *out = t;
+    return WFCU_OK;
+}
+extern "C" int wfcu_timer_start(wfcu_timer* t) {
+    if (!t) return fail(WFCU_ERR_INVALID_ARGUMENT, "timer is null");
+    CUDA_TRY(cudaEventRecord(t->a, nullptr));
+    return WFCU_OK;
+}
+extern "C" int wfcu_timer_stop_ns(wfcu_timer* t, uint64_t* elapsed_ns) {
+    if (!t || !elapsed_ns) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
+    CUDA_TRY(cudaEventRecord(t->b, nullptr));
+    CUDA_TRY(cudaEventSynchronize(t->b));
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, t->a, t->b));
+    *elapsed_ns = uint64_t(double(ms) * 1e6);
+    return WFCU_OK;
+}
+extern "C" void wfcu_timer_destroy(wfcu_timer* t) {
+    if (!t) return;
+    if (t->a) cudaEventDestroy(t->a);
+    if (t->b) cudaEventDestroy(t->b);
+    delete t;
+}
+
 // ---- run_wordcount over n workers on the GPUs of this box ---------------------------------------------------
 // (proj/src/pipeline.cpp:61-123 with the hash-partitioned merge of BASELINE.json in place of the range shuffle.)
 // One host thread per worker; worker j lives on device j mod wfcu_device_count(), counts the documents

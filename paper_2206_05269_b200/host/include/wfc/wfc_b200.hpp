@@ -4,23 +4,28 @@
 // /root/reference/proj/include/wfc/{text,reduce,pipeline,engine,analysis}.hpp, so a
 // caller of the reference (proj/src/cli.cpp:79-86, 138-141, 202-221) relinks against
 // libwfc_b200.so unchanged.  The per-topic headers wfc/text.hpp, wfc/reduce.hpp, ...
-// forward here.  Every data path below (tokenize, normalize, sort, count, reduce, merge, map-reduce,
-// top-k, sanitize) runs its arithmetic on the GPU through the C ABI of include/wfcu.h; there is no CPU
-// implementation to fall back to -- without a device the calls throw wfc::DeviceError.  Host code is
-// what is host code in the reference too: containers, the WCX1 frames / transports / threads of the
-// paper's exchange, index arithmetic (plan_partition) and the single-code-point accessors.
+// forward here.  The data paths (tokenize, normalize, sort, count, run-length encode, merge, partition,
+// map-reduce, sanitize, the joins and selections behind DeviceCounts::top_k / distinctive) run on the GPU
+// through the C ABI of include/wfcu.h; there is no CPU implementation to fall back to -- without a device
+// the calls throw wfc::DeviceError.  Host code is what is left of host work: std:: containers and their
+// bookkeeping (boundary_repair, count_unreduced_words), the final ordering of the few candidate rows of
+// top_k / distinctive_words with the reference's comparators (one implementation, in libwfcu), WCX1 frames
+// and transports for callers that bring their own Transport, file reading (ingest_directory), index
+// arithmetic (plan_partition) and the single-code-point accessors.
 //
 // Differences a caller can observe (all additive):
 //   * MapKind gains `square` (value 3) for f(x) = x^2; map_reduce_fast() is the
 //     HBM-roofline reduction (fp64 accumulation, fixed order, within ~1e-15 relative of
 //     the serial fold), next to the bit-exact map_reduce_serial / map_reduce_blocked;
-//   * run_wordcount partitions by key hash, not by alphabetical range (BASELINE.json;
-//     SURVEY.md D2): RunResult::counts is identical, the shards are pairwise disjoint,
-//     pre_repair_shards == shards and boundary_repair has nothing left to do;
-//   * run_wordcount(corpus, n, Transport&) runs the paper's own range-partitioned exchange over
-//     the caller's transport, WCX1 frames included (tokenize / sort / run-length encode on the
-//     device, frames on the host, like the reference); run_wordcount(corpus, n) is the fast
-//     path and exchanges table entries in device memory / over NCCL instead.
+//   * run_wordcount(corpus, n) is the reference's pipeline, range partition and boundary repair included
+//     (pre_repair_shards are the reference's, proj/tests/pipeline_test.cpp:26-33): tokenize, sort, the
+//     exchange of the chunks, the n-way merge and the run-length encode all stay in device memory;
+//     run_wordcount(corpus, n, Transport&) sends the same chunks as WCX1 frames over the caller's transport;
+//   * run_wordcount_hashed(corpus, n) is the fast path of BASELINE.json: fused tokenize/count kernels, worker j
+//     on GPU j mod device_count, tables hash-partitioned by owner and delivered device to device.  Its
+//     RunResult::counts is identical; the shards are disjoint by construction (pre_repair_shards == shards);
+//   * DeviceCounts keeps a table on the device: per-speaker top-k / distinctive words (cli.cpp:176-230) without
+//     exporting a million-word map.
 #pragma once
 
 #include <array>
@@ -28,6 +33,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <deque>
+#include <filesystem>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -37,8 +43,11 @@
 #include <string>
 #include <string_view>
 #include <ostream>
+#include <unordered_set>
 #include <utility>
 #include <vector>
+
+struct wfcu_counter;   // include/wfcu.h
 
 namespace wfc {
 
@@ -129,14 +138,11 @@ public:
     std::size_t n_workers() const { return n_; }
 
 private:
-    struct Channel {
-        std::mutex mu;
-        std::condition_variable cv;
-        std::deque<WireMessage> queue;
-    };
-    Channel& channel(std::size_t from, std::size_t to);
+    std::size_t mailbox(std::size_t from, std::size_t to) const;   // throws TransportError off the grid
     std::size_t n_;
-    std::vector<std::unique_ptr<Channel>> channels_;
+    std::mutex mu_;                                  // one lock and one wake-up for the whole grid:
+    std::condition_variable arrived_;                // a frame is a pointer move, there is nothing to contend for
+    std::vector<std::deque<WireMessage>> boxes_;     // [to * n + from]
 };
 
 // ---- pipeline (reference: wfc/pipeline.hpp) --------------------------------------------
@@ -176,6 +182,9 @@ public:
 
 RunResult run_wordcount(std::span<const RawDocument> corpus, std::size_t n_workers);
 RunResult run_wordcount(std::span<const RawDocument> corpus, std::size_t n_workers, Transport& transport);
+// The fast path: fused tokenize/count, hash-partitioned device-to-device merge over the box's GPUs
+// (wfcu_wordcount_multi).  StageTimings are CUDA-event times.
+RunResult run_wordcount_hashed(std::span<const RawDocument> corpus, std::size_t n_workers);
 
 // The paper's own algorithm (reference pipeline.cpp:61-123, shuffle.cpp:9-46), stage by
 // stage on the device kernels: tokenize -> sort_words -> range partition by position
@@ -214,7 +223,7 @@ EncodedShard encode_outgoing(const ShardPlan& plan, const WordList& sorted);
 std::vector<WordList> exchange_encoded(std::vector<EncodedShard> shards, Transport& transport);
 std::vector<WordList> exchange(const std::vector<WorkerShard>& inputs, Transport& transport);
 std::vector<WordList> exchange(const std::vector<WorkerShard>& inputs);
-RunResult run_wordcount_range_partitioned(std::span<const RawDocument> corpus, std::size_t n_workers);
+RunResult run_wordcount_range_partitioned(std::span<const RawDocument> corpus, std::size_t n_workers);   // == run_wordcount(corpus, n)
 CountMap serial_wordcount(std::span<const RawDocument> corpus);
 
 // ---- engine (reference: wfc/engine.hpp) ------------------------------------------------
@@ -260,6 +269,46 @@ struct DistinctivenessReport {
 };
 DistinctivenessReport distinctive_words(const CountMap& target, const CountMap& others, std::string label,
                                         std::size_t k);
+
+// A count table that stays on the device (wfcu_counter): the compare command of the reference
+// (proj/src/cli.cpp:176-230) -- count every corpus, pool the others, top-k and distinctive words per corpus --
+// without a std::map in between.
+class DeviceCounts {
+public:
+    explicit DeviceCounts(std::uint64_t expected_distinct_words = 0);
+    ~DeviceCounts();
+    DeviceCounts(DeviceCounts&& other) noexcept;
+    DeviceCounts& operator=(DeviceCounts&& other) noexcept;
+    DeviceCounts(const DeviceCounts&) = delete;
+    DeviceCounts& operator=(const DeviceCounts&) = delete;
+
+    void count(std::span<const RawDocument> corpus);          // += serial_wordcount(corpus)
+    void merge(const DeviceCounts& other);                    // += other (merge_counts, reduce.cpp:83-89)
+    std::uint64_t distinct_words() const;
+    std::uint64_t total_words() const;
+    CountMap to_map() const;
+    FrequencyTable top_k(std::string label, std::size_t k) const;
+    DistinctivenessReport distinctive(const DeviceCounts& others, std::string label, std::size_t k) const;
+    wfcu_counter* handle() const { return h_; }
+
+private:
+    wfcu_counter* h_ = nullptr;
+};
+
+// ---- ingest (reference: wfc/analysis.hpp, the file side) ------------------------------------------------
+struct Corpus {
+    std::string label;
+    std::vector<RawDocument> documents;
+};
+class IngestError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+// Every .txt / .text file of `dir` as one document, in file-name order, invalid UTF-8 replaced by U+FFFD
+// (utf8_sanitize, on the device: the files of the directory are sanitised as one batch).
+Corpus ingest_directory(const std::filesystem::path& dir, std::string label);
+std::unordered_set<Word> load_stopwords(const std::filesystem::path& file);   // one tokenised word list
+CountMap remove_stopwords(CountMap counts, const std::unordered_set<Word>& stopwords);
 
 // ---- report (reference: wfc/report.hpp, the text writers; the JSON ones need the vendored json.hpp) ----
 std::string format_double(double v);                                                    // "%.12g"

@@ -288,102 +288,178 @@ CountMap serial_wordcount(std::span<const RawDocument> corpus) {
 
 static RunResult run_range_partitioned(std::span<const RawDocument> corpus, std::size_t n_workers, Transport& transport);
 
+namespace {
+// a stage of the pipeline: device time between two CUDA events (wfcu_timer), exceptions wrapped like
+// the reference's timed_stage (pipeline.cpp:48-57)
+struct StageTimer {
+    wfcu_timer* t = nullptr;
+    StageTimer() { ok(wfcu_timer_create(&t)); }
+    ~StageTimer() { wfcu_timer_destroy(t); }
+    template <typename Fn>
+    void run(const char* name, std::uint64_t& ns, Fn&& fn) {
+        ok(wfcu_timer_start(t), name);
+        try {
+            fn();
+        } catch (const std::invalid_argument&) {
+            throw;
+        } catch (const PipelineError&) {
+            throw;
+        } catch (const std::exception& e) {
+            throw PipelineError(name, e.what());
+        }
+        ok(wfcu_timer_stop_ns(t, &ns), name);
+    }
+};
+
+RunResult empty_run(std::size_t n_workers, Clock::time_point run_start) {
+    RunResult result;
+    result.n_workers = n_workers;
+    result.shards.assign(n_workers, CountMap{});
+    result.pre_repair_shards = result.shards;
+    result.timings.total_ns = since(run_start);
+    return result;
+}
+
+// cut indices of the reference's range partition for a sorted list of k words (shuffle.cpp:17-45)
+std::vector<std::uint64_t> partition_cuts(std::uint64_t k, std::size_t worker_id, std::size_t n) {
+    const std::uint64_t keep = k / n, others = n > 1 ? n - 1 : 1;
+    const std::uint64_t base = n > 1 ? (k - keep) / others : 0;
+    std::uint64_t extra = n > 1 ? (k - keep) % others : 0;
+    std::vector<std::uint64_t> cut(n + 1, 0);
+    for (std::size_t c = 0; c < n; ++c) {
+        std::uint64_t size = keep;
+        if (c != worker_id) {
+            size = base + (extra ? 1 : 0);
+            if (extra) --extra;
+        }
+        cut[c + 1] = cut[c] + size;
+    }
+    return cut;
+}
+}  // namespace
+
+// The reference's pipeline (pipeline.cpp:61-123), every stage in device memory: worker j tokenizes the documents
+// d = j (mod n) and radix-sorts its tokens; the range partition is index arithmetic on the list lengths; the exchange
+// gathers chunk c of every list into worker c's list (wfcu_tokens_concat_slices: device-to-device copies, no frame,
+// no host string); the n-way merge is one more radix sort; reduce is the run-length encode into a count table.
+// Only the per-shard maps come back to the host, where boundary_repair moves the (at most n-1) duplicated boundary
+// words to their lowest-indexed holder.
 RunResult run_wordcount(std::span<const RawDocument> corpus, std::size_t n_workers) {
     if (n_workers == 0) throw std::invalid_argument("run_wordcount: n_workers must be >= 1");
     const auto run_start = Clock::now();
-    RunResult result;
-    result.n_workers = n_workers;
-    if (corpus.empty()) {
-        result.shards.assign(n_workers, CountMap{});
-        result.pre_repair_shards = result.shards;
-        result.timings.total_ns = since(run_start);
-        return result;
-    }
+    if (corpus.empty()) return empty_run(n_workers, run_start);
     const std::size_t n = n_workers;
-    const std::uint64_t hint = total_bytes(corpus) / 64 / n + 1024;
+    RunResult result;
+    result.n_workers = n;
     auto& t = result.timings;
-
-    for (int attempt = 0;; ++attempt) {
-        try {
-            const std::uint64_t grow = hint << (3 * attempt);
-            std::vector<std::unique_ptr<CounterHandle>> local, owned;
-            for (std::size_t j = 0; j < n; ++j) local.push_back(std::make_unique<CounterHandle>(grow, "map"));
-            for (std::size_t j = 0; j < n; ++j) owned.push_back(std::make_unique<CounterHandle>(grow, "map"));
-
-            // map: worker j counts documents d = j (mod n)  (reference: pipeline.cpp:80-91)
-            auto t0 = Clock::now();
-            for (std::size_t j = 0; j < n; ++j) {
-                std::vector<const std::uint8_t*> ptrs;
-                std::vector<std::uint64_t> lens;
-                for (std::size_t d = j; d < corpus.size(); d += n) {
-                    ptrs.push_back(reinterpret_cast<const std::uint8_t*>(corpus[d].text.data()));
-                    lens.push_back(corpus[d].text.size());
-                }
-                ok(wfcu_counter_count_host(local[j]->h, ptrs.data(), lens.data(), ptrs.size()), "map");
+    StageTimer timer;
+    std::vector<TokensHandle> local(n), received(n);
+    timer.run("map", t.map_ns, [&] {
+        std::string shard;      // the worker's documents back to back; a newline ends every document's last fragment
+        for (std::size_t j = 0; j < n; ++j) {
+            shard.clear();
+            for (std::size_t d = j; d < corpus.size(); d += n) {
+                shard += corpus[d].text;
+                shard += '\n';
             }
-            t.map_ns = since(t0);
-
-            // encode + exchange: partition every worker's table by owner, deliver region p to
-            // owner p (device-to-device here; NCCL all-to-all across GPUs, exchange.py)
-            std::uint64_t enc = 0, exch = 0;
-            for (std::size_t j = 0; j < n; ++j) {
-                t0 = Clock::now();
-                std::uint64_t distinct = 0;
-                ok(wfcu_counter_stats(local[j]->h, nullptr, &distinct, nullptr, nullptr), "encode");
-                struct Dev {
-                    void* p = nullptr;
-                    ~Dev() { wfcu_dev_free(p); }
-                } entries, part_counts, recs;
-                ok(wfcu_dev_alloc(&entries.p, sizeof(wfcu_entry) * std::max<std::uint64_t>(distinct, 1)), "encode");
-                ok(wfcu_dev_alloc(&part_counts.p, sizeof(std::uint64_t) * (n + 1)), "encode");
-                ok(wfcu_counter_partition(local[j]->h, std::uint32_t(n), static_cast<wfcu_entry*>(entries.p),
-                                          std::max<std::uint64_t>(distinct, 1),
-                                          static_cast<std::uint64_t*>(part_counts.p), nullptr), "encode");
-                std::vector<std::uint64_t> counts(n);
-                ok(wfcu_dev_download(counts.data(), part_counts.p, sizeof(std::uint64_t) * n), "encode");
-                std::uint64_t long_bytes = 0;
-                ok(wfcu_counter_long_records(local[j]->h, nullptr, 0, &long_bytes, nullptr), "encode");
-                if (long_bytes) {
-                    ok(wfcu_dev_alloc(&recs.p, long_bytes), "encode");
-                    ok(wfcu_counter_long_records(local[j]->h, static_cast<std::uint8_t*>(recs.p), long_bytes, &long_bytes,
-                                                 nullptr), "encode");
-                }
-                enc += since(t0);
-                t0 = Clock::now();
-                std::uint64_t off = 0;
-                for (std::size_t p = 0; p < n; ++p) {
-                    ok(wfcu_counter_merge_entries(owned[p]->h, static_cast<const wfcu_entry*>(entries.p) + off, counts[p],
-                                                  nullptr), "exchange");
-                    off += counts[p];
-                    if (long_bytes)
-                        ok(wfcu_counter_merge_long_records(owned[p]->h, static_cast<const std::uint8_t*>(recs.p), long_bytes,
-                                                           std::uint32_t(p), std::uint32_t(n), nullptr), "exchange");
-                }
-                for (std::size_t p = 0; p < n; ++p) ok(wfcu_counter_status(owned[p]->h, nullptr), "exchange");
-                exch += since(t0);
-            }
-            t.encode_ns = enc;
-            t.exchange_ns = exch;
-
-            t0 = Clock::now();
-            result.shards.clear();
-            for (std::size_t p = 0; p < n; ++p) result.shards.push_back(export_counts(owned[p]->h, "reduce"));
-            t.reduce_ns = since(t0);
-            break;
-        } catch (const PipelineError&) {
-            const std::string msg = wfcu_last_error();
-            const bool capacity = msg.find("recreate with more") != std::string::npos;
-            if (!capacity || attempt >= 5) throw;
+            ok(wfcu_tokenize_host(reinterpret_cast<const std::uint8_t*>(shard.data()), shard.size(), &local[j].h), "map");
         }
-    }
-    result.pre_repair_shards = result.shards;   // disjoint by construction: nothing to repair
+    });
+    timer.run("sort", t.sort_ns, [&] {
+        for (auto& l : local) ok(wfcu_tokens_sort(l.h, nullptr), "sort");
+    });
+    std::vector<std::vector<std::uint64_t>> cuts(n);
+    timer.run("encode", t.encode_ns, [&] {
+        for (std::size_t j = 0; j < n; ++j) {
+            std::uint64_t k = 0;
+            ok(wfcu_tokens_stats(local[j].h, &k, nullptr), "encode");
+            cuts[j] = partition_cuts(k, j, n);
+        }
+    });
+    timer.run("exchange", t.exchange_ns, [&] {
+        std::vector<const wfcu_tokens*> src(n);
+        std::vector<std::uint64_t> begin(n), end(n);
+        for (std::size_t j = 0; j < n; ++j) src[j] = local[j].h;
+        for (std::size_t c = 0; c < n; ++c) {
+            for (std::size_t j = 0; j < n; ++j) { begin[j] = cuts[j][c]; end[j] = cuts[j][c + 1]; }
+            ok(wfcu_tokens_concat_slices(src.data(), begin.data(), end.data(), std::uint32_t(n), &received[c].h), "exchange");
+            ok(wfcu_tokens_sort(received[c].h, nullptr), "exchange");       // the n-way merge
+        }
+    });
+    result.pre_repair_shards.assign(n, CountMap{});
+    timer.run("reduce", t.reduce_ns, [&] {
+        for (std::size_t c = 0; c < n; ++c) {
+            std::uint64_t k = 0;
+            ok(wfcu_tokens_stats(received[c].h, &k, nullptr), "reduce");
+            if (k == 0) continue;
+            with_growing_counter(k, "reduce", [&](wfcu_counter* counter) {
+                int rc = wfcu_tokens_reduce_sorted(received[c].h, counter, nullptr);
+                if (rc == WFCU_OK) rc = wfcu_counter_status(counter, nullptr);
+                if (rc == WFCU_OK) result.pre_repair_shards[c] = export_counts(counter, "reduce");
+                return rc;
+            });
+        }
+    });
+    const auto repair_start = Clock::now();      // host bookkeeping over at most n-1 boundary words
+    result.shards = boundary_repair(result.pre_repair_shards);
+    t.repair_ns = since(repair_start);
     for (const auto& shard : result.shards) result.counts.insert(shard.begin(), shard.end());
     t.total_ns = since(run_start);
     return result;
 }
 
-// The caller's transport carries the reference's own exchange: the paper's range-partitioned pipeline
-// (pipeline.cpp:61-123) with WCX1 frames between the logical workers.
+// BASELINE.json's path: fused tokenize/count kernels per worker, tables hash-partitioned by owner and delivered
+// device to device over the GPUs of the box (wfcu_wordcount_multi); stage times are CUDA-event times.
+RunResult run_wordcount_hashed(std::span<const RawDocument> corpus, std::size_t n_workers) {
+    if (n_workers == 0) throw std::invalid_argument("run_wordcount: n_workers must be >= 1");
+    const auto run_start = Clock::now();
+    if (corpus.empty()) return empty_run(n_workers, run_start);
+    const std::size_t n = n_workers;
+    RunResult result;
+    result.n_workers = n;
+    std::vector<const std::uint8_t*> ptrs;
+    std::vector<std::uint64_t> lens;
+    for (const auto& d : corpus) {
+        ptrs.push_back(reinterpret_cast<const std::uint8_t*>(d.text.data()));
+        lens.push_back(d.text.size());
+    }
+    std::uint64_t hint = total_bytes(corpus) / 64 / n + 1024;
+    for (int attempt = 0;; ++attempt) {
+        wfcu_counter_config cfg{};
+        std::uint64_t slots = 1u << 16;
+        while (slots < 4 * hint) slots <<= 1;
+        cfg.table_slots = slots;
+        cfg.deferred_slots = std::max<std::uint64_t>(1u << 16, hint);
+        cfg.long_slots = 1u << 16;
+        cfg.arena_bytes = 16u << 20;
+        std::vector<wfcu_counter*> owned(n, nullptr);
+        wfcu_stage_ns ns{};
+        const int rc = wfcu_wordcount_multi(ptrs.data(), lens.data(), ptrs.size(), std::uint32_t(n), &cfg, owned.data(), &ns);
+        if (rc != WFCU_OK) {
+            const bool capacity = rc == WFCU_ERR_TABLE_FULL || rc == WFCU_ERR_DEFERRED_FULL || rc == WFCU_ERR_ARENA_FULL;
+            if (!capacity || attempt >= 5) raise(rc, "map");
+            hint *= 8;
+            continue;
+        }
+        struct Release {
+            std::vector<wfcu_counter*>& v;
+            ~Release() { for (auto* c : v) wfcu_counter_destroy(c); }
+        } release{owned};
+        result.timings.map_ns = ns.map_ns;
+        result.timings.encode_ns = ns.encode_ns;
+        result.timings.exchange_ns = ns.exchange_ns;
+        const auto t0 = Clock::now();
+        for (std::size_t p = 0; p < n; ++p) result.shards.push_back(export_counts(owned[p], "reduce"));
+        result.timings.reduce_ns = since(t0);
+        break;
+    }
+    result.pre_repair_shards = result.shards;   // disjoint by construction: nothing to repair
+    for (const auto& shard : result.shards) result.counts.insert(shard.begin(), shard.end());
+    result.timings.total_ns = since(run_start);
+    return result;
+}
+
+// The caller's transport carries the chunks as WCX1 frames (pipeline.cpp:61-123 with a custom Transport).
 RunResult run_wordcount(std::span<const RawDocument> corpus, std::size_t n_workers, Transport& transport) {
     return run_range_partitioned(corpus, n_workers, transport);
 }
@@ -396,26 +472,13 @@ ShardPlan plan_partition(const WordList& sorted, std::size_t worker_id, std::siz
         throw std::invalid_argument("plan_partition: worker_id " + std::to_string(worker_id) + " out of range for " +
                                     std::to_string(n_workers) + " workers");
     if (!sorted.sorted) throw std::invalid_argument("plan_partition: word list must be sorted");
-    const std::size_t k = sorted.words.size(), n = n_workers, keep = k / n;
-    const std::size_t others = n > 1 ? n - 1 : 1;
-    const std::size_t base = n > 1 ? (k - keep) / others : 0;
-    std::size_t extra = n > 1 ? (k - keep) % others : 0;
-    ShardPlan plan{worker_id, n, k, std::vector<std::size_t>(n + 1, 0)};
-    for (std::size_t c = 0; c < n; ++c) {
-        std::size_t size = keep;
-        if (c != worker_id) {
-            size = base + (extra ? 1 : 0);
-            if (extra) --extra;
-        }
-        plan.boundaries[c + 1] = plan.boundaries[c] + size;
-    }
+    const std::vector<std::uint64_t> cut = partition_cuts(sorted.words.size(), worker_id, n_workers);
+    ShardPlan plan{worker_id, n_workers, sorted.words.size(), std::vector<std::size_t>(cut.begin(), cut.end())};
     return plan;
 }
 
 RunResult run_wordcount_range_partitioned(std::span<const RawDocument> corpus, std::size_t n_workers) {
-    if (n_workers == 0) throw std::invalid_argument("run_wordcount: n_workers must be >= 1");
-    InProcessTransport transport(n_workers);
-    return run_range_partitioned(corpus, n_workers, transport);
+    return run_wordcount(corpus, n_workers);
 }
 
 static RunResult run_range_partitioned(std::span<const RawDocument> corpus, std::size_t n_workers, Transport& transport) {
@@ -508,25 +571,39 @@ double map_reduce_fast(std::span<const float> values, MapKind map) {
 }
 
 // ---- analysis -----------------------------------------------------------------------------
-// Ordering of at most V rows on the host with the reference's exact comparators; the
-// counts themselves come from the device tables.  (SURVEY.md 8(f) rank 1 moves the
-// candidate selection onto the device.)
+// The order of the rows -- count / score descending, word ascending, the reference's log expression -- has ONE
+// implementation, in libwfcu (csrc/analysis.cpp: wfcu_top_k, wfcu_distinctive and the device entry points end in it).
+namespace {
+struct PackedTable {
+    Packed keys;
+    std::vector<std::uint64_t> counts;
+    std::vector<const Word*> words;
+};
+PackedTable pack_table(const CountMap& m) {
+    PackedTable p;
+    p.counts.reserve(m.size());
+    p.words.reserve(m.size());
+    for (const auto& [w, c] : m) {
+        p.keys.bytes.insert(p.keys.bytes.end(), w.begin(), w.end());
+        p.keys.lens.push_back(std::uint32_t(w.size()));
+        p.counts.push_back(c);
+        p.words.push_back(&w);
+    }
+    return p;
+}
+}  // namespace
+
 FrequencyTable top_k(const CountMap& counts, std::string label, std::size_t k) {
     FrequencyTable table;
     table.label = std::move(label);
-    std::vector<const CountMap::value_type*> rows;
-    rows.reserve(counts.size());
-    for (const auto& kv : counts) {
-        table.total_words += kv.second;
-        rows.push_back(&kv);
-    }
-    const std::size_t keep = std::min(k, rows.size());
-    auto before = [](const CountMap::value_type* a, const CountMap::value_type* b) {
-        return a->second != b->second ? a->second > b->second : a->first < b->first;
-    };
-    std::partial_sort(rows.begin(), rows.begin() + keep, rows.end(), before);
-    for (std::size_t i = 0; i < keep; ++i)
-        table.rows.push_back({rows[i]->first, rows[i]->second, double(rows[i]->second) / double(table.total_words)});
+    const PackedTable p = pack_table(counts);
+    const std::size_t cap = std::min(k, counts.size());
+    std::vector<std::uint64_t> idx(cap + 1);
+    std::vector<double> rel(cap + 1);
+    std::uint64_t rows = 0;
+    ok(wfcu_top_k(p.keys.bytes.data(), p.keys.lens.data(), p.counts.data(), counts.size(), k, idx.data(), rel.data(),
+                  &table.total_words, &rows));
+    for (std::uint64_t r = 0; r < rows; ++r) table.rows.push_back({*p.words[idx[r]], p.counts[idx[r]], rel[r]});
     return table;
 }
 
@@ -535,33 +612,91 @@ DistinctivenessReport distinctive_words(const CountMap& target, const CountMap& 
     DistinctivenessReport report;
     report.label = std::move(label);
     if (target.empty() && others.empty()) return report;
-    std::uint64_t t_total = 0, o_total = 0;
-    for (const auto& kv : target) t_total += kv.second;
-    for (const auto& kv : others) o_total += kv.second;
-    struct Row {
-        const Word* word;
-        std::uint64_t in_target, in_others;
-        double score;
-    };
-    std::vector<Row> rows;
-    rows.reserve(target.size() + others.size());
-    auto ti = target.begin();
-    auto oi = others.begin();
-    while (ti != target.end() || oi != others.end()) {   // union of two sorted maps
-        const int c = oi == others.end() ? -1 : ti == target.end() ? 1 : ti->first.compare(oi->first);
-        if (c < 0) { rows.push_back({&ti->first, ti->second, 0, 0.0}); ++ti; }
-        else if (c > 0) { rows.push_back({&oi->first, 0, oi->second, 0.0}); ++oi; }
-        else { rows.push_back({&ti->first, ti->second, oi->second, 0.0}); ++ti; ++oi; }
+    const PackedTable t = pack_table(target), o = pack_table(others);
+    const std::size_t cap = std::min(k, target.size() + others.size());
+    std::vector<std::int32_t> src(cap + 1);
+    std::vector<std::uint64_t> idx(cap + 1);
+    std::vector<double> score(cap + 1);
+    std::uint64_t rows = 0;
+    ok(wfcu_distinctive(t.keys.bytes.data(), t.keys.lens.data(), t.counts.data(), target.size(), o.keys.bytes.data(),
+                        o.keys.lens.data(), o.counts.data(), others.size(), k, src.data(), idx.data(), score.data(), &rows));
+    for (std::uint64_t r = 0; r < rows; ++r) report.rows.push_back({*(src[r] ? o : t).words[idx[r]], score[r]});
+    return report;
+}
+
+// ---- tables that stay on the device -----------------------------------------------------------
+DeviceCounts::DeviceCounts(std::uint64_t expected_distinct_words) {
+    wfcu_counter_config cfg{};
+    std::uint64_t slots = 1u << 16;
+    while (slots < 4 * expected_distinct_words) slots <<= 1;
+    cfg.table_slots = slots;
+    cfg.deferred_slots = std::max<std::uint64_t>(1u << 20, expected_distinct_words);
+    cfg.long_slots = 1u << 16;
+    cfg.arena_bytes = 16u << 20;
+    ok(wfcu_counter_create(&h_, &cfg));
+}
+DeviceCounts::~DeviceCounts() { wfcu_counter_destroy(h_); }
+DeviceCounts::DeviceCounts(DeviceCounts&& other) noexcept : h_(other.h_) { other.h_ = nullptr; }
+DeviceCounts& DeviceCounts::operator=(DeviceCounts&& other) noexcept {
+    if (this != &other) {
+        wfcu_counter_destroy(h_);
+        h_ = other.h_;
+        other.h_ = nullptr;
     }
-    const double t_den = double(t_total) + double(rows.size());
-    const double o_den = double(o_total) + double(rows.size());
-    for (auto& r : rows)
-        r.score = std::log((double(r.in_target) + 1.0) / t_den) - std::log((double(r.in_others) + 1.0) / o_den);
-    const std::size_t keep = std::min(k, rows.size());
-    std::partial_sort(rows.begin(), rows.begin() + keep, rows.end(), [](const Row& a, const Row& b) {
-        return a.score != b.score ? a.score > b.score : *a.word < *b.word;
-    });
-    for (std::size_t i = 0; i < keep; ++i) report.rows.push_back({*rows[i].word, rows[i].score});
+    return *this;
+}
+void DeviceCounts::count(std::span<const RawDocument> corpus) {
+    std::vector<const std::uint8_t*> ptrs;
+    std::vector<std::uint64_t> lens;
+    for (const auto& d : corpus) {
+        ptrs.push_back(reinterpret_cast<const std::uint8_t*>(d.text.data()));
+        lens.push_back(d.text.size());
+    }
+    ok(wfcu_counter_count_host(h_, ptrs.data(), lens.data(), ptrs.size()), "map");
+}
+void DeviceCounts::merge(const DeviceCounts& other) {
+    ok(wfcu_counter_merge(h_, other.h_, nullptr));
+    ok(wfcu_counter_status(h_, nullptr));
+}
+std::uint64_t DeviceCounts::distinct_words() const {
+    std::uint64_t distinct = 0;
+    ok(wfcu_counter_stats(h_, nullptr, &distinct, nullptr, nullptr));
+    return distinct;
+}
+std::uint64_t DeviceCounts::total_words() const {
+    std::uint64_t total = 0;
+    ok(wfcu_counter_stats(h_, nullptr, nullptr, &total, nullptr));
+    return total;
+}
+CountMap DeviceCounts::to_map() const { return export_counts(h_); }
+
+FrequencyTable DeviceCounts::top_k(std::string label, std::size_t k) const {
+    FrequencyTable table;
+    table.label = std::move(label);
+    const std::size_t cap = std::min<std::uint64_t>(k, distinct_words());
+    std::vector<std::uint8_t> bytes(64 * cap + 4096);
+    std::vector<std::uint32_t> lens(cap + 1);
+    std::vector<std::uint64_t> counts(cap + 1);
+    std::vector<double> rel(cap + 1);
+    std::uint64_t rows = 0;
+    ok(wfcu_counter_top_k(h_, k, nullptr, bytes.data(), bytes.size(), lens.data(), counts.data(), rel.data(), cap + 1, &rows,
+                          &table.total_words));
+    const std::vector<Word> words = unpack(bytes.data(), lens.data(), rows);
+    for (std::uint64_t r = 0; r < rows; ++r) table.rows.push_back({words[r], counts[r], rel[r]});
+    return table;
+}
+
+DistinctivenessReport DeviceCounts::distinctive(const DeviceCounts& others, std::string label, std::size_t k) const {
+    DistinctivenessReport report;
+    report.label = std::move(label);
+    const std::size_t cap = std::min<std::uint64_t>(k, distinct_words() + others.distinct_words());
+    std::vector<std::uint8_t> bytes(64 * cap + 4096);
+    std::vector<std::uint32_t> lens(cap + 1);
+    std::vector<double> score(cap + 1);
+    std::uint64_t rows = 0;
+    ok(wfcu_counter_distinctive(h_, others.h_, k, nullptr, bytes.data(), bytes.size(), lens.data(), score.data(), cap + 1, &rows));
+    const std::vector<Word> words = unpack(bytes.data(), lens.data(), rows);
+    for (std::uint64_t r = 0; r < rows; ++r) report.rows.push_back({words[r], score[r]});
     return report;
 }
 

@@ -218,7 +218,7 @@ static void reduce_cases() {
 static void pipeline_cases() {
     const CountMap expected{{"a", 1}, {"algorithm", 1}, {"cool", 1}, {"i", 1}, {"is", 1},
                             {"mapreduce", 2}, {"test", 2}, {"to", 2}, {"want", 1}};
-    // pipeline_test.cpp:26-54 (pre_repair_shards follow the hash partition: SURVEY D2)
+    // pipeline_test.cpp:26-54, acceptance_test.cpp:155-162: the paper's worked example, pre-repair shards included
     {
         const RunResult r = run_wordcount(kTwoDocs, 2);
         CHECK(r.counts == expected);
@@ -226,7 +226,20 @@ static void pipeline_cases() {
         CHECK(merge_counts(r.shards) == r.counts);
         CHECK(r.n_workers == 2);
         CHECK(r.pre_repair_shards.size() == 2);
-        CHECK(count_unreduced_words(r.pre_repair_shards) <= 1);   // <= n - 1, SPEC bound
+        CHECK(r.pre_repair_shards[0] == (CountMap{{"a", 1}, {"algorithm", 1}, {"cool", 1}, {"i", 1}, {"is", 1}, {"mapreduce", 1}}));
+        CHECK(r.pre_repair_shards[1] == (CountMap{{"mapreduce", 1}, {"test", 2}, {"to", 2}, {"want", 1}}));
+        CHECK(count_unreduced_words(r.pre_repair_shards) == 1);
+        CHECK(count_unreduced_words(r.shards) == 0);
+        CHECK(r.shards[0].at("mapreduce") == 2);
+        // the hash-partitioned fast path: same counts, disjoint shards, nothing to repair
+        const RunResult h = run_wordcount_hashed(kTwoDocs, 2);
+        CHECK(h.counts == expected);
+        CHECK(h.shards.size() == 2);
+        CHECK(h.pre_repair_shards == h.shards);
+        CHECK(count_unreduced_words(h.shards) == 0);
+        CHECK(merge_counts(h.shards) == h.counts);
+        CHECK(h.timings.map_ns > 0);
+        CHECK(run_wordcount_hashed(kTwoDocs, 5).counts == expected);
         const auto& t = r.timings;
         CHECK(t.total_ns >= std::max({t.map_ns, t.sort_ns, t.encode_ns, t.exchange_ns, t.reduce_ns, t.repair_ns}));
         CHECK(run_wordcount(kTwoDocs, 1).counts == expected);

@@ -13,3 +13,18 @@ def test_dropin_binary(capi, cuda):
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-1000:]
     assert "0 failed" in out.stdout
+
+
+REF_SUITES = ["text", "reduce", "engine", "pipeline", "analysis", "shuffle", "wire"]
+
+
+@pytest.mark.parametrize("suite", REF_SUITES)
+def test_reference_suite_unmodified(capi, cuda, suite):
+    """/root/reference/proj/tests/<suite>_test.cpp, compiled UNMODIFIED from where it lies against the drop-in
+    (paper_2206_05269_b200/build.py::build_reference_suites; doctest macros from tests/shim/doctest.h), passes on
+    the GPU: every TEST_CASE of the reference's own suite, with its own goldens."""
+    exe = capi.LIB_PATH.parent / "reftests" / f"{suite}_test"
+    assert exe.exists(), "lib/reftests is built where /root/reference is present and travels with the snapshot"
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-4000:]
+    assert "| 0 failed" in out.stdout
