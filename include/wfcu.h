@@ -90,7 +90,10 @@ WFCU_API int wfcu_map_reduce_dev(const void* dev_values, int dtype, uint64_t n, 
                         int map_kind, void* stream, double* out);
 
 /* Same, but leaves the result in a device double (no host sync) -- what bench.py
- * times for the resident-data number and what precedes the allreduce. */
+ * times for the resident-data number and what precedes the allreduce.
+ * The map-reduce entry points are NOT re-entrant per device: the per-CTA partials (and, for the synchronous forms,
+ * the result word) live in one buffer per device, so at most one reduction per device may be in flight -- calls on
+ * one stream, or calls separated by a synchronisation, are fine; two streams or two host threads are not. */
 WFCU_API int wfcu_map_reduce_dev_async(const void* dev_values, int dtype, uint64_t n, uint64_t position_base,
                               int map_kind, void* stream, double* dev_out);
 

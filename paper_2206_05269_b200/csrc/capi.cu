@@ -207,6 +207,9 @@ static int check_map_args(int dtype, int kind, const void* values, uint64_t n) {
     return WFCU_OK;
 }
 
+// NOT re-entrant per device: the per-CTA partials live in one buffer per device (and the synchronous forms share one
+// result word), so two reductions of one device must not be in flight at the same time -- neither on two streams nor
+// from two host threads.  include/wfcu.h says so; callers that need overlap serialise on their side.
 extern "C" int wfcu_map_reduce_dev_async(const void* dev_values, int dtype, uint64_t n, uint64_t position_base,
                                          int map_kind, void* stream, double* dev_out) {
     DeviceState* d;
@@ -1659,7 +1662,9 @@ static int tokenize_unordered(const uint8_t* dev_text, uint64_t n, cudaStream_t 
             // unless the deferred list or the arena cut the run short)
             if (produced > cap) cap = produced + 1024;
             if (st & kStatusDeferredFull) { deferred_cap = n / 2 + 1024; cap = std::max<u64>(cap, n / 2 + 1024); }
-            if (st & kStatusArenaFull) arena_cap = 3 * n + 4096;
+            // worst case per fragment: an 8-byte header + the normalised bytes (an invalid byte becomes the 3 bytes of
+            // U+FFFD) padded to 8, i.e. below 3 * len + 16 for a fragment of len + 1 input bytes: 5 n + 4096 covers any text
+            if (st & kStatusArenaFull) arena_cap = 5 * n + 4096;
             continue;
         }
         t->recs = recs.as<TokenRec>();

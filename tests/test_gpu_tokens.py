@@ -148,3 +148,12 @@ def test_concat_slices_is_the_range_exchange(capi, cuda, port):
     assert empty.words() == []
     with pytest.raises(capi.InvalidArgument):
         capi.Tokens.concat_slices(handles, [0] * n, [10 ** 6] * n)
+
+
+def test_tokenize_arena_worst_case(capi, cuda, port):
+    """long fragments full of invalid bytes: every byte becomes the three bytes of U+FFFD, so the long-token arena
+    needs several times the text size (the retry used to stop at 3 n and fail with ARENA_FULL)"""
+    text = (b"a" + b"\xff" * 5 + b"b ") * 40000
+    want = port.tokenize(text)
+    assert capi.Tokens.tokenize_host(text).words() == want
+    assert len(want) == 40000 and len(want[0]) == 17
