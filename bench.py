@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """bench.py -- the headline benchmark of the word-frequency hot path on B200.
 
-    python bench.py --gpus N --steps K --warmup W [--impl reference] [--workload cfg3|cfg4]
+    python bench.py --gpus N --steps K --warmup W [--impl reference] [--workload cfg3|cfg4|cfg5]
 
 metric   word-count corpus GB/s (BASELINE.json): bytes of corpus counted per second,
          whole job over all N GPUs, GB = 1e9 bytes.
@@ -9,6 +9,9 @@ workload cfg3 (default): synthetic Zipf(s=1.1) corpus, 50k-word vocabulary, 954 
          documents (1.0003 GB) PER GPU, documents assigned round-robin (d mod N); at
          N > 1 every step ends with the hash-partitioned all-to-all merge.  Weak scaling.
          cfg4: 32 GB total, 1M-word vocabulary, document-sharded over N >= 2 GPUs.
+         cfg5: four speaker corpora (1 GB each, 1 M-word vocabulary, 1 % speaker-specific words), N = 1:
+         a step counts the four corpora, pools the other three per speaker (device merges) and produces
+         the per-speaker top-25 and 25 most distinctive words (proj/src/cli.cpp:176-230) on the device.
 step     reset the count table + one pass of the fused tokenizer/count kernels over the
          rank's resident shard (+ partition / all-to-all / merge-insert at N > 1).
 value    inputs resident in HBM, CUDA-event timed, max over ranks.
@@ -480,6 +483,92 @@ def run_b200(args) -> None:
         dist.destroy_process_group()
 
 
+def run_cfg5(args) -> None:
+    """BASELINE.json config 5 on one GPU: four synthetic speakers -> per-speaker top-k and distinctive words."""
+    import numpy as np
+    import torch
+    from paper_2206_05269_b200 import capi
+    import oracle
+    if max(args.gpus, 1) != 1 or int(os.environ.get("WORLD_SIZE", "1")) != 1:
+        raise SystemExit("bench.py: --workload cfg5 runs on one GPU (the four tables and their pooled complements are rank-local)")
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device: the product has no CPU path")
+    torch.cuda.set_device(0)
+    device = torch.device("cuda", 0)
+    speakers, vocab, k = [1, 2, 3, 4], 1000000, 25
+    docs = args.docs or 954
+    stream = torch.cuda.current_stream(device).cuda_stream
+    dev = {}
+    for sp in speakers:
+        host = torch.empty(docs * DOC_BYTES, dtype=torch.uint8).pin_memory()
+        capi.synth_corpus_strided(SEED, 0, 1, docs, vocab, ZIPF_S, sp, DOC_BYTES, out=host.numpy())
+        dev[sp] = host.to(device)
+    torch.cuda.synchronize()
+    counters = {sp: capi.Counter(table_slots=1 << 22) for sp in speakers}
+    pooled = {sp: capi.Counter(table_slots=1 << 23) for sp in speakers}
+    nbytes = docs * DOC_BYTES * len(speakers)
+    report = {}
+
+    def step():
+        for sp in speakers:
+            counters[sp].reset(stream)
+            counters[sp].count_dev(dev[sp].data_ptr(), docs * DOC_BYTES, stream)
+        for sp in speakers:
+            pooled[sp].reset(stream)
+            for o in speakers:
+                if o != sp:
+                    pooled[sp].merge(counters[o], stream)
+            report[sp] = (counters[sp].top_k(k, stream), counters[sp].distinctive(pooled[sp], k, stream))
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    launches0 = capi.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clocks:
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = capi.launch_count() - launches0
+    # parity on a bounded sample: the first documents of every speaker, reports against the oracle
+    sample_docs = 4
+    small, cpu = {}, {}
+    for sp in speakers:
+        small[sp] = capi.Counter(table_slots=1 << 20)
+        small[sp].count_dev(dev[sp].data_ptr(), sample_docs * DOC_BYTES)
+        cpu[sp] = oracle.port().wordcount([dev[sp][:sample_docs * DOC_BYTES].cpu().numpy()])
+    equal = True
+    for sp in speakers:
+        others_dev = capi.Counter(table_slots=1 << 21)
+        others_cpu = {}
+        for o in speakers:
+            if o != sp:
+                others_dev.merge(small[o])
+                for wd, c in cpu[o].items():
+                    others_cpu[wd] = others_cpu.get(wd, 0) + c
+        equal &= small[sp].top_k(k) == oracle.port().top_k(cpu[sp], k)
+        equal &= small[sp].distinctive(others_dev, k) == oracle.port().distinctive(cpu[sp], others_cpu, k)
+    line = {
+        "metric": METRIC, "value": nbytes / (ms * 1e-3) / 1e9, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u8", "data": "synthetic",
+        "config": {"workload": "four synthetic speaker corpora (1 M-word vocabulary, 1 % speaker-specific words), counted, pooled and "
+                               "reported (top-25, 25 most distinctive words per speaker) on 1 GPU",
+                   "speakers": len(speakers), "documents_per_speaker": docs, "job_bytes": nbytes, "k": k,
+                   "distinct_words_per_speaker": [counters[sp].stats()[0] for sp in speakers],
+                   "most_distinctive": {str(sp): report[sp][1][0][0].decode("utf-8", "replace") for sp in speakers},
+                   "l2": "inputs (4 x 1 GB) larger than the 126 MB L2; no flush needed"},
+        "parity": {"checked": True, "docs_per_speaker": sample_docs, "equal": bool(equal),
+                   "against": "oracle top_k / distinctive_words (words, counts and doubles) on the same bytes"},
+        "gpu_launches": int(launches), "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def mapreduce_line(capi, torch, device, stream, peak, with_cpu: bool) -> dict:
     """BASELINE.json config 2: sum of f(x) over 2^28 fp32 (1 GiB), f = identity and x^2.
     Input = the reference bench's recipe (proj/src/cli.cpp:122-124: mt19937_64(seed 1), uniform(0,1)), rounded to
@@ -579,7 +668,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS) + ["cfg5"], default="cfg3")
     ap.add_argument("--docs", type=int, default=None, help="override document count (per GPU for cfg3, total for cfg4)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--sync-exchange", action="store_true",
@@ -605,7 +694,11 @@ def main() -> None:
             if (native.LIB / "libwfcu.so").exists():
                 break
             time.sleep(0.5)
-    if args.impl == "reference":
+    if args.workload == "cfg5":
+        if args.impl == "reference":
+            raise SystemExit("bench.py: the reference arm times cfg3 / cfg4 (run_wordcount); cfg5's reports are checked inside the b200 arm")
+        run_cfg5(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_b200(args)

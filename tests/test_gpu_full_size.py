@@ -88,3 +88,31 @@ def test_host_path_equals_resident_path_at_full_size(capi, cuda, corpus):
     d.count_dev(dev.data_ptr(), n)
     assert table(h) == table(d)
     assert h.stats() == d.stats()
+
+
+def _reference_table(docs):
+    """The unmodified reference on all host cores: sharded serial counts merged (exact by associativity,
+    proj/tests/reduce_test.cpp:138-155) through run_wordcount; the C restatement when the compiled reference is not
+    on this box."""
+    import os
+    import oracle
+    if oracle.ref_available():
+        return oracle.ref().run_wordcount(docs, os.cpu_count() or 1)[0]
+    return oracle.port().wordcount(docs)
+
+
+@pytest.mark.parametrize("vocab,slots", [(50000, 1 << 20), (1000000, 1 << 22)], ids=["cfg3", "cfg4-shard"])
+def test_full_size_exact_against_the_reference(capi, cuda, vocab, slots):
+    """The WHOLE 954-document shard of bench.py (cfg3: 50 k words; cfg4: a 1 GB shard of the 1 M-word corpus), counted
+    by the timed kernels and exported, equals the reference's table entry by entry -- std::map order, exact counts."""
+    corpus = capi.synth_corpus(seed=1, doc_begin=0, doc_end=DOCS, vocab=vocab)
+    dev, n = to_dev(cuda, corpus)
+    c = capi.Counter(table_slots=slots)
+    c.count_dev(dev.data_ptr(), n)
+    blob, lens, counts = c.export()
+    words = capi.unpack_words(blob, lens)
+    doc_bytes = corpus.size // DOCS
+    want = sorted(_reference_table([corpus[i * doc_bytes:(i + 1) * doc_bytes] for i in range(DOCS)]).items())
+    assert len(words) == len(want)
+    assert words == [w for w, _ in want]
+    assert counts.tolist() == [v for _, v in want]
