@@ -1,7 +1,7 @@
 """Developer tool: executed warp-instruction mix per opcode / pipe of the kernel in an .ncu-rep (source page)."""
 import csv, subprocess, sys, io, collections
 rep = sys.argv[1]
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--launch-count", "1"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
 hdr = rows[1]; data = rows[2:]
 ia, isrc = hdr.index("Instructions Executed"), hdr.index("Source")

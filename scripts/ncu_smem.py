@@ -1,7 +1,7 @@
 """Developer tool: shared-memory wavefronts per instruction of the kernel in an .ncu-rep (source page)."""
 import csv, subprocess, sys, io
 rep = sys.argv[1]; rows_hint = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--launch-count", "1"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
 hdr = rows[1]; data = rows[2:]
 ia, isrc, iaddr = hdr.index("Instructions Executed"), hdr.index("Source"), hdr.index("Address")

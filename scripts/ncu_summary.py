@@ -21,7 +21,7 @@ st = [(h, int(float(v))) for h, v in zip(hdr, vals) if 'pcsamp_warps_issue_stall
 tot = sum(v for _, v in st) or 1
 for h, v in sorted(st, key=lambda x: -x[1])[:10]:
     print(f"{h.split('stalled_')[1]:28s} {v:8d} {100*v/tot:5.1f}%")
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--launch-count", "1"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
 hdr = rows[1]; data = rows[2:]
 ia, isamp, isrc, iaddr = hdr.index("Instructions Executed"), hdr.index("# Samples"), hdr.index("Source"), hdr.index("Address")
