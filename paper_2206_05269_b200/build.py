@@ -123,10 +123,41 @@ def build_reference_suites(force: bool = False) -> list[Path]:
     return built
 
 
+def build_relink_demo(force: bool = False) -> Path | None:
+    """INTEGRATION.md section 1, tried for real: the reference's own report.cpp (unmodified, compiled where it lies,
+    against ITS wfc/report.hpp -- reached through a symlink so that every other wfc/ header comes from the drop-in) +
+    tests/relink/relink_main.cpp (the cli.cpp flows without CLI11) + libwfc_b200.so.  nlohmann's json.hpp is the
+    copy the image carries (cudnn_frontend's thirdparty directory); without it the demo is skipped."""
+    ref = Path("/root/reference/proj")
+    out_dir = LIB / "reftests"
+    exe = out_dir / "relink_demo"
+    if not ref.exists() or not (LIB / "libwfc_b200.so").exists():
+        return exe if exe.exists() else None
+    json_dirs = [Path(p) for p in sys.path if p and (Path(p) / "include/cudnn_frontend/thirdparty/nlohmann/json.hpp").exists()]
+    if not json_dirs:
+        return None
+    json_inc = json_dirs[0] / "include/cudnn_frontend/thirdparty/nlohmann"
+    out_dir.mkdir(exist_ok=True)
+    view = out_dir / "relink_include" / "wfc"          # the one header a maintainer keeps from proj/include
+    view.mkdir(parents=True, exist_ok=True)
+    link = view / "report.hpp"
+    if not link.exists():
+        link.symlink_to(ref / "include/wfc/report.hpp")
+    main = ROOT / "tests" / "relink" / "relink_main.cpp"
+    deps = [main, ref / "src/report.cpp", LIB / "libwfc_b200.so"] + sorted((HOST / "include" / "wfc").glob("*.hpp"))
+    if force or _stale(exe, deps):
+        cxx = os.environ.get("CXX") or shutil.which("g++") or "g++"
+        _run([cxx, "-std=c++20", "-O1", "-pthread", f"-I{view.parent}", f"-I{HOST / 'include'}", f"-I{json_inc}",
+              "-o", str(exe), str(main), str(ref / "src/report.cpp"), f"-L{LIB}", "-lwfc_b200", "-lwfcu",
+              "-Wl,-rpath,$ORIGIN/.."])
+    return exe
+
+
 def build_all(force: bool = False, verbose: bool = False) -> None:
     build_wfcu(force, verbose)
     build_host(force)
     build_reference_suites(force)
+    build_relink_demo(force)
 
 
 if __name__ == "__main__":

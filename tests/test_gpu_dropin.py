@@ -28,3 +28,33 @@ def test_reference_suite_unmodified(capi, cuda, suite):
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-4000:]
     assert "| 0 failed" in out.stdout
+
+
+def test_relink_with_the_references_own_report_cpp(capi, cuda, tmp_path):
+    """INTEGRATION.md section 1 tried for real: the reference's report.cpp (unmodified) + a caller written against
+    the reference's headers, linked with libwfc_b200.so, prints the byte-exact golden table of
+    proj/tests/cli_test.cpp:51-60 for the two-document fixture, and the JSON form through the reference's
+    frequency_json."""
+    import json
+    import os
+    exe = capi.LIB_PATH.parent / "reftests" / "relink_demo"
+    if not exe.exists():
+        pytest.skip("relink demo not built (no json.hpp in this image)")
+    fixtures = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fixtures.json")))
+    two = tmp_path / "two-docs"
+    two.mkdir()
+    for i, hexdoc in enumerate(fixtures["two-docs"]["docs"]):
+        (two / f"doc{i + 1}.txt").write_bytes(bytes.fromhex(hexdoc))
+    (two / "ignored.md").write_text("not a text file")
+    out = subprocess.run([str(exe), "wordcount", str(two), "2", "tsv"], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    assert out.stdout == ("mapreduce\t2\t0.166666666667\ntest\t2\t0.166666666667\nto\t2\t0.166666666667\n"
+                          "a\t1\t0.0833333333333\nalgorithm\t1\t0.0833333333333\ncool\t1\t0.0833333333333\n"
+                          "i\t1\t0.0833333333333\nis\t1\t0.0833333333333\nwant\t1\t0.0833333333333\n")
+    assert [l.split("\t")[:2] for l in out.stderr.splitlines()][-1] == ["timing", "total"]
+    js = subprocess.run([str(exe), "wordcount", str(two), "3", "json"], capture_output=True, text=True, timeout=300)
+    assert js.returncode == 0, js.stderr
+    rows = json.loads(js.stdout)      # frequency_json (proj/src/report.cpp:19-25): an array of {word, count, relfreq}
+    assert len(rows) == 9 and rows[0] == {"word": "mapreduce", "count": 2, "relfreq": 2 / 12}
+    bad = subprocess.run([str(exe), "wordcount", str(tmp_path / "missing"), "2"], capture_output=True, text=True, timeout=300)
+    assert bad.returncode == 1 and "not a readable directory" in bad.stderr
