@@ -229,9 +229,15 @@ WFCU_API uint64_t wfcu_counter_max_entries(const wfcu_counter* c);
  * sticky flags the caller reads once, after any number of steps.  Asynchronous on `stream`. */
 WFCU_API int wfcu_counter_partition_fixed(wfcu_counter* c, uint32_t n_parts, wfcu_entry* dev_entries,
                                  uint64_t cap_per_part, uint64_t* dev_counts, void* stream);
+/* Same, self-describing: entry 0 of every region is a header {0, 0, entries that follow, 0} and at most
+ * cap_per_part - 1 entries follow, so ONE all-to-all of the regions is the whole exchange (the n x 8-byte all-to-all
+ * of the sizes was pure latency).  dev_counts as above.  Asynchronous on `stream`. */
+WFCU_API int wfcu_counter_partition_framed(wfcu_counter* c, uint32_t n_parts, wfcu_entry* dev_entries,
+                                  uint64_t cap_per_part, uint64_t* dev_counts, void* stream);
 /* The receiving side (replaces merge_sorted + reduce_sorted + merge_counts, proj/src/shuffle.cpp:75-96,
  * proj/src/reduce.cpp:8-21,83-89): adds the first min(dev_region_counts[p], cap_per_part) entries of
- * every region; the counts are read on the device.  Asynchronous on `stream`. */
+ * every region; the counts are read on the device.  dev_region_counts == NULL: the regions are framed
+ * (wfcu_counter_partition_framed) and carry their own counts.  Asynchronous on `stream`. */
 WFCU_API int wfcu_counter_merge_regions(wfcu_counter* c, const wfcu_entry* dev_entries, uint32_t n_parts,
                                uint64_t cap_per_part, const uint64_t* dev_region_counts, void* stream);
 

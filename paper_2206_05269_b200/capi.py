@@ -92,6 +92,7 @@ SIGNATURES = {
     "wfcu_counter_partition": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
     "wfcu_counter_max_entries": (C.c_uint64, [C.c_void_p]),
     "wfcu_counter_partition_fixed": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
+    "wfcu_counter_partition_framed": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
     "wfcu_counter_merge_regions": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p]),
     "wfcu_counter_merge_entries": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "wfcu_counter_long_records": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, u64p, C.c_void_p]),
@@ -389,6 +390,10 @@ class Counter:
     def partition_fixed(self, n_parts: int, entries_ptr: int, cap_per_part: int, counts_ptr: int, stream: int = 0) -> None:
         check(lib.wfcu_counter_partition_fixed(self._h, n_parts, C.c_void_p(entries_ptr), cap_per_part,
                                                C.c_void_p(counts_ptr), C.c_void_p(stream)))
+
+    def partition_framed(self, n_parts: int, entries_ptr: int, cap_per_part: int, counts_ptr: int, stream: int = 0) -> None:
+        check(lib.wfcu_counter_partition_framed(self._h, n_parts, C.c_void_p(entries_ptr), cap_per_part,
+                                                C.c_void_p(counts_ptr), C.c_void_p(stream)))
 
     def merge_regions(self, entries_ptr: int, n_parts: int, cap_per_part: int, counts_ptr: int, stream: int = 0) -> None:
         check(lib.wfcu_counter_merge_regions(self._h, C.c_void_p(entries_ptr), n_parts, cap_per_part,

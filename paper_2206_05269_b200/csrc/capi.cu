@@ -46,7 +46,7 @@ cudaError_t tb_key_bytes(const TableView& t, u64* dev_bytes, int sm, cudaStream_
 cudaError_t tb_partition(const TableView& t, u32 n_parts, Slot* out, u64 cap, u64* dev_part_counts, u64* cursors,
                          int sm, cudaStream_t s, u64* launches);
 cudaError_t tb_merge_entries(const TableView& t, const Slot* in, u64 n, int sm, cudaStream_t s, u64* launches);
-cudaError_t tb_partition_fixed(const TableView& t, u32 n_parts, u64 cap, Slot* out, u64* dev_counts, int sm,
+cudaError_t tb_partition_fixed(const TableView& t, u32 n_parts, u64 cap, bool framed, Slot* out, u64* dev_counts, int sm,
                                cudaStream_t s, u64* launches);
 cudaError_t tb_merge_regions(const TableView& t, const Slot* in, u32 n_parts, u64 cap, const u64* region_counts, int sm,
                              cudaStream_t s, u64* launches);
@@ -1271,7 +1271,18 @@ extern "C" int wfcu_counter_partition_fixed(wfcu_counter* c, uint32_t n_parts, w
     if (n_parts == 0 || n_parts > 4096) return fail(WFCU_ERR_INVALID_ARGUMENT, "n_parts must be in 1..4096");
     if (!dev_entries || !dev_counts || cap_per_part == 0) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
     LaunchTally tally;
-    CUDA_TRY(tb_partition_fixed(c->v, n_parts, cap_per_part, reinterpret_cast<Slot*>(dev_entries),
+    CUDA_TRY(tb_partition_fixed(c->v, n_parts, cap_per_part, false, reinterpret_cast<Slot*>(dev_entries),
+                                reinterpret_cast<u64*>(dev_counts), c->sm_count, (cudaStream_t)stream, &tally.n));
+    return WFCU_OK;
+}
+
+extern "C" int wfcu_counter_partition_framed(wfcu_counter* c, uint32_t n_parts, wfcu_entry* dev_entries,
+                                             uint64_t cap_per_part, uint64_t* dev_counts, void* stream) {
+    if (!c) return fail(WFCU_ERR_INVALID_ARGUMENT, "counter is null");
+    if (n_parts == 0 || n_parts > 4096) return fail(WFCU_ERR_INVALID_ARGUMENT, "n_parts must be in 1..4096");
+    if (!dev_entries || !dev_counts || cap_per_part < 2) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument or capacity below 2");
+    LaunchTally tally;
+    CUDA_TRY(tb_partition_fixed(c->v, n_parts, cap_per_part, true, reinterpret_cast<Slot*>(dev_entries),
                                 reinterpret_cast<u64*>(dev_counts), c->sm_count, (cudaStream_t)stream, &tally.n));
     return WFCU_OK;
 }
@@ -1279,7 +1290,7 @@ extern "C" int wfcu_counter_partition_fixed(wfcu_counter* c, uint32_t n_parts, w
 extern "C" int wfcu_counter_merge_regions(wfcu_counter* c, const wfcu_entry* dev_entries, uint32_t n_parts,
                                           uint64_t cap_per_part, const uint64_t* dev_region_counts, void* stream) {
     if (!c) return fail(WFCU_ERR_INVALID_ARGUMENT, "counter is null");
-    if (!dev_entries || !dev_region_counts) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
+    if (!dev_entries) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
     LaunchTally tally;
     CUDA_TRY(tb_merge_regions(c->v, reinterpret_cast<const Slot*>(dev_entries), n_parts, cap_per_part,
                               reinterpret_cast<const u64*>(dev_region_counts), c->sm_count, (cudaStream_t)stream, &tally.n));

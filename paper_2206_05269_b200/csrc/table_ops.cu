@@ -143,7 +143,9 @@ __global__ void tb_partition_scatter_kernel(TableView t, u32 n_parts, u64* __res
 // One-pass form for the synchronisation-free exchange: partition p owns the fixed region
 // out[p * cap, (p+1) * cap); counts[p] = entries written, counts[n_parts] += long tokens in
 // the table, counts[n_parts + 1] += entries that did not fit (both sticky flags for the host).
-__global__ void tb_partition_fixed_kernel(TableView t, u32 n_parts, u64 cap, Slot* __restrict__ out,
+// hdr = 1: the first entry of every region is left free for a header (tb_region_headers_kernel): the region then
+// describes itself and the exchange needs no separate all-to-all of the sizes.
+__global__ void tb_partition_fixed_kernel(TableView t, u32 n_parts, u64 cap, u32 hdr, Slot* __restrict__ out,
                                           u64* __restrict__ counts) {
     const u32 lane = threadIdx.x & 31;
     for (u64 i0 = (u64)blockIdx.x * blockDim.x + threadIdx.x - lane; i0 <= t.mask; i0 += (u64)gridDim.x * blockDim.x) {
@@ -154,13 +156,19 @@ __global__ void tb_partition_fixed_kernel(TableView t, u32 n_parts, u64 cap, Slo
         const u32 p = live ? owner_mix32(s.k0, s.k1) % n_parts : 0u;
         const u64 j = warp_claim(counts, p, live);
         if (live) {
-            if (j < cap) out[(u64)p * cap + j] = Slot{s.k0, s.k1, s.count, 0};
+            if (j + hdr < cap) out[(u64)p * cap + hdr + j] = Slot{s.k0, s.k1, s.count, 0};
             else atomicAdd(&counts[n_parts + 1], 1ull);
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0 && *t.n_long) atomicAdd(&counts[n_parts], *t.n_long);
 }
+// header of region p: {0, 0, entries that follow, 0}
+__global__ void tb_region_headers_kernel(Slot* __restrict__ out, u32 n_parts, u64 cap, const u64* __restrict__ counts) {
+    const u32 p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n_parts) out[(u64)p * cap] = Slot{0ull, 0ull, counts[p] < cap - 1 ? counts[p] : cap - 1, 0ull};
+}
 // counts[key] += count for the first min(region_counts[p], cap) entries of every region
+// region_counts == nullptr: the regions carry their own header (first entry, count field)
 __global__ void tb_merge_regions_kernel(TableView t, const Slot* __restrict__ in, u32 n_parts, u64 cap,
                                         const u64* __restrict__ region_counts) {
     u64 tokens = 0;
@@ -168,7 +176,8 @@ __global__ void tb_merge_regions_kernel(TableView t, const Slot* __restrict__ in
     const u64 total = (u64)n_parts * cap;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (u64)gridDim.x * blockDim.x) {
         const u64 p = i / cap, j = i - p * cap;
-        if (j < region_counts[p]) {
+        const bool mine = region_counts ? j < region_counts[p] : (j >= 1 && j - 1 < in[p * cap].count);
+        if (mine) {
             const Slot s = in[i];
             if (s.k0 != 0 && s.count != 0) {
                 table_add(t, s.k0, s.k1, s.count, &inserted);
@@ -417,12 +426,16 @@ cudaError_t tb_partition(const TableView& t, u32 n_parts, Slot* out, u64 cap, u6
     return cudaGetLastError();
 }
 
-cudaError_t tb_partition_fixed(const TableView& t, u32 n_parts, u64 cap, Slot* out, u64* dev_counts, int sm,
+cudaError_t tb_partition_fixed(const TableView& t, u32 n_parts, u64 cap, bool framed, Slot* out, u64* dev_counts, int sm,
                                cudaStream_t s, u64* launches) {
     cudaError_t e = cudaMemsetAsync(dev_counts, 0, sizeof(u64) * n_parts, s);   // the two flags stay sticky
     if (e != cudaSuccess) return e;
-    tb_partition_fixed_kernel<<<grid_for(t.mask + 1, sm), 256, 0, s>>>(t, n_parts, cap, out, dev_counts);
+    tb_partition_fixed_kernel<<<grid_for(t.mask + 1, sm), 256, 0, s>>>(t, n_parts, cap, framed ? 1u : 0u, out, dev_counts);
     *launches += 1;
+    if (framed) {
+        tb_region_headers_kernel<<<(n_parts + 127) / 128, 128, 0, s>>>(out, n_parts, cap, dev_counts);
+        *launches += 1;
+    }
     return cudaGetLastError();
 }
 

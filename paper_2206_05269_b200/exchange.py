@@ -64,8 +64,12 @@ class DeviceOps:
     def partition_fixed(self, counter, n_parts: int, entries, cap_per_part: int, counts) -> None:
         counter.partition_fixed(n_parts, entries.data_ptr(), cap_per_part, counts.data_ptr(), self.stream())
 
+    def partition_framed(self, counter, n_parts: int, entries, cap_per_part: int, counts) -> None:
+        counter.partition_framed(n_parts, entries.data_ptr(), cap_per_part, counts.data_ptr(), self.stream())
+
     def merge_regions(self, counter, entries, n_parts: int, cap_per_part: int, counts) -> None:
-        counter.merge_regions(entries.data_ptr(), n_parts, cap_per_part, counts.data_ptr(), self.stream())
+        counter.merge_regions(entries.data_ptr(), n_parts, cap_per_part, counts.data_ptr() if counts is not None else 0,
+                              self.stream())
 
     def empty_entries(self, n: int):
         t = self.torch
@@ -143,8 +147,9 @@ class ExchangeOverflow(RuntimeError):
 class AsyncExchange:
     """The same merge with NO host synchronisation per step, for pipelines that count and merge
     repeatedly (bench.py's N>1 step): partition p of the local table is scattered into a region of
-    fixed capacity, so both all-to-alls (region sizes, then the regions themselves) have
-    host-independent shapes and the receiving kernel reads the sizes on the device.  What the
+    fixed capacity whose first entry is a header with the number of entries that follow, so ONE
+    all-to-all of host-independent shape is the whole exchange and the receiving kernel reads the
+    sizes out of the regions (round 1 sent the sizes in an all-to-all of their own: pure latency).  What the
     fixed shapes cannot carry -- a region that overflows, tokens longer than 16 bytes (their
     variable-length record stream needs sizes on the host) -- raises sticky device flags that
     finish() reads ONCE, after any number of steps; the caller then falls back to
@@ -158,21 +163,19 @@ class AsyncExchange:
         self.world = dist.get_world_size(group)
         bound = local.max_entries()
         want = bound if entries_hint is None else min(bound, 2 * ((entries_hint + self.world - 1) // self.world) + 1024)
-        self.cap = max(int(want), 16)
+        self.cap = max(int(want), 16) + 1          # + the header entry of a region
         t = ops.torch
         self.send = ops.empty_entries(self.world * self.cap)
         self.recv = ops.empty_entries(self.world * self.cap)
         self.counts = t.zeros(self.world + 2, dtype=t.int64, device=self.send.device)
-        self.recv_counts = t.zeros(self.world, dtype=t.int64, device=self.send.device)
         self.steps = 0
 
     def step(self, local, owned) -> None:
         """Collective.  Asynchronous on the current stream: returns before anything has run."""
         ops, world = self.ops, self.world
-        ops.partition_fixed(local, world, self.send, self.cap, self.counts)
-        self.dist.all_to_all_single(self.recv_counts, self.counts[:world], group=self.group)
+        ops.partition_framed(local, world, self.send, self.cap, self.counts)
         self.dist.all_to_all_single(self.recv, self.send, group=self.group)
-        ops.merge_regions(owned, self.recv, world, self.cap, self.recv_counts)
+        ops.merge_regions(owned, self.recv, world, self.cap, None)
         self.steps += 1
 
     def finish(self) -> None:

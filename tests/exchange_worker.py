@@ -92,9 +92,28 @@ class OracleOps:
             else:
                 counts[n_parts + 1] += 1
 
+    def partition_framed(self, counter, n_parts, entries, cap, counts):
+        counts[:n_parts] = 0
+        for w, c in counter.table.items():
+            if len(w) > 16:
+                counts[n_parts] += 1
+                continue
+            p = capi.owner_of(w, n_parts)
+            j = int(counts[p])
+            counts[p] += 1
+            if j + 1 < cap:
+                entries[p * cap + 1 + j] = torch.tensor([*key_words(w), c, 0], dtype=torch.int64)
+            else:
+                counts[n_parts + 1] += 1
+        for p in range(n_parts):
+            entries[p * cap] = torch.tensor([0, 0, min(int(counts[p]), cap - 1), 0], dtype=torch.int64)
+
     def merge_regions(self, counter, entries, n_parts, cap, counts):
         for p in range(n_parts):
-            self.merge_entries(counter, entries[p * cap:(p + 1) * cap], min(int(counts[p]), cap))
+            if counts is None:
+                self.merge_entries(counter, entries[p * cap + 1:(p + 1) * cap], int(entries[p * cap][2]))
+            else:
+                self.merge_entries(counter, entries[p * cap:(p + 1) * cap], min(int(counts[p]), cap))
 
     def empty_entries(self, n):
         return torch.zeros((max(n, 1), 4), dtype=torch.int64)

@@ -92,7 +92,8 @@ def test_host_docs_marshals_pointers_and_lengths(capi):
 
 
 def test_async_exchange_region_capacity():
-    """the fixed region capacity: 2 x the uniform share of the hint (+ slack), never above what the table can hold"""
+    """the fixed region capacity: 2 x the uniform share of the hint (+ slack), never above what the table can hold,
+    plus the header entry that makes a region self-describing"""
     from paper_2206_05269_b200.exchange import AsyncExchange
 
     class Table:
@@ -115,8 +116,8 @@ def test_async_exchange_region_capacity():
         def __init__(self, w): self.w = w
         def get_world_size(self, group=None): return self.w
 
-    assert AsyncExchange(Table(), Ops(), Dist(8), entries_hint=50000).cap == 2 * 6250 + 1024
-    assert AsyncExchange(Table(), Ops(), Dist(2), entries_hint=50000).cap == 2 * 25000 + 1024
-    assert AsyncExchange(Table(), Ops(), Dist(4)).cap == 524288                     # no hint: cannot overflow
-    assert AsyncExchange(Table(), Ops(), Dist(1), entries_hint=10 ** 9).cap == 524288
-    assert AsyncExchange(Table(), Ops(), Dist(8), entries_hint=50000).send.rows == 8 * (2 * 6250 + 1024)
+    assert AsyncExchange(Table(), Ops(), Dist(8), entries_hint=50000).cap == 2 * 6250 + 1024 + 1
+    assert AsyncExchange(Table(), Ops(), Dist(2), entries_hint=50000).cap == 2 * 25000 + 1024 + 1
+    assert AsyncExchange(Table(), Ops(), Dist(4)).cap == 524288 + 1                 # no hint: cannot overflow
+    assert AsyncExchange(Table(), Ops(), Dist(1), entries_hint=10 ** 9).cap == 524288 + 1
+    assert AsyncExchange(Table(), Ops(), Dist(8), entries_hint=50000).send.rows == 8 * (2 * 6250 + 1024 + 1)

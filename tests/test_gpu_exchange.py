@@ -223,3 +223,30 @@ def test_wordcount_multi_rejects_bad_arguments(capi, cuda):
         capi.wordcount_multi([b"a b"], 0)
     shards, _ = capi.wordcount_multi([], 3)
     assert [s.to_dict() for s in shards] == [{}, {}, {}]
+
+
+@pytest.mark.parametrize("n_parts", [1, 2, 5])
+def test_framed_regions_describe_themselves(capi, cuda, port, n_parts):
+    """wfcu_counter_partition_framed: entry 0 of every region is its header; merge_regions with no counts array reads
+    it -- the union of the regions is the table, every entry sits in its owner's region, overflow raises the flag"""
+    text = capi.synth_corpus(seed=8, doc_begin=0, doc_end=1, vocab=50000, doc_bytes=1 << 18).tobytes() + b" " + b"x" * 30
+    dev, n = to_dev(cuda, text)
+    c = capi.Counter(table_slots=1 << 16)
+    c.count_dev(dev.data_ptr(), n)
+    want = {w: v for w, v in port.wordcount([text]).items() if len(w) <= 16}
+    cap = len(want) + 2
+    entries = cuda.zeros((n_parts * cap, 4), dtype=cuda.int64, device="cuda")
+    counts = cuda.zeros(n_parts + 2, dtype=cuda.int64, device="cuda")
+    c.partition_framed(n_parts, entries.data_ptr(), cap, counts.data_ptr())
+    host = entries.cpu().numpy().reshape(n_parts, cap, 4)
+    assert counts[n_parts].item() == 1 and counts[n_parts + 1].item() == 0          # one long token, no overflow
+    assert [int(host[p, 0, 2]) for p in range(n_parts)] == counts[:n_parts].tolist()
+    assert all(int(host[p, 0, 0]) == 0 and int(host[p, 0, 1]) == 0 for p in range(n_parts))
+    merged = capi.Counter(table_slots=1 << 16)
+    merged.merge_regions(entries.data_ptr(), n_parts, cap, 0)
+    assert merged.to_dict() == want
+    # a capacity of 3 entries per region overflows: the sticky flag counts what did not fit
+    small = cuda.zeros((n_parts * 4, 4), dtype=cuda.int64, device="cuda")
+    c.partition_framed(n_parts, small.data_ptr(), 4, counts.data_ptr())
+    assert counts[n_parts + 1].item() == len(want) - sum(min(int(v), 3) for v in counts[:n_parts].tolist())
+    assert [int(v) for v in small.cpu().numpy().reshape(n_parts, 4, 4)[:, 0, 2]] == [min(int(v), 3) for v in counts[:n_parts].tolist()]
