@@ -61,17 +61,32 @@ constexpr int kMissCap = 64;
 // typographic apostrophes and quotes, dashes, ellipsis ...): valid, never word characters, never
 // whitespace, so their three bytes behave like ASCII punctuation (kept inside a token, trimmed at
 // its edges) and need not defer the fragment.
-struct HiMasks { u32 s7, a7, h7, c7, l7, x7, e7, z7, k7; };   // whitespace, ASCII alnum, >= 0x80, continuation, lead C3..DF,
-                                                              // x / division sign, == E2, == 80, third byte of the punctuation above
-__device__ __forceinline__ HiMasks classify16_hi(const uint4& x, u32 prev_c3, uint4& f) {
+//
+// Round 2: three-byte LETTERS too.  A sequence  lead second third  with lead in E0, E1, E3..EE (E2 and EF hold the
+// punctuation, whitespace and specials the reference's is_word_char / is_unicode_space single out,
+// proj/src/unicode.cpp:90-115) is a word character that nothing folds, provided it is strict UTF-8 (E0 needs a second
+// byte >= A0, ED one <= 9F) and is not one of the two pinned exceptions inside those leads: E1 9A xx (U+1680 OGHAM
+// SPACE MARK is whitespace; its whole 64-code-point block is left to the slow path) and E3 80 xx (U+3000..U+303F).
+// Devanagari, Hangul, Georgian, Vietnamese tone letters (E1 BA/BB xx), kana, ideographs ...: their fragments used to
+// go to the one-thread-per-fragment slow kernel.  l3 flags those leads, b2 the continuation bytes that may NOT follow
+// the lead in front of them; the pairing is done on the gathered masks like the rest.
+struct HiMasks { u32 s7, a7, h7, c7, l7, x7, e7, z7, k7, l3, b2; };   // whitespace, ASCII alnum, >= 0x80, continuation, lead C3..DF,
+                                                                      // x / division sign, == E2, == 80, third byte of the punctuation
+                                                                      // above, three-byte letter lead, bad second byte
+// prev_byte: the byte in front of the chunk (0 if unknown / none).  U3 = false: the three-byte-letter flags are not
+// computed (rows without such a lead: accented Latin, Greek, Cyrillic, typographic punctuation keep their round-1 cost).
+template <bool U3>
+__device__ __forceinline__ HiMasks classify16_hi(const uint4& x, u32 prev_byte, uint4& f) {
     const u32 M = 0x80808080u;
     const u32 xs[4] = {x.x, x.y, x.z, x.w};
     u32 fs[4];
-    u32 acc[9][2];        // 128 * (8-bit mask) of words {0,1} and {2,3}, per class
-    u32 c3_prev = prev_c3;
+    u32 acc[11][2];       // 128 * (8-bit mask) of words {0,1} and {2,3}, per class
+    u32 c3_prev = prev_byte == 0xC3u ? 0x80000000u : 0u;
+    u32 e0_prev = prev_byte == 0xE0u ? 0x80000000u : 0u, ed_prev = prev_byte == 0xEDu ? 0x80000000u : 0u;
+    u32 e1_prev = prev_byte == 0xE1u ? 0x80000000u : 0u, e3_prev = prev_byte == 0xE3u ? 0x80000000u : 0u;
 #pragma unroll
     for (int pair = 0; pair < 2; ++pair) {       // two words at a time keeps the live flag words few
-        u32 fl[9][2];
+        u32 fl[11][2];
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
             const int w = 2 * pair + k;
@@ -95,9 +110,20 @@ __device__ __forceinline__ HiMasks classify16_hi(const uint4& x, u32 prev_c3, ui
             fl[6][k] = xw & ~((v ^ 0x62626262u) + 0x7F7F7F7Fu) & M;                   // == 0xE2
             fl[7][k] = xw & ~(v + 0x7F7F7F7Fu) & M;                                   // == 0x80
             fl[8][k] = co & (((v + 0x70707070u) & ~(v + 0x58585858u)) | (v + 0x50505050u));   // 90..A7 or B0..BF
+            fl[9][k] = 0;
+            fl[10][k] = 0;
+            if (!U3) continue;
+            fl[9][k] = xw & (v + 0x20202020u) & ~(v + 0x11111111u) & ~fl[6][k] & M;           // E0..EE without E2
+            const u32 e0 = xw & ~((v ^ 0x60606060u) + 0x7F7F7F7Fu) & M, ed = xw & ~((v ^ 0x6D6D6D6Du) + 0x7F7F7F7Fu) & M;
+            const u32 e1 = xw & ~((v ^ 0x61616161u) + 0x7F7F7F7Fu) & M, e3 = xw & ~((v ^ 0x63636363u) + 0x7F7F7F7Fu) & M;
+            const u32 ge_a0 = v + 0x60606060u;                                                 // bit 7: byte >= A0 (continuation bytes)
+            fl[10][k] = co & ((__funnelshift_l(e0_prev, e0, 8) & ~ge_a0) | (__funnelshift_l(ed_prev, ed, 8) & ge_a0) |
+                              (__funnelshift_l(e1_prev, e1, 8) & ~((v ^ 0x1A1A1A1Au) + 0x7F7F7F7Fu)) |
+                              (__funnelshift_l(e3_prev, e3, 8) & fl[7][k]));
+            e0_prev = e0; ed_prev = ed; e1_prev = e1; e3_prev = e3;
         }
 #pragma unroll
-        for (int c = 0; c < 9; ++c) acc[c][pair] = gather8(fl[c][0], fl[c][1], 0);
+        for (int c = 0; c < 11; ++c) acc[c][pair] = (c < 9 || U3) ? gather8(fl[c][0], fl[c][1], 0) : 0u;
     }
     f = make_uint4(fs[0], fs[1], fs[2], fs[3]);
     HiMasks m;
@@ -110,6 +136,8 @@ __device__ __forceinline__ HiMasks classify16_hi(const uint4& x, u32 prev_c3, ui
     m.e7 = acc[6][1] * 256u + acc[6][0];
     m.z7 = acc[7][1] * 256u + acc[7][0];
     m.k7 = acc[8][1] * 256u + acc[8][0];
+    m.l3 = acc[9][1] * 256u + acc[9][0];
+    m.b2 = acc[10][1] * 256u + acc[10][0];
     return m;
 }
 // Pairs leads with continuation bytes on packed masks (low 16 bits = half a, high = half b).
@@ -122,10 +150,17 @@ __device__ __forceinline__ HiMasks classify16_hi(const uint4& x, u32 prev_c3, ui
 // chunk in front when the unmatched lead is there).  A chunk cannot know whether an E2 (80) at its
 // end will be completed, so it flags them; clear_before tells the caller which of the last two
 // bytes of the chunk in front the sequences completed HERE clear again.
-struct HiIn { u32 Hi, C, L, X, E2, Z, K; };
-__device__ __forceinline__ u32 hi_tails(u32 E2, u32 Z) { return ((E2 >> 14) & 0x00030003u) | ((Z >> 13) & 0x00040004u); }
+struct HiIn { u32 Hi, C, L, X, E2, Z, K, L3, B2; };
+// per half: bits 0,1 = the second-last / last byte is E2, bit 2 = the last byte is 80, bit 3 = the last byte is a
+// three-byte letter lead, bit 4 = the second-last byte is one and the last byte may follow it
+__device__ __forceinline__ u32 hi_tails(const HiIn& in) {
+    return ((in.E2 >> 14) & 0x00030003u) | ((in.Z >> 13) & 0x00040004u) | ((in.L3 >> 12) & 0x00080008u) |
+           ((in.L3 >> 10) & (in.C >> 11) & ~(in.B2 >> 11) & 0x00100010u);
+}
+// alnum_before: the bytes among them that are word characters (the first bytes of a three-byte letter completed here).
+template <bool U3>
 __device__ __forceinline__ void hi_masks_finish(const HiIn& in, u32 lead_before, u32 tails_before, u32& A, u32& H,
-                                                u32& bad_first, u32& clear_before) {
+                                                u32& bad_first, u32& clear_before, u32& alnum_before) {
     const u32 Lsh = ((in.L << 1) & 0xFFFEFFFEu) | (lead_before & 0x00010001u);  // the byte in front is a lead
     const u32 validC = in.C & Lsh;
     const u32 badnext = Lsh & ~in.C;                                              // successor of an unmatched lead
@@ -134,9 +169,22 @@ __device__ __forceinline__ void hi_masks_finish(const HiIn& in, u32 lead_before,
     const u32 Esh = ((in.E2 << 2) & 0xFFFCFFFCu) | (tails_before & 0x00030003u);          // the byte two in front is E2
     const u32 T3 = in.K & Zsh & Esh;                                              // third byte of a punctuation sequence
     const u32 P3 = T3 | ((T3 >> 1) & 0x7FFF7FFFu) | ((T3 >> 2) & 0x3FFF3FFFu);    // its bytes inside the chunk
-    clear_before = ((T3 & 0x00010001u) << 15) | ((T3 & 0x00010001u) << 14) | ((T3 & 0x00020002u) << 14);
-    H = (in.Hi & ~(validC | in.L | P3)) | in.X | badnext | ((badnext >> 1) & 0x7FFF7FFFu);
-    A |= (validC | in.L) & ~H;
+    // three-byte letters: second = continuation after a lead that admits it, third = continuation after a second.
+    // Only sequences COMPLETED here are cleared (those that began in the chunk in front through clear_before): a
+    // lead or lead + second at the end of a chunk stays flagged until the next chunk sees the rest.
+    u32 thr = 0;
+    if (U3) {
+        const u32 L3sh = ((in.L3 << 1) & 0xFFFEFFFEu) | ((tails_before >> 3) & 0x00010001u);
+        const u32 sec = in.C & L3sh & ~in.B2;
+        const u32 secsh = ((sec << 1) & 0xFFFEFFFEu) | ((tails_before >> 4) & 0x00010001u);
+        thr = in.C & secsh;
+    }
+    const u32 G3 = thr | ((thr >> 1) & 0x7FFF7FFFu) | ((thr >> 2) & 0x3FFF3FFFu);
+    const u32 done = T3 | thr;                                                    // third bytes of either kind
+    clear_before = ((done & 0x00010001u) << 15) | ((done & 0x00010001u) << 14) | ((done & 0x00020002u) << 14);
+    alnum_before = ((thr & 0x00010001u) << 15) | ((thr & 0x00010001u) << 14) | ((thr & 0x00020002u) << 14);
+    H = (in.Hi & ~(validC | in.L | P3 | G3)) | in.X | badnext | ((badnext >> 1) & 0x7FFF7FFFu);
+    A |= (validC | in.L | G3) & ~H;
 }
 
 template <int WARPS, int SETS, int MSLOTS>
@@ -166,7 +214,8 @@ using namespace cnt3;
 // CTA picks its variant from a sample of its own part of the text (wc_count_kernel below): the
 // choice affects speed only.
 template <int WARPS, int SETS, int MSLOTS, bool HI>
-__device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, u32 one, const TableView& gt) {
+__device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, u32 one, bool u3_cta,
+                                              const TableView& gt) {
     extern __shared__ uint8_t smem_raw[];
     typedef Smem<WARPS, SETS, MSLOTS> SM;
     const u32 sbase = (u32)__cvta_generic_to_shared(smem_raw);
@@ -419,7 +468,7 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
 
         // masks of the chunk in front of the strip (16 bits): "position -1" is whitespace
         u32 carryS = 0xFFFFu, carryA = 0, carryH = 0;
-        u32 carryL = 0, carryC3 = 0;   // HI: lead mask of that chunk; 0x80000000 if it ends in 0xC3
+        u32 carryL = 0, carryC3 = 0;   // HI: lead mask of that chunk; its last byte
         u32 carryT = 0;                // HI: hi_tails of that chunk (E2 / 80 in its last two bytes)
         bool general_prev = false;
         if (r_begin > 0) {
@@ -428,13 +477,13 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
             uint4 f;
             if constexpr (HI) {
                 // what lies in front of THEM is unknown: a leading continuation byte is flagged (conservative)
-                const HiMasks m = classify16_hi(x, 0u, f);
-                u32 A = m.a7 >> 7, H, bad_first, clear_before;
-                const HiIn in{m.h7 >> 7, m.c7 >> 7, m.l7 >> 7, m.x7 >> 7, m.e7 >> 7, m.z7 >> 7, m.k7 >> 7};
-                hi_masks_finish(in, 0u, 0u, A, H, bad_first, clear_before);
+                const HiMasks m = classify16_hi<true>(x, 0u, f);
+                u32 A = m.a7 >> 7, H, bad_first, clear_before, alnum_before;
+                const HiIn in{m.h7 >> 7, m.c7 >> 7, m.l7 >> 7, m.x7 >> 7, m.e7 >> 7, m.z7 >> 7, m.k7 >> 7, m.l3 >> 7, m.b2 >> 7};
+                hi_masks_finish<true>(in, 0u, 0u, A, H, bad_first, clear_before, alnum_before);
                 carryS = m.s7 >> 7; carryA = A & 0xFFFFu; carryH = H & 0xFFFFu; carryL = (m.l7 >> 7) & 0xFFFFu;
-                carryT = hi_tails(in.E2, in.Z) & 0xFFFFu;
-                carryC3 = (x.w >> 24) == 0xC3u ? 0x80000000u : 0u;
+                carryT = hi_tails(in) & 0xFFFFu;
+                carryC3 = x.w >> 24;
             } else {
                 const Masks m = classify16<false>(x, one, f);
                 carryS = m.s7 >> 7; carryA = m.a7 >> 7; carryH = m.h7 >> 7;
@@ -453,7 +502,7 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
             uint4 fa, fb;
             const u32 anyhi = (xa.x | xa.y | xa.z | xa.w | xb.x | xb.y | xb.z | xb.w) & 0x80808080u;
             const bool ascii_row = !__any_sync(kFull, anyhi != 0) && (carryH | carryL) == 0;
-            u32 pH_fix = 0, pH_clear = 0;
+            u32 pH_fix = 0, pH_clear = 0, pA_set = 0, H_open = 0;
             if (ascii_row) {
                 const Masks ma = classify16<true>(xa, one, fa), mb = classify16<true>(xb, one, fb);
                 S = pack7(ma.s7, mb.s7);
@@ -462,14 +511,21 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
             } else if constexpr (HI) {
                 // is the byte in front of each chunk 0xC3 (chunk a: lane-1's a, lane 0: the previous row's
                 // last chunk; chunk b: lane-1's b, lane 0: this row's a of lane 31)
-                const u32 last_c3 = ((xa.w >> 24) == 0xC3u ? 1u : 0u) | ((xb.w >> 24) == 0xC3u ? 2u : 0u);
-                const u32 l31 = __shfl_sync(kFull, last_c3, 31);
-                u32 pc3 = __shfl_up_sync(kFull, last_c3, 1);
-                if (lane == 0) pc3 = (carryC3 ? 1u : 0u) | ((l31 & 1u) << 1);
-                carryC3 = (l31 & 2u) ? 0x80000000u : 0u;
-                const HiMasks ma = classify16_hi(xa, (pc3 & 1u) ? 0x80000000u : 0u, fa);
+                // (the last byte of the chunk in front decides what its successor may be: C3 folds, E0 / ED / E1 / E3
+                // restrict the second byte of a three-byte letter)
+                const u32 last_bytes = (xa.w >> 24) | ((xb.w >> 24) << 8);
+                const u32 l31 = __shfl_sync(kFull, last_bytes, 31);
+                u32 pc3 = __shfl_up_sync(kFull, last_bytes, 1);
+                if (lane == 0) pc3 = (carryC3 & 0xFFu) | ((l31 & 0xFFu) << 8);
+                carryC3 = l31 >> 8;
+                // the CTA's sample saw three-byte letter leads (or one is open in front of the row) -> the flags for them
+                const bool u3_row = u3_cta || (carryT & 0x18u) != 0;
+                u32 tails = 0;
+                auto classify_row = [&](auto u3_) {
+                    constexpr bool U3 = decltype(u3_)::value;
+                const HiMasks ma = classify16_hi<U3>(xa, pc3 & 0xFFu, fa);
                 asm volatile("" ::: "memory");     // one chunk after the other: fewer live flag words
-                const HiMasks mb = classify16_hi(xb, (pc3 & 2u) ? 0x80000000u : 0u, fb);
+                const HiMasks mb = classify16_hi<U3>(xb, pc3 >> 8, fb);
                 S = pack7(ma.s7, mb.s7);
                 A = pack7(ma.a7, mb.a7);
                 const u32 L = pack7(ma.l7, mb.l7);
@@ -479,16 +535,26 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
                 if (lane == 0) pL = __byte_perm(carryL, L31, 0x5410);
                 carryL = L31 >> 16;
                 const HiIn in{pack7(ma.h7, mb.h7), pack7(ma.c7, mb.c7), L, pack7(ma.x7, mb.x7),
-                              pack7(ma.e7, mb.e7), pack7(ma.z7, mb.z7), pack7(ma.k7, mb.k7)};
-                // E2 / 80 in the last two bytes of the chunk in front
-                const u32 tails = hi_tails(in.E2, in.Z);
+                              pack7(ma.e7, mb.e7), pack7(ma.z7, mb.z7), pack7(ma.k7, mb.k7), pack7(ma.l3, mb.l3), pack7(ma.b2, mb.b2)};
+                // E2 / 80 / an open three-byte letter in the last two bytes of the chunk in front
+                tails = hi_tails(in);
                 const u32 t31 = __shfl_sync(kFull, tails, 31);
                 u32 pT = __shfl_up_sync(kFull, tails, 1);
                 if (lane == 0) pT = __byte_perm(carryT, t31, 0x5410);
                 carryT = t31 >> 16;
                 u32 bad_first;
-                hi_masks_finish(in, pL >> 15, pT, A, H, bad_first, pH_clear);
+                hi_masks_finish<U3>(in, pL >> 15, pT, A, H, bad_first, pH_clear, pA_set);
                 pH_fix = bad_first << 15;     // an unmatched lead at the end of the chunk in front
+                // Sequences left open at the end of a chunk stay flagged in H until the chunk behind completes them:
+                // what THAT chunk cleared (lane + 1 for both halves; for lane 31's first half, lane 0's second) must
+                // not send this row to the careful loop, nor must the open tail of the row's very last chunk -- no
+                // fragment that ends in this row can hold it, and the next row sees it through carryH.
+                };
+                if (u3_row) classify_row(std::true_type{}); else classify_row(std::false_type{});
+                const u32 nclr = __shfl_down_sync(kFull, pH_clear, 1), clr0 = __shfl_sync(kFull, pH_clear, 0);
+                const u32 tb = tails >> 16;                     // what the row's last chunk leaves open (lane 31)
+                const u32 open_end = ((tb & 0x10u) || ((tb & 0x1u) && (tb & 0x4u))) ? 0xC0000000u : ((tb & 0xAu) ? 0x80000000u : 0u);
+                H_open = lane == 31 ? ((clr0 >> 16) | open_end) : nclr;
             } else {
                 const Masks ma = classify16<false>(xa, one, fa), mb = classify16<false>(xb, one, fb);
                 S = pack7(ma.s7, mb.s7);
@@ -516,6 +582,7 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
                 pH = __shfl_up_sync(kFull, H, 1);
                 if (lane == 0) pH = carryH | (h31 << 16);
                 pH = (pH & ~pH_clear) | pH_fix;
+                pA |= pA_set;
                 carryH = h31 >> 16;
             }
             // fragment ends: whitespace byte whose predecessor is not whitespace
@@ -531,7 +598,7 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
             // A fragment that ends in the chunk but has no whitespace in the 16 bytes in front
             // of the chunk may start out of sight: the careful loop decides end by end.
             // (HI: rows whose bytes >= 0x80 are all two-byte letters stay on the bit-parallel emission)
-            bool careful = (HI ? __any_sync(kFull, (H | pH) != 0) : !ascii_row) ||
+            bool careful = (HI ? __any_sync(kFull, ((H & ~H_open) | pH) != 0) : !ascii_row) ||
                            __any_sync(kFull, (Ta != 0 && prev_a == 0) || (Tb != 0 && prev_b == 0));
             bool general_row = true;
             u32 total;
@@ -680,9 +747,11 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
 template <int WARPS, int SETS, int MSLOTS, bool HI>
 __global__ void __launch_bounds__(WARPS * 32, 1)
 wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, int force, u32 one, TableView gt) {
-    const bool hi = variant_is_hi(text, n, (u64)blockIdx.x * WARPS * rows_per_warp * kRow, (u64)WARPS * rows_per_warp * kRow, force);
+    bool u3 = false;
+    const bool hi = variant_is_hi(text, n, (u64)blockIdx.x * WARPS * rows_per_warp * kRow, (u64)WARPS * rows_per_warp * kRow, force,
+                                  HI ? &u3 : nullptr);
     if (hi != HI) return;
-    wc_count_body<WARPS, SETS, MSLOTS, HI>(text, n, rows_per_warp, one, gt);
+    wc_count_body<WARPS, SETS, MSLOTS, HI>(text, n, rows_per_warp, one, u3, gt);
 }
 
 // ---- host-side launcher (called from wordcount.cu) ---------------------------------
@@ -720,7 +789,7 @@ cudaError_t wc_count_launch(const uint8_t* text, u64 n, const TableView& gt, int
     const u64 rows_per_warp = (n_rows + grid * kCountWarps - 1) / (grid * kCountWarps);
     static const int force = [] { const char* v = getenv("WFCU_COUNT_VARIANT"); return v ? atoi(v) : -1; }();   // tests: 0 / 1
     static const bool gen4_ascii = [] { const char* v = getenv("WFCU_COUNT_KERNEL"); return v && v[0] == '4'; }();
-    if (force != 1) {
+    if (force != 1 && force != 2) {
         if (!gen4_ascii) {
             k_ascii<<<(unsigned)grid, kCountWarps * 32, smem, stream>>>(text, n, (u32)rows_per_warp, force, 1u, gt);
         } else {
@@ -729,7 +798,7 @@ cudaError_t wc_count_launch(const uint8_t* text, u64 n, const TableView& gt, int
         }
     }
     if (force != 0) k_hi<<<(unsigned)grid, kCountWarps * 32, smem, stream>>>(text, n, (u32)rows_per_warp, force, 1u, gt);
-    *launches += (force == 0 || force == 1) ? 1 : 2;
+    *launches += (force == 0 || force == 1 || force == 2) ? 1 : 2;
     return cudaGetLastError();
 }
 

@@ -133,15 +133,29 @@ __device__ __forceinline__ bool medium_add(u64* __restrict__ k0s, u64* __restric
 #define WFCU_COUNT_WARPS 28
 #endif
 constexpr int kCountVariantWarps = WFCU_COUNT_WARPS;
-__device__ __forceinline__ bool variant_is_hi(const uint8_t* __restrict__ text, u64 n, u64 first, u64 span, int force) {
+// *u3 (may be null): the HI variant should also keep three-byte letters on the fast path (two or more sampled chunks
+// hold a lead E0, E1, E3..EE); force = 2 asks for HI with that for every CTA.
+__device__ __forceinline__ bool variant_is_hi(const uint8_t* __restrict__ text, u64 n, u64 first, u64 span, int force,
+                                              bool* u3 = nullptr) {
     if (force == 0) return false;
-    if (force == 1) return true;
     const u64 at = (first + (u64)((unsigned __int128)threadIdx.x * span / (kCountVariantWarps * 32))) & ~15ull;
-    bool hit = false;
+    bool hit = false, hit3 = false;
     if (at + 16 <= n) {
-        const uint4 v = *reinterpret_cast<const uint4*>(text + at);
-        hit = ((v.x | v.y | v.z | v.w) & 0x80808080u) != 0;
+        const uint4 q = *reinterpret_cast<const uint4*>(text + at);
+        hit = ((q.x | q.y | q.z | q.w) & 0x80808080u) != 0;
+        if (hit && u3) {
+            const u32 w4[4] = {q.x, q.y, q.z, q.w};
+            u32 any = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const u32 xw = w4[k], v = xw & 0x7F7F7F7Fu;
+                any |= xw & (v + 0x20202020u) & ~(v + 0x11111111u) & ((v ^ 0x62626262u) + 0x7F7F7F7Fu);   // E0..EE, not E2
+            }
+            hit3 = (any & 0x80808080u) != 0;
+        }
     }
+    if (u3) *u3 = force == 2 || __syncthreads_count(hit3) >= 2;
+    if (force == 1 || force == 2) return true;
     return __syncthreads_count(hit) >= 2;
 }
 

@@ -5,7 +5,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np, torch
 from helpers import random_text
-from test_gpu_count_kernel import latin_text
+from test_gpu_count_kernel import latin_text, three_byte_text
 from paper_2206_05269_b200 import capi
 import oracle
 
@@ -16,13 +16,14 @@ port = oracle.port()
 t0 = time.time(); cases = 0; total = 0
 synth = capi.synth_corpus(7, 0, 2, 50000).tobytes()
 while time.time() - t0 < seconds:
-    kind = rng.choice(["ascii", "unicode", "long", "latin", "synth", "mix", "dense"])
+    kind = rng.choice(["ascii", "unicode", "long", "latin", "three", "three", "synth", "mix", "dense"])
     n = rng.choice([rng.randint(0, 64), rng.randint(0, 3000), rng.randint(0, 70000), rng.randint(0, 400000)])
     if kind == "latin": text = latin_text(rng, n)
+    elif kind == "three": text = three_byte_text(rng, n)
     elif kind == "synth":
         o = rng.randint(0, len(synth) - n - 1); text = synth[o:o + n]
     elif kind == "mix":
-        text = b" ".join(rng.choice([random_text, lambda r, k, f: latin_text(r, k)])(rng, rng.randint(0, max(1, n // 4)), rng.choice(["ascii", "unicode", "long"])) for _ in range(4))
+        text = b" ".join(rng.choice([random_text, lambda r, k, f: latin_text(r, k), lambda r, k, f: three_byte_text(r, k)])(rng, rng.randint(0, max(1, n // 4)), rng.choice(["ascii", "unicode", "long"])) for _ in range(4))
     elif kind == "dense":
         text = b" ".join(bytes([rng.choice(b"abcXYZ019")]) * rng.randint(1, 3) for _ in range(n // 3))
     else: text = random_text(rng, n, kind)

@@ -181,3 +181,49 @@ def test_three_byte_punctuation_across_boundaries(capi, cuda, port, shift):
         text = b"q" * shift + b" " + body + tail
         check(capi, cuda, port, text)
         check(capi, cuda, port, text[:len(text) - 1])
+
+
+# ---- three-byte letters on the fast path (round 2) -------------------------------------------------
+THREE = ["한", "국", "어", "는", "हि", "न्", "दी", "あ", "カ", "漢", "字", "ế", "ộ", "ữ", "ქ", "ა", "ἀ", "ᚠ",           # letters (ᚠ: E1 9A A0, its block defers)
+         "　", "、", "。", " ", "‐", "’", "…", "！", "ａ", "�", "ࠀ", "퟿", "", "￿", " ", "𐍈"]   # E3 80 xx, E2 xx xx, EF xx xx, edges of the ranges
+
+
+def three_byte_text(rng, n):
+    """dense in three-byte characters: words of ASCII letters and THREE characters with edge punctuation, plus the
+    invalid neighbours of every rule: overlong E0 80..9F xx, surrogates ED A0..BF xx, truncated sequences at random
+    distances from whitespace and from the 16-byte chunk boundaries, stray continuation bytes, two-byte letters"""
+    out = bytearray()
+    while len(out) < n:
+        r = rng.random()
+        if r < 0.16:
+            out += rng.choice([b" ", b"\n", b"  ", b"\t"])
+        elif r < 0.22:
+            out += bytes([rng.choice(b".,;!?-'\"()")])
+        elif r < 0.55:
+            out += rng.choice(THREE).encode()
+        elif r < 0.60:
+            out += rng.choice([b"\xe0\x80\x80", b"\xe0\x9f\xbf", b"\xe0\xa0\x80", b"\xed\xa0\x80", b"\xed\x9f\xbf", b"\xed\xbf\xbf",
+                               b"\xe1\x9a\x80", b"\xe1\x9a", b"\xe1", b"\xe3\x80", b"\xe3\x81", b"\xea\xb0", b"\xea", b"\x80", b"\xbf",
+                               b"\xe4\xb8", b"\xe4\xb8\x80\x80", b"\xee\x80\x80", b"\xef\xbb\xbf", b"\xf0\x90\x8d\x88", b"\xc3\xa9", b"\xc3"])
+        else:
+            out += bytes([rng.choice(b"abcdefghijklmnopqrstuvwxyzABCDEFGHIJKLMNOPQRSTUVWXYZ0123456789")])
+    return bytes(out[:n])
+
+
+@pytest.mark.parametrize("size", [1, 2, 3, 15, 16, 17, 18, 31, 33, 511, 513, 1023, 1024, 1025, 1026, 2049, 30011, 400003])
+def test_three_byte_letters_match_oracle(capi, cuda, port, size):
+    rng = random.Random(size * 13 + 5)
+    for rep in range(4):
+        check(capi, cuda, port, three_byte_text(rng, size))
+        check(capi, cuda, port, bytes(rng.choice(b"q \n") for _ in range(rng.randint(0, 40))) + three_byte_text(rng, size))
+
+
+def test_three_byte_words_stay_on_the_fast_path(capi, cuda, port):
+    """Korean / Hindi / Vietnamese / Georgian words (at most 16 bytes) are counted by the counting kernel itself: the
+    deferred list stays (almost) empty, so the slow kernel has nothing to do"""
+    unit = ("한국어 는 말 हिन्दी भाषा tiếng Việt ngữ ქართული ენა カタカナ 漢字 한국어. (हिन्दी) —Việt— ").encode()
+    text = unit * 400
+    got, _ = gpu_wordcount(capi, cuda, [text])
+    want = port.wordcount([text])
+    assert got == want
+    assert got["한국어".encode()] == 800 and got["việt".encode()] == 800 and got["हिन्दी".encode()] == 800
