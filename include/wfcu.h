@@ -44,6 +44,10 @@ extern "C" {
 #define WFCU_ERR_ARENA_FULL (-6)       /* long-token arena / long table over capacity            */
 #define WFCU_ERR_BUFFER_TOO_SMALL (-7) /* caller-provided output buffer too small                */
 #define WFCU_ERR_NOT_SORTED (-8)       /* reduce_sorted on an unsorted list (std::invalid_argument) */
+#define WFCU_ERR_FRAME_MAGIC (-9)      /* WCX1 frame: WireError::Kind::BadMagic (proj/include/wfc/wire.hpp:26-31) */
+#define WFCU_ERR_FRAME_TRUNCATED (-10) /*             WireError::Kind::Truncated                                   */
+#define WFCU_ERR_FRAME_TRAILING (-11)  /*             WireError::Kind::TrailingBytes                               */
+#define WFCU_ERR_FRAME_ENCODING (-12)  /*             WireError::Kind::BadEncoding                                 */
 
 /* MapKind, proj/include/wfc/engine.hpp:12-16; the first three values are the
  * reference's, `square` is appended for BASELINE.json config 2 (f(x)=x^2). */
@@ -294,6 +298,17 @@ WFCU_API int wfcu_tokens_from_words(const uint8_t* bytes, const uint32_t* lens, 
  * that order.  Device-to-device copies (peer copies between GPUs); no frame, no host string. */
 WFCU_API int wfcu_tokens_concat_slices(const wfcu_tokens* const* src, const uint64_t* begin, const uint64_t* end,
                                        uint32_t n_src, wfcu_tokens** out);
+/* WCX1 frames in device memory (the paper's exchange with an NCCL-backed transport).
+ * encode_message (proj/src/wire.cpp:27-48) of the slice [begin, end) of a device token list: "WCX1", u32-LE word
+ * count, u32-LE length of every word, the payloads.  dev_frame == NULL: only *frame_bytes.  The frame never exists in
+ * host memory; dev_frame must be 4-byte aligned. */
+WFCU_API int wfcu_tokens_encode_frame(const wfcu_tokens* t, uint64_t begin, uint64_t end, uint8_t* dev_frame,
+                                      uint64_t frame_cap, uint64_t* frame_bytes, void* stream);
+/* decode_message (proj/src/wire.cpp:50-87) of a frame in device memory into a device token list: the reference's
+ * checks in its order -- WFCU_ERR_FRAME_MAGIC / _TRUNCATED / _TRAILING / _ENCODING map WireError::Kind one to one
+ * (the UTF-8 check is one device pass over the payload).  A frame with an empty word is not a token list
+ * (WFCU_ERR_INVALID_ARGUMENT). */
+WFCU_API int wfcu_tokens_decode_frame(const uint8_t* dev_frame, uint64_t frame_bytes, wfcu_tokens** out, void* stream);
 /* sort_words (proj/src/text.cpp:59-63): stable byte-wise sort, in place. */
 WFCU_API int wfcu_tokens_sort(wfcu_tokens* t, void* stream);
 /* reduce_sorted (proj/src/reduce.cpp:8-21): run-length encodes a sorted list

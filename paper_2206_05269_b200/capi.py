@@ -23,6 +23,7 @@ ERR_DEFERRED_FULL = -5
 ERR_ARENA_FULL = -6
 ERR_BUFFER_TOO_SMALL = -7
 ERR_NOT_SORTED = -8
+ERR_FRAME_MAGIC, ERR_FRAME_TRUNCATED, ERR_FRAME_TRAILING, ERR_FRAME_ENCODING = -9, -10, -11, -12
 
 MAP_IDENTITY, MAP_SQUARE_ROOT, MAP_ALTERNATING_HARMONIC_TERM, MAP_SQUARE = 0, 1, 2, 3
 DTYPE_F32, DTYPE_F64 = 0, 1
@@ -83,6 +84,8 @@ SIGNATURES = {
     "wfcu_timer_stop_ns": (C.c_int, [C.c_void_p, u64p]),
     "wfcu_timer_destroy": (None, [C.c_void_p]),
     "wfcu_wordcount_multi": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "wfcu_tokens_encode_frame": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint64, u64p, C.c_void_p]),
+    "wfcu_tokens_decode_frame": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p), C.c_void_p]),
     "wfcu_tokens_concat_slices": (C.c_int, [C.c_void_p, u64p, u64p, C.c_uint32, C.POINTER(C.c_void_p)]),
     "wfcu_counter_distinctive": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64,
                                            C.c_void_p, C.c_void_p, C.c_uint64, u64p]),
@@ -466,6 +469,25 @@ class Tokens:
         e = (C.c_uint64 * max(n, 1))(*ends)
         h = C.c_void_p()
         check(lib.wfcu_tokens_concat_slices(hs, b, e, n, C.byref(h)))
+        return cls(h)
+
+    def frame_bytes(self, begin: int, end: int, stream: int = 0) -> int:
+        """size of the WCX1 frame of tokens [begin, end)"""
+        n = C.c_uint64()
+        check(lib.wfcu_tokens_encode_frame(self._h, begin, end, None, 0, C.byref(n), C.c_void_p(stream)))
+        return n.value
+
+    def encode_frame(self, begin: int, end: int, out_ptr: int, out_cap: int, stream: int = 0) -> int:
+        """WCX1 frame of tokens [begin, end) into device memory at out_ptr; returns its size"""
+        n = C.c_uint64()
+        check(lib.wfcu_tokens_encode_frame(self._h, begin, end, C.c_void_p(out_ptr), out_cap, C.byref(n), C.c_void_p(stream)))
+        return n.value
+
+    @classmethod
+    def decode_frame(cls, frame_ptr: int, frame_bytes: int, stream: int = 0) -> "Tokens":
+        """decode_message of a WCX1 frame in device memory (WfcuError with ERR_FRAME_* codes on a bad frame)"""
+        h = C.c_void_p()
+        check(lib.wfcu_tokens_decode_frame(C.c_void_p(frame_ptr), frame_bytes, C.byref(h), C.c_void_p(stream)))
         return cls(h)
 
     def close(self) -> None:

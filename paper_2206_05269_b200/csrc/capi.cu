@@ -82,6 +82,15 @@ cudaError_t sanitize_launch(const uint8_t* text, u64 n, uint8_t* out, u64 out_ca
 cudaError_t tokens_compact_count(u64* keys_a, u64* keys_b, u64 nk, u64 vary, u64* hist, u64* tmp, u64* flags, u64* run_start,
                                  const TableView& t, int sm, cudaStream_t s, u64* launches, const u32* tile_counts,
                                  u64 tiled_tiles);
+cudaError_t exclusive_scan_u64(const u64* in, u64* out, u64 n, u64* tmp, cudaStream_t s, u64* launches);   // tokens.cu
+// frames.cu
+cudaError_t frame_lengths(const TokenRec* recs, u64 m, const uint8_t* arena, u64* lens_scan, u64* tmp, int sm, cudaStream_t s,
+                          u64* launches);
+cudaError_t frame_pack(const TokenRec* recs, u64 m, const uint8_t* arena, const u64* offs, uint8_t* frame, int sm, cudaStream_t s,
+                       u64* launches);
+cudaError_t frame_read_lens(const uint8_t* frame, u64 m, u64* lens, u64* arena_need, int sm, cudaStream_t s, u64* launches);
+cudaError_t frame_build(const uint8_t* frame, u64 m, const u64* offs, const u64* arena_offs, TokenRec* recs, uint8_t* arena,
+                        int* flags, int sm, cudaStream_t s, u64* launches);
 // analysis.cpp
 uint64_t analysis_top_k(const uint8_t* bytes, const uint32_t* lens, const uint64_t* counts, uint64_t n, uint64_t k,
                         uint64_t* out_idx, double* out_rel, uint64_t* total);
@@ -1867,6 +1876,128 @@ extern "C" int wfcu_tokens_concat_slices(const wfcu_tokens* const* src, const ui
         return fail(WFCU_ERR_CUDA, "concat of token slices: %s", cudaGetErrorString(e));
     }
     *out = t;
+    return WFCU_OK;
+}
+
+// ---- WCX1 frames on the device (frames.cu) ---------------------------------------------------------------------
+// encode_message (proj/src/wire.cpp:27-48) of the slice [begin, end) of a device token list, into device memory.
+// dev_frame == NULL: only *frame_bytes (what the frame takes).
+extern "C" int wfcu_tokens_encode_frame(const wfcu_tokens* t, uint64_t begin, uint64_t end, uint8_t* dev_frame,
+                                        uint64_t frame_cap, uint64_t* frame_bytes, void* stream) {
+    if (!t || !frame_bytes) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
+    if (begin > end || end > t->n) return fail(WFCU_ERR_INVALID_ARGUMENT, "slice out of range");
+    if (dev_frame && (reinterpret_cast<uintptr_t>(dev_frame) & 3u)) return fail(WFCU_ERR_INVALID_ARGUMENT, "frame buffer must be 4-byte aligned");
+    const u64 m = end - begin;
+    if (m > 0xFFFFFFFFull) return fail(WFCU_ERR_INVALID_ARGUMENT, "word batch exceeds 2^32-1 words");
+    cudaStream_t s = (cudaStream_t)stream;
+    DevBuf offs, tmp;
+    u64 payload = 0;
+    LaunchTally tally;
+    if (m) {
+        CUDA_TRY(offs.alloc(sizeof(u64) * (m + 1)));
+        CUDA_TRY(tmp.alloc(sizeof(u64) * scan_tmp_words(m)));
+        CUDA_TRY(frame_lengths(t->recs + begin, m, t->arena, offs.as<u64>(), tmp.as<u64>(), t->sm_count, s, &tally.n));
+        // payload bytes = offset of the last token + its length: read the last offset, add the last length on the host
+        u64 last_off = 0;
+        TokenRec last;
+        CUDA_TRY(cudaMemcpyAsync(&last_off, offs.as<u64>() + (m - 1), sizeof(u64), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(&last, t->recs + end - 1, sizeof(TokenRec), cudaMemcpyDeviceToHost, s));
+        u32 last_len = 0;
+        if (true) {
+            CUDA_TRY(cudaStreamSynchronize(s));
+            if (last.ext) CUDA_TRY(cudaMemcpy(&last_len, t->arena + last.ext, 4, cudaMemcpyDeviceToHost));
+            else last_len = key_len(last.k0, last.k1);
+        }
+        payload = last_off + last_len;
+    }
+    *frame_bytes = 8 + 4 * m + payload;
+    if (!dev_frame) return WFCU_OK;
+    if (frame_cap < *frame_bytes) return fail(WFCU_ERR_BUFFER_TOO_SMALL, "frame needs %llu bytes", (unsigned long long)*frame_bytes);
+    if (m == 0) {
+        const uint8_t empty[8] = {0x57, 0x43, 0x58, 0x31, 0, 0, 0, 0};
+        CUDA_TRY(cudaMemcpyAsync(dev_frame, empty, 8, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        return WFCU_OK;
+    }
+    CUDA_TRY(frame_pack(t->recs + begin, m, t->arena, offs.as<u64>(), dev_frame, t->sm_count, s, &tally.n));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return WFCU_OK;
+}
+
+// decode_message (proj/src/wire.cpp:50-87) of a frame in device memory: the structural checks of the reference in
+// its order (magic, word count, length table, payload short / trailing bytes), the UTF-8 check of the payload as one
+// sanitize pass (nothing replaced) plus "no word starts with a continuation byte", and the token list.
+extern "C" int wfcu_tokens_decode_frame(const uint8_t* dev_frame, uint64_t frame_bytes, wfcu_tokens** out, void* stream) {
+    if (!out) return fail(WFCU_ERR_INVALID_ARGUMENT, "out is null");
+    *out = nullptr;
+    DeviceState* d;
+    if (int rc = current_device_state(&d)) return rc;
+    if (frame_bytes && !dev_frame) return fail(WFCU_ERR_INVALID_ARGUMENT, "frame is null");
+    if (reinterpret_cast<uintptr_t>(dev_frame) & 3u) return fail(WFCU_ERR_INVALID_ARGUMENT, "frame must be 4-byte aligned");
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t head[8] = {0};
+    if (frame_bytes) CUDA_TRY(cudaMemcpyAsync(head, dev_frame, std::min<u64>(frame_bytes, 8), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    static const uint8_t magic[4] = {0x57, 0x43, 0x58, 0x31};
+    if (frame_bytes < 4 || std::memcmp(head, magic, 4) != 0) return fail(WFCU_ERR_FRAME_MAGIC, "malformed frame: bad magic");
+    if (frame_bytes < 8) return fail(WFCU_ERR_FRAME_TRUNCATED, "truncated frame: missing word count");
+    u32 count32;
+    std::memcpy(&count32, head + 4, 4);
+    const u64 m = count32;
+    if ((frame_bytes - 8) / 4 < m) return fail(WFCU_ERR_FRAME_TRUNCATED, "truncated frame: missing word lengths");
+    const u64 payload_bytes = frame_bytes - 8 - 4 * m;
+    auto* t = new wfcu_tokens;
+    cudaGetDevice(&t->device);
+    t->sm_count = d->sm_count;
+    t->n = m;
+    struct Guard { wfcu_tokens*& t; ~Guard() { if (t) tokens_free(t); } } guard{t};
+    if (m == 0) {
+        if (payload_bytes) return fail(WFCU_ERR_FRAME_TRAILING, "framing error: trailing bytes after payload");
+        *out = t; t = nullptr;
+        return WFCU_OK;
+    }
+    DevBuf lens, need, tmp, flags, aligned, clean;
+    CUDA_TRY(lens.alloc(sizeof(u64) * (m + 1)));
+    CUDA_TRY(need.alloc(sizeof(u64) * (m + 1)));
+    CUDA_TRY(tmp.alloc(sizeof(u64) * scan_tmp_words(m)));
+    CUDA_TRY(flags.alloc(sizeof(int)));
+    CUDA_TRY(cudaMemsetAsync(flags.p, 0, sizeof(int), s));
+    LaunchTally tally;
+    CUDA_TRY(frame_read_lens(dev_frame, m, lens.as<u64>(), need.as<u64>(), d->sm_count, s, &tally.n));
+    u64 last[2] = {0, 0}, last_off[2] = {0, 0};
+    CUDA_TRY(cudaMemcpyAsync(&last[0], lens.as<u64>() + (m - 1), sizeof(u64), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&last[1], need.as<u64>() + (m - 1), sizeof(u64), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(exclusive_scan_u64(lens.as<u64>(), lens.as<u64>(), m, tmp.as<u64>(), s, &tally.n));
+    CUDA_TRY(exclusive_scan_u64(need.as<u64>(), need.as<u64>(), m, tmp.as<u64>(), s, &tally.n));
+    CUDA_TRY(cudaMemcpyAsync(&last_off[0], lens.as<u64>() + (m - 1), sizeof(u64), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&last_off[1], need.as<u64>() + (m - 1), sizeof(u64), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    const u64 declared = last_off[0] + last[0], arena_bytes = 8 + last_off[1] + last[1];
+    if (declared > payload_bytes) return fail(WFCU_ERR_FRAME_TRUNCATED, "truncated frame: payload short of declared lengths");
+    if (declared < payload_bytes) return fail(WFCU_ERR_FRAME_TRAILING, "framing error: trailing bytes after payload");
+    void* p = nullptr;
+    CUDA_TRY(scratch_alloc(&p, sizeof(TokenRec) * m));
+    t->recs = static_cast<TokenRec*>(p);
+    CUDA_TRY(scratch_alloc(&p, arena_bytes));
+    t->arena = static_cast<uint8_t*>(p);
+    t->arena_used = t->arena_cap = arena_bytes;
+    CUDA_TRY(cudaMemsetAsync(t->arena, 0, 8, s));
+    CUDA_TRY(frame_build(dev_frame, m, lens.as<u64>(), need.as<u64>(), t->recs, t->arena, flags.as<int>(), d->sm_count, s, &tally.n));
+    int fl = 0;
+    CUDA_TRY(cudaMemcpyAsync(&fl, flags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    u64 clean_len = payload_bytes;
+    if (payload_bytes) {     // UTF-8: the sanitize pass replaces nothing (its input must be 16-byte aligned: copy)
+        CUDA_TRY(aligned.alloc(payload_bytes + 16));
+        CUDA_TRY(clean.alloc(3 * payload_bytes + 64));
+        CUDA_TRY(cudaMemcpyAsync(aligned.p, dev_frame + 8 + 4 * m, payload_bytes, cudaMemcpyDeviceToDevice, s));
+        uint64_t got = 0;
+        if (int rc = wfcu_utf8_sanitize_dev(aligned.as<uint8_t>(), payload_bytes, clean.as<uint8_t>(), 3 * payload_bytes + 64, &got, stream)) return rc;
+        clean_len = got;
+    }
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (fl & 1) return fail(WFCU_ERR_INVALID_ARGUMENT, "frame holds an empty word: not a token list");
+    if ((fl & 2) || clean_len != payload_bytes) return fail(WFCU_ERR_FRAME_ENCODING, "encoding error: word payload is not UTF-8");
+    *out = t; t = nullptr;
     return WFCU_OK;
 }
 

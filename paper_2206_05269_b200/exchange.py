@@ -190,6 +190,69 @@ class AsyncExchange:
                                    f"{long_tokens} tokens longer than 16 bytes in {self.steps} steps")
 
 
+def partition_cuts(k: int, worker_id: int, n_workers: int) -> list[int]:
+    """plan_partition (/root/reference/proj/src/shuffle.cpp:9-46): the kept chunk gets floor(k/n) words, the rest is
+    spread over the other chunks, one extra each from chunk 0 upward.  Index arithmetic on the list length."""
+    n = n_workers
+    keep = k // n
+    others = n - 1 if n > 1 else 1
+    base = (k - keep) // others if n > 1 else 0
+    extra = (k - keep) % others if n > 1 else 0
+    cut = [0]
+    for c in range(n):
+        size = keep
+        if c != worker_id:
+            size = base + (1 if extra else 0)
+            extra -= 1 if extra else 0
+        cut.append(cut[-1] + size)
+    return cut
+
+
+def range_partition_exchange(local, dist, torch, device, group=None):
+    """The paper's own exchange between ranks (proj/src/shuffle.cpp:98-130), one rank per GPU, with the WCX1 frame as
+    wire format and the collective library as transport: chunk c of this rank's SORTED token list (capi.Tokens) is
+    framed on the device (wfcu_tokens_encode_frame), an all-to-all of the frame sizes tells every rank what arrives
+    (the one host read: frames have variable length), an all-to-all of the frame bytes delivers them -- device buffers
+    end to end, NCCL over NVLink -- and every received frame is validated and decoded on the device
+    (wfcu_tokens_decode_frame: a bad frame raises capi.WfcuError with the ERR_FRAME_* code, the reference's
+    WireError kinds).  The kept chunk and the decoded chunks are gathered in source order and radix-sorted: the n-way
+    merge.  Returns this rank's range of the global sorted list (capi.Tokens, sorted); reduce_sorted of it is the
+    reference's pre-repair shard."""
+    from . import capi
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    k, _ = local.stats()
+    cut = partition_cuts(k, rank, world)
+    if world == 1:
+        return capi.Tokens.concat_slices([local], [0], [k])
+    pad = lambda b: (b + 15) & ~15
+    sizes = [0 if c == rank else local.frame_bytes(cut[c], cut[c + 1]) for c in range(world)]
+    send = torch.zeros(max(sum(pad(b) for b in sizes), 16), dtype=torch.uint8, device=device)
+    off = 0
+    for c in range(world):
+        if c != rank:
+            local.encode_frame(cut[c], cut[c + 1], send.data_ptr() + off, pad(sizes[c]))
+            off += pad(sizes[c])
+    send_sizes = torch.tensor(sizes, dtype=torch.int64, device=device)
+    recv_sizes = torch.empty_like(send_sizes)
+    dist.all_to_all_single(recv_sizes, send_sizes, group=group)
+    got = [int(v) for v in recv_sizes.cpu().tolist()]
+    recv = torch.zeros(max(sum(pad(b) for b in got), 16), dtype=torch.uint8, device=device)
+    dist.all_to_all_single(recv[:sum(pad(b) for b in got)], send[:sum(pad(b) for b in sizes)],
+                           output_split_sizes=[pad(b) for b in got], input_split_sizes=[pad(b) for b in sizes], group=group)
+    torch.cuda.synchronize(device) if device is not None and str(device).startswith("cuda") else None
+    parts, off = [], 0
+    for src in range(world):
+        if src == rank:
+            parts.append((local, cut[rank], cut[rank + 1]))
+        else:
+            t = capi.Tokens.decode_frame(recv.data_ptr() + off, got[src])
+            parts.append((t, 0, t.stats()[0]))
+            off += pad(got[src])
+    merged = capi.Tokens.concat_slices([p[0] for p in parts], [p[1] for p in parts], [p[2] for p in parts])
+    merged.sort()
+    return merged
+
+
 def allreduce_scalar(partial, dist, group=None, reproducible: bool = True):
     """Finishes a sharded map-then-reduce: sum of the ranks' partial sums.
 

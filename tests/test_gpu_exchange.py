@@ -250,3 +250,86 @@ def test_framed_regions_describe_themselves(capi, cuda, port, n_parts):
     c.partition_framed(n_parts, small.data_ptr(), 4, counts.data_ptr())
     assert counts[n_parts + 1].item() == len(want) - sum(min(int(v), 3) for v in counts[:n_parts].tolist())
     assert [int(v) for v in small.cpu().numpy().reshape(n_parts, 4, 4)[:, 0, 2]] == [min(int(v), 3) for v in counts[:n_parts].tolist()]
+
+
+def test_frame_codec_on_the_device(capi, cuda, port):
+    """wfcu_tokens_encode_frame / decode_frame: the reference's golden bytes (proj/tests/wire_test.cpp:38-50), the
+    round trip of sorted slices with long tokens, and every WireError kind (wire_test.cpp:72-118) as its own code"""
+    import numpy as np
+    t = capi.Tokens.from_words([b"to", b"a"])
+    buf = cuda.zeros(256, dtype=cuda.uint8, device="cuda")
+    n = t.encode_frame(0, 2, buf.data_ptr(), 256)
+    assert bytes(buf[:n].cpu().numpy()) == bytes([0x57, 0x43, 0x58, 0x31, 2, 0, 0, 0, 2, 0, 0, 0, 1, 0, 0, 0, 0x74, 0x6F, 0x61])
+    assert t.frame_bytes(0, 2) == n == 19
+    n1 = t.encode_frame(1, 2, buf.data_ptr(), 256)
+    assert bytes(buf[:n1].cpu().numpy()) == bytes([0x57, 0x43, 0x58, 0x31, 1, 0, 0, 0, 1, 0, 0, 0, 0x61])
+    n0 = t.encode_frame(1, 1, buf.data_ptr(), 256)
+    assert bytes(buf[:n0].cpu().numpy()) == bytes([0x57, 0x43, 0x58, 0x31, 0, 0, 0, 0])
+    assert capi.Tokens.decode_frame(buf.data_ptr(), n0).words() == []
+    words = sorted([b"alpha", b"b", "café".encode(), b"L" * 17, b"M" * 40, "한국어".encode(), b"zz"] * 3)
+    big = capi.Tokens.from_words(words)
+    fb = cuda.zeros(4096, dtype=cuda.uint8, device="cuda")
+    m = big.encode_frame(2, len(words) - 1, fb.data_ptr(), 4096)
+    back = capi.Tokens.decode_frame(fb.data_ptr(), m)
+    assert back.words() == words[2:-1]
+    back.sort()
+    c = capi.Counter(table_slots=1 << 10)
+    back.reduce_sorted(c)
+    assert c.to_dict() == {w: words[2:-1].count(w) for w in set(words[2:-1])}
+
+    def decode(raw: bytes):
+        dev = cuda.zeros(max(len(raw), 4) + 16, dtype=cuda.uint8, device="cuda")
+        if raw:
+            dev[:len(raw)] = cuda.from_numpy(np.frombuffer(raw, dtype=np.uint8).copy()).cuda()
+        return capi.Tokens.decode_frame(dev.data_ptr(), len(raw))
+    good = bytes(fb[:m].cpu().numpy())
+    for raw, code in ((b"WCX2" + good[4:], capi.ERR_FRAME_MAGIC), (b"WC", capi.ERR_FRAME_MAGIC), (good[:6], capi.ERR_FRAME_TRUNCATED),
+                      (good[:12], capi.ERR_FRAME_TRUNCATED), (good[:-1], capi.ERR_FRAME_TRUNCATED), (good + b"x", capi.ERR_FRAME_TRAILING),
+                      (b"WCX1" + bytes([1, 0, 0, 0, 2, 0, 0, 0, 0xC3, 0x28]), capi.ERR_FRAME_ENCODING),
+                      (b"WCX1" + bytes([2, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0, 0xC3, 0xA9]), capi.ERR_FRAME_ENCODING)):
+        with pytest.raises(capi.WfcuError) as e:
+            decode(raw)
+        assert e.value.code == code, (raw, e.value.code)
+    with pytest.raises(capi.InvalidArgument):
+        t.encode_frame(0, 3, buf.data_ptr(), 256)
+    with pytest.raises(capi.WfcuError) as e:
+        t.encode_frame(0, 2, buf.data_ptr(), 8)
+    assert e.value.code == capi.ERR_BUFFER_TOO_SMALL
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_range_exchange_with_frames(capi, cuda, port, world):
+    """exchange.range_partition_exchange: `world` ranks (sharing this GPU, gloo) run the paper's range exchange with
+    device WCX1 frames; the shards they print are the reference's pre-repair shards (reduce_sorted of the exchanged
+    chunks, proj/src/pipeline.cpp:104-114): their merge is serial_wordcount, each is a contiguous alphabetical range,
+    and the sizes follow plan_partition."""
+    import json
+    import os
+    import subprocess
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import range_exchange_worker as rw
+    from paper_2206_05269_b200.exchange import partition_cuts
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world), "--master-addr",
+           "127.0.0.1", "--master-port", str(29540 + world), os.path.join(root, "tests", "range_exchange_worker.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-3000:]
+    shards = sorted((json.loads(l[6:]) for l in out.stdout.splitlines() if l.startswith("SHARD ")), key=lambda s: s["rank"])
+    assert [s["rank"] for s in shards] == list(range(world)) and all(s["sorted"] for s in shards)
+    docs = rw.corpus()
+    # the oracle's version of the same pipeline: tokenize per worker, sort, cut, gather, reduce
+    locals_ = [sorted(w for d in range(j, len(docs), world) for w in port.tokenize(docs[d])) for j in range(world)]
+    cuts = [partition_cuts(len(locals_[j]), j, world) for j in range(world)]
+    merged = {}
+    for c in range(world):
+        want = {}
+        for j in range(world):
+            for w in locals_[j][cuts[j][c]:cuts[j][c + 1]]:
+                want[w] = want.get(w, 0) + 1
+        got = {bytes.fromhex(k): v for k, v in shards[c]["table"].items()}
+        assert got == want
+        assert shards[c]["n"] == sum(cuts[j][c + 1] - cuts[j][c] for j in range(world))
+        for w, v in got.items():
+            merged[w] = merged.get(w, 0) + v
+    assert merged == port.wordcount(docs)
