@@ -200,6 +200,7 @@ struct __align__(1024) Smem {
     uint4 landing[WARPS][32];                  // where the global slot keys of a drain in flight arrive (cp.async)
     uint4 ring[WARPS][kRingBytes / 16];
     u32 mcnt[MSLOTS];
+    u32 dummy[WARPS];                          // where the count of a token that missed goes (no branch around the atomic)
 };
 
 }  // namespace cnt3
@@ -248,6 +249,7 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
     u32 qhead = 0, qtail = 0;     // token queue (warp-uniform, free running, in entries)
     u32 qrd = lane * 2;           // byte offset of this lane's entry in the next pass (free running)
     u32 mhead = 0, mtail = 0;     // miss buffer (warp-uniform, free running)
+    bool filling = true;          // look for empty combiner ways: while the combiner fills, and every 16th row after
 
     auto q_store = [&](u32 off2, u32 v) {
         asm volatile("st.shared.u16 [%0], %1;" ::"r"(q_s | (off2 & (2 * kQueueCap - 2))), "r"(v) : "memory");
@@ -407,10 +409,12 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
         const bool hb0 = r0 == b0 && r1 == b1, hb1 = r2 == b0 && r3 == b1;
         const bool live0 = e0 != 0, live1 = e1 != 0;
         const bool fa = (ha0 || ha1) && live0, fb = (hb0 || hb1) && live1;
-        if (fa) atomicAdd(reinterpret_cast<u32*>(sm.scnt) + seta * 2u + (ha1 ? 1u : 0u), 1u);
-        if (fb) atomicAdd(reinterpret_cast<u32*>(sm.scnt) + setb * 2u + (hb1 ? 1u : 0u), 1u);
+        // round 2 (from the fourth-generation experiment, +1.9 %): a token that missed counts into the warp's dummy word
+        // -- no branch around the two ATOMS.POPC.INC -- and empty ways are only looked for while the combiner fills
+        atomicAdd(fa ? reinterpret_cast<u32*>(sm.scnt) + seta * 2u + (ha1 ? 1u : 0u) : &sm.dummy[warp], 1u);
+        atomicAdd(fb ? reinterpret_cast<u32*>(sm.scnt) + setb * 2u + (hb1 ? 1u : 0u) : &sm.dummy[warp], 1u);
         const bool ca = live0 && !fa && (p0 == 0 || p2 == 0), cb = live1 && !fb && (r0 == 0 || r2 == 0);
-        if (__any_sync(kFull, ca || cb)) {
+        if (filling && __any_sync(kFull, ca || cb)) {
             if (ca) {
                 const u64 key = ((u64)a1 << 32) | a0;
                 u64* slot = reinterpret_cast<u64*>(&sm.sk[seta]);
@@ -495,6 +499,7 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
 
         for (u32 row = r_begin; row < r_end; ++row) {
             const uint4 xa = nxa, xb = nxb;
+            filling = row - r_begin < 64u || (row & 15u) == 0;
             const u32 slotpos = (row & 1u) * kSlotStride;
 
             // ------------------------------ phase 1 ------------------------------
