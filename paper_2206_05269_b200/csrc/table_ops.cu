@@ -266,7 +266,28 @@ __global__ void tb_long_merge_kernel(TableView t, const uint8_t* __restrict__ re
         const u64 need = long_record_bytes(len);
         if (off + need > n_bytes) break;
         const bool mine = (n_parts <= 1) || ((hash * 0x9E3779B1u) >> 7) % n_parts == part;
+        // a token the table already holds only adds its count: no arena record is spent on it (repeated merges used
+        // to leak one record per incoming token until ARENA_FULL)
+        bool known = false;
         if (mine && count) {
+            u64 i = hash & t.long_mask;
+            for (u64 probes = 0; probes <= t.long_mask; ++probes) {
+                const u64 r = *reinterpret_cast<volatile u64*>(t.long_ref + i);
+                if (r == 0) break;
+                if (*reinterpret_cast<const u32*>(t.arena + r) == len && *reinterpret_cast<const u32*>(t.arena + r + 4) == hash) {
+                    bool same = true;
+                    for (u32 k = 0; k < len && same; ++k) same = t.arena[r + 8 + k] == recs[off + 16 + k];
+                    if (same) {
+                        atomicAdd(t.long_count + i, count);
+                        atomicAdd(t.n_tokens, count);
+                        known = true;
+                        break;
+                    }
+                }
+                i = (i + 1) & t.long_mask;
+            }
+        }
+        if (mine && count && !known) {
             const u64 rec = arena_alloc(t, len);
             if (rec) {
                 *reinterpret_cast<u32*>(t.arena + rec) = len;

@@ -333,3 +333,20 @@ def test_range_exchange_with_frames(capi, cuda, port, world):
         for w, v in got.items():
             merged[w] = merged.get(w, 0) + v
     assert merged == port.wordcount(docs)
+
+
+def test_repeated_long_record_merges_do_not_leak_the_arena(capi, cuda):
+    """merging the same long-token record stream again and again only adds counts: the arena of the receiving table
+    stays at one record per distinct token (it used to spend a record per incoming token until ARENA_FULL)"""
+    text = (b"L" * 300 + b" " + b"M" * 200 + b" ") * 4
+    dev, n = to_dev(cuda, text)
+    src = capi.Counter(table_slots=1 << 10)
+    src.count_dev(dev.data_ptr(), n)
+    nlong = src.long_records()
+    rec = cuda.empty(nlong, dtype=cuda.uint8, device="cuda")
+    src.long_records(rec.data_ptr(), nlong)
+    dst = capi.Counter(table_slots=1 << 10, arena_bytes=4096)      # room for a handful of records only
+    for _ in range(200):
+        dst.merge_long_records(rec.data_ptr(), nlong, 0, 1)
+    dst.status()
+    assert dst.to_dict() == {b"l" * 300: 800, b"m" * 200: 800}
