@@ -37,6 +37,7 @@ cudaError_t tb_union_rows(const TableView& target, const TableView& others, Toke
                           u64* dev_cursor, int sm, cudaStream_t s, u64* launches);
 cudaError_t tb_score_rows(TokenRec* recs, const u64* ct, const u64* co, const u64* dev_n_rows, u64 max_rows, u64 extra_vocab,
                           u64 t_total, u64 o_total, int sm, cudaStream_t s, u64* launches);
+cudaError_t tb_reset_aux(const TableView& t, u64* counters, unsigned int* done, int sm, cudaStream_t s, u64* launches);
 cudaError_t tk_rebase_ext(TokenRec* recs, u64 n, u64 delta, int sm, cudaStream_t s, u64* launches);
 cudaError_t tb_gather_counts(const TokenRec* recs, u64 first, u64 n, const u64* ct, const u64* co, u64* out_ct, u64* out_co,
                              int sm, cudaStream_t s, u64* launches);
@@ -328,7 +329,8 @@ struct wfcu_counter {
     TableView v{};
     u64 table_slots = 0, long_slots = 0;
     u64* counters = nullptr;    // device: [0] n_used [1] n_tokens [2] n_deferred [3] n_long [4] arena_used
-                                //         [5] status(int) [6..15] scratch
+                                //         [5] status(int) [6..15] scratch [16] CTA ticket of the reset kernel
+    bool aux_clean = false;     // the long table and the counters have been initialised once
     // host staging for count_host
     uint8_t* pinned[2] = {nullptr, nullptr};
     uint8_t* devbuf[2] = {nullptr, nullptr};
@@ -385,11 +387,18 @@ extern "C" int wfcu_counter_reset(wfcu_counter* c, void* stream) {
     if (!c) return fail(WFCU_ERR_INVALID_ARGUMENT, "counter is null");
     cudaStream_t s = (cudaStream_t)stream;
     CUDA_TRY(cudaMemsetAsync(c->v.slots, 0, sizeof(Slot) * c->table_slots, s));
-    CUDA_TRY(cudaMemsetAsync(c->v.long_ref, 0, sizeof(u64) * c->long_slots, s));
-    CUDA_TRY(cudaMemsetAsync(c->v.long_count, 0, sizeof(u64) * c->long_slots, s));
-    CUDA_TRY(cudaMemsetAsync(c->counters, 0, sizeof(u64) * 16, s));
-    const u64 arena_start = 8;   // offset 0 means "empty"
-    CUDA_TRY(cudaMemcpyAsync(c->v.arena_used, &arena_start, sizeof(u64), cudaMemcpyHostToDevice, s));
+    if (!c->aux_clean) {      // first reset: the long table and the counters are raw memory
+        CUDA_TRY(cudaMemsetAsync(c->v.long_ref, 0, sizeof(u64) * c->long_slots, s));
+        CUDA_TRY(cudaMemsetAsync(c->v.long_count, 0, sizeof(u64) * c->long_slots, s));
+        CUDA_TRY(cudaMemsetAsync(c->counters, 0, sizeof(u64) * 17, s));
+        const u64 arena_start = 8;   // offset 0 means "empty"
+        CUDA_TRY(cudaMemcpyAsync(c->v.arena_used, &arena_start, sizeof(u64), cudaMemcpyHostToDevice, s));
+        c->aux_clean = true;
+        return WFCU_OK;
+    }
+    // afterwards one small kernel: clears the long table only if it holds something, then the counters
+    LaunchTally tally;
+    CUDA_TRY(tb_reset_aux(c->v, c->counters, reinterpret_cast<unsigned int*>(c->counters + 16), c->sm_count, s, &tally.n));
     return WFCU_OK;
 }
 
@@ -416,7 +425,7 @@ extern "C" int wfcu_counter_create(wfcu_counter** out, const wfcu_counter_config
     alloc((void**)&c->v.long_ref, sizeof(u64) * c->long_slots);
     alloc((void**)&c->v.long_count, sizeof(u64) * c->long_slots);
     alloc((void**)&c->v.arena, arena);
-    alloc((void**)&c->counters, sizeof(u64) * 16);
+    alloc((void**)&c->counters, sizeof(u64) * 17);
     if (e != cudaSuccess) {
         counter_free(c);
         return fail(WFCU_ERR_CUDA, "counter allocation: %s", cudaGetErrorString(e));
@@ -429,6 +438,7 @@ extern "C" int wfcu_counter_create(wfcu_counter** out, const wfcu_counter_config
     c->v.n_long = c->counters + 3;
     c->v.arena_used = c->counters + 4;
     c->v.status = reinterpret_cast<int*>(c->counters + 5);
+    c->v.ticket = reinterpret_cast<unsigned int*>(c->counters + 16);
     c->v.deferred_cap = deferred;
     c->v.long_mask = c->long_slots - 1;
     c->v.arena_cap = arena;

@@ -380,6 +380,28 @@ __global__ void tk_rebase_ext_kernel(TokenRec* __restrict__ recs, u64 n, u64 del
         if (recs[i].ext) recs[i].ext += delta;
 }
 
+// Reset of everything but the inline table: the long-token table is only cleared when it holds something (the
+// common corpus has no token longer than 16 bytes: two 8 MB memsets per reset for nothing), then the counters.
+// The grid cooperates on the clear; the last CTA to finish resets the counters (they hold n_long, which every CTA
+// has to read first).
+__global__ void tb_reset_aux_kernel(TableView t, u64* __restrict__ counters, unsigned int* __restrict__ done) {
+    __shared__ bool last;
+    if (*t.n_long != 0) {
+        for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= t.long_mask; i += (u64)gridDim.x * blockDim.x) {
+            t.long_ref[i] = 0;
+            t.long_count[i] = 0;
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(done, 1u) + 1 == gridDim.x;
+    __syncthreads();
+    if (last && threadIdx.x < 16) {
+        counters[threadIdx.x] = threadIdx.x == 4 ? 8ull : 0ull;     // [4] arena_used: offset 0 means "empty"
+        if (threadIdx.x == 0) *done = 0;
+    }
+}
+
 // ---- launchers ----------------------------------------------------------------------
 static inline unsigned grid_for(u64 items, int sm_count) {
     u64 g = (items + 255) / 256;
@@ -526,6 +548,12 @@ cudaError_t tb_gather_counts(const TokenRec* recs, u64 first, u64 n, const u64* 
 cudaError_t tk_rebase_ext(TokenRec* recs, u64 n, u64 delta, int sm, cudaStream_t s, u64* launches) {
     if (n == 0 || delta == 0) return cudaSuccess;
     tk_rebase_ext_kernel<<<grid_for(n, sm), 256, 0, s>>>(recs, n, delta);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+cudaError_t tb_reset_aux(const TableView& t, u64* counters, unsigned int* done, int sm, cudaStream_t s, u64* launches) {
+    tb_reset_aux_kernel<<<sm, 256, 0, s>>>(t, counters, done);
     *launches += 1;
     return cudaGetLastError();
 }

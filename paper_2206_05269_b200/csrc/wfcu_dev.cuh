@@ -50,6 +50,7 @@ struct TableView {
     u64 arena_cap;
     u64* arena_used;
     int* status;
+    unsigned int* ticket = nullptr;   // a zeroed word for "last CTA" decisions (null: the caller launches the follow-up itself)
 };
 
 // One token of a device-resident token list (wfcu_tokens), 32 bytes.

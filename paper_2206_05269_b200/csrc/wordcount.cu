@@ -661,10 +661,28 @@ __device__ __forceinline__ bool ascii_space(u32 b) { return b == 0x20 || (b >= 0
 
 // One thread per deferred fragment END (offset of the terminating ASCII
 // whitespace byte, or n).  The fragment start is found by scanning backwards.
+// The deferred list is consumed: the last CTA to finish empties it for the next call (one launch less per count than
+// a reset kernel of its own; every CTA has read the count before it takes its ticket).
+__device__ __forceinline__ void slow_kernel_done(const TableView& gt) {
+    if (!gt.ticket) return;
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(gt.ticket, 1u) + 1 == gridDim.x;
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        *gt.n_deferred = 0;
+        *gt.ticket = 0;
+    }
+}
+
 __global__ void wc_slow_kernel(const uint8_t* __restrict__ text, u64 n, TableView gt, EmitView em, int emit) {
     u64 count = *gt.n_deferred;
     if (count > gt.deferred_cap) count = gt.deferred_cap;
-    if (count == 0) return;
+    if (count == 0) {
+        slow_kernel_done(gt);
+        return;
+    }
     u32 tokens = 0, inserted = 0;
     for (u64 idx = (u64)blockIdx.x * blockDim.x + threadIdx.x; idx < count; idx += (u64)gridDim.x * blockDim.x) {
         const u64 e = gt.deferred[idx];
@@ -696,6 +714,7 @@ __global__ void wc_slow_kernel(const uint8_t* __restrict__ text, u64 n, TableVie
     }
     if ((threadIdx.x & 31) == 0) table_note_inserted(gt, inserted);
     if ((threadIdx.x & 31) == 0 && tokens) atomicAdd(gt.n_tokens, (u64)tokens);
+    slow_kernel_done(gt);
 }
 
 __global__ void wc_reset_deferred_kernel(TableView gt) { *gt.n_deferred = 0; }
@@ -761,8 +780,11 @@ static cudaError_t wc_launch_impl(const uint8_t* text, u64 n, const TableView& g
     }
     if (ev_after_fast) cudaEventRecord(*ev_after_fast, stream);
     wc_slow_kernel<<<sm_count * 16, 128, 0, stream>>>(text, n, gt, em, EMIT ? 1 : 0);
-    wc_reset_deferred_kernel<<<1, 1, 0, stream>>>(gt);
-    *launches += 2;
+    *launches += 1;
+    if (!gt.ticket) {
+        wc_reset_deferred_kernel<<<1, 1, 0, stream>>>(gt);
+        *launches += 1;
+    }
     return cudaGetLastError();
 }
 
