@@ -476,7 +476,8 @@ def run_b200(args) -> None:
                 print("PARITY FAILURE: the device table differs from the reference's", file=sys.stderr)
         if not args.no_mapreduce:
             line["extra"] = {"mapreduce": mapreduce_line(capi, torch, device, stream, peak, world == 1 and not args.no_cpu),
-                             "sanitize": sanitize_line(capi, torch, dev, nbytes, peak)}
+                             "sanitize": sanitize_line(capi, torch, dev, nbytes, peak),
+                             "non_ascii": non_ascii_line(capi, torch, device, stream, peak)}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -622,6 +623,45 @@ def mapreduce_line(capi, torch, device, stream, peak, with_cpu: bool) -> dict:
                                 "map_reduce_serial": {"GBps_of_fp64": 8 * m / (t1 - t0) / 1e9, "cores": 1, "value": v1},
                                 "map_reduce_blocked_256": {"GBps_of_fp64": 8 * m / (t2 - t1) / 1e9, "cores": cores, "value": v2}}
     return line
+
+
+def non_ascii_line(capi, torch, device, stream, peak) -> dict:
+    """Text that is not ASCII: the first 256 documents of the cfg3 corpus with bigrams replaced by
+    two-byte letters (accented), by U+2019 inside words (typographic), by three-byte letters in 13 % / 97 % of the
+    words (kana).  Resident, CUDA-event timed; all of them are counted exactly (tests/test_gpu_count_kernel.py)."""
+    import numpy as np
+    base = capi.synth_corpus(SEED, 0, 256, 50000, ZIPF_S, 0, DOC_BYTES).tobytes()
+    kana = list(zip((b"ba", b"ca", b"da", b"fa", b"ga", b"a", b"e", b"i"), "あいうえお漢字語"))
+    flavours = {
+        "accented": [(b"ba", "é"), (b"ca", "ü"), (b"da", "ö"), (b"fa", "ß"), (b"ga", "ñ")],
+        "typographic": [(a, a[:1].decode() + "’" + a[1:].decode()) for a in (b"ab", b"ba", b"ca")],
+        "kana_13pct": kana[:5],
+        "kana_97pct": kana,
+    }
+    res = {}
+    for name, subs in flavours.items():
+        raw = base
+        for a, b in subs:
+            raw = raw.replace(a, b.encode())
+        raw = raw[:len(raw) & ~15]
+        dev = torch.from_numpy(np.frombuffer(raw, dtype=np.uint8).copy()).to(device)
+        c = capi.Counter(table_slots=1 << 21, deferred_slots=1 << 27)
+        for _ in range(3):
+            c.reset(stream); c.count_dev(dev.data_ptr(), dev.numel(), stream)
+        torch.cuda.synchronize()
+        c.status()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            c.reset(stream); c.count_dev(dev.data_ptr(), dev.numel(), stream)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 5
+        distinct, tokens, _ = c.stats()
+        res[name] = {"bytes": dev.numel(), "ms": ms, "GBps": dev.numel() / ms / 1e6, "frac_of_hbm_peak": dev.numel() / ms / 1e6 / peak,
+                     "tokens": tokens, "distinct_words": distinct}
+        c.close()
+    return {"config": "first 256 cfg3 documents with bigrams replaced by non-ASCII letters, 1 GPU, resident", **res}
 
 
 def sanitize_line(capi, torch, dev, nbytes, peak) -> dict:
