@@ -23,7 +23,7 @@
 namespace wfcu {
 // wordcount.cu
 cudaError_t wc_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream, u64* launches,
-                      cudaEvent_t* ev_before_fast, cudaEvent_t* ev_after_fast);
+                      cudaEvent_t* ev_before_fast, cudaEvent_t* ev_after_fast, u32 variant_hint);
 // mapreduce.cu
 cudaError_t mr_launch(const void* values, int is_f64, u64 n, u64 base, int kind, int grid, double* partials,
                       double* dev_out, cudaStream_t s, u64* launches);
@@ -331,6 +331,8 @@ struct wfcu_counter {
     u64* counters = nullptr;    // device: [0] n_used [1] n_tokens [2] n_deferred [3] n_long [4] arena_used
                                 //         [5] status(int) [6..15] scratch [16] CTA ticket of the reset kernel
     bool aux_clean = false;     // the long table and the counters have been initialised once
+    u32 variant_hint = 7;       // kernel variants the texts counted so far asked for (counters[17]), read at every
+                                // synchronising call: later counts launch only those (and the narrow one)
     // host staging for count_host
     uint8_t* pinned[2] = {nullptr, nullptr};
     uint8_t* devbuf[2] = {nullptr, nullptr};
@@ -390,7 +392,7 @@ extern "C" int wfcu_counter_reset(wfcu_counter* c, void* stream) {
     if (!c->aux_clean) {      // first reset: the long table and the counters are raw memory
         CUDA_TRY(cudaMemsetAsync(c->v.long_ref, 0, sizeof(u64) * c->long_slots, s));
         CUDA_TRY(cudaMemsetAsync(c->v.long_count, 0, sizeof(u64) * c->long_slots, s));
-        CUDA_TRY(cudaMemsetAsync(c->counters, 0, sizeof(u64) * 17, s));
+        CUDA_TRY(cudaMemsetAsync(c->counters, 0, sizeof(u64) * 18, s));
         const u64 arena_start = 8;   // offset 0 means "empty"
         CUDA_TRY(cudaMemcpyAsync(c->v.arena_used, &arena_start, sizeof(u64), cudaMemcpyHostToDevice, s));
         c->aux_clean = true;
@@ -425,7 +427,7 @@ extern "C" int wfcu_counter_create(wfcu_counter** out, const wfcu_counter_config
     alloc((void**)&c->v.long_ref, sizeof(u64) * c->long_slots);
     alloc((void**)&c->v.long_count, sizeof(u64) * c->long_slots);
     alloc((void**)&c->v.arena, arena);
-    alloc((void**)&c->counters, sizeof(u64) * 17);
+    alloc((void**)&c->counters, sizeof(u64) * 18);
     if (e != cudaSuccess) {
         counter_free(c);
         return fail(WFCU_ERR_CUDA, "counter allocation: %s", cudaGetErrorString(e));
@@ -439,6 +441,7 @@ extern "C" int wfcu_counter_create(wfcu_counter** out, const wfcu_counter_config
     c->v.arena_used = c->counters + 4;
     c->v.status = reinterpret_cast<int*>(c->counters + 5);
     c->v.ticket = reinterpret_cast<unsigned int*>(c->counters + 16);
+    c->v.wanted = reinterpret_cast<unsigned int*>(c->counters + 17);
     c->v.deferred_cap = deferred;
     c->v.long_mask = c->long_slots - 1;
     c->v.arena_cap = arena;
@@ -482,7 +485,7 @@ extern "C" int wfcu_counter_count_dev(wfcu_counter* c, const uint8_t* dev_text, 
         ev0 = &c->timed.back().first;
         ev1 = &c->timed.back().second;
     }
-    CUDA_TRY(wc_launch(dev_text, n, c->v, c->sm_count, (cudaStream_t)stream, &tally.n, ev0, ev1));
+    CUDA_TRY(wc_launch(dev_text, n, c->v, c->sm_count, (cudaStream_t)stream, &tally.n, ev0, ev1, c->variant_hint));
     return WFCU_OK;
 }
 
@@ -519,8 +522,11 @@ static int status_to_rc(int st) {
 extern "C" int wfcu_counter_status(wfcu_counter* c, void* stream) {
     if (!c) return fail(WFCU_ERR_INVALID_ARGUMENT, "counter is null");
     int st = 0;
+    u32 wanted = 0;
     CUDA_TRY(cudaMemcpyAsync(&st, c->v.status, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    CUDA_TRY(cudaMemcpyAsync(&wanted, c->v.wanted, sizeof(u32), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
     CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    if (wanted) c->variant_hint = wanted | 1u;
     return status_to_rc(st);
 }
 
@@ -531,8 +537,11 @@ extern "C" int wfcu_counter_stats(wfcu_counter* c, void* stream, uint64_t* disti
     LaunchTally tally;
     CUDA_TRY(tb_key_bytes(c->v, c->counters + 6, c->sm_count, s, &tally.n));
     u64 h[8];
+    u32 wanted = 0;
     CUDA_TRY(cudaMemcpyAsync(h, c->counters, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&wanted, c->v.wanted, sizeof(u32), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
+    if (wanted) c->variant_hint = wanted | 1u;
     if (int rc = status_to_rc((int)(h[5] & 0xFFFFFFFFu))) return rc;
     if (distinct) *distinct = h[0] + h[3];
     if (total_tokens) *total_tokens = h[1];

@@ -214,7 +214,7 @@ using namespace cnt3;
 // HI = true keeps two-byte letters (accented Latin, Greek, Cyrillic ...) on the fast path.  Every
 // CTA picks its variant from a sample of its own part of the text (wc_count_kernel below): the
 // choice affects speed only.
-template <int WARPS, int SETS, int MSLOTS, bool HI>
+template <int WARPS, int SETS, int MSLOTS, bool HI, bool WIDE>
 __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, u32 one, bool u3_cta,
                                               const TableView& gt) {
     extern __shared__ uint8_t smem_raw[];
@@ -439,6 +439,64 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
         if (m1) missbuf[(mtail + n0 + __popc(mm1 & lt_mask)) & (kMissCap - 1)] = make_uint4(b0, b1, 0u, 0u);
         mtail += n0 + __popc(mm1);
     };
+    // WIDE variant (round 2): text where words of 9..16 bytes are common (English prose, the 1 M-word corpus) sent every
+    // pass through the one-token general form above -- 170 instructions per 32 tokens against 125 per 64 for the
+    // two-token short form.  Here ONE direct-mapped combiner of 16-byte keys (the medium table, instantiated with
+    // most of the shared memory) takes every token of up to 16 bytes, two per lane and pass: fetch of five words,
+    // both length masks, one hash over the four key words, key low / key high by two 8-byte loads (low first: a
+    // published low word implies the high word is in place, medium_add's claim protocol), one shared atomic.
+    auto wide_pass = [&](u32 count) {      // count <= 64
+        u32 e0 = q_load(qrd), e1 = q_load(qrd + 64);
+        if ((u32)lane >= count) e0 = 0;
+        if ((u32)lane + 32u >= count) e1 = 0;
+        qrd += 2 * count;
+        qhead += count;
+        const bool live0 = e0 != 0, live1 = e1 != 0;
+        const u32* wp0 = reinterpret_cast<const u32*>(ring + (e0 & 0xFFCu));
+        const u32* wp1 = reinterpret_cast<const u32*>(ring + (e1 & 0xFFCu));
+        const u32 x0 = wp0[0], x1 = wp0[1], x2 = wp0[2], x3 = wp0[3], x4 = wp0[4];
+        const u32 y0 = wp1[0], y1 = wp1[1], y2 = wp1[2], y3 = wp1[3], y4 = wp1[4];
+        const u32 li0 = (e0 >> 9) & 0x78u, li1 = (e1 >> 9) & 0x78u;
+        const uint2 lm0 = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(sm.lomask) + li0);
+        const uint2 hm0 = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(sm.himask) + li0);
+        const uint2 lm1 = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(sm.lomask) + li1);
+        const uint2 hm1 = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(sm.himask) + li1);
+        const u32 a0 = __funnelshift_r(x0, x1, e0 << 3) & lm0.x, a1 = __funnelshift_r(x1, x2, e0 << 3) & lm0.y;
+        const u32 a2 = __funnelshift_r(x2, x3, e0 << 3) & hm0.x, a3 = __funnelshift_r(x3, x4, e0 << 3) & hm0.y;
+        const u32 b0 = __funnelshift_r(y0, y1, e1 << 3) & lm1.x, b1 = __funnelshift_r(y1, y2, e1 << 3) & lm1.y;
+        const u32 b2 = __funnelshift_r(y2, y3, e1 << 3) & hm1.x, b3 = __funnelshift_r(y3, y4, e1 << 3) & hm1.y;
+        u32 ha = a0 * 0x9E3779B1u + a1 * 0x85EBCA77u + a2 * 0xC2B2AE3Du + a3 * 0x27D4EB2Fu;
+        u32 hb = b0 * 0x9E3779B1u + b1 * 0x85EBCA77u + b2 * 0xC2B2AE3Du + b3 * 0x27D4EB2Fu;
+        ha ^= ha >> 16; ha *= 0x2C1B3C6Du;
+        hb ^= hb >> 16; hb *= 0x2C1B3C6Du;
+        const u32 ia = __umulhi(ha, (u32)MSLOTS), ib = __umulhi(hb, (u32)MSLOTS);
+        const u64 ka0 = *reinterpret_cast<volatile u64*>(sm.mk0 + ia), kb0 = *reinterpret_cast<volatile u64*>(sm.mk0 + ib);
+        const u64 ka1 = *reinterpret_cast<volatile u64*>(sm.mk1 + ia), kb1 = *reinterpret_cast<volatile u64*>(sm.mk1 + ib);
+        const u64 wa0 = ((u64)a1 << 32) | a0, wa1 = ((u64)a3 << 32) | a2, wb0 = ((u64)b1 << 32) | b0, wb1 = ((u64)b3 << 32) | b2;
+        const bool fa = live0 && ka0 == wa0 && ka1 == wa1, fb = live1 && kb0 == wb0 && kb1 == wb1;
+        atomicAdd(fa ? sm.mcnt + ia : &sm.dummy[warp], 1u);
+        atomicAdd(fb ? sm.mcnt + ib : &sm.dummy[warp], 1u);
+        const bool ca = live0 && !fa && ka0 == 0, cb = live1 && !fb && kb0 == 0;
+        if (filling && __any_sync(kFull, ca || cb)) {       // claims for FUTURE occurrences; this one still goes out
+            if (ca && atomicCAS(sm.mk0 + ia, 0ull, kSlotLocked) == 0) {
+                *reinterpret_cast<volatile u64*>(sm.mk1 + ia) = wa1;
+                __threadfence_block();
+                atomicExch(sm.mk0 + ia, wa0);
+            }
+            if (cb && atomicCAS(sm.mk0 + ib, 0ull, kSlotLocked) == 0) {
+                *reinterpret_cast<volatile u64*>(sm.mk1 + ib) = wb1;
+                __threadfence_block();
+                atomicExch(sm.mk0 + ib, wb0);
+            }
+        }
+        const bool m0 = live0 && !fa, m1 = live1 && !fb;
+        const u32 mm0 = __ballot_sync(kFull, m0), mm1 = __ballot_sync(kFull, m1);
+        const u32 n0 = __popc(mm0);
+        if ((mtail - mhead) + n0 + __popc(mm1) > (u32)kMissCap) make_room(n0 + __popc(mm1));
+        if (m0) missbuf[(mtail + __popc(mm0 & lt_mask)) & (kMissCap - 1)] = make_uint4(a0, a1, a2, a3);
+        if (m1) missbuf[(mtail + n0 + __popc(mm1 & lt_mask)) & (kMissCap - 1)] = make_uint4(b0, b1, b2, b3);
+        mtail += n0 + __popc(mm1);
+    };
     const std::true_type kFullPass{};
     const std::false_type kPartialPass{};
 
@@ -629,7 +687,8 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
                 const u32 incl = warp_inclusive_sum(cnt);
                 total = __shfl_sync(kFull, incl, 31);
                 if ((qtail - qhead) + total > (u32)kQueueCap) {   // pathological row (tokens of 1-2 bytes): make room first
-                    token_pass(kPartialPass, qtail - qhead, true);
+                    if constexpr (WIDE) wide_pass(qtail - qhead);
+                    else token_pass(kPartialPass, qtail - qhead, true);
                     __syncwarp();
                 }
                 u32 qwr = (qtail + incl - cnt) * 2;               // byte offset of this lane's first entry
@@ -706,16 +765,24 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
             const bool general = general_row || general_prev;   // leftovers are at most one row old
             general_prev = general_row;
             u32 consumed = 0;
-            if (!general) {
-                while (qtail - qhead >= 64) { token_pass2(); consumed += 64; drain_step(); }
+            if constexpr (WIDE) {
+                while (qtail - qhead >= 64) { wide_pass(64u); consumed += 64; drain_step(); }
+                if (still_carried > consumed) wide_pass(qtail - qhead);
+            } else {
+                if (!general) {
+                    while (qtail - qhead >= 64) { token_pass2(); consumed += 64; drain_step(); }
+                }
+                while (qtail - qhead >= 32) { token_pass(kFullPass, 32u, general); consumed += 32; drain_step(); }
+                // ... unless it would outlive its bytes in the ring (the next row overwrites the
+                // slot of the previous one)
+                if (still_carried > consumed) token_pass(kPartialPass, qtail - qhead, general);
             }
-            while (qtail - qhead >= 32) { token_pass(kFullPass, 32u, general); consumed += 32; drain_step(); }
-            // ... unless it would outlive its bytes in the ring (the next row overwrites the
-            // slot of the previous one)
-            if (still_carried > consumed) token_pass(kPartialPass, qtail - qhead, general);
             __syncwarp();
         }
-        if (qtail != qhead) token_pass(kPartialPass, qtail - qhead, true);
+        if (qtail != qhead) {
+            if constexpr (WIDE) wide_pass(qtail - qhead);
+            else token_pass(kPartialPass, qtail - qhead, true);
+        }
         __syncwarp();
         while (mtail != mhead || __any_sync(kFull, dleft != 0)) drain_round();
     }
@@ -742,21 +809,16 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
     if (lane == 0) table_note_inserted(gt, inserted);
 }
 
-// One kernel per variant (a kernel holding both bodies compiles the ASCII one measurably worse);
-// both are launched, and every CTA runs in exactly one of them: it samples one 16-byte chunk per
-// thread, spread evenly over its own rows, and takes HI as soon as two of them hold a byte >= 0x80
-// (HI costs 4 % on pure ASCII; the ASCII body on text with one such fragment in a few hundred
-// already loses more than that to the slow kernel).  The CTA of the other variant sees the same
-// sample and returns.
-// force: 0 / 1 = variant for every CTA (tests), anything else = sample.
-template <int WARPS, int SETS, int MSLOTS, bool HI>
+// One kernel per variant (a kernel holding two bodies compiles the ASCII one measurably worse); every CTA runs in
+// exactly one of the launched kernels (variant_of_cta, wc_count_common.cuh).
+template <int WARPS, int SETS, int MSLOTS, int VARIANT>
 __global__ void __launch_bounds__(WARPS * 32, 1)
 wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, int force, u32 one, TableView gt) {
     bool u3 = false;
-    const bool hi = variant_is_hi(text, n, (u64)blockIdx.x * WARPS * rows_per_warp * kRow, (u64)WARPS * rows_per_warp * kRow, force,
-                                  HI ? &u3 : nullptr);
-    if (hi != HI) return;
-    wc_count_body<WARPS, SETS, MSLOTS, HI>(text, n, rows_per_warp, one, u3, gt);
+    const int v = variant_of_cta(text, n, (u64)blockIdx.x * WARPS * rows_per_warp * kRow, (u64)WARPS * rows_per_warp * kRow, force,
+                                 gt.launched, VARIANT == kVarNarrow ? gt.wanted : nullptr, &u3);
+    if (v != VARIANT) return;
+    wc_count_body<WARPS, SETS, MSLOTS, VARIANT == kVarHi, VARIANT == kVarWide>(text, n, rows_per_warp, one, u3, gt);
 }
 
 // ---- host-side launcher (called from wordcount.cu) ---------------------------------
@@ -766,11 +828,17 @@ wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, int 
 #ifndef WFCU_COUNT_MED_SLOTS
 #define WFCU_COUNT_MED_SLOTS 256
 #endif
+#ifndef WFCU_WIDE_SLOTS
+#define WFCU_WIDE_SLOTS 4800
+#endif
 constexpr int kCountWarps = kCountVariantWarps;
 constexpr int kCountSets = WFCU_COUNT_SETS;             // two 8-byte keys + two counts per set (24 bytes)
 constexpr int kCountMedSlots = WFCU_COUNT_MED_SLOTS;    // 20 bytes each
+constexpr int kWideSets = 64, kWideSlots = WFCU_WIDE_SLOTS;   // WIDE variant: (almost) all of the combiner memory is the 16-byte-key table
 typedef Smem<kCountWarps, kCountSets, kCountMedSlots> CountSmem;
+typedef Smem<kCountWarps, kWideSets, kWideSlots> WideSmem;
 static_assert(sizeof(CountSmem) + 1024 <= 227 * 1024, "shared memory budget");
+static_assert(sizeof(WideSmem) + 1024 <= 227 * 1024, "shared memory budget");
 static_assert(2 * kSlotStride + 20 <= 4096, "queue entries keep ring positions in 12 bits");
 
 // wc_count4.cu: the fourth-generation ASCII body (bulk-TMA rows, tokens counted straight from the masks).  Exact, but
@@ -779,31 +847,43 @@ static_assert(2 * kSlotStride + 20 <= 4096, "queue entries keep ring positions i
 cudaError_t wc_count4_launch(const uint8_t* text, u64 n, u32 rows_per_warp, unsigned grid, int force, const TableView& gt,
                              cudaStream_t stream);
 
-cudaError_t wc_count_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream, u64* launches) {
-    const size_t smem = sizeof(CountSmem) + 1024;   // + slack for the 1 KiB alignment
-    auto k_ascii = wc_count_kernel<kCountWarps, kCountSets, kCountMedSlots, false>;
-    auto k_hi = wc_count_kernel<kCountWarps, kCountSets, kCountMedSlots, true>;
-    cudaError_t e = cudaFuncSetAttribute(k_ascii, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_hi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+// hint: variants the counter's recent texts asked for (bit per variant; the narrow one is always launched)
+cudaError_t wc_count_launch(const uint8_t* text, u64 n, const TableView& gt_in, int sm_count, cudaStream_t stream, u64* launches,
+                            u32 hint) {
+    const size_t smem = sizeof(CountSmem) + 1024, smem_wide = sizeof(WideSmem) + 1024;   // + slack for the 1 KiB alignment
+    auto k_narrow = wc_count_kernel<kCountWarps, kCountSets, kCountMedSlots, kVarNarrow>;
+    auto k_hi = wc_count_kernel<kCountWarps, kCountSets, kCountMedSlots, kVarHi>;
+    auto k_wide = wc_count_kernel<kCountWarps, kWideSets, kWideSlots, kVarWide>;
+    cudaError_t e = cudaFuncSetAttribute(k_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_hi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_wide);
     if (e != cudaSuccess) return e;
     const u64 n_rows = n / kRow + 1;
     u64 grid = (u64)sm_count;
     if (grid * kCountWarps > n_rows) grid = (n_rows + kCountWarps - 1) / kCountWarps;   // at least one row per warp
     if (grid == 0) grid = 1;
     const u64 rows_per_warp = (n_rows + grid * kCountWarps - 1) / (grid * kCountWarps);
-    static const int force = [] { const char* v = getenv("WFCU_COUNT_VARIANT"); return v ? atoi(v) : -1; }();   // tests: 0 / 1
+    static const int force = [] { const char* v = getenv("WFCU_COUNT_VARIANT"); return v ? atoi(v) : -1; }();   // tests: 0..3
     static const bool gen4_ascii = [] { const char* v = getenv("WFCU_COUNT_KERNEL"); return v && v[0] == '4'; }();
-    if (force != 1 && force != 2) {
+    TableView gt = gt_in;
+    gt.launched = force == 0 ? 1u : (force == 1 || force == 2) ? 2u : force == 3 ? 4u : ((hint & 7u) | 1u);
+    if (gt.launched & 1u) {
         if (!gen4_ascii) {
-            k_ascii<<<(unsigned)grid, kCountWarps * 32, smem, stream>>>(text, n, (u32)rows_per_warp, force, 1u, gt);
+            k_narrow<<<(unsigned)grid, kCountWarps * 32, smem, stream>>>(text, n, (u32)rows_per_warp, force, 1u, gt);
         } else {
             e = wc_count4_launch(text, n, (u32)rows_per_warp, (unsigned)grid, force, gt, stream);
             if (e != cudaSuccess) return e;
         }
+        *launches += 1;
     }
-    if (force != 0) k_hi<<<(unsigned)grid, kCountWarps * 32, smem, stream>>>(text, n, (u32)rows_per_warp, force, 1u, gt);
-    *launches += (force == 0 || force == 1 || force == 2) ? 1 : 2;
+    if (gt.launched & 4u) {
+        k_wide<<<(unsigned)grid, kCountWarps * 32, smem_wide, stream>>>(text, n, (u32)rows_per_warp, force, 1u, gt);
+        *launches += 1;
+    }
+    if (gt.launched & 2u) {
+        k_hi<<<(unsigned)grid, kCountWarps * 32, smem, stream>>>(text, n, (u32)rows_per_warp, force, 1u, gt);
+        *launches += 1;
+    }
     return cudaGetLastError();
 }
 

@@ -126,37 +126,61 @@ __device__ __forceinline__ bool medium_add(u64* __restrict__ k0s, u64* __restric
 // ---- which kernel variant a CTA runs ----------------------------------------------------------------
 // Every counting kernel has kCountVariantWarps warps and the same partition of the text (a strip of
 // rows_per_warp KiB rows per warp).  A CTA samples one 16-byte chunk per thread, spread evenly over its own
-// part of the text, and takes the HI variant (two-byte letters on the fast path, wc_count.cu) as soon as two
-// of them hold a byte >= 0x80; the CTA of the other kernel sees the same sample and returns.  The choice
-// affects speed only.  force: 0 / 1 = variant for every CTA (tests), anything else = sample.
+// part of the text, and asks for
+//   kVarHi     (two- and, *u3, three-byte letters on the fast path) as soon as two chunks hold a byte >= 0x80,
+//   kVarWide   (one combiner for all tokens of up to 16 bytes) when 40 of the 896 chunks hold a run of nine or more
+//              non-whitespace bytes (words longer than 8 bytes are common: English prose, the 1 M-word corpus),
+//   kVarNarrow otherwise.
+// The CTA of every other kernel sees the same sample and returns.  The choice affects speed only.  Not every
+// variant is launched every time (TableView::launched: the host launches what the counter's recent texts asked
+// for, TableView::wanted): a CTA whose variant is missing runs the narrow body, which is always there.
+// force: 0 / 1 / 3 = narrow / HI / wide for every CTA, 2 = HI with three-byte letters (tests); else sample.
 #ifndef WFCU_COUNT_WARPS
 #define WFCU_COUNT_WARPS 28
 #endif
 constexpr int kCountVariantWarps = WFCU_COUNT_WARPS;
-// *u3 (may be null): the HI variant should also keep three-byte letters on the fast path (two or more sampled chunks
-// hold a lead E0, E1, E3..EE); force = 2 asks for HI with that for every CTA.
-__device__ __forceinline__ bool variant_is_hi(const uint8_t* __restrict__ text, u64 n, u64 first, u64 span, int force,
-                                              bool* u3 = nullptr) {
-    if (force == 0) return false;
-    const u64 at = (first + (u64)((unsigned __int128)threadIdx.x * span / (kCountVariantWarps * 32))) & ~15ull;
-    bool hit = false, hit3 = false;
-    if (at + 16 <= n) {
-        const uint4 q = *reinterpret_cast<const uint4*>(text + at);
-        hit = ((q.x | q.y | q.z | q.w) & 0x80808080u) != 0;
-        if (hit && u3) {
-            const u32 w4[4] = {q.x, q.y, q.z, q.w};
-            u32 any = 0;
+constexpr int kVarNarrow = 0, kVarHi = 1, kVarWide = 2;
+__device__ __forceinline__ int variant_of_cta(const uint8_t* __restrict__ text, u64 n, u64 first, u64 span, int force,
+                                              u32 launched, unsigned int* wanted_word, bool* u3) {
+    int want = kVarNarrow;
+    *u3 = false;
+    if (force == 0) {
+        want = kVarNarrow;
+    } else if (force == 1 || force == 2) {
+        want = kVarHi;
+        *u3 = force == 2;
+    } else if (force == 3) {
+        want = kVarWide;
+    } else {
+        const u64 at = (first + (u64)((unsigned __int128)threadIdx.x * span / (kCountVariantWarps * 32))) & ~15ull;
+        bool hit = false, hit3 = false, hit9 = false;
+        if (at + 16 <= n) {
+            const uint4 q = *reinterpret_cast<const uint4*>(text + at);
+            hit = ((q.x | q.y | q.z | q.w) & 0x80808080u) != 0;
+            if (hit) {
+                const u32 w4[4] = {q.x, q.y, q.z, q.w};
+                u32 any = 0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const u32 xw = w4[k], v = xw & 0x7F7F7F7Fu;
-                any |= xw & (v + 0x20202020u) & ~(v + 0x11111111u) & ((v ^ 0x62626262u) + 0x7F7F7F7Fu);   // E0..EE, not E2
+                for (int k = 0; k < 4; ++k) {
+                    const u32 xw = w4[k], v = xw & 0x7F7F7F7Fu;
+                    any |= xw & (v + 0x20202020u) & ~(v + 0x11111111u) & ((v ^ 0x62626262u) + 0x7F7F7F7Fu);   // E0..EE, not E2
+                }
+                hit3 = (any & 0x80808080u) != 0;
+            } else {
+                uint4 f;
+                const u32 N = ~(classify16<true>(q, 1u, f).s7 >> 7) & 0xFFFFu;      // non-whitespace bytes of the chunk
+                u32 r = N & (N >> 1);
+                r &= r >> 2;
+                r &= r >> 4;
+                hit9 = (r & (N >> 8)) != 0;
             }
-            hit3 = (any & 0x80808080u) != 0;
         }
+        const int c_hi = __syncthreads_count(hit), c3 = __syncthreads_count(hit3), c9 = __syncthreads_count(hit9);
+        want = c_hi >= 2 ? kVarHi : (c9 >= 40 ? kVarWide : kVarNarrow);
+        *u3 = c3 >= 2;
     }
-    if (u3) *u3 = force == 2 || __syncthreads_count(hit3) >= 2;
-    if (force == 1 || force == 2) return true;
-    return __syncthreads_count(hit) >= 2;
+    if (wanted_word && threadIdx.x == 0) atomicOr(wanted_word, 1u << want);
+    return ((launched >> want) & 1u) ? want : kVarNarrow;
 }
 
 }  // namespace cntc

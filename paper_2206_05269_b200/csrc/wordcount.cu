@@ -748,7 +748,8 @@ size_t wc_fast_smem_bytes() { return sizeof(FastSmem<kFastWarps, kFastSlots, kFa
 
 // wc_count.cu: the counting kernel (third generation).  wc_fast_kernel<.., EMIT = false> stays
 // selectable (WFCU_COUNT_KERNEL=2 in the environment) for A/B runs on the same box.
-cudaError_t wc_count_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream, u64* launches);
+cudaError_t wc_count_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream, u64* launches,
+                            u32 hint);
 static bool use_gen2_count_kernel() {
     static const bool v = [] { const char* e = getenv("WFCU_COUNT_KERNEL"); return e && e[0] == '2'; }();
     return v;
@@ -757,7 +758,7 @@ static bool use_gen2_count_kernel() {
 template <bool EMIT>
 static cudaError_t wc_launch_impl(const uint8_t* text, u64 n, const TableView& gt, const EmitView& em, int sm_count,
                                   cudaStream_t stream, u64* launches, cudaEvent_t* ev_before_fast,
-                                  cudaEvent_t* ev_after_fast) {
+                                  cudaEvent_t* ev_after_fast, u32 variant_hint) {
     const size_t smem = wc_fast_smem_bytes();
     auto kernel = wc_fast_kernel<kFastWarps, kFastSlots, kFastMedSlots, EMIT>;
     {
@@ -772,7 +773,7 @@ static cudaError_t wc_launch_impl(const uint8_t* text, u64 n, const TableView& g
     const u64 rows_per_warp = (n_rows + grid * kFastWarps - 1) / (grid * kFastWarps);
     if (ev_before_fast) cudaEventRecord(*ev_before_fast, stream);
     if (!EMIT && !use_gen2_count_kernel()) {
-        cudaError_t e = wc_count_launch(text, n, gt, sm_count, stream, launches);
+        cudaError_t e = wc_count_launch(text, n, gt, sm_count, stream, launches, variant_hint);
         if (e != cudaSuccess) return e;
     } else {
         kernel<<<(unsigned)grid, kFastWarps * 32, smem, stream>>>(text, n, rows_per_warp, gt, em);
@@ -790,9 +791,9 @@ static cudaError_t wc_launch_impl(const uint8_t* text, u64 n, const TableView& g
 
 // count text[0..n) into the tables of gt
 cudaError_t wc_launch(const uint8_t* text, u64 n, const TableView& gt, int sm_count, cudaStream_t stream,
-                      u64* launches, cudaEvent_t* ev_before_fast, cudaEvent_t* ev_after_fast) {
+                      u64* launches, cudaEvent_t* ev_before_fast, cudaEvent_t* ev_after_fast, u32 variant_hint) {
     return wc_launch_impl<false>(text, n, gt, EmitView{}, sm_count, stream, launches,
-                                 ev_before_fast, ev_after_fast);
+                                 ev_before_fast, ev_after_fast, variant_hint);
 }
 
 cudaError_t wc_normalize_launch(const uint8_t* text, const u64* offsets, u64 n_frag, const TableView& gt,
@@ -809,7 +810,7 @@ cudaError_t wc_normalize_launch(const uint8_t* text, const u64* offsets, u64 n_f
 // deferred list, the long-token arena and the status word; its tables stay untouched)
 cudaError_t wc_tokenize_launch(const uint8_t* text, u64 n, const TableView& gt, const EmitView& em, int sm_count,
                                cudaStream_t stream, u64* launches) {
-    return wc_launch_impl<true>(text, n, gt, em, sm_count, stream, launches, nullptr, nullptr);
+    return wc_launch_impl<true>(text, n, gt, em, sm_count, stream, launches, nullptr, nullptr, 7u);
 }
 
 }  // namespace wfcu
