@@ -331,7 +331,7 @@ struct wfcu_counter {
     u64* counters = nullptr;    // device: [0] n_used [1] n_tokens [2] n_deferred [3] n_long [4] arena_used
                                 //         [5] status(int) [6..15] scratch [16] CTA ticket of the reset kernel
     bool aux_clean = false;     // the long table and the counters have been initialised once
-    u32 variant_hint = 7;       // kernel variants the texts counted so far asked for (counters[17]), read at every
+    u32 variant_hint = 15;       // kernel variants the texts counted so far asked for (counters[17]), read at every
                                 // synchronising call: later counts launch only those (and the narrow one)
     // host staging for count_host
     uint8_t* pinned[2] = {nullptr, nullptr};

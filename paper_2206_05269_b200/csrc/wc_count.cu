@@ -479,12 +479,12 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
         const bool ca = live0 && !fa && ka0 == 0, cb = live1 && !fb && kb0 == 0;
         if (filling && __any_sync(kFull, ca || cb)) {       // claims for FUTURE occurrences; this one still goes out
             if (ca && atomicCAS(sm.mk0 + ia, 0ull, kSlotLocked) == 0) {
-                *reinterpret_cast<volatile u64*>(sm.mk1 + ia) = wa1;
+                atomicExch(sm.mk1 + ia, wa1);      // (an atomic: other warps read the high word before they know whether the low one matches)
                 __threadfence_block();
                 atomicExch(sm.mk0 + ia, wa0);
             }
             if (cb && atomicCAS(sm.mk0 + ib, 0ull, kSlotLocked) == 0) {
-                *reinterpret_cast<volatile u64*>(sm.mk1 + ib) = wb1;
+                atomicExch(sm.mk1 + ib, wb1);
                 __threadfence_block();
                 atomicExch(sm.mk0 + ib, wb0);
             }
@@ -810,15 +810,15 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
 }
 
 // One kernel per variant (a kernel holding two bodies compiles the ASCII one measurably worse); every CTA runs in
-// exactly one of the launched kernels (variant_of_cta, wc_count_common.cuh).
+// exactly one of the launched kernels, the same one for all CTAs of a call (variant_of_text, wc_count_common.cuh).
 template <int WARPS, int SETS, int MSLOTS, int VARIANT>
 __global__ void __launch_bounds__(WARPS * 32, 1)
 wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, int force, u32 one, TableView gt) {
     bool u3 = false;
-    const int v = variant_of_cta(text, n, (u64)blockIdx.x * WARPS * rows_per_warp * kRow, (u64)WARPS * rows_per_warp * kRow, force,
-                                 gt.launched, VARIANT == kVarNarrow ? gt.wanted : nullptr, &u3);
+    const int v = variant_of_text(text, n, force, gt.launched, VARIANT == kVarNarrow ? gt.wanted : nullptr, &u3);
     if (v != VARIANT) return;
-    wc_count_body<WARPS, SETS, MSLOTS, VARIANT == kVarHi, VARIANT == kVarWide>(text, n, rows_per_warp, one, u3, gt);
+    wc_count_body<WARPS, SETS, MSLOTS, VARIANT == kVarHi || VARIANT == kVarHiWide, VARIANT == kVarWide || VARIANT == kVarHiWide>(
+        text, n, rows_per_warp, one, u3, gt);
 }
 
 // ---- host-side launcher (called from wordcount.cu) ---------------------------------
@@ -854,19 +854,21 @@ cudaError_t wc_count_launch(const uint8_t* text, u64 n, const TableView& gt_in, 
     auto k_narrow = wc_count_kernel<kCountWarps, kCountSets, kCountMedSlots, kVarNarrow>;
     auto k_hi = wc_count_kernel<kCountWarps, kCountSets, kCountMedSlots, kVarHi>;
     auto k_wide = wc_count_kernel<kCountWarps, kWideSets, kWideSlots, kVarWide>;
+    auto k_hiwide = wc_count_kernel<kCountWarps, kWideSets, kWideSlots, kVarHiWide>;
     cudaError_t e = cudaFuncSetAttribute(k_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_hi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_wide);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_hiwide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_wide);
     if (e != cudaSuccess) return e;
     const u64 n_rows = n / kRow + 1;
     u64 grid = (u64)sm_count;
     if (grid * kCountWarps > n_rows) grid = (n_rows + kCountWarps - 1) / kCountWarps;   // at least one row per warp
     if (grid == 0) grid = 1;
     const u64 rows_per_warp = (n_rows + grid * kCountWarps - 1) / (grid * kCountWarps);
-    static const int force = [] { const char* v = getenv("WFCU_COUNT_VARIANT"); return v ? atoi(v) : -1; }();   // tests: 0..3
+    static const int force = [] { const char* v = getenv("WFCU_COUNT_VARIANT"); return v ? atoi(v) : -1; }();   // tests: 0..5
     static const bool gen4_ascii = [] { const char* v = getenv("WFCU_COUNT_KERNEL"); return v && v[0] == '4'; }();
     TableView gt = gt_in;
-    gt.launched = force == 0 ? 1u : (force == 1 || force == 2) ? 2u : force == 3 ? 4u : ((hint & 7u) | 1u);
+    gt.launched = force == 0 ? 1u : (force == 1 || force == 2) ? 2u : force == 3 ? 4u : (force == 4 || force == 5) ? 8u : ((hint & 15u) | 1u);
     if (gt.launched & 1u) {
         if (!gen4_ascii) {
             k_narrow<<<(unsigned)grid, kCountWarps * 32, smem, stream>>>(text, n, (u32)rows_per_warp, force, 1u, gt);
@@ -878,6 +880,10 @@ cudaError_t wc_count_launch(const uint8_t* text, u64 n, const TableView& gt_in, 
     }
     if (gt.launched & 4u) {
         k_wide<<<(unsigned)grid, kCountWarps * 32, smem_wide, stream>>>(text, n, (u32)rows_per_warp, force, 1u, gt);
+        *launches += 1;
+    }
+    if (gt.launched & 8u) {
+        k_hiwide<<<(unsigned)grid, kCountWarps * 32, smem_wide, stream>>>(text, n, (u32)rows_per_warp, force, 1u, gt);
         *launches += 1;
     }
     if (gt.launched & 2u) {

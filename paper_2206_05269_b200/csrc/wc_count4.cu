@@ -577,8 +577,7 @@ template <int WARPS, int SETS, int MSLOTS>
 __global__ void __launch_bounds__(WARPS * 32, 1)
 wc_count4_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, int force, TableView gt) {
     bool u3 = false;
-    if (variant_of_cta(text, n, (u64)blockIdx.x * WARPS * rows_per_warp * kRow, (u64)WARPS * rows_per_warp * kRow, force,
-                       gt.launched, gt.wanted, &u3) != kVarNarrow)
+    if (variant_of_text(text, n, force, gt.launched, gt.wanted, &u3) != kVarNarrow)
         return;
     wc_count4_body<WARPS, SETS, MSLOTS>(text, n, rows_per_warp, gt);
 }

@@ -123,25 +123,33 @@ __device__ __forceinline__ bool medium_add(u64* __restrict__ k0s, u64* __restric
     return false;
 }
 
-// ---- which kernel variant a CTA runs ----------------------------------------------------------------
+// ---- which kernel variant counts a text ------------------------------------------------------------
 // Every counting kernel has kCountVariantWarps warps and the same partition of the text (a strip of
-// rows_per_warp KiB rows per warp).  A CTA samples one 16-byte chunk per thread, spread evenly over its own
-// part of the text, and asks for
+// rows_per_warp KiB rows per warp).  Every CTA of every launched kernel reads the SAME sample -- one 16-byte chunk per
+// thread, spread evenly over the whole text -- and so reaches the same answer without communicating:
 //   kVarHi     (two- and, *u3, three-byte letters on the fast path) as soon as two chunks hold a byte >= 0x80,
-//   kVarWide   (one combiner for all tokens of up to 16 bytes) when 40 of the 896 chunks hold a run of nine or more
-//              non-whitespace bytes (words longer than 8 bytes are common: English prose, the 1 M-word corpus),
+//   kVarWide   (one combiner for all tokens of up to 16 bytes) when 20 of the 896 chunks hold a run of nine or more
+//              word characters (non-whitespace bytes in chunks with bytes >= 0x80): words longer than 8 bytes are
+//              common -- English prose, the 1 M-word corpus,
+//   kVarHiWide (both) when both hold,
 //   kVarNarrow otherwise.
-// The CTA of every other kernel sees the same sample and returns.  The choice affects speed only.  Not every
-// variant is launched every time (TableView::launched: the host launches what the counter's recent texts asked
-// for, TableView::wanted): a CTA whose variant is missing runs the narrow body, which is always there.
-// force: 0 / 1 / 3 = narrow / HI / wide for every CTA, 2 = HI with three-byte letters (tests); else sample.
+// The CTAs of the other kernels return.  The choice affects speed only.  It is one choice per call, not per CTA: the
+// kernels of a call run one after the other, each with one CTA per SM, so CTAs that disagreed (a sample near a
+// threshold, a mixed corpus) would leave SMs idle in every kernel -- measured: text with 13 % kana words at 194 GB/s
+// when its CTAs split between two variants, 400 GB/s under either of them.  Callers that stream a corpus in chunks
+// (wfcu_counter_count_host: 32 MiB) get one choice per chunk.
+// Not every variant is launched every time (TableView::launched: the host launches what the counter's recent texts
+// asked for, TableView::wanted): a text whose variant is missing runs the narrow body, which is always there (HI if it
+// wanted HI + wide and only HI was launched).
+// force: 0 / 1 / 3 / 4 = narrow / HI / wide / HI + wide, 2 / 5 = HI / HI + wide with three-byte letters (tests);
+// else sample.
 #ifndef WFCU_COUNT_WARPS
 #define WFCU_COUNT_WARPS 28
 #endif
 constexpr int kCountVariantWarps = WFCU_COUNT_WARPS;
-constexpr int kVarNarrow = 0, kVarHi = 1, kVarWide = 2;
-__device__ __forceinline__ int variant_of_cta(const uint8_t* __restrict__ text, u64 n, u64 first, u64 span, int force,
-                                              u32 launched, unsigned int* wanted_word, bool* u3) {
+constexpr int kVarNarrow = 0, kVarHi = 1, kVarWide = 2, kVarHiWide = 3;
+__device__ __forceinline__ int variant_of_text(const uint8_t* __restrict__ text, u64 n, int force, u32 launched,
+                                               unsigned int* wanted_word, bool* u3) {
     int want = kVarNarrow;
     *u3 = false;
     if (force == 0) {
@@ -151,8 +159,11 @@ __device__ __forceinline__ int variant_of_cta(const uint8_t* __restrict__ text, 
         *u3 = force == 2;
     } else if (force == 3) {
         want = kVarWide;
+    } else if (force == 4 || force == 5) {
+        want = kVarHiWide;
+        *u3 = force == 5;
     } else {
-        const u64 at = (first + (u64)((unsigned __int128)threadIdx.x * span / (kCountVariantWarps * 32))) & ~15ull;
+        const u64 at = ((u64)threadIdx.x * (n / (u64)(kCountVariantWarps * 32))) & ~15ull;
         bool hit = false, hit3 = false, hit9 = false;
         if (at + 16 <= n) {
             const uint4 q = *reinterpret_cast<const uint4*>(text + at);
@@ -166,21 +177,24 @@ __device__ __forceinline__ int variant_of_cta(const uint8_t* __restrict__ text, 
                     any |= xw & (v + 0x20202020u) & ~(v + 0x11111111u) & ((v ^ 0x62626262u) + 0x7F7F7F7Fu);   // E0..EE, not E2
                 }
                 hit3 = (any & 0x80808080u) != 0;
-            } else {
-                uint4 f;
-                const u32 N = ~(classify16<true>(q, 1u, f).s7 >> 7) & 0xFFFFu;      // non-whitespace bytes of the chunk
-                u32 r = N & (N >> 1);
-                r &= r >> 2;
-                r &= r >> 4;
-                hit9 = (r & (N >> 8)) != 0;
             }
+            // a run of nine: of word characters in an ASCII chunk (a token longer than 8 bytes for certain), of
+            // non-whitespace bytes in a chunk with bytes >= 0x80 (what is a letter there is the kernels' business)
+            uint4 f;
+            const Masks m = classify16<false>(q, 1u, f);
+            const u32 N = (hit ? ~(m.s7 >> 7) : (m.a7 >> 7)) & 0xFFFFu;
+            u32 r = N & (N >> 1);
+            r &= r >> 2;
+            r &= r >> 4;
+            hit9 = (r & (N >> 8)) != 0;
         }
         const int c_hi = __syncthreads_count(hit), c3 = __syncthreads_count(hit3), c9 = __syncthreads_count(hit9);
-        want = c_hi >= 2 ? kVarHi : (c9 >= 40 ? kVarWide : kVarNarrow);
+        want = c_hi >= 2 ? (c9 >= 20 ? kVarHiWide : kVarHi) : (c9 >= 20 ? kVarWide : kVarNarrow);
         *u3 = c3 >= 2;
     }
-    if (wanted_word && threadIdx.x == 0) atomicOr(wanted_word, 1u << want);
-    return ((launched >> want) & 1u) ? want : kVarNarrow;
+    if (wanted_word && threadIdx.x == 0 && blockIdx.x == 0) atomicOr(wanted_word, 1u << want);
+    if ((launched >> want) & 1u) return want;
+    return (want == kVarHiWide && ((launched >> kVarHi) & 1u)) ? kVarHi : kVarNarrow;
 }
 
 }  // namespace cntc
