@@ -141,6 +141,147 @@ struct LaunchTally {   // adds to the global launch counter on scope exit
 };
 
 // ---- device state -----------------------------------------------------------------
+namespace {
+// Device-memory cache.  cudaMalloc + cudaFree of the library's buffers cost more host time than the kernels that use
+// them -- gigabyte-sized scratch of the token / export paths, but also the 240 MB of a default counter (38 ms per
+// create + destroy on the virtualised B200 hosts) and the staging buffer of every *_host call.  Every device
+// allocation of the library comes from here: freed blocks are kept (per device, up to kScratchKeepBytes in all,
+// WFCU_CACHE_KEEP_MB overrides) and handed out again to requests they fit within a factor of two; an allocation
+// that fails gives the cached blocks back to the driver and tries once more.  scratch_free waits for the block's
+// device like cudaFree does, so callers keep cudaFree's ordering guarantees; blocks that did not come from here
+// (wfcu_dev_free of a foreign pointer) go to cudaFree.
+struct ScratchBlock { void* p; size_t bytes; int device; };
+std::mutex g_scratch_mu;
+std::vector<ScratchBlock> g_scratch_free;
+std::vector<ScratchBlock> g_scratch_live;
+size_t scratch_keep_bytes() {
+    static const size_t keep = [] {
+        const char* v = getenv("WFCU_CACHE_KEEP_MB");
+        return v ? (size_t)strtoull(v, nullptr, 10) << 20 : size_t(24) << 30;
+    }();
+    return keep;
+}
+
+cudaError_t scratch_alloc(void** out, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lock(g_scratch_mu);
+        size_t best = g_scratch_free.size();
+        for (size_t i = 0; i < g_scratch_free.size(); ++i) {
+            const ScratchBlock& b = g_scratch_free[i];
+            if (b.device == dev && b.bytes >= bytes && b.bytes <= 2 * bytes + 4096 &&
+                (best == g_scratch_free.size() || b.bytes < g_scratch_free[best].bytes))
+                best = i;
+        }
+        if (best != g_scratch_free.size()) {
+            *out = g_scratch_free[best].p;
+            g_scratch_live.push_back(g_scratch_free[best]);
+            g_scratch_free.erase(g_scratch_free.begin() + best);
+            return cudaSuccess;
+        }
+    }
+    cudaError_t e = cudaMalloc(out, bytes);
+    if (e != cudaSuccess) {   // give the cached blocks back and try once more
+        cudaGetLastError();
+        std::lock_guard<std::mutex> lock(g_scratch_mu);
+        for (const ScratchBlock& b : g_scratch_free) cudaFree(b.p);
+        g_scratch_free.clear();
+        e = cudaMalloc(out, bytes);
+        if (e != cudaSuccess) return e;
+    }
+    std::lock_guard<std::mutex> lock(g_scratch_mu);
+    g_scratch_live.push_back({*out, bytes, dev});
+    return cudaSuccess;
+}
+template <typename T>
+cudaError_t scratch_alloc(T** out, size_t bytes) { return scratch_alloc(reinterpret_cast<void**>(out), bytes); }
+
+void scratch_free(void* p) {
+    if (!p) return;
+    ScratchBlock blk{nullptr, 0, -1};
+    {
+        std::lock_guard<std::mutex> lock(g_scratch_mu);
+        for (size_t i = 0; i < g_scratch_live.size(); ++i) {
+            if (g_scratch_live[i].p != p) continue;
+            blk = g_scratch_live[i];
+            g_scratch_live.erase(g_scratch_live.begin() + i);
+            break;
+        }
+    }
+    if (!blk.p) {
+        cudaFree(p);                  // not ours
+        return;
+    }
+    int cur = 0;                      // what cudaFree would have done: wait for the device that owns the block
+    cudaGetDevice(&cur);
+    if (cur != blk.device) cudaSetDevice(blk.device);
+    cudaDeviceSynchronize();
+    if (cur != blk.device) cudaSetDevice(cur);
+    std::vector<void*> release;
+    {
+        std::lock_guard<std::mutex> lock(g_scratch_mu);
+        g_scratch_free.push_back(blk);
+        size_t kept = 0;
+        for (const ScratchBlock& b : g_scratch_free) kept += b.bytes;
+        while (kept > scratch_keep_bytes() && !g_scratch_free.empty()) {   // oldest first
+            kept -= g_scratch_free.front().bytes;
+            release.push_back(g_scratch_free.front().p);
+            g_scratch_free.erase(g_scratch_free.begin());
+        }
+    }
+    for (void* q : release) cudaFree(q);
+}
+
+
+// The same for page-locked host staging (cudaHostAlloc of 2 x 32 MiB costs tens of milliseconds): exact-size reuse,
+// at most 1 GiB kept.  A buffer is only released by its counter after the copies out of it have completed.
+struct PinnedBlock { void* p; size_t bytes; };
+std::vector<PinnedBlock> g_pinned_free;
+std::vector<PinnedBlock> g_pinned_live;
+cudaError_t pinned_alloc(void** out, size_t bytes) {
+    {
+        std::lock_guard<std::mutex> lock(g_scratch_mu);
+        for (size_t i = 0; i < g_pinned_free.size(); ++i) {
+            if (g_pinned_free[i].bytes != bytes) continue;
+            *out = g_pinned_free[i].p;
+            g_pinned_live.push_back(g_pinned_free[i]);
+            g_pinned_free.erase(g_pinned_free.begin() + i);
+            return cudaSuccess;
+        }
+    }
+    const cudaError_t e = cudaHostAlloc(out, bytes, cudaHostAllocPortable);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(g_scratch_mu);
+    g_pinned_live.push_back({*out, bytes});
+    return cudaSuccess;
+}
+void pinned_free(void* p) {
+    if (!p) return;
+    std::vector<void*> release;
+    {
+        std::lock_guard<std::mutex> lock(g_scratch_mu);
+        for (size_t i = 0; i < g_pinned_live.size(); ++i) {
+            if (g_pinned_live[i].p != p) continue;
+            g_pinned_free.push_back(g_pinned_live[i]);
+            g_pinned_live.erase(g_pinned_live.begin() + i);
+            size_t kept = 0;
+            for (const PinnedBlock& b : g_pinned_free) kept += b.bytes;
+            while (kept > (size_t(1) << 30) && !g_pinned_free.empty()) {
+                kept -= g_pinned_free.front().bytes;
+                release.push_back(g_pinned_free.front().p);
+                g_pinned_free.erase(g_pinned_free.begin());
+            }
+            p = nullptr;
+            break;
+        }
+    }
+    if (p) release.push_back(p);      // not ours
+    for (void* q : release) cudaFreeHost(q);
+}
+}  // namespace
+
 struct DeviceState {
     bool ready = false;
     int sm_count = 0;
@@ -258,9 +399,9 @@ extern "C" int wfcu_map_reduce_blocked_dev(const void* dev_values, int dtype, ui
     if (!out) return fail(WFCU_ERR_INVALID_ARGUMENT, "out is null");
     const u64 nb = (n + block_size - 1) / block_size;
     double *a = nullptr, *b = nullptr;
-    CUDA_TRY(cudaMalloc(&a, sizeof(double) * std::max<u64>(nb, 1)));
-    if (cudaMalloc(&b, sizeof(double) * std::max<u64>(nb / 2 + 1, 1)) != cudaSuccess) {
-        cudaFree(a);
+    CUDA_TRY(scratch_alloc(&a, sizeof(double) * std::max<u64>(nb, 1)));
+    if (scratch_alloc(&b, sizeof(double) * std::max<u64>(nb / 2 + 1, 1)) != cudaSuccess) {
+        scratch_free(a);
         return fail(WFCU_ERR_CUDA, "cudaMalloc of the partials failed");
     }
     LaunchTally tally;
@@ -268,8 +409,8 @@ extern "C" int wfcu_map_reduce_blocked_dev(const void* dev_values, int dtype, ui
                                       d->mr_out, d->sm_count, (cudaStream_t)stream, &tally.n);
     if (e == cudaSuccess) e = cudaMemcpyAsync(out, d->mr_out, sizeof(double), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
-    cudaFree(a);
-    cudaFree(b);
+    scratch_free(a);
+    scratch_free(b);
     if (e != cudaSuccess) return fail(WFCU_ERR_CUDA, "blocked map-reduce: %s", cudaGetErrorString(e));
     return WFCU_OK;
 }
@@ -277,10 +418,10 @@ extern "C" int wfcu_map_reduce_blocked_dev(const void* dev_values, int dtype, ui
 static int upload(const void* host, uint64_t bytes, void** dev) {
     *dev = nullptr;
     if (bytes == 0) return WFCU_OK;
-    CUDA_TRY(cudaMalloc(dev, bytes));
+    CUDA_TRY(scratch_alloc(dev, bytes));
     cudaError_t e = cudaMemcpy(*dev, host, bytes, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
-        cudaFree(*dev);
+        scratch_free(*dev);
         *dev = nullptr;
         return fail(WFCU_ERR_CUDA, "H2D copy: %s", cudaGetErrorString(e));
     }
@@ -297,7 +438,7 @@ extern "C" int wfcu_map_reduce_host(const void* host_values, int dtype, uint64_t
     if (map_kind != WFCU_MAP_ALTERNATING_HARMONIC_TERM)
         if (int rc = upload(host_values, n * esz, &dev)) return rc;
     const int rc = wfcu_map_reduce_dev(dev, dtype, n, 0, map_kind, nullptr, out);
-    cudaFree(dev);
+    scratch_free(dev);
     return rc;
 }
 
@@ -313,7 +454,7 @@ extern "C" int wfcu_map_reduce_blocked_host(const void* host_values, int dtype, 
     if (map_kind != WFCU_MAP_ALTERNATING_HARMONIC_TERM)
         if (int rc = upload(host_values, n * esz, &dev)) return rc;
     const int rc = wfcu_map_reduce_blocked_dev(dev, dtype, n, 0, map_kind, block_size, nullptr, out);
-    cudaFree(dev);
+    scratch_free(dev);
     return rc;
 }
 
@@ -361,23 +502,30 @@ static u64 round_pow2(u64 x) {
 
 static void counter_free(wfcu_counter* c) {
     if (!c) return;
-    cudaFree(c->v.slots);
-    cudaFree(c->v.deferred);
-    cudaFree(c->v.long_ref);
-    cudaFree(c->v.long_count);
-    cudaFree(c->v.arena);
-    cudaFree(c->counters);
+    {   // nothing of this counter may still be running when its buffers go back to the caches
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (cur != c->device) cudaSetDevice(c->device);
+        cudaDeviceSynchronize();
+        if (cur != c->device) cudaSetDevice(cur);
+    }
+    scratch_free(c->v.slots);
+    scratch_free(c->v.deferred);
+    scratch_free(c->v.long_ref);
+    scratch_free(c->v.long_count);
+    scratch_free(c->v.arena);
+    scratch_free(c->counters);
     for (int i = 0; i < 2; ++i) {
-        if (c->pinned[i]) cudaFreeHost(c->pinned[i]);
-        if (c->devbuf[i]) cudaFree(c->devbuf[i]);
+        if (c->pinned[i]) pinned_free(c->pinned[i]);
+        if (c->devbuf[i]) scratch_free(c->devbuf[i]);
         if (c->done[i]) cudaEventDestroy(c->done[i]);
     }
     for (int i = 0; i < 2; ++i) {
-        if (c->dma_buf[i]) cudaFree(c->dma_buf[i]);
+        if (c->dma_buf[i]) scratch_free(c->dma_buf[i]);
         if (c->copied[i]) cudaEventDestroy(c->copied[i]);
         if (c->counted[i]) cudaEventDestroy(c->counted[i]);
     }
-    for (void* b : c->ex_buf) if (b) cudaFree(b);
+    for (void* b : c->ex_buf) if (b) scratch_free(b);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->stream) cudaStreamDestroy(c->stream);
     for (auto& pr : c->timed) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
@@ -420,7 +568,7 @@ extern "C" int wfcu_counter_create(wfcu_counter** out, const wfcu_counter_config
     const u64 arena = k.arena_bytes ? std::max<u64>(k.arena_bytes, 4096) : (64ull << 20);
     cudaError_t e = cudaSuccess;
     auto alloc = [&](void** p, u64 bytes) {
-        if (e == cudaSuccess) e = cudaMalloc(p, bytes);
+        if (e == cudaSuccess) e = scratch_alloc(p, bytes);
     };
     alloc((void**)&c->v.slots, sizeof(Slot) * c->table_slots);
     alloc((void**)&c->v.deferred, sizeof(u64) * deferred);
@@ -550,70 +698,6 @@ extern "C" int wfcu_counter_stats(wfcu_counter* c, void* stream, uint64_t* disti
 }
 
 namespace {
-// Scratch cache: the token / export paths need gigabyte-sized scratch per call, and cudaMalloc + cudaFree
-// of such buffers cost more host time than their kernels.  Freed blocks are kept (per device, up to
-// kScratchKeepBytes) and handed out again to requests they fit within a factor of two.  scratch_free
-// waits for the device like cudaFree does, so callers keep cudaFree's ordering guarantees.
-constexpr size_t kScratchKeepBytes = size_t(24) << 30;
-struct ScratchBlock { void* p; size_t bytes; int device; };
-std::mutex g_scratch_mu;
-std::vector<ScratchBlock> g_scratch_free;
-std::vector<ScratchBlock> g_scratch_live;
-
-cudaError_t scratch_alloc(void** out, size_t bytes) {
-    if (bytes == 0) bytes = 16;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    {
-        std::lock_guard<std::mutex> lock(g_scratch_mu);
-        size_t best = g_scratch_free.size();
-        for (size_t i = 0; i < g_scratch_free.size(); ++i) {
-            const ScratchBlock& b = g_scratch_free[i];
-            if (b.device == dev && b.bytes >= bytes && b.bytes <= 2 * bytes + 4096 &&
-                (best == g_scratch_free.size() || b.bytes < g_scratch_free[best].bytes))
-                best = i;
-        }
-        if (best != g_scratch_free.size()) {
-            *out = g_scratch_free[best].p;
-            g_scratch_live.push_back(g_scratch_free[best]);
-            g_scratch_free.erase(g_scratch_free.begin() + best);
-            return cudaSuccess;
-        }
-    }
-    cudaError_t e = cudaMalloc(out, bytes);
-    if (e != cudaSuccess) {   // give the cached blocks back and try once more
-        cudaGetLastError();
-        std::lock_guard<std::mutex> lock(g_scratch_mu);
-        for (const ScratchBlock& b : g_scratch_free) cudaFree(b.p);
-        g_scratch_free.clear();
-        e = cudaMalloc(out, bytes);
-        if (e != cudaSuccess) return e;
-    }
-    std::lock_guard<std::mutex> lock(g_scratch_mu);
-    g_scratch_live.push_back({*out, bytes, dev});
-    return cudaSuccess;
-}
-
-void scratch_free(void* p) {
-    if (!p) return;
-    cudaDeviceSynchronize();          // what cudaFree would have done
-    std::lock_guard<std::mutex> lock(g_scratch_mu);
-    for (size_t i = 0; i < g_scratch_live.size(); ++i) {
-        if (g_scratch_live[i].p != p) continue;
-        g_scratch_free.push_back(g_scratch_live[i]);
-        g_scratch_live.erase(g_scratch_live.begin() + i);
-        size_t kept = 0;
-        for (const ScratchBlock& b : g_scratch_free) kept += b.bytes;
-        while (kept > kScratchKeepBytes && !g_scratch_free.empty()) {   // oldest first
-            kept -= g_scratch_free.front().bytes;
-            cudaFree(g_scratch_free.front().p);
-            g_scratch_free.erase(g_scratch_free.begin());
-        }
-        return;
-    }
-    cudaFree(p);                      // not ours
-}
-
 struct DevBuf {   // RAII device scratch
     void* p = nullptr;
     cudaError_t alloc(size_t bytes) { return scratch_alloc(&p, bytes); }
@@ -688,11 +772,11 @@ static int counter_pull_sorted(wfcu_counter* c, cudaStream_t s, std::vector<Host
 // grow-only device scratch of the counter (slot i), so that an export allocates nothing in steady state
 static int ex_reserve(wfcu_counter* c, int i, u64 bytes) {
     if (c->ex_cap[i] >= bytes) return WFCU_OK;
-    if (c->ex_buf[i]) cudaFree(c->ex_buf[i]);
+    if (c->ex_buf[i]) scratch_free(c->ex_buf[i]);
     c->ex_buf[i] = nullptr;
     c->ex_cap[i] = 0;
     const u64 want = std::max<u64>(bytes + bytes / 4, 4096);
-    CUDA_TRY(cudaMalloc(&c->ex_buf[i], want));
+    CUDA_TRY(scratch_alloc(&c->ex_buf[i], want));
     c->ex_cap[i] = want;
     return WFCU_OK;
 }
@@ -977,14 +1061,14 @@ extern "C" int wfcu_counter_merge(wfcu_counter* dst, const wfcu_counter* src, vo
     if (h[3]) {
         uint8_t* buf = nullptr;
         const u64 cap = h[4] + 16 * h[3] + 64;
-        CUDA_TRY(cudaMalloc(&buf, cap));
+        CUDA_TRY(scratch_alloc(&buf, cap));
         cudaError_t e = tb_long_serialize(src->v, buf, cap, dst->counters + 8, dst->sm_count, s, &tally.n);
         u64 nbytes = 0;
         if (e == cudaSuccess) e = cudaMemcpyAsync(&nbytes, dst->counters + 8, sizeof(u64), cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e == cudaSuccess) e = tb_long_merge(dst->v, buf, nbytes, 0, 1, s, &tally.n);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        cudaFree(buf);
+        scratch_free(buf);
         if (e != cudaSuccess) return fail(WFCU_ERR_CUDA, "long-token merge: %s", cudaGetErrorString(e));
     }
     return WFCU_OK;
@@ -1024,7 +1108,7 @@ extern "C" int wfcu_counter_add_words(wfcu_counter* c, const uint8_t* key_bytes,
         if (int rc = upload(inl.data(), inl.size() * sizeof(Slot), &dev)) return rc;
         cudaError_t e = tb_merge_entries(c->v, static_cast<const Slot*>(dev), inl.size(), c->sm_count, nullptr, &tally.n);
         if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
-        cudaFree(dev);
+        scratch_free(dev);
         if (e != cudaSuccess) return fail(WFCU_ERR_CUDA, "add_words: %s", cudaGetErrorString(e));
     }
     if (!longs.empty()) {
@@ -1032,7 +1116,7 @@ extern "C" int wfcu_counter_add_words(wfcu_counter* c, const uint8_t* key_bytes,
         if (int rc = upload(longs.data(), longs.size(), &dev)) return rc;
         cudaError_t e = tb_long_merge(c->v, static_cast<const uint8_t*>(dev), longs.size(), 0, 1, nullptr, &tally.n);
         if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
-        cudaFree(dev);
+        scratch_free(dev);
         if (e != cudaSuccess) return fail(WFCU_ERR_CUDA, "add_words: %s", cudaGetErrorString(e));
     }
     return WFCU_OK;
@@ -1041,16 +1125,17 @@ extern "C" int wfcu_counter_add_words(wfcu_counter* c, const uint8_t* key_bytes,
 // ---- host-buffer counting (the reference-facing call) ----------------------------------
 static int ensure_staging(wfcu_counter* c, u64 want) {
     if (c->chunk_cap >= want) return WFCU_OK;
+    if (c->chunk_cap) CUDA_TRY(cudaDeviceSynchronize());
     for (int i = 0; i < 2; ++i) {
-        if (c->pinned[i]) cudaFreeHost(c->pinned[i]);
-        if (c->devbuf[i]) cudaFree(c->devbuf[i]);
+        if (c->pinned[i]) pinned_free(c->pinned[i]);
+        if (c->devbuf[i]) scratch_free(c->devbuf[i]);
         c->pinned[i] = nullptr;
         c->devbuf[i] = nullptr;
     }
     c->chunk_cap = 0;
     for (int i = 0; i < 2; ++i) {
-        CUDA_TRY(cudaHostAlloc((void**)&c->pinned[i], want, cudaHostAllocDefault));
-        CUDA_TRY(cudaMalloc((void**)&c->devbuf[i], want));
+        CUDA_TRY(pinned_alloc((void**)&c->pinned[i], want));
+        CUDA_TRY(scratch_alloc((void**)&c->devbuf[i], want));
         if (!c->done[i]) CUDA_TRY(cudaEventCreateWithFlags(&c->done[i], cudaEventDisableTiming));
     }
     if (!c->stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -1070,11 +1155,11 @@ static int ensure_dma(wfcu_counter* c, u64 want) {
     if (c->dma_cap >= want) return WFCU_OK;
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     for (int i = 0; i < 2; ++i) {
-        if (c->dma_buf[i]) cudaFree(c->dma_buf[i]);
+        if (c->dma_buf[i]) scratch_free(c->dma_buf[i]);
         c->dma_buf[i] = nullptr;
     }
     c->dma_cap = 0;
-    for (int i = 0; i < 2; ++i) CUDA_TRY(cudaMalloc((void**)&c->dma_buf[i], want));
+    for (int i = 0; i < 2; ++i) CUDA_TRY(scratch_alloc((void**)&c->dma_buf[i], want));
     c->dma_cap = want;
     return WFCU_OK;
 }
@@ -1468,8 +1553,8 @@ extern "C" int wfcu_wordcount_multi(const uint8_t* const* docs, const uint64_t* 
             cudaEventRecord(ev[1], nullptr);
             uint64_t distinct = 0;
             if (failed(wfcu_counter_stats(me.local, nullptr, &distinct, nullptr, nullptr))) break;
-            if (cuda(cudaMalloc((void**)&me.entries, sizeof(Slot) * std::max<u64>(distinct, 1)), "cudaMalloc entries")) break;
-            if (cuda(cudaMalloc((void**)&dev_counts, sizeof(u64) * (n + 1)), "cudaMalloc counts")) break;
+            if (cuda(scratch_alloc((void**)&me.entries, sizeof(Slot) * std::max<u64>(distinct, 1)), "cudaMalloc entries")) break;
+            if (cuda(scratch_alloc((void**)&dev_counts, sizeof(u64) * (n + 1)), "cudaMalloc counts")) break;
             if (failed(wfcu_counter_partition(me.local, n, reinterpret_cast<wfcu_entry*>(me.entries), std::max<u64>(distinct, 1),
                                               reinterpret_cast<uint64_t*>(dev_counts), nullptr))) break;
             me.part_counts.assign(n + 1, 0);
@@ -1477,11 +1562,11 @@ extern "C" int wfcu_wordcount_multi(const uint8_t* const* docs, const uint64_t* 
             if (me.part_counts[n]) {   // long-token records: serialise, keep a host copy for the owners
                 uint8_t* dev_recs = nullptr;
                 uint64_t bytes = me.part_counts[n];
-                if (cuda(cudaMalloc((void**)&dev_recs, bytes), "cudaMalloc records")) break;
+                if (cuda(scratch_alloc((void**)&dev_recs, bytes), "cudaMalloc records")) break;
                 int rc = wfcu_counter_long_records(me.local, dev_recs, bytes, &bytes, nullptr);
                 me.long_records.resize(bytes);
                 if (rc == WFCU_OK && cudaMemcpy(me.long_records.data(), dev_recs, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) rc = WFCU_ERR_CUDA;
-                cudaFree(dev_recs);
+                scratch_free(dev_recs);
                 if (rc) { failed(rc); break; }
             }
             cudaEventRecord(ev[2], nullptr);
@@ -1493,7 +1578,7 @@ extern "C" int wfcu_wordcount_multi(const uint8_t* const* docs, const uint64_t* 
             do {   // phase 2: exchange + merge-insert of what this worker owns
                 u64 most = 1;
                 for (const MultiWorker& o : w) most = std::max(most, o.part_counts[j]);
-                if (cuda(cudaMalloc((void**)&recv, sizeof(Slot) * most), "cudaMalloc receive buffer")) break;
+                if (cuda(scratch_alloc((void**)&recv, sizeof(Slot) * most), "cudaMalloc receive buffer")) break;
                 for (u32 k = 0; k < n && me.rc == WFCU_OK; ++k) {
                     const MultiWorker& o = w[(j + k) % n];        // start with the own region: spreads the peers
                     const u64 cnt = o.part_counts[j];
@@ -1506,11 +1591,11 @@ extern "C" int wfcu_wordcount_multi(const uint8_t* const* docs, const uint64_t* 
                     }
                     if (!o.long_records.empty()) {
                         uint8_t* dev_recs = nullptr;
-                        if (cuda(cudaMalloc((void**)&dev_recs, o.long_records.size()), "cudaMalloc records")) break;
+                        if (cuda(scratch_alloc((void**)&dev_recs, o.long_records.size()), "cudaMalloc records")) break;
                         int rc = cudaMemcpy(dev_recs, o.long_records.data(), o.long_records.size(), cudaMemcpyHostToDevice) == cudaSuccess ? WFCU_OK : WFCU_ERR_CUDA;
                         if (rc == WFCU_OK) rc = wfcu_counter_merge_long_records(me.owned, dev_recs, o.long_records.size(), j, n, nullptr);
                         cudaDeviceSynchronize();
-                        cudaFree(dev_recs);
+                        scratch_free(dev_recs);
                         if (rc) { failed(rc); break; }
                     }
                 }
@@ -1524,9 +1609,9 @@ extern "C" int wfcu_wordcount_multi(const uint8_t* const* docs, const uint64_t* 
             } while (false);
         }
         barrier.wait();     // nobody frees a partition a peer may still be reading
-        cudaFree(recv);
-        cudaFree(dev_counts);
-        cudaFree(me.entries);
+        scratch_free(recv);
+        scratch_free(dev_counts);
+        scratch_free(me.entries);
         me.entries = nullptr;
         wfcu_counter_destroy(me.local);
         me.local = nullptr;
@@ -1746,7 +1831,7 @@ extern "C" int wfcu_tokenize_host(const uint8_t* text, uint64_t n, wfcu_tokens**
     void* dev = nullptr;
     if (int rc = upload(text, n, &dev)) return rc;
     const int rc = wfcu_tokenize_dev(static_cast<const uint8_t*>(dev), n, nullptr, out);
-    cudaFree(dev);
+    scratch_free(dev);
     return rc;
 }
 
@@ -2103,10 +2188,10 @@ extern "C" int wfcu_utf8_sanitize_dev(const uint8_t* dev_text, uint64_t n, uint8
     const u64 need = sanitize_scratch_bytes(n);
     if (d->sn_cap < need) {
         CUDA_TRY(cudaDeviceSynchronize());
-        if (d->sn_scratch) cudaFree(d->sn_scratch);
+        if (d->sn_scratch) scratch_free(d->sn_scratch);
         d->sn_scratch = nullptr;
         d->sn_cap = 0;
-        CUDA_TRY(cudaMalloc(&d->sn_scratch, need + need / 4));
+        CUDA_TRY(scratch_alloc(&d->sn_scratch, need + need / 4));
         d->sn_cap = need + need / 4;
     }
     LaunchTally tally;
@@ -2211,11 +2296,11 @@ extern "C" int wfcu_dev_alloc(void** out, uint64_t bytes) {
     if (!out) return fail(WFCU_ERR_INVALID_ARGUMENT, "out is null");
     DeviceState* d;
     if (int rc = current_device_state(&d)) return rc;
-    CUDA_TRY(cudaMalloc(out, bytes ? bytes : 16));
+    CUDA_TRY(scratch_alloc(out, bytes ? bytes : 16));
     return WFCU_OK;
 }
 extern "C" void wfcu_dev_free(void* p) {
-    if (p) cudaFree(p);
+    if (p) scratch_free(p);
 }
 extern "C" int wfcu_dev_upload(void* dev_dst, const void* host_src, uint64_t bytes) {
     if (bytes) CUDA_TRY(cudaMemcpy(dev_dst, host_src, bytes, cudaMemcpyHostToDevice));
