@@ -1675,6 +1675,11 @@ struct wfcu_tokens {
     u64 arena_used = 0;
     u64 arena_cap = 0;
     bool sorted = false;        // WordList::sorted (proj/include/wfc/text.hpp:18-21)
+    // The tokenizer kernels leave the records in no particular order; text order costs a five-pass radix sort on the
+    // position.  It is restored on first use (ensure_text_order) -- a list that is sorted by key right away, the map
+    // stage of the paper's algorithm, never pays for it.
+    bool text_order_pending = false;
+    std::mutex order_mu;
 };
 
 static void tokens_free(wfcu_tokens* t) {
@@ -1701,6 +1706,15 @@ static int sort_device_tokens(wfcu_tokens* t, bool by_position, cudaStream_t s) 
     LaunchTally tally;
     CUDA_TRY(tokens_sort(t->recs, t->n, by_position, t->arena, sc, t->sm_count, s, &tally.n));
     CUDA_TRY(cudaStreamSynchronize(s));
+    return WFCU_OK;
+}
+
+static int ensure_text_order(const wfcu_tokens* ct, cudaStream_t s) {
+    auto* t = const_cast<wfcu_tokens*>(ct);     // the order is a cache of the object, not its value
+    std::lock_guard<std::mutex> lock(t->order_mu);
+    if (!t->text_order_pending) return WFCU_OK;
+    if (int rc = sort_device_tokens(t, /*by_position=*/true, s)) return rc;
+    t->text_order_pending = false;
     return WFCU_OK;
 }
 
@@ -1815,11 +1829,7 @@ static int tokenize_unordered(const uint8_t* dev_text, uint64_t n, cudaStream_t 
 extern "C" int wfcu_tokenize_dev(const uint8_t* dev_text, uint64_t n, void* stream, wfcu_tokens** out) {
     if (!out) return fail(WFCU_ERR_INVALID_ARGUMENT, "out is null");
     if (int rc = tokenize_unordered(dev_text, n, (cudaStream_t)stream, out)) return rc;
-    if (int rc = sort_device_tokens(*out, /*by_position=*/true, (cudaStream_t)stream)) {
-        tokens_free(*out);
-        *out = nullptr;
-        return rc;
-    }
+    (*out)->text_order_pending = true;      // restored by the first call that reads the order
     return WFCU_OK;
 }
 
@@ -1863,6 +1873,7 @@ extern "C" int wfcu_tokens_export(const wfcu_tokens* t, uint8_t* bytes, uint64_t
                                   uint64_t lens_cap) {
     if (!t) return fail(WFCU_ERR_INVALID_ARGUMENT, "tokens is null");
     if (t->n > lens_cap) return fail(WFCU_ERR_BUFFER_TOO_SMALL, "export needs %llu lengths", (unsigned long long)t->n);
+    if (int rc = ensure_text_order(t, nullptr)) return rc;
     std::vector<TokenRec> h(t->n);
     std::vector<uint8_t> arena(t->arena_used);
     if (t->n) CUDA_TRY(cudaMemcpy(h.data(), t->recs, sizeof(TokenRec) * t->n, cudaMemcpyDeviceToHost));
@@ -1947,6 +1958,7 @@ extern "C" int wfcu_tokens_concat_slices(const wfcu_tokens* const* src, const ui
     for (u32 i = 0; i < n_src; ++i) {
         if (!src[i] || begin[i] > end[i] || end[i] > src[i]->n)
             return fail(WFCU_ERR_INVALID_ARGUMENT, "slice %u is out of range", i);
+        if (int rc = ensure_text_order(src[i], nullptr)) return rc;
         total += end[i] - begin[i];
         if (src[i]->arena_used > 8 && end[i] > begin[i]) arena_total += src[i]->arena_used - 8;
     }
@@ -1994,6 +2006,7 @@ extern "C" int wfcu_tokens_encode_frame(const wfcu_tokens* t, uint64_t begin, ui
     const u64 m = end - begin;
     if (m > 0xFFFFFFFFull) return fail(WFCU_ERR_INVALID_ARGUMENT, "word batch exceeds 2^32-1 words");
     cudaStream_t s = (cudaStream_t)stream;
+    if (int rc = ensure_text_order(t, s)) return rc;
     DevBuf offs, tmp;
     u64 payload = 0;
     LaunchTally tally;
@@ -2107,6 +2120,10 @@ extern "C" int wfcu_tokens_decode_frame(const uint8_t* dev_frame, uint64_t frame
 
 extern "C" int wfcu_tokens_sort(wfcu_tokens* t, void* stream) {
     if (!t) return fail(WFCU_ERR_INVALID_ARGUMENT, "tokens is null");
+    {   // sorting by key makes the text order irrelevant: a pending position sort is dropped
+        std::lock_guard<std::mutex> lock(t->order_mu);
+        t->text_order_pending = false;
+    }
     if (int rc = sort_device_tokens(t, /*by_position=*/false, (cudaStream_t)stream)) return rc;
     t->sorted = true;
     return WFCU_OK;
@@ -2116,6 +2133,7 @@ extern "C" int wfcu_tokens_reduce_sorted(const wfcu_tokens* t, wfcu_counter* int
     if (!t || !into) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
     if (t->n == 0) return WFCU_OK;
     cudaStream_t s = (cudaStream_t)stream;
+    if (int rc = ensure_text_order(t, s)) return rc;
     DevBuf flags, starts, tmp, status;
     CUDA_TRY(flags.alloc(sizeof(u64) * t->n));
     CUDA_TRY(starts.alloc(sizeof(u64) * t->n));
