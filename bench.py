@@ -48,13 +48,15 @@ METRIC = "wordcount_corpus_GBps"
 UNIT = "GB/s"
 
 
-def ncu_traffic(kernel: str, nbytes: int):
-    """dram__bytes_read + dram__bytes_write of one launch, from the committed ncu capture of this config."""
+def ncu_traffic(kernel: str, nbytes: int, vocab: int):
+    """dram__bytes_read + dram__bytes_write of one launch, from the committed ncu capture of this config
+    (same kernel, same shard size, same vocabulary), else None."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            t = json.load(f)[kernel]
-        if t["bytes_per_gpu"] == nbytes:
-            return t["dram_bytes_read"] + t["dram_bytes_write"]
+            entries = json.load(f)
+        for name, t in entries.items():
+            if name.split(":")[0] == kernel and t["bytes_per_gpu"] == nbytes and t.get("vocab") == vocab:
+                return t["dram_bytes_read"] + t["dram_bytes_write"]
     except Exception:
         pass
     return None
@@ -330,17 +332,27 @@ def run_b200(args) -> None:
     # N > 1: the merge runs without a host synchronisation per step (fixed-capacity regions, sizes read
     # on the device); its sticky overflow / long-token flags are read once, inside the timed region,
     # after the K steps -- if they are raised the run is repeated with the synchronising merge.
-    ax = AsyncExchange(local, ops, dist, entries_hint=w["vocab"]) if world > 1 and not args.sync_exchange else None
+    # By default the all-to-all and the merge of step k run on a second stream under the count of step k+1 (two owned
+    # tables alternate; --no-overlap-exchange keeps everything on one stream).
+    overlap = world > 1 and not args.sync_exchange and not args.no_overlap_exchange
+    ax = AsyncExchange(local, ops, dist, entries_hint=w["vocab"], overlap=overlap) if world > 1 and not args.sync_exchange else None
+    owned_pair = [owned, capi.Counter(table_slots=slots)] if overlap else [owned]
+    last_owned = [owned]
 
     def step():
         local.reset(stream)
         local.count_dev(dev.data_ptr(), nbytes, stream)
         if world > 1:
-            owned.reset(stream)
             if ax is not None:
-                ax.step(local, owned)
+                o = owned_pair[ax.steps % len(owned_pair)]
+                ax.slot_ready()          # overlap: the merge that last used this table has run (an event, no host wait)
+                o.reset(stream)
+                ax.step(local, o)
+                last_owned[0] = o
             else:
+                owned.reset(stream)
                 hash_partition_merge(local, owned, ops, dist)
+                last_owned[0] = owned
 
     def barrier():
         torch.cuda.synchronize()
@@ -384,7 +396,7 @@ def run_b200(args) -> None:
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    table = owned if world > 1 else local
+    table = last_owned[0] if world > 1 else local
     table.status(stream)
     distinct, tokens, _ = table.stats(stream)
     all_bytes = torch.tensor([nbytes, distinct, tokens], dtype=torch.int64, device=device)
@@ -454,11 +466,13 @@ def run_b200(args) -> None:
             "config": {"workload": w["name"], "vocab": w["vocab"], "zipf_s": ZIPF_S, "doc_bytes": DOC_BYTES,
                        "seed": SEED, "documents": total_docs, "bytes_per_gpu": nbytes, "job_bytes": job_bytes,
                        "tokens": job_tokens, "distinct_words": job_distinct,
-                       "parallelism": f"document shard d mod {world}" + (", hash-partitioned all-to-all merge" + (" (no host sync per step)" if ax is not None else "") if world > 1 else ""),
+                       "parallelism": f"document shard d mod {world}" + (", hash-partitioned all-to-all merge" + (" (no host sync per step" + (", exchange of step k on a second stream under the count of step k+1" if overlap and ax is not None else "") + ")" if ax is not None else "") if world > 1 else ""),
                        "l2": "inputs (1 GB per GPU) larger than the 126 MB L2; no flush needed"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak if peak else None, "traffic": ncu_traffic("wc_count_kernel", nbytes),
-                         "traffic_source": "static: ncu --set full capture of this kernel on this config (profiles/traffic.json), not re-measured in this run",
+                         "frac": achieved / peak if peak else None, "traffic": ncu_traffic("wc_count_kernel", nbytes, w["vocab"]),
+                         "traffic_source": ("static: ncu --set full capture of this kernel on this config (profiles/traffic.json), not re-measured in this run"
+                                            if ncu_traffic("wc_count_kernel", nbytes, w["vocab"]) is not None else
+                                            "none: no committed ncu capture for this shard size / vocabulary"),
                          "kernel": "wc_count_kernel", "kernel_ms": k_ms, "kernel_launches": kernel_launches,
                          "algorithmic_bytes_per_launch": nbytes, "peak_source": peak_src},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": d2h,
@@ -711,6 +725,9 @@ def main() -> None:
     ap.add_argument("--workload", choices=sorted(WORKLOADS) + ["cfg5"], default="cfg3")
     ap.add_argument("--docs", type=int, default=None, help="override document count (per GPU for cfg3, total for cfg4)")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-overlap-exchange", action="store_true",
+                    help="N > 1: keep the all-to-all and the merge on the counting stream (default: a second stream, "
+                         "overlapping the next step's count)")
     ap.add_argument("--sync-exchange", action="store_true",
                     help="N > 1: use the merge that reads the region sizes on the host every step")
     ap.add_argument("--sample-docs", type=int, default=None, help="reference arm: documents per step")

@@ -79,6 +79,24 @@ class DeviceOps:
         t = self.torch
         return t.empty(max(n, 1), dtype=t.uint8, device=self.device)
 
+    # stream plumbing of AsyncExchange(overlap=True): a second stream for the collective and the merge
+    def new_stream(self):
+        return self.torch.cuda.Stream(device=self.device)
+
+    def record(self):
+        """an event at the current point of the current stream"""
+        ev = self.torch.cuda.Event()
+        ev.record(self.torch.cuda.current_stream(self.device))
+        return ev
+
+    def wait(self, event) -> None:
+        """the current stream waits for the event (no host wait)"""
+        self.torch.cuda.current_stream(self.device).wait_event(event)
+
+    def on(self, stream):
+        """context manager: the current stream inside is `stream`"""
+        return self.torch.cuda.stream(stream)
+
 
 @dataclass
 class ExchangeStats:
@@ -156,9 +174,16 @@ class AsyncExchange:
     hash_partition_merge for those steps.
 
     entries_hint: expected distinct words of a local table (regions hold 2x the uniform share);
-    default = the table's capacity, which can never overflow."""
+    default = the table's capacity, which can never overflow.
 
-    def __init__(self, local, ops, dist, group=None, entries_hint: int | None = None):
+    overlap=True: the all-to-all and the merge of step k run on a second stream while the caller's stream goes on to
+    reset and count step k+1 (`local` is free again as soon as its partition kernel has run; `owned` belongs to the
+    second stream until finish(), which joins the two).  Two send buffers alternate, so the partition of step k+2
+    waits for the all-to-all of step k by an event, never the host.  The caller must not touch `owned` (reset
+    included) between step() and finish() on its own stream -- give every step its own table or call
+    owned_ready() first."""
+
+    def __init__(self, local, ops, dist, group=None, entries_hint: int | None = None, overlap: bool = False):
         self.ops, self.dist, self.group = ops, dist, group
         self.world = dist.get_world_size(group)
         bound = local.max_entries()
@@ -169,18 +194,49 @@ class AsyncExchange:
         self.recv = ops.empty_entries(self.world * self.cap)
         self.counts = t.zeros(self.world + 2, dtype=t.int64, device=self.send.device)
         self.steps = 0
+        self.overlap = bool(overlap) and hasattr(ops, "new_stream")
+        if self.overlap:
+            self.comm = ops.new_stream()
+            self.sends = [self.send, ops.empty_entries(self.world * self.cap)]
+            self.sent = [None, None]        # event: the all-to-all that read sends[k] (and its merge) has run
+            self.merged = None              # event: the latest merge on the second stream
 
     def step(self, local, owned) -> None:
         """Collective.  Asynchronous on the current stream: returns before anything has run."""
         ops, world = self.ops, self.world
-        ops.partition_framed(local, world, self.send, self.cap, self.counts)
-        self.dist.all_to_all_single(self.recv, self.send, group=self.group)
-        ops.merge_regions(owned, self.recv, world, self.cap, None)
+        if not self.overlap:
+            ops.partition_framed(local, world, self.send, self.cap, self.counts)
+            self.dist.all_to_all_single(self.recv, self.send, group=self.group)
+            ops.merge_regions(owned, self.recv, world, self.cap, None)
+            self.steps += 1
+            return
+        k = self.steps & 1
+        if self.sent[k] is not None:
+            ops.wait(self.sent[k])          # sends[k] is free again
+        ops.partition_framed(local, world, self.sends[k], self.cap, self.counts)
+        ready = ops.record()
+        with ops.on(self.comm):
+            ops.wait(ready)
+            self.dist.all_to_all_single(self.recv, self.sends[k], group=self.group)
+            ops.merge_regions(owned, self.recv, world, self.cap, None)
+            self.sent[k] = self.merged = ops.record()
         self.steps += 1
+
+    def slot_ready(self) -> None:
+        """overlap=True: the caller's stream waits (no host wait) for the merge of the step two steps back -- after it
+        the `owned` table of that step may be reset and handed to the next step() (two tables alternate)."""
+        if self.overlap and self.sent[self.steps & 1] is not None:
+            self.ops.wait(self.sent[self.steps & 1])
+
+    def owned_ready(self) -> None:
+        """overlap=True: the caller's stream waits (no host wait) until every merge issued so far has run."""
+        if self.overlap and self.merged is not None:
+            self.ops.wait(self.merged)
 
     def finish(self) -> None:
         """The one host read: raises ExchangeOverflow if any step since the last finish() left
         something behind (on any rank), and clears the flags."""
+        self.owned_ready()
         flags = self.counts[self.world:self.world + 2].clone()
         self.dist.all_reduce(flags, group=self.group)
         long_tokens, overflow = (int(v) for v in flags.cpu().tolist())

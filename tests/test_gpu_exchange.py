@@ -173,6 +173,20 @@ def test_nccl_collective_path_with_one_rank(capi, cuda, port):
             ax2.step(loc2, own3)
             assert own3.to_dict() == want2
         ax2.finish()
+        # ... the same with the exchange on a second stream (overlap=True): four steps, two owned tables alternating,
+        # the caller's stream runs ahead (reset + count of the next step) and only finish() joins the streams
+        ax4 = AsyncExchange(loc2, ops, dist, entries_hint=len(want2), overlap=True)
+        assert ax4.overlap
+        pair = [capi.Counter(table_slots=1 << 15), capi.Counter(table_slots=1 << 15)]
+        s = ops.stream()
+        for k in range(4):
+            loc2.reset(s); loc2.count_dev(dev2.data_ptr(), n2, s)
+            ax4.slot_ready()
+            pair[k & 1].reset(s)
+            ax4.step(loc2, pair[k & 1])
+        ax4.finish()
+        torch.cuda.synchronize()
+        assert pair[0].to_dict() == want2 and pair[1].to_dict() == want2
         # ... and regions that are too small are reported, not silently truncated
         ax3 = AsyncExchange(loc2, ops, dist, entries_hint=1)
         ax3.cap = 8
