@@ -472,8 +472,12 @@ struct wfcu_counter {
     u64* counters = nullptr;    // device: [0] n_used [1] n_tokens [2] n_deferred [3] n_long [4] arena_used
                                 //         [5] status(int) [6..15] scratch [16] CTA ticket of the reset kernel
     bool aux_clean = false;     // the long table and the counters have been initialised once
-    u32 variant_hint = 15;       // kernel variants the texts counted so far asked for (counters[17]), read at every
+    u32 variant_hint = 63;       // kernel variants the texts counted so far asked for (counters[17]), read at every
                                 // synchronising call: later counts launch only those (and the narrow one)
+    u32* wanted_host = nullptr; // page-locked mirror of counters[17]: copied back (asynchronously, never waited for)
+                                // after the first two counts and every 64th, so that callers who never make a
+                                // synchronising call stop paying for the kernels their texts do not use
+    u64 count_calls = 0;
     // host staging for count_host
     uint8_t* pinned[2] = {nullptr, nullptr};
     uint8_t* devbuf[2] = {nullptr, nullptr};
@@ -515,6 +519,7 @@ static void counter_free(wfcu_counter* c) {
     scratch_free(c->v.long_count);
     scratch_free(c->v.arena);
     scratch_free(c->counters);
+    pinned_free(c->wanted_host);
     for (int i = 0; i < 2; ++i) {
         if (c->pinned[i]) pinned_free(c->pinned[i]);
         if (c->devbuf[i]) scratch_free(c->devbuf[i]);
@@ -576,6 +581,7 @@ extern "C" int wfcu_counter_create(wfcu_counter** out, const wfcu_counter_config
     alloc((void**)&c->v.long_count, sizeof(u64) * c->long_slots);
     alloc((void**)&c->v.arena, arena);
     alloc((void**)&c->counters, sizeof(u64) * 18);
+    if (e == cudaSuccess && pinned_alloc((void**)&c->wanted_host, 64) == cudaSuccess) *c->wanted_host = 0;
     if (e != cudaSuccess) {
         counter_free(c);
         return fail(WFCU_ERR_CUDA, "counter allocation: %s", cudaGetErrorString(e));
@@ -633,7 +639,14 @@ extern "C" int wfcu_counter_count_dev(wfcu_counter* c, const uint8_t* dev_text, 
         ev0 = &c->timed.back().first;
         ev1 = &c->timed.back().second;
     }
+    if (c->wanted_host) {
+        const u32 seen = *reinterpret_cast<volatile u32*>(c->wanted_host);     // whatever has landed so far; speed only
+        if (seen) c->variant_hint = seen | 1u;
+    }
     CUDA_TRY(wc_launch(dev_text, n, c->v, c->sm_count, (cudaStream_t)stream, &tally.n, ev0, ev1, c->variant_hint));
+    if (c->wanted_host && (c->count_calls < 2 || (c->count_calls & 63u) == 0))
+        CUDA_TRY(cudaMemcpyAsync(c->wanted_host, c->v.wanted, sizeof(u32), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    c->count_calls += 1;
     return WFCU_OK;
 }
 

@@ -214,8 +214,8 @@ using namespace cnt3;
 // HI = true keeps two-byte letters (accented Latin, Greek, Cyrillic ...) on the fast path.  Every
 // CTA picks its variant from a sample of its own part of the text (wc_count_kernel below): the
 // choice affects speed only.
-template <int WARPS, int SETS, int MSLOTS, bool HI, bool WIDE>
-__device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, u32 one, bool u3_cta,
+template <int WARPS, int SETS, int MSLOTS, bool HI, bool WIDE, bool U3K>
+__device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, u32 one,
                                               const TableView& gt) {
     extern __shared__ uint8_t smem_raw[];
     typedef Smem<WARPS, SETS, MSLOTS> SM;
@@ -539,10 +539,10 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
             uint4 f;
             if constexpr (HI) {
                 // what lies in front of THEM is unknown: a leading continuation byte is flagged (conservative)
-                const HiMasks m = classify16_hi<true>(x, 0u, f);
+                const HiMasks m = classify16_hi<U3K>(x, 0u, f);
                 u32 A = m.a7 >> 7, H, bad_first, clear_before, alnum_before;
                 const HiIn in{m.h7 >> 7, m.c7 >> 7, m.l7 >> 7, m.x7 >> 7, m.e7 >> 7, m.z7 >> 7, m.k7 >> 7, m.l3 >> 7, m.b2 >> 7};
-                hi_masks_finish<true>(in, 0u, 0u, A, H, bad_first, clear_before, alnum_before);
+                hi_masks_finish<U3K>(in, 0u, 0u, A, H, bad_first, clear_before, alnum_before);
                 carryS = m.s7 >> 7; carryA = A & 0xFFFFu; carryH = H & 0xFFFFu; carryL = (m.l7 >> 7) & 0xFFFFu;
                 carryT = hi_tails(in) & 0xFFFFu;
                 carryC3 = x.w >> 24;
@@ -581,8 +581,8 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
                 u32 pc3 = __shfl_up_sync(kFull, last_bytes, 1);
                 if (lane == 0) pc3 = (carryC3 & 0xFFu) | ((l31 & 0xFFu) << 8);
                 carryC3 = l31 >> 8;
-                // the CTA's sample saw three-byte letter leads (or one is open in front of the row) -> the flags for them
-                const bool u3_row = u3_cta || (carryT & 0x18u) != 0;
+                // U3K: the call's sample saw three-byte letter leads -> the flags for them are compiled in (a kernel of
+                // its own: the flags cost the other HI kernel registers and 10-20 % even when a branch skips them)
                 u32 tails = 0;
                 auto classify_row = [&](auto u3_) {
                     constexpr bool U3 = decltype(u3_)::value;
@@ -613,7 +613,7 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
                 // not send this row to the careful loop, nor must the open tail of the row's very last chunk -- no
                 // fragment that ends in this row can hold it, and the next row sees it through carryH.
                 };
-                if (u3_row) classify_row(std::true_type{}); else classify_row(std::false_type{});
+                classify_row(std::integral_constant<bool, U3K>{});
                 const u32 nclr = __shfl_down_sync(kFull, pH_clear, 1), clr0 = __shfl_sync(kFull, pH_clear, 0);
                 const u32 tb = tails >> 16;                     // what the row's last chunk leaves open (lane 31)
                 const u32 open_end = ((tb & 0x10u) || ((tb & 0x1u) && (tb & 0x4u))) ? 0xC0000000u : ((tb & 0xAu) ? 0x80000000u : 0u);
@@ -814,11 +814,10 @@ __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, 
 template <int WARPS, int SETS, int MSLOTS, int VARIANT>
 __global__ void __launch_bounds__(WARPS * 32, 1)
 wc_count_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, int force, u32 one, TableView gt) {
-    bool u3 = false;
-    const int v = variant_of_text(text, n, force, gt.launched, VARIANT == kVarNarrow ? gt.wanted : nullptr, &u3);
+    const int v = variant_of_text(text, n, force, gt.launched, VARIANT == kVarNarrow ? gt.wanted : nullptr);
     if (v != VARIANT) return;
-    wc_count_body<WARPS, SETS, MSLOTS, VARIANT == kVarHi || VARIANT == kVarHiWide, VARIANT == kVarWide || VARIANT == kVarHiWide>(
-        text, n, rows_per_warp, one, u3, gt);
+    wc_count_body<WARPS, SETS, MSLOTS, variant_is_hi(VARIANT), variant_is_wide(VARIANT), variant_is_u3(VARIANT)>(
+        text, n, rows_per_warp, one, gt);
 }
 
 // ---- host-side launcher (called from wordcount.cu) ---------------------------------
@@ -852,14 +851,23 @@ cudaError_t wc_count_launch(const uint8_t* text, u64 n, const TableView& gt_in, 
                             u32 hint) {
     const size_t smem = sizeof(CountSmem) + 1024, smem_wide = sizeof(WideSmem) + 1024;   // + slack for the 1 KiB alignment
     auto k_narrow = wc_count_kernel<kCountWarps, kCountSets, kCountMedSlots, kVarNarrow>;
-    auto k_hi = wc_count_kernel<kCountWarps, kCountSets, kCountMedSlots, kVarHi>;
-    auto k_wide = wc_count_kernel<kCountWarps, kWideSets, kWideSlots, kVarWide>;
-    auto k_hiwide = wc_count_kernel<kCountWarps, kWideSets, kWideSlots, kVarHiWide>;
-    cudaError_t e = cudaFuncSetAttribute(k_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_hi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_wide);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_hiwide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_wide);
-    if (e != cudaSuccess) return e;
+    typedef void (*Kernel)(const uint8_t*, u64, u32, int, u32, TableView);
+    static const Kernel kernels[kVarCount] = {      // indexed by variant
+        k_narrow,
+        wc_count_kernel<kCountWarps, kCountSets, kCountMedSlots, kVarHi>,
+        wc_count_kernel<kCountWarps, kWideSets, kWideSlots, kVarWide>,
+        wc_count_kernel<kCountWarps, kWideSets, kWideSlots, kVarHiWide>,
+        wc_count_kernel<kCountWarps, kCountSets, kCountMedSlots, kVarHi3>,
+        wc_count_kernel<kCountWarps, kWideSets, kWideSlots, kVarHiWide3>,
+    };
+    static const cudaError_t attr = [&] {
+        cudaError_t e = cudaSuccess;
+        for (int v = 0; v < kVarCount && e == cudaSuccess; ++v)
+            e = cudaFuncSetAttribute(kernels[v], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(variant_is_wide(v) ? smem_wide : smem));
+        return e;
+    }();
+    if (attr != cudaSuccess) return attr;
+    cudaError_t e = cudaSuccess;
     const u64 n_rows = n / kRow + 1;
     u64 grid = (u64)sm_count;
     if (grid * kCountWarps > n_rows) grid = (n_rows + kCountWarps - 1) / kCountWarps;   // at least one row per warp
@@ -868,26 +876,17 @@ cudaError_t wc_count_launch(const uint8_t* text, u64 n, const TableView& gt_in, 
     static const int force = [] { const char* v = getenv("WFCU_COUNT_VARIANT"); return v ? atoi(v) : -1; }();   // tests: 0..5
     static const bool gen4_ascii = [] { const char* v = getenv("WFCU_COUNT_KERNEL"); return v && v[0] == '4'; }();
     TableView gt = gt_in;
-    gt.launched = force == 0 ? 1u : (force == 1 || force == 2) ? 2u : force == 3 ? 4u : (force == 4 || force == 5) ? 8u : ((hint & 15u) | 1u);
-    if (gt.launched & 1u) {
-        if (!gen4_ascii) {
-            k_narrow<<<(unsigned)grid, kCountWarps * 32, smem, stream>>>(text, n, (u32)rows_per_warp, force, 1u, gt);
-        } else {
+    gt.launched = (force >= 0 && force < kVarCount) ? (1u << force) : ((hint & ((1u << kVarCount) - 1u)) | 1u);
+    // narrow first (it publishes the choice), the others in any order: all but one return after the sample
+    for (int v = 0; v < kVarCount; ++v) {
+        if (!((gt.launched >> v) & 1u)) continue;
+        if (v == kVarNarrow && gen4_ascii) {
             e = wc_count4_launch(text, n, (u32)rows_per_warp, (unsigned)grid, force, gt, stream);
             if (e != cudaSuccess) return e;
+        } else {
+            kernels[v]<<<(unsigned)grid, kCountWarps * 32, variant_is_wide(v) ? smem_wide : smem, stream>>>(
+                text, n, (u32)rows_per_warp, force, 1u, gt);
         }
-        *launches += 1;
-    }
-    if (gt.launched & 4u) {
-        k_wide<<<(unsigned)grid, kCountWarps * 32, smem_wide, stream>>>(text, n, (u32)rows_per_warp, force, 1u, gt);
-        *launches += 1;
-    }
-    if (gt.launched & 8u) {
-        k_hiwide<<<(unsigned)grid, kCountWarps * 32, smem_wide, stream>>>(text, n, (u32)rows_per_warp, force, 1u, gt);
-        *launches += 1;
-    }
-    if (gt.launched & 2u) {
-        k_hi<<<(unsigned)grid, kCountWarps * 32, smem, stream>>>(text, n, (u32)rows_per_warp, force, 1u, gt);
         *launches += 1;
     }
     return cudaGetLastError();

@@ -576,8 +576,7 @@ __device__ __forceinline__ void wc_count4_body(const uint8_t* __restrict__ text,
 template <int WARPS, int SETS, int MSLOTS>
 __global__ void __launch_bounds__(WARPS * 32, 1)
 wc_count4_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, int force, TableView gt) {
-    bool u3 = false;
-    if (variant_of_text(text, n, force, gt.launched, gt.wanted, &u3) != kVarNarrow)
+    if (variant_of_text(text, n, force, gt.launched, gt.wanted) != kVarNarrow)
         return;
     wc_count4_body<WARPS, SETS, MSLOTS>(text, n, rows_per_warp, gt);
 }

@@ -127,11 +127,12 @@ __device__ __forceinline__ bool medium_add(u64* __restrict__ k0s, u64* __restric
 // Every counting kernel has kCountVariantWarps warps and the same partition of the text (a strip of
 // rows_per_warp KiB rows per warp).  Every CTA of every launched kernel reads the SAME sample -- one 16-byte chunk per
 // thread, spread evenly over the whole text -- and so reaches the same answer without communicating:
-//   kVarHi     (two- and, *u3, three-byte letters on the fast path) as soon as two chunks hold a byte >= 0x80,
+//   kVarHi     (two-byte letters on the fast path) as soon as two chunks hold a byte >= 0x80,
+//   kVarHi3    (two- and three-byte letters) when two chunks hold a lead byte E0..EE other than E2,
 //   kVarWide   (one combiner for all tokens of up to 16 bytes) when 20 of the 896 chunks hold a run of nine or more
 //              word characters (non-whitespace bytes in chunks with bytes >= 0x80): words longer than 8 bytes are
 //              common -- English prose, the 1 M-word corpus,
-//   kVarHiWide (both) when both hold,
+//   kVarHiWide / kVarHiWide3 when that holds too,
 //   kVarNarrow otherwise.
 // The CTAs of the other kernels return.  The choice affects speed only.  It is one choice per call, not per CTA: the
 // kernels of a call run one after the other, each with one CTA per SM, so CTAs that disagreed (a sample near a
@@ -139,29 +140,22 @@ __device__ __forceinline__ bool medium_add(u64* __restrict__ k0s, u64* __restric
 // when its CTAs split between two variants, 400 GB/s under either of them.  Callers that stream a corpus in chunks
 // (wfcu_counter_count_host: 32 MiB) get one choice per chunk.
 // Not every variant is launched every time (TableView::launched: the host launches what the counter's recent texts
-// asked for, TableView::wanted): a text whose variant is missing runs the narrow body, which is always there (HI if it
-// wanted HI + wide and only HI was launched).
-// force: 0 / 1 / 3 / 4 = narrow / HI / wide / HI + wide, 2 / 5 = HI / HI + wide with three-byte letters (tests);
-// else sample.
+// asked for, TableView::wanted): a text whose variant is missing runs the nearest HI kernel that was launched, else
+// the narrow body, which is always there.
+// force (WFCU_COUNT_VARIANT, tests): the variant number 0..5; else sample.
 #ifndef WFCU_COUNT_WARPS
 #define WFCU_COUNT_WARPS 28
 #endif
 constexpr int kCountVariantWarps = WFCU_COUNT_WARPS;
-constexpr int kVarNarrow = 0, kVarHi = 1, kVarWide = 2, kVarHiWide = 3;
+constexpr int kVarNarrow = 0, kVarHi = 1, kVarWide = 2, kVarHiWide = 3, kVarHi3 = 4, kVarHiWide3 = 5, kVarCount = 6;
+__host__ __device__ constexpr bool variant_is_hi(int v) { return v == kVarHi || v == kVarHiWide || v == kVarHi3 || v == kVarHiWide3; }
+__host__ __device__ constexpr bool variant_is_wide(int v) { return v == kVarWide || v == kVarHiWide || v == kVarHiWide3; }
+__host__ __device__ constexpr bool variant_is_u3(int v) { return v == kVarHi3 || v == kVarHiWide3; }
 __device__ __forceinline__ int variant_of_text(const uint8_t* __restrict__ text, u64 n, int force, u32 launched,
-                                               unsigned int* wanted_word, bool* u3) {
+                                               unsigned int* wanted_word) {
     int want = kVarNarrow;
-    *u3 = false;
-    if (force == 0) {
-        want = kVarNarrow;
-    } else if (force == 1 || force == 2) {
-        want = kVarHi;
-        *u3 = force == 2;
-    } else if (force == 3) {
-        want = kVarWide;
-    } else if (force == 4 || force == 5) {
-        want = kVarHiWide;
-        *u3 = force == 5;
+    if (force >= 0 && force < kVarCount) {
+        want = force;
     } else {
         const u64 at = ((u64)threadIdx.x * (n / (u64)(kCountVariantWarps * 32))) & ~15ull;
         bool hit = false, hit3 = false, hit9 = false;
@@ -189,12 +183,21 @@ __device__ __forceinline__ int variant_of_text(const uint8_t* __restrict__ text,
             hit9 = (r & (N >> 8)) != 0;
         }
         const int c_hi = __syncthreads_count(hit), c3 = __syncthreads_count(hit3), c9 = __syncthreads_count(hit9);
-        want = c_hi >= 2 ? (c9 >= 20 ? kVarHiWide : kVarHi) : (c9 >= 20 ? kVarWide : kVarNarrow);
-        *u3 = c3 >= 2;
+        const bool wide = c9 >= 20;
+        want = c_hi < 2 ? (wide ? kVarWide : kVarNarrow)
+                        : c3 >= 2 ? (wide ? kVarHiWide3 : kVarHi3) : (wide ? kVarHiWide : kVarHi);
     }
     if (wanted_word && threadIdx.x == 0 && blockIdx.x == 0) atomicOr(wanted_word, 1u << want);
-    if ((launched >> want) & 1u) return want;
-    return (want == kVarHiWide && ((launched >> kVarHi) & 1u)) ? kVarHi : kVarNarrow;
+    // the wanted kernel, else the nearest launched one that is exact AND fast on the same kind of text, else narrow
+    // (four candidates per wanted variant, one per nibble, first choice lowest)
+    const u32 prefer = want == kVarHi ? 0x5341u : want == kVarHiWide ? 0x4153u : want == kVarHi3 ? 0x3154u
+                     : want == kVarHiWide3 ? 0x1345u : (u32)want * 0x1111u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int cand = (int)((prefer >> (4 * k)) & 15u);
+        if ((launched >> cand) & 1u) return cand;
+    }
+    return kVarNarrow;
 }
 
 }  // namespace cntc

@@ -52,7 +52,7 @@ struct TableView {
     int* status;
     unsigned int* ticket = nullptr;   // a zeroed word for "last CTA" decisions (null: the caller launches the follow-up itself)
     unsigned int* wanted = nullptr;   // OR of (1 << variant) the CTAs of the counting kernels asked for (a hint for later launches)
-    unsigned int launched = 15;       // variants launched in this call: a CTA whose variant is missing runs the narrow body
+    unsigned int launched = 63;       // variants launched in this call: a CTA whose variant is missing runs the narrow body
 };
 
 // One token of a device-resident token list (wfcu_tokens), 32 bytes.

@@ -810,7 +810,7 @@ cudaError_t wc_normalize_launch(const uint8_t* text, const u64* offsets, u64 n_f
 // deferred list, the long-token arena and the status word; its tables stay untouched)
 cudaError_t wc_tokenize_launch(const uint8_t* text, u64 n, const TableView& gt, const EmitView& em, int sm_count,
                                cudaStream_t stream, u64* launches) {
-    return wc_launch_impl<true>(text, n, gt, em, sm_count, stream, launches, nullptr, nullptr, 15u);
+    return wc_launch_impl<true>(text, n, gt, em, sm_count, stream, launches, nullptr, nullptr, 63u);
 }
 
 }  // namespace wfcu

@@ -1,5 +1,5 @@
 """Developer probe: cfg3 text in which a share of the words is lengthened past 8 bytes (k bigrams get three more
-letters) -- where the narrow / WIDE crossover lies (run under WFCU_COUNT_VARIANT=0, 3 and unset)."""
+letters) -- where the narrow / WIDE crossover lies (run under WFCU_COUNT_VARIANT=0, 2 and unset)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch

@@ -1,7 +1,8 @@
 """The counting kernels that the environment can select are all exact: the kernel-level suites are run again, in a
 child process each (the switches are read once per process), with the fourth-generation ASCII body
-(WFCU_COUNT_KERNEL=4, csrc/wc_count4.cu) and with one variant forced for every CTA (WFCU_COUNT_VARIANT=0: ASCII body, 1: two-byte letters, 2: two- and three-byte
-letters, 3: the wide combiner for tokens of up to 16 bytes, 5: two- and three-byte letters with the wide combiner)."""
+(WFCU_COUNT_KERNEL=4, csrc/wc_count4.cu) and with one variant forced for the whole text (WFCU_COUNT_VARIANT = 0: narrow
+ASCII body, 1: two-byte letters, 2: the wide combiner for tokens of up to 16 bytes, 3: both, 4 / 5: 1 / 3 with
+three-byte letters as well)."""
 import os
 import subprocess
 import sys
@@ -19,6 +20,7 @@ SUITES = ["tests/test_gpu_count_kernel.py", "tests/test_gpu_fuzz.py"]
     {"WFCU_COUNT_VARIANT": "1"},
     {"WFCU_COUNT_VARIANT": "2"},
     {"WFCU_COUNT_VARIANT": "3"},
+    {"WFCU_COUNT_VARIANT": "4"},
     {"WFCU_COUNT_VARIANT": "5"},
 ], ids=lambda e: ",".join(f"{k[11:]}={v}" for k, v in e.items()))
 def test_suites_under_switch(cuda, env):
