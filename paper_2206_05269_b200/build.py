@@ -153,11 +153,29 @@ def build_relink_demo(force: bool = False) -> Path | None:
     return exe
 
 
+def build_api_bench(force: bool = False) -> Path | None:
+    """tests/relink/api_bench.cpp -- a caller of the public wfc:: API that includes only wfc/ headers -- linked with the
+    drop-in (its twin oracle/_ref/api_bench_ref, linked with the reference, is built by oracle/Makefile)."""
+    out_dir = LIB / "reftests"
+    exe = out_dir / "api_bench_b200"
+    main = ROOT / "tests" / "relink" / "api_bench.cpp"
+    if not (LIB / "libwfc_b200.so").exists() or not main.exists():
+        return None
+    out_dir.mkdir(exist_ok=True)
+    deps = [main, LIB / "libwfc_b200.so"] + sorted((HOST / "include" / "wfc").glob("*.hpp"))
+    if force or _stale(exe, deps):
+        cxx = os.environ.get("CXX") or shutil.which("g++") or "g++"
+        _run([cxx, "-std=c++20", "-O2", "-pthread", f"-I{HOST / 'include'}", "-o", str(exe), str(main),
+              f"-L{LIB}", "-lwfc_b200", "-lwfcu", "-Wl,-rpath,$ORIGIN/.."])
+    return exe
+
+
 def build_all(force: bool = False, verbose: bool = False) -> None:
     build_wfcu(force, verbose)
     build_host(force)
     build_reference_suites(force)
     build_relink_demo(force)
+    build_api_bench(force)
 
 
 if __name__ == "__main__":

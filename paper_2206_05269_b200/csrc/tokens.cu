@@ -180,10 +180,67 @@ __device__ __forceinline__ int long_compare(const uint8_t* arena, u64 a, u64 b) 
     return la < lb ? -1 : (la > lb ? 1 : 0);
 }
 
-// After the radix passes, long tokens with the same 16-byte prefix are adjacent and in
-// original order; order each such run by the full string (stable insertion sort, one
-// thread per run -- long tokens are rare).
-__global__ void sort_long_fixup_kernel(TokenRec* __restrict__ recs, u64 n, const uint8_t* __restrict__ arena) {
+// Long tokens (ext != 0) are ordered among themselves by the bytes behind their 16-byte prefix with the same LSD radix
+// sort, window by window: the `pos` field, which only means something in text order, is overwritten with the sort
+// key of the current window -- bytes [16 + 8w, 24 + 8w) of the string, big-endian, zero padded -- or, for the least
+// significant pass of all, with the length (a string sorts behind its own prefixes; zero padding alone cannot tell
+// "ab" from "ab\0").  range[5] / range[6] collect OR / AND of the key so that constant digit positions are skipped,
+// range[4] the longest string (window < 0 only).
+__global__ void sort_fill_window_kernel(TokenRec* __restrict__ recs, u64 n, const uint8_t* __restrict__ arena, int window,
+                                        u64* __restrict__ range) {
+    u64 o = 0, a = ~0ull, longest = 0;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const u64 ext = recs[i].ext;
+        u64 key = 0;
+        if (ext) {
+            const u32 len = *reinterpret_cast<const u32*>(arena + ext);
+            if (window < 0) {
+                key = len;
+                longest = longest > len ? longest : len;
+            } else {
+                const uint8_t* p = arena + ext + 8;
+                const u32 lo = 16u + 8u * (u32)window;
+                const u32 hi = len < lo + 8u ? len : lo + 8u;
+                for (u32 j = lo; j < hi; ++j) key |= (u64)p[j] << (8 * (lo + 7 - j));
+            }
+        }
+        recs[i].pos = key;
+        o |= key; a &= key;
+    }
+    for (int d = 16; d > 0; d >>= 1) {
+        o |= __shfl_xor_sync(0xFFFFFFFFu, o, d);
+        a &= __shfl_xor_sync(0xFFFFFFFFu, a, d);
+        const u64 other = __shfl_xor_sync(0xFFFFFFFFu, longest, d);
+        longest = longest > other ? longest : other;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicOr(range + 5, o);
+        atomicAnd(range + 6, a);
+        if (window < 0) atomicMax(reinterpret_cast<unsigned long long*>(range + 4), (unsigned long long)longest);
+    }
+}
+
+// Safety net behind the window passes (which stop at kLongWindows * 8 bytes): every long record compares itself with
+// its predecessor, in parallel, and only if some pair with the same prefix descends (*descents != 0 -- strings that
+// agree in their first 32 KiB) does the fix-up run: a stable insertion sort by the full string, one thread per run.
+// (Round 1 ran the insertion sort unconditionally after sorting by the 16-byte prefix alone: a corpus whose most
+// frequent word is longer than 16 bytes spent 28 ms per list in ONE thread walking its 23 000 equal records -- 89 % of
+// wfc::run_wordcount -- and two such words with a common prefix, interleaved, took 87 SECONDS for 26 000 records.)
+__global__ void sort_long_check_kernel(const TokenRec* __restrict__ recs, u64 n, const uint8_t* __restrict__ arena,
+                                       u64* __restrict__ descents) {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x + 1; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const TokenRec r = recs[i];
+        if (!r.ext) continue;
+        const TokenRec p = recs[i - 1];
+        if (p.ext && p.k0 == r.k0 && p.k1 == r.k1 && long_compare(arena, p.ext, r.ext) > 0) {
+            atomicOr(descents, 1ull);
+            return;
+        }
+    }
+}
+__global__ void sort_long_fixup_kernel(TokenRec* __restrict__ recs, u64 n, const uint8_t* __restrict__ arena,
+                                       const u64* __restrict__ descents) {
+    if (*descents == 0) return;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
         const TokenRec r = recs[i];
         if (!r.ext) continue;
@@ -287,6 +344,8 @@ static inline unsigned blocks_for(u64 items, int threads, int sm) {
     return (unsigned)g;
 }
 
+constexpr int kLongWindows = 4096;   // windows of 8 bytes behind the 16-byte prefix that the radix passes order (32 KiB + 16)
+
 struct SortScratch {
     TokenRec* alt;   // n records
     u64* hist;       // 256 * n_tiles
@@ -341,7 +400,42 @@ cudaError_t tokens_sort(TokenRec* recs, u64 n, bool by_position, const uint8_t* 
         for (int p = 0; p < 8; ++p)
             if ((vary_pos >> (8 * p)) & 0xFF) run(1, p);
     } else {
-        if (mixed_long) run(2, 0);                      // least significant: inline before long
+        const u64 m = range[4];                         // long tokens
+        if (m != 0) {
+            // inline tokens to the front, long ones behind them (stable): the relative order of the two kinds is
+            // settled -- inline before long under equal prefixes -- and the long ones form a sub-array of their own
+            if (mixed_long) run(2, 0);
+            // order the sub-array by what follows the prefix: LSD over the length, then the 8-byte windows from the
+            // last one to the first; the stable passes over k1 / k0 below keep that order inside equal prefixes
+            TokenRec* sa = a + (n - m);
+            TokenRec* sb = b + (n - m);
+            int windows = 0;
+            for (int w = -1; e == cudaSuccess; ) {
+                const u64 init2[3] = {0, 0, ~0ull};
+                e = cudaMemcpyAsync(sc.tmp + 4, init2, sizeof(init2), cudaMemcpyHostToDevice, s);
+                if (e != cudaSuccess) break;
+                sort_fill_window_kernel<<<blocks_for(m, 256, sm), 256, 0, s>>>(sa, m, arena, w, sc.tmp);
+                *launches += 1;
+                u64 r3[3];
+                e = cudaMemcpyAsync(r3, sc.tmp + 4, sizeof(r3), cudaMemcpyDeviceToHost, s);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+                if (e != cudaSuccess) break;
+                const u64 vary = r3[1] ^ r3[2];
+                for (int p = 0; p < 8 && e == cudaSuccess; ++p) {
+                    if (!((vary >> (8 * p)) & 0xFF)) continue;
+                    e = radix_pass(sa, sb, m, 1, p, sc, sm, s, launches);
+                    TokenRec* t = sa; sa = sb; sb = t;
+                }
+                if (w < 0) {
+                    const u64 longest = r3[0];
+                    windows = (int)std::min<u64>((longest > 16 ? (longest - 16 + 7) / 8 : 0), (u64)kLongWindows);
+                    w = windows;
+                }
+                if (--w < 0) break;
+            }
+            if (e == cudaSuccess && sa != a + (n - m))
+                e = cudaMemcpyAsync(a + (n - m), sa, sizeof(TokenRec) * m, cudaMemcpyDeviceToDevice, s);
+        }
         for (int p = 0; p < 8; ++p)
             if ((vary_k1 >> (8 * p)) & 0xFF) run(0, p);
         for (int p = 0; p < 8; ++p)
@@ -353,8 +447,9 @@ cudaError_t tokens_sort(TokenRec* recs, u64 n, bool by_position, const uint8_t* 
         if (e != cudaSuccess) return e;
     }
     if (!by_position && range[4] != 0) {
-        sort_long_fixup_kernel<<<blocks_for(n, 256, sm), 256, 0, s>>>(recs, n, arena);
-        *launches += 1;
+        sort_long_check_kernel<<<blocks_for(n, 256, sm), 256, 0, s>>>(recs, n, arena, sc.tmp + 7);
+        sort_long_fixup_kernel<<<blocks_for(n, 256, sm), 256, 0, s>>>(recs, n, arena, sc.tmp + 7);
+        *launches += 2;
     }
     return cudaGetLastError();
 }

@@ -58,3 +58,24 @@ def test_relink_with_the_references_own_report_cpp(capi, cuda, tmp_path):
     assert len(rows) == 9 and rows[0] == {"word": "mapreduce", "count": 2, "relfreq": 2 / 12}
     bad = subprocess.run([str(exe), "wordcount", str(tmp_path / "missing"), "2"], capture_output=True, text=True, timeout=300)
     assert bad.returncode == 1 and "not a readable directory" in bad.stderr
+
+
+def test_one_caller_two_libraries(capi, cuda):
+    """tests/relink/api_bench.cpp includes only wfc/ headers and is linked twice: with libwfc_b200.so and (in the build
+    container, travelling as oracle/_ref/api_bench_ref) with the unmodified reference.  Every result of the public API
+    -- the merged counts, the serial count, the pre-repair shards of run_wordcount(corpus, n), the tokens of a document
+    in text order, top-25, the bit-exact blocked fold -- must be identical between the two processes."""
+    import json
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    ours = capi.LIB_PATH.parent / "reftests" / "api_bench_b200"
+    ref = os.path.join(root, "oracle", "_ref", "api_bench_ref")
+    assert ours.exists() and os.path.exists(ref), "built where /root/reference is present; travels with the snapshot"
+    for docs, workers in ((3, 1), (8, 3)):
+        a = subprocess.run([str(ours), str(docs), str(workers), "1"], capture_output=True, text=True, timeout=600)
+        b = subprocess.run([ref, str(docs), str(workers), "1"], capture_output=True, text=True, timeout=600)
+        assert a.returncode == 0 and b.returncode == 0, a.stderr[-2000:] + b.stderr[-2000:]
+        ja, jb = json.loads(a.stdout), json.loads(b.stdout)
+        for key in ("counts", "counts_checksum", "serial_checksum", "pre_repair_checksum", "tokens_doc0", "tokens_checksum",
+                    "top25_checksum", "fold"):
+            assert ja[key] == jb[key], (key, ja[key], jb[key])

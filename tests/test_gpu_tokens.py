@@ -157,3 +157,33 @@ def test_tokenize_arena_worst_case(capi, cuda, port):
     want = port.tokenize(text)
     assert capi.Tokens.tokenize_host(text).words() == want
     assert len(want) == 40000 and len(want[0]) == 17
+
+
+@pytest.mark.gpu
+def test_sort_with_frequent_long_words(capi, cuda, port):
+    """Words longer than 16 bytes are ordered by the radix sort itself (the length, then 8-byte windows behind the
+    prefix), not by a serial fix-up: thousands of interleaved occurrences of long words that share 16, 24 or 40 bytes,
+    one a prefix of the other, one with a NUL behind the common part, kilobyte words, and a few that agree beyond the
+    32 KiB the windows cover (the insertion-sort safety net) --
+    sort_words order, in well under the seconds the round-1 insertion sort took (87 s for 26 000 records)."""
+    import time
+    stem = b"abcdefghijklmnopqrstuvwx"                      # 24 bytes
+    longs = [stem + b"yz", stem + b"ab", stem, stem[:20], stem + b"q" * 16 + b"1", stem + b"q" * 16 + b"0",
+             stem + b"a\x00b", stem + b"a", b"k" * 1100 + b"b", b"k" * 1100 + b"a", b"k" * 1100]
+    rng = random.Random(3)
+    words = []
+    for _ in range(6000):
+        words.append(rng.choice(longs))
+        words.extend(rng.choice([b"hello", b"world", b"abcdefghijklmnop", b"abcdefgh"]) for _ in range(3))
+    words += [b"m" * 33000 + b"b", b"m" * 33000 + b"a", b"m" * 33000 + b"b", b"m" * 33000]
+    text = b" ".join(words) + b" "
+    tk = capi.Tokens.tokenize_host(text)
+    assert tk.words() == port.tokenize(text)
+    t0 = time.perf_counter()
+    tk.sort()
+    got = tk.words()
+    assert time.perf_counter() - t0 < 5.0
+    assert got == sorted(port.tokenize(text))
+    c = capi.Counter(table_slots=1 << 12, arena_bytes=1 << 24)
+    tk.reduce_sorted(c)
+    assert c.to_dict() == port.wordcount([text])
