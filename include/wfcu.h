@@ -285,6 +285,10 @@ WFCU_API int wfcu_normalize_words_host(const uint8_t* bytes, const uint32_t* len
 /* wfc::tokenize on a device buffer: tokens in text order. */
 WFCU_API int wfcu_tokenize_dev(const uint8_t* dev_text, uint64_t n, void* stream, wfcu_tokens** out);
 WFCU_API int wfcu_tokenize_host(const uint8_t* text, uint64_t n, wfcu_tokens** out);
+/* The tokens of several documents as ONE list (a worker's map stage, proj/src/pipeline.cpp:25-33: the tokens of its
+ * documents back to back): document d is docs[d][0 .. doc_lens[d]); the documents are gathered on the device with a
+ * whitespace byte behind each (a document's end is a fragment's end, text.cpp:55), no host-side concatenation. */
+WFCU_API int wfcu_tokenize_docs_host(const uint8_t* const* docs, const uint64_t* doc_lens, uint64_t n_docs, wfcu_tokens** out);
 WFCU_API void wfcu_tokens_destroy(wfcu_tokens* t);
 WFCU_API int wfcu_tokens_stats(const wfcu_tokens* t, uint64_t* n_tokens, uint64_t* n_bytes);
 /* Packed copy-out: token bytes concatenated + per-token lengths. */

@@ -105,6 +105,7 @@ SIGNATURES = {
     "wfcu_normalize_words_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p]),
     "wfcu_tokenize_dev": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.POINTER(C.c_void_p)]),
     "wfcu_tokenize_host": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p)]),
+    "wfcu_tokenize_docs_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p)]),
     "wfcu_tokens_destroy": (None, [C.c_void_p]),
     "wfcu_tokens_stats": (C.c_int, [C.c_void_p, u64p, u64p]),
     "wfcu_tokens_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),
@@ -445,6 +446,14 @@ class Tokens:
         buf = np.frombuffer(text, dtype=np.uint8)
         h = C.c_void_p()
         check(lib.wfcu_tokenize_host(_ptr(buf) if buf.size else None, buf.size, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def tokenize_docs_host(cls, docs) -> "Tokens":
+        """one list for several host documents (a whitespace byte behind each), gathered on the device"""
+        hd = docs if isinstance(docs, HostDocs) else HostDocs(docs)
+        h = C.c_void_p()
+        check(lib.wfcu_tokenize_docs_host(hd.ptrs, hd.lens, hd.n, C.byref(h)))
         return cls(h)
 
     @classmethod

@@ -1858,6 +1858,30 @@ extern "C" int wfcu_tokenize_host(const uint8_t* text, uint64_t n, wfcu_tokens**
     return rc;
 }
 
+extern "C" int wfcu_tokenize_docs_host(const uint8_t* const* docs, const uint64_t* doc_lens, uint64_t n_docs, wfcu_tokens** out) {
+    if (!out) return fail(WFCU_ERR_INVALID_ARGUMENT, "out is null");
+    *out = nullptr;
+    DeviceState* d;
+    if (int rc = current_device_state(&d)) return rc;
+    if (n_docs && (!docs || !doc_lens)) return fail(WFCU_ERR_INVALID_ARGUMENT, "null argument");
+    u64 total = 0;
+    for (u64 i = 0; i < n_docs; ++i) {
+        if (doc_lens[i] && !docs[i]) return fail(WFCU_ERR_INVALID_ARGUMENT, "document %llu is null", (unsigned long long)i);
+        total += doc_lens[i] + 1;
+    }
+    if (total == 0) return wfcu_tokenize_dev(nullptr, 0, nullptr, out);
+    DevBuf text;
+    CUDA_TRY(text.alloc(total));
+    // every byte that no document overwrites is a separator
+    CUDA_TRY(cudaMemsetAsync(text.p, '\n', total, nullptr));
+    u64 off = 0;
+    for (u64 i = 0; i < n_docs; ++i) {
+        if (doc_lens[i]) CUDA_TRY(cudaMemcpyAsync(text.as<uint8_t>() + off, docs[i], doc_lens[i], cudaMemcpyHostToDevice, nullptr));
+        off += doc_lens[i] + 1;
+    }
+    return wfcu_tokenize_dev(text.as<uint8_t>(), total, nullptr, out);     // synchronises before `text` is released
+}
+
 extern "C" int wfcu_tokens_stats(const wfcu_tokens* t, uint64_t* n_tokens, uint64_t* n_bytes) {
     if (!t) return fail(WFCU_ERR_INVALID_ARGUMENT, "tokens is null");
     if (n_tokens) *n_tokens = t->n;

@@ -355,14 +355,17 @@ RunResult run_wordcount(std::span<const RawDocument> corpus, std::size_t n_worke
     StageTimer timer;
     std::vector<TokensHandle> local(n), received(n);
     timer.run("map", t.map_ns, [&] {
-        std::string shard;      // the worker's documents back to back; a newline ends every document's last fragment
+        // worker j's documents, gathered on the device (a newline ends every document's last fragment)
+        std::vector<const std::uint8_t*> ptrs;
+        std::vector<std::uint64_t> lens;
         for (std::size_t j = 0; j < n; ++j) {
-            shard.clear();
+            ptrs.clear();
+            lens.clear();
             for (std::size_t d = j; d < corpus.size(); d += n) {
-                shard += corpus[d].text;
-                shard += '\n';
+                ptrs.push_back(reinterpret_cast<const std::uint8_t*>(corpus[d].text.data()));
+                lens.push_back(corpus[d].text.size());
             }
-            ok(wfcu_tokenize_host(reinterpret_cast<const std::uint8_t*>(shard.data()), shard.size(), &local[j].h), "map");
+            ok(wfcu_tokenize_docs_host(ptrs.data(), lens.data(), ptrs.size(), &local[j].h), "map");
         }
     });
     timer.run("sort", t.sort_ns, [&] {

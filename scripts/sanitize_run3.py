@@ -44,4 +44,17 @@ assert m.to_dict() == {w: v for w, v in port.wordcount([t2]).items() if len(w) <
 x = capi.synth_uniform(1, 70001, np.float64)
 assert capi.map_reduce_blocked_host(x, capi.MAP_SQUARE_ROOT, 256) == port.map_reduce_blocked(x, capi.MAP_SQUARE_ROOT, 256)
 assert capi.map_reduce_blocked_host(x, capi.MAP_SQUARE_ROOT, 70001) == port.map_reduce_serial(x, capi.MAP_SQUARE_ROOT)
+# long tokens in the key sort: partition, length / window passes over the long sub-array, the check + fix-up safety net
+stem = b"abcdefghijklmnopqrstuvwx"
+lw = [stem + b"yz", stem + b"ab", stem, stem[:20], stem + b"a\x00b", b"k" * 300 + b"b", b"k" * 300 + b"a", b"m" * 33000 + b"b", b"m" * 33000 + b"a"]
+wl = []
+for i in range(600):
+    wl.append(lw[rng.randrange(len(lw) - (0 if i % 100 == 0 else 2))]); wl += [b"hello", b"abcdefghijklmnop", b"world"]
+lt = b" ".join(wl) + b" "
+tl = capi.Tokens.tokenize_host(lt)
+assert tl.words() == port.tokenize(lt)
+tl.sort()
+assert tl.words() == sorted(port.tokenize(lt))
+for _ in range(3):      # recycled buffers of the device-memory cache
+    cc = capi.Counter(table_slots=1 << 12, arena_bytes=1 << 22); tl.reduce_sorted(cc); assert cc.to_dict() == port.wordcount([lt]); cc.close()
 print("sanitize workload 3 ok", os.environ.get("WFCU_COUNT_KERNEL", "3"), os.environ.get("WFCU_COUNT_VARIANT", "auto"))

@@ -187,3 +187,18 @@ def test_sort_with_frequent_long_words(capi, cuda, port):
     c = capi.Counter(table_slots=1 << 12, arena_bytes=1 << 24)
     tk.reduce_sorted(c)
     assert c.to_dict() == port.wordcount([text])
+
+
+@pytest.mark.gpu
+def test_tokenize_docs_is_the_concatenation(capi, cuda, port):
+    """wfcu_tokenize_docs_host: the tokens of several documents as one list, in document order -- no fragment spans
+    a document boundary, empty documents and an empty list are fine"""
+    rng = random.Random(11)
+    docs = [random_text(rng, rng.randint(0, 4000), rng.choice(["ascii", "unicode", "long"])) for _ in range(9)]
+    docs[3] = b""
+    docs[5] = b"endswithoutspace"
+    docs[6] = b"startsrightaway here"
+    want = [w for d in docs for w in port.tokenize(d)]
+    assert capi.Tokens.tokenize_docs_host(docs).words() == want
+    assert capi.Tokens.tokenize_docs_host([]).words() == []
+    assert capi.Tokens.tokenize_docs_host([b"", b""]).words() == []
