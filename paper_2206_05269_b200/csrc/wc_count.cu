@@ -211,9 +211,9 @@ using namespace cnt3;
 // Position n acts as a whitespace byte, so does "position -1".
 // Two variants of the body, both exact: HI = false treats every fragment with a byte >= 0x80 as
 // the slow kernel's business (the ASCII corpora of the benchmarks never pay for anything else);
-// HI = true keeps two-byte letters (accented Latin, Greek, Cyrillic ...) on the fast path.  Every
-// CTA picks its variant from a sample of its own part of the text (wc_count_kernel below): the
-// choice affects speed only.
+// HI = true keeps two-byte letters (accented Latin, Greek, Cyrillic ...) on the fast path, U3K three-byte letters
+// as well, WIDE replaces the two combiners by one for tokens of up to 16 bytes.  The variant is chosen per call from
+// a sample of the text (wc_count_kernel below): the choice affects speed only.
 template <int WARPS, int SETS, int MSLOTS, bool HI, bool WIDE, bool U3K>
 __device__ __forceinline__ void wc_count_body(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, u32 one,
                                               const TableView& gt) {

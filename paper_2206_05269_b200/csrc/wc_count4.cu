@@ -29,8 +29,8 @@
 //   * everything else -- tokens of 9..16 bytes, rows with a byte >= 0x80, fragments that start
 //     out of sight -- goes through a small per-warp queue and a general one-token pass, or to the
 //     deferred list of wc_slow_kernel (tokens longer than 16 bytes, fragments with bytes >= 0x80).
-// Text with two-byte letters runs on the third generation's HI variant (wc_count.cu); every CTA
-// picks its kernel from the same sample of its part of the text.
+// Text with letters >= 0x80 or long words runs on the third generation's other variants (wc_count.cu); the
+// variant is chosen per call from one sample of the text (variant_of_text).
 #include "wc_count_common.cuh"
 
 namespace wfcu {
@@ -590,8 +590,8 @@ wc_count4_kernel(const uint8_t* __restrict__ text, u64 n, u32 rows_per_warp, int
 #define WFCU_COUNT4_MED_SLOTS 256
 #endif
 
-// the ASCII body for every CTA whose sample of the text holds (almost) no byte >= 0x80; warps and the partition of
-// the text are the third generation's, whose HI variant takes the other CTAs (wc_count.cu)
+// the ASCII body for texts whose sample asks for the narrow variant; warps and the partition of the text are the
+// third generation's, whose other variants take the other texts (wc_count.cu)
 cudaError_t wc_count4_launch(const uint8_t* text, u64 n, u32 rows_per_warp, unsigned grid, int force, const TableView& gt,
                              cudaStream_t stream) {
     typedef cnt4::Smem<cntc::kCountVariantWarps, WFCU_COUNT4_SETS, WFCU_COUNT4_MED_SLOTS> SM;
