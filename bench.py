@@ -467,7 +467,7 @@ def run_b200(args) -> None:
                        "seed": SEED, "documents": total_docs, "bytes_per_gpu": nbytes, "job_bytes": job_bytes,
                        "tokens": job_tokens, "distinct_words": job_distinct,
                        "parallelism": f"document shard d mod {world}" + (", hash-partitioned all-to-all merge" + (" (no host sync per step" + (", exchange of step k on a second stream under the count of step k+1" if overlap and ax is not None else "") + ")" if ax is not None else "") if world > 1 else ""),
-                       "l2": "inputs (1 GB per GPU) larger than the 126 MB L2; no flush needed"},
+                       "l2": f"inputs ({nbytes / 1e9:.2f} GB per GPU) larger than the 126 MB L2; no flush needed" if nbytes > (252 << 20) else f"inputs of {nbytes / 1e6:.0f} MB per GPU: NOT larger than twice the 126 MB L2 (reduced --docs run)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if peak else None, "traffic": ncu_traffic("wc_count_kernel", nbytes, w["vocab"]),
                          "traffic_source": ("static: ncu --set full capture of this kernel on this config (profiles/traffic.json), not re-measured in this run"
