@@ -271,7 +271,8 @@ __global__ void tb_long_merge_kernel(TableView t, const uint8_t* __restrict__ re
         bool known = false;
         if (mine && count) {
             u64 i = hash & t.long_mask;
-            for (u64 probes = 0; probes <= t.long_mask; ++probes) {
+            const u64 limit = t.long_mask < kMaxProbes ? t.long_mask : kMaxProbes;      // long_add's bound
+            for (u64 probes = 0; probes <= limit; ++probes) {
                 const u64 r = *reinterpret_cast<volatile u64*>(t.long_ref + i);
                 if (r == 0) break;
                 if (*reinterpret_cast<const u32*>(t.arena + r) == len && *reinterpret_cast<const u32*>(t.arena + r + 4) == hash) {
@@ -307,7 +308,8 @@ __global__ void tb_long_merge_kernel(TableView t, const uint8_t* __restrict__ re
 // counts[key] of the table, 0 if the key is absent (read only: the table is not being written)
 __device__ __forceinline__ bool table_find(const TableView& t, u64 k0, u64 k1, u64* count) {
     u64 i = mix32(k0, k1) & t.mask;
-    for (u64 probes = 0; probes <= t.mask; ++probes) {
+    const u64 limit = t.mask < kMaxProbes ? t.mask : kMaxProbes;      // table_add never places a key further from home
+    for (u64 probes = 0; probes <= limit; ++probes) {
         const Slot s = t.slots[i];
         if (s.k0 == 0) return false;
         if (s.k0 == k0 && s.k1 == k1) { *count = s.count; return true; }

@@ -136,9 +136,14 @@ __device__ __forceinline__ ulonglong2 ld_key(const Slot* s) {
 // re-read through the CAS before the probe moves on.
 // inserted != nullptr: a newly claimed slot is counted there instead of in t.n_used; the caller adds its total
 // with table_note_inserted (a million first occurrences are a million atomics on ONE address otherwise).
+// Probing gives up after kMaxProbes slots: below the load limit a probe sequence is orders of magnitude shorter, and
+// a table that is filling up beyond it (a vocabulary larger than the caller sized the table for) would otherwise
+// make every insertion walk the whole table before the call fails -- minutes instead of a prompt WFCU_ERR_TABLE_FULL.
+constexpr u64 kMaxProbes = 8192;
 __device__ __forceinline__ void table_add(const TableView& t, u64 k0, u64 k1, u64 add, u32* inserted = nullptr) {
     u64 i = mix32(k0, k1) & t.mask;
-    for (u64 probes = 0; probes <= t.mask; ++probes) {
+    const u64 limit = t.mask < kMaxProbes ? t.mask : kMaxProbes;
+    for (u64 probes = 0; probes <= limit; ++probes) {
         Slot* s = t.slots + i;
         ulonglong2 cur = ld_key(s);
         if (cur.x == 0 || (cur.x == k0 && cur.y != k1)) {
@@ -176,7 +181,8 @@ __device__ __forceinline__ void long_add(const TableView& t, u64 rec, u64 add) {
     const u32 len = *reinterpret_cast<const u32*>(t.arena + rec);
     const u32 hash = *reinterpret_cast<const u32*>(t.arena + rec + 4);
     u64 i = hash & t.long_mask;
-    for (u64 probes = 0; probes <= t.long_mask; ++probes) {
+    const u64 limit = t.long_mask < kMaxProbes ? t.long_mask : kMaxProbes;
+    for (u64 probes = 0; probes <= limit; ++probes) {
         u64 r = *reinterpret_cast<volatile u64*>(t.long_ref + i);
         if (r == 0) {
             r = atomicCAS(t.long_ref + i, 0ull, rec);

@@ -26,6 +26,7 @@
 #include <cstdlib>
 
 #include "wfcu_dev.cuh"
+#include "wc_count_common.cuh"
 
 namespace wfcu {
 
@@ -676,6 +677,165 @@ __device__ __forceinline__ void slow_kernel_done(const TableView& gt) {
     }
 }
 
+// One forward walk over the fragment [s, e): a valid non-ASCII whitespace code point ends a piece (text.cpp:45-55),
+// anything else feeds the piece's normalisation.  Decoding against the end of the fragment instead of the end of the
+// piece changes nothing: the byte that follows a piece is the lead of the whitespace character, which no sequence
+// accepts as a continuation byte.
+__device__ void slow_fragment(const uint8_t* text, u64 s, u64 e, const TableView& gt, const EmitView* emp, u32& tokens,
+                              u32& inserted) {
+    Piece p;
+    piece_reset(p);
+    for (u64 pos = s; pos < e;) {
+        const Dec d = utf8_dec(text, pos, e);
+        if (d.valid && uni_space(d.cp)) {
+            tokens += piece_finish(text, p, gt, emp, &inserted);
+            piece_reset(p);
+        } else {
+            piece_feed(p, pos, d);
+        }
+        pos += d.len;
+    }
+    tokens += piece_finish(text, p, gt, emp, &inserted);
+}
+
+// ---- giant fragments ------------------------------------------------------------------------------------
+// A whitespace-free run is ONE fragment however long it is (a base64 blob, a hex dump, minified code), and one thread
+// walks a fragment byte by byte at ~2 MB/s: 64 MiB of 'a' took 32 s.  A fragment whose start is not found within
+// kGiantBytes of its end is handed to the whole warp instead: 16 bytes per lane and step for the backwards search
+// for its start and for one forward pass (any byte >= 0x80?  first / last word character), then -- pure ASCII, the
+// case that occurs -- a parallel copy of the folded bytes into the arena; only the FNV hash of the record stays
+// serial (one lane, 8 bytes per load).  A giant fragment with bytes >= 0x80 falls back to the one-thread walk.
+constexpr u64 kGiantBytes = 4096;
+
+__device__ __forceinline__ uint4 load16_clipped(const uint8_t* text, u64 n, u64 g) {
+    if (g + 16 <= n) return *reinterpret_cast<const uint4*>(text + g);
+    u32 w[4] = {0, 0, 0, 0};
+    for (u64 k = g; k < n; ++k) w[(k - g) >> 2] |= (u32)text[k] << (8 * ((k - g) & 3));
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__device__ void giant_fragment(const uint8_t* text, u64 n, u64 e, const TableView& gt, const EmitView* emp, u32& tokens,
+                               u32& inserted) {
+    const u32 kFull = 0xFFFFFFFFu;
+    const u32 lane = threadIdx.x & 31;
+    // the start: one behind the last ASCII whitespace in front of e (0 if there is none)
+    u64 s = 0;
+    for (u64 pos = e; pos > 0;) {
+        const u64 wb = (pos - 1) & ~511ull;
+        const u64 g = wb + 16 * lane;
+        u32 ws = 0;
+        if (g < pos) {
+            uint4 f;
+            ws = cntc::classify16<false>(load16_clipped(text, n, g), 1u, f).s7 >> 7;
+            if (g + 16 > pos) ws &= (1u << (u32)(pos - g)) - 1u;
+        }
+        const u32 m = __ballot_sync(kFull, ws != 0);
+        if (m) {
+            const int hl = 31 - __clz(m);
+            const u32 w = __shfl_sync(kFull, ws, hl);
+            s = wb + 16 * (u64)hl + (u64)(31 - __clz(w)) + 1;
+            break;
+        }
+        pos = wb;
+    }
+    // one pass over [s, e): bytes >= 0x80, first and last ASCII word character
+    u32 hi = 0;
+    u64 first = ~0ull, last = 0;
+    for (u64 wb = s & ~511ull; wb < e; wb += 512) {
+        const u64 g = wb + 16 * lane;
+        if (g < e && g + 16 > s) {
+            uint4 f;
+            const cntc::Masks m = cntc::classify16<false>(load16_clipped(text, n, g), 1u, f);
+            u32 keep = 0xFFFFu;
+            if (g < s) keep &= ~((1u << (u32)(s - g)) - 1u);
+            if (g + 16 > e) keep &= (1u << (u32)(e - g)) - 1u;
+            const u32 a = (m.a7 >> 7) & keep;
+            hi |= (m.h7 >> 7) & keep;
+            if (a) {
+                const u64 lo = g + (u64)(__ffs(a) - 1), up = g + (u64)(31 - __clz(a));
+                first = first < lo ? first : lo;
+                last = last > up ? last : up;
+            }
+        }
+    }
+    hi = __any_sync(kFull, hi != 0);
+    for (int d = 16; d > 0; d >>= 1) {
+        const u64 of = __shfl_xor_sync(kFull, first, d), ol = __shfl_xor_sync(kFull, last, d);
+        first = first < of ? first : of;
+        last = last > ol ? last : ol;
+    }
+    if (hi) {                           // not the ASCII case: the exact one-thread walk
+        if (lane == 0) slow_fragment(text, s, e, gt, emp, tokens, inserted);
+        __syncwarp();
+        return;
+    }
+    if (first == ~0ull) return;         // no word character
+    const u64 len = last + 1 - first;
+    if (len <= 16) {
+        if (lane == 0) tokens += slow_count_piece(text, first, last + 1, gt, emp, &inserted);
+        __syncwarp();
+        return;
+    }
+    u64 rec = 0;
+    if (lane == 0) {
+        if (len > 0xFFFFFFFFull) atomicOr(gt.status, kStatusArenaFull);
+        else rec = arena_alloc(gt, (u32)len);
+        tokens += 1;                    // as piece_finish: the token exists even if the arena cannot hold it
+    }
+    rec = __shfl_sync(kFull, rec, 0);
+    if (!rec) return;
+    uint8_t* out = gt.arena + rec + 8;
+    // four bytes per lane and step (the record is 8-byte aligned, the source is not), two steps in flight
+    const u64 len4 = len & ~3ull;
+    auto fold4 = [&](u64 i) {
+        const uint8_t* src = text + first + i;
+        u32 w = (u32)src[0] | ((u32)src[1] << 8) | ((u32)src[2] << 16) | ((u32)src[3] << 24);
+        const u32 y = w | 0x20202020u;
+        const u32 upper = (y + 0x1F1F1F1Fu) & ~(y + 0x05050505u) & ~w & 0x80808080u & ~((w & 0x20202020u) << 2);
+        return w | (upper >> 2);        // 'A'..'Z' -> 'a'..'z' (all bytes are < 0x80 here)
+    };
+    u64 i = 4ull * lane;
+    for (; i + 128 < len4; i += 256) {
+        const u32 w0 = fold4(i), w1 = fold4(i + 128);
+        *reinterpret_cast<u32*>(out + i) = w0;
+        *reinterpret_cast<u32*>(out + i + 128) = w1;
+    }
+    for (; i < len4; i += 128) *reinterpret_cast<u32*>(out + i) = fold4(i);
+    for (u64 k = len4 + lane; k < len; k += 32) {
+        u32 c = text[first + k];
+        if (c >= 'A' && c <= 'Z') c |= 0x20u;
+        out[k] = (uint8_t)c;
+    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) {
+        u32 h = 2166136261u;            // fnv32 of the record's bytes (wfcu_dev.cuh), eight bytes per load
+        u64 i = 0;
+        for (; i + 8 <= len; i += 8) {
+            u64 w = *reinterpret_cast<const volatile u64*>(out + i);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) { h = (h ^ (u32)(w & 0xFF)) * 16777619u; w >>= 8; }
+        }
+        for (; i < len; ++i) h = (h ^ *reinterpret_cast<const volatile uint8_t*>(out + i)) * 16777619u;
+        u64 p0 = 0, p1 = 0;
+        for (u32 k = 0; k < 16; ++k) {
+            const u64 byte = *reinterpret_cast<const volatile uint8_t*>(out + k);
+            if (k < 8) p0 |= byte << (56 - 8 * k);
+            else p1 |= byte << (56 - 8 * (k - 8));
+        }
+        *reinterpret_cast<u32*>(gt.arena + rec) = (u32)len;
+        *reinterpret_cast<u32*>(gt.arena + rec + 4) = h;
+        if (emp) {
+            const u64 at = atomicAdd(emp->n_out, 1ull);
+            if (at < emp->cap) emp->out[at] = TokenRec{p0, p1, rec, first};
+        } else {
+            __threadfence();
+            long_add(gt, rec, 1ull);
+        }
+    }
+    __syncwarp();
+}
+
 __global__ void wc_slow_kernel(const uint8_t* __restrict__ text, u64 n, TableView gt, EmitView em, int emit) {
     u64 count = *gt.n_deferred;
     if (count > gt.deferred_cap) count = gt.deferred_cap;
@@ -684,28 +844,27 @@ __global__ void wc_slow_kernel(const uint8_t* __restrict__ text, u64 n, TableVie
         return;
     }
     u32 tokens = 0, inserted = 0;
-    for (u64 idx = (u64)blockIdx.x * blockDim.x + threadIdx.x; idx < count; idx += (u64)gridDim.x * blockDim.x) {
-        const u64 e = gt.deferred[idx];
-        u64 s = e;
-        while (s > 0 && !ascii_space(text[s - 1])) --s;
-        // one forward walk: a valid non-ASCII whitespace code point ends a piece (text.cpp:45-55), anything else
-        // feeds the piece's normalisation.  Decoding against the end of the fragment instead of the end of the
-        // piece changes nothing: the byte that follows a piece is the lead of the whitespace character, which no
-        // sequence accepts as a continuation byte.
-        const EmitView* emp = emit ? &em : nullptr;
-        Piece p;
-        piece_reset(p);
-        for (u64 pos = s; pos < e;) {
-            const Dec d = utf8_dec(text, pos, e);
-            if (d.valid && uni_space(d.cp)) {
-                tokens += piece_finish(text, p, gt, emp, &inserted);
-                piece_reset(p);
-            } else {
-                piece_feed(p, pos, d);
-            }
-            pos += d.len;
+    const EmitView* emp = emit ? &em : nullptr;
+    const u32 lane = threadIdx.x & 31;
+    // warp-uniform trip count: a lane whose fragment turns out to be a giant brings it back to the whole warp
+    for (u64 base = (u64)blockIdx.x * blockDim.x + (threadIdx.x - lane); base < count; base += (u64)gridDim.x * blockDim.x) {
+        const u64 idx = base + lane;
+        u64 e = 0;
+        bool giant = false;
+        if (idx < count) {
+            e = gt.deferred[idx];
+            const u64 stop = e > kGiantBytes ? e - kGiantBytes : 0;
+            u64 s = e;
+            while (s > stop && !ascii_space(text[s - 1])) --s;
+            giant = s == stop && s > 0 && !ascii_space(text[s - 1]);
+            if (!giant) slow_fragment(text, s, e, gt, emp, tokens, inserted);
         }
-        tokens += piece_finish(text, p, gt, emp, &inserted);
+        u32 gm = __ballot_sync(0xFFFFFFFFu, giant);
+        while (gm) {
+            const int src = __ffs(gm) - 1;
+            gm &= gm - 1;
+            giant_fragment(text, n, __shfl_sync(0xFFFFFFFFu, e, src), gt, emp, tokens, inserted);
+        }
     }
     // token and claimed-slot totals: one atomic per warp (a per-token atomic on one address was most of this kernel's time)
     for (int d = 16; d > 0; d >>= 1) {

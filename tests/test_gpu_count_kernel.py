@@ -227,3 +227,36 @@ def test_three_byte_words_stay_on_the_fast_path(capi, cuda, port):
     want = port.wordcount([text])
     assert got == want
     assert got["한국어".encode()] == 800 and got["việt".encode()] == 800 and got["हिन्दी".encode()] == 800
+
+
+@pytest.mark.parametrize("lead", [0, 1, 7, 15, 16, 17, 500, 4095, 4096, 4097])
+def test_giant_fragments(capi, cuda, port, lead):
+    """Fragments longer than the 4 KiB a single thread scans back are handled by a whole warp (wc_slow_kernel,
+    giant_fragment): sizes around the threshold and around the 512-byte windows, every alignment of the start, the
+    fragment at the very start / very end of the text, punctuation at both ends, upper case, a NUL inside, a giant
+    with no word character, one that shrinks to <= 16 bytes, the same giant twice, and giants with bytes >= 0x80
+    (the one-thread fallback).  ASCII blobs like these used to cost 0.5 us per byte."""
+    rng = random.Random(lead)
+    blob = lambda k: bytes(rng.choice(b"abcXYZ019+/=_-") for _ in range(k))
+    pieces = [
+        b"x" * lead,
+        b"...," + blob(5000) + b"!!",
+        blob(4096), blob(4095), blob(4097), blob(4111), blob(4112), blob(4113), blob(8191), blob(70001),
+        b"(" * 6000,                                        # no word character
+        b"." * 5000 + b"Ab9" + b"." * 3000,                 # shrinks to three bytes
+        b"-" * 4500 + b"SixteenBytesLong" + b"-" * 100,     # exactly 16
+        b"-" * 4500 + b"SeventeenBytesLng" + b"-" * 100,    # 17
+        b"q" * 3000 + b"\x00" + b"Q" * 3000,
+        b"dup" + b"D" * 6000, b"DUP" + b"d" * 6000,         # equal after folding
+        b"a" * 3000 + "é".encode() + b"b" * 3000,           # two-byte letter inside: fallback
+        "あ".encode() * 2000,                                # three-byte letters only
+        b"z" * 5000 + b"\xff" + b"z" * 10,                   # an invalid byte
+        b"m" * 5000 + "　".encode() + b"n" * 5000,       # ideographic space splits it
+    ]
+    rng.shuffle(pieces)
+    text = b" ".join(pieces)
+    check(capi, cuda, port, text, arena_bytes=8 << 20, deferred_slots=1 << 16)
+    check(capi, cuda, port, blob(9000), arena_bytes=8 << 20)                      # the whole text is one fragment
+    check(capi, cuda, port, b" " * lead + blob(9000) + b"\n", arena_bytes=8 << 20)
+    tk = capi.Tokens.tokenize_host(text)                                          # the emitting form of the same kernel
+    assert tk.words() == port.tokenize(text)

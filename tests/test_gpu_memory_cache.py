@@ -57,3 +57,30 @@ def test_create_destroy_is_cheap(cuda, capi):
     for _ in range(5):
         capi.Counter().close()
     assert (time.perf_counter() - t0) / 5 < 0.02
+
+
+@pytest.mark.gpu
+def test_undersized_tables_fail_promptly(cuda, capi):
+    """a vocabulary (or a set of long tokens) far larger than the table was sized for is reported as TABLE_FULL /
+    ARENA_FULL within a bounded number of probes per insertion -- not after every insertion has walked the whole
+    table (64 MiB of random bytes into a 1 M-slot long table took 33 s before the bound)"""
+    import torch
+    rng = np.random.default_rng(5)
+    words = rng.integers(0, 26, (600_000, 8), dtype=np.uint8) + ord("a")
+    text = np.concatenate([words, np.full((600_000, 1), 32, np.uint8)], axis=1).reshape(-1)      # ~600 k distinct words
+    dev = torch.from_numpy(text).cuda()
+    c = capi.Counter(table_slots=1 << 14)
+    t0 = time.perf_counter()
+    with pytest.raises(capi.WfcuError) as e:
+        c.count_dev(dev.data_ptr(), text.size)
+        c.status()
+    assert e.value.code == capi.ERR_TABLE_FULL and time.perf_counter() - t0 < 5.0
+    longs = rng.integers(0, 26, (300_000, 20), dtype=np.uint8) + ord("a")
+    text2 = np.concatenate([longs, np.full((300_000, 1), 32, np.uint8)], axis=1).reshape(-1)   # 300 k distinct long tokens
+    dev2 = torch.from_numpy(text2).cuda()
+    c2 = capi.Counter(table_slots=1 << 14, long_slots=1 << 12, arena_bytes=64 << 20, deferred_slots=1 << 20)
+    t0 = time.perf_counter()
+    with pytest.raises(capi.WfcuError) as e:
+        c2.count_dev(dev2.data_ptr(), text2.size)
+        c2.status()
+    assert e.value.code == capi.ERR_ARENA_FULL and time.perf_counter() - t0 < 5.0
