@@ -142,6 +142,13 @@ sn_write_kernel(const uint8_t* __restrict__ text, u64 n, u64 n_blocks, const uin
                 v = make_uint4(w[0], w[1], w[2], w[3]);
             }
         }
+        // a CTA whose 4 KiB hold nothing to replace (all of a valid text's) and whose output is 16-byte aligned copies
+        // its registers out: no staging, no scan
+        if (__syncthreads_and(valid == 16 && keep == 0xFFFFu) && ((reinterpret_cast<uintptr_t>(out) + boff) & 15) == 0) {
+            if (boff + kSnBlockBytes <= out_cap) *reinterpret_cast<uint4*>(out + boff + 16 * threadIdx.x) = v;
+            if (b + 1 == n_blocks && threadIdx.x == 0) *total = boff + kSnBlockBytes;
+            continue;
+        }
         const u32 size = valid + 2 * (valid - __popc(keep));
         // exclusive scan of the chunk sizes inside the CTA
         u32 incl = size;
