@@ -65,7 +65,6 @@ struct SortScratch {
     TokenRec* alt;
     u64* hist;
     u64* tmp;
-    int* flag;
 };
 u64 sort_hist_words(u64 n);
 u64 sort_n_tiles(u64 n);
@@ -418,7 +417,9 @@ extern "C" int wfcu_map_reduce_blocked_dev(const void* dev_values, int dtype, ui
 static int upload(const void* host, uint64_t bytes, void** dev) {
     *dev = nullptr;
     if (bytes == 0) return WFCU_OK;
-    CUDA_TRY(scratch_alloc(dev, bytes));
+    // + 16: the tokenizer's last chunk is fetched with cp.async src-size < 16 (only the bytes below n are read, but
+    // compute-sanitizer checks the full 16) -- keep the whole chunk inside the allocation
+    CUDA_TRY(scratch_alloc(dev, bytes + 16));
     cudaError_t e = cudaMemcpy(*dev, host, bytes, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         scratch_free(*dev);
@@ -740,15 +741,14 @@ static int counter_pull_sorted(wfcu_counter* c, cudaStream_t s, std::vector<Host
     LaunchTally tally;
     std::vector<TokenRec> hs(n_inline);
     if (n_inline) {
-        DevBuf dense, alt, hist, tmp, flag;
+        DevBuf dense, alt, hist, tmp;
         const u64 hw = sort_hist_words(n_inline);
         CUDA_TRY(dense.alloc(sizeof(TokenRec) * n_inline));
         CUDA_TRY(alt.alloc(sizeof(TokenRec) * n_inline));
         CUDA_TRY(hist.alloc(sizeof(u64) * hw));
         CUDA_TRY(tmp.alloc(sizeof(u64) * scan_tmp_words(hw)));
-        CUDA_TRY(flag.alloc(sizeof(int)));
         CUDA_TRY(tb_compact_recs(c->v, dense.as<TokenRec>(), n_inline, c->counters + 7, c->sm_count, s, &tally.n));
-        SortScratch sc{alt.as<TokenRec>(), hist.as<u64>(), tmp.as<u64>(), flag.as<int>()};
+        SortScratch sc{alt.as<TokenRec>(), hist.as<u64>(), tmp.as<u64>()};
         CUDA_TRY(tokens_sort(dense.as<TokenRec>(), n_inline, /*by_position=*/false, nullptr, sc, c->sm_count, s, &tally.n));
         CUDA_TRY(cudaMemcpyAsync(hs.data(), dense.p, sizeof(TokenRec) * n_inline, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
@@ -817,7 +817,7 @@ extern "C" int wfcu_counter_export(wfcu_counter* c, void* stream, uint8_t* key_b
             if (int rc = ex_reserve(c, i, need[i])) return rc;
         TokenRec* dense = static_cast<TokenRec*>(c->ex_buf[0]);
         SortScratch sc{static_cast<TokenRec*>(c->ex_buf[1]), static_cast<u64*>(c->ex_buf[2]),
-                       static_cast<u64*>(c->ex_buf[3]), static_cast<int*>(c->ex_buf[4])};
+                       static_cast<u64*>(c->ex_buf[3])};
         uint8_t* d_bytes = static_cast<uint8_t*>(c->ex_buf[6]);
         u64* d_counts = static_cast<u64*>(c->ex_buf[7]);
         u32* d_lens = reinterpret_cast<u32*>(d_counts + n);
@@ -872,15 +872,14 @@ extern "C" int wfcu_counter_top_k(wfcu_counter* c, uint64_t k, void* stream, uin
     std::vector<HostEntry> cand;
     LaunchTally tally;
     if (n_inline && k) {
-        DevBuf dense, alt, hist, tmp, flag;
+        DevBuf dense, alt, hist, tmp;
         const u64 hw = sort_hist_words(n_inline);
         CUDA_TRY(dense.alloc(sizeof(TokenRec) * n_inline));
         CUDA_TRY(alt.alloc(sizeof(TokenRec) * n_inline));
         CUDA_TRY(hist.alloc(sizeof(u64) * hw));
         CUDA_TRY(tmp.alloc(sizeof(u64) * scan_tmp_words(hw)));
-        CUDA_TRY(flag.alloc(sizeof(int)));
         CUDA_TRY(tb_compact_recs(c->v, dense.as<TokenRec>(), n_inline, c->counters + 7, c->sm_count, s, &tally.n));
-        SortScratch sc{alt.as<TokenRec>(), hist.as<u64>(), tmp.as<u64>(), flag.as<int>()};
+        SortScratch sc{alt.as<TokenRec>(), hist.as<u64>(), tmp.as<u64>()};
         CUDA_TRY(tokens_sort(dense.as<TokenRec>(), n_inline, /*by_position=*/true, nullptr, sc, c->sm_count, s, &tally.n));
         // threshold = count of the k-th largest inline row (long rows can only push it up)
         const u64 kth = n_inline > k ? n_inline - k : 0;
@@ -997,7 +996,7 @@ extern "C" int wfcu_counter_distinctive(wfcu_counter* target, wfcu_counter* othe
     u64 n_union = 0;
     LaunchTally tally;
     if (cap) {
-        DevBuf recs, alt, ct, co, hist, tmp, flag, oct, oco;
+        DevBuf recs, alt, ct, co, hist, tmp, oct, oco;
         const u64 hw = sort_hist_words(cap);
         CUDA_TRY(recs.alloc(sizeof(TokenRec) * cap));
         CUDA_TRY(alt.alloc(sizeof(TokenRec) * cap));
@@ -1005,7 +1004,6 @@ extern "C" int wfcu_counter_distinctive(wfcu_counter* target, wfcu_counter* othe
         CUDA_TRY(co.alloc(sizeof(u64) * cap));
         CUDA_TRY(hist.alloc(sizeof(u64) * hw));
         CUDA_TRY(tmp.alloc(sizeof(u64) * scan_tmp_words(hw)));
-        CUDA_TRY(flag.alloc(sizeof(int)));
         u64* cursor = target->counters + 10;     // [10] rows of the union, [11] words in both tables
         CUDA_TRY(tb_union_rows(target->v, others->v, recs.as<TokenRec>(), ct.as<u64>(), co.as<u64>(), cap, cursor,
                                target->sm_count, s, &tally.n));
@@ -1014,7 +1012,7 @@ extern "C" int wfcu_counter_distinctive(wfcu_counter* target, wfcu_counter* othe
         CUDA_TRY(cudaMemcpyAsync(&n_union, cursor, sizeof(u64), cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
         if (n_union && k) {
-            SortScratch sc{alt.as<TokenRec>(), hist.as<u64>(), tmp.as<u64>(), flag.as<int>()};
+            SortScratch sc{alt.as<TokenRec>(), hist.as<u64>(), tmp.as<u64>()};
             CUDA_TRY(tokens_sort(recs.as<TokenRec>(), n_union, /*by_position=*/true, nullptr, sc, target->sm_count, s, &tally.n));
             const u64 kth = n_union > k ? n_union - k : 0;
             TokenRec pivot;
@@ -1709,13 +1707,12 @@ extern "C" void wfcu_tokens_destroy(wfcu_tokens* t) {
 
 static int sort_device_tokens(wfcu_tokens* t, bool by_position, cudaStream_t s) {
     if (t->n < 2) return WFCU_OK;
-    DevBuf alt, hist, tmp, flag;
+    DevBuf alt, hist, tmp;
     const u64 hw = sort_hist_words(t->n);
     CUDA_TRY(alt.alloc(sizeof(TokenRec) * t->n));
     CUDA_TRY(hist.alloc(sizeof(u64) * hw));
     CUDA_TRY(tmp.alloc(sizeof(u64) * scan_tmp_words(hw)));
-    CUDA_TRY(flag.alloc(sizeof(int)));
-    SortScratch sc{alt.as<TokenRec>(), hist.as<u64>(), tmp.as<u64>(), flag.as<int>()};
+    SortScratch sc{alt.as<TokenRec>(), hist.as<u64>(), tmp.as<u64>()};
     LaunchTally tally;
     CUDA_TRY(tokens_sort(t->recs, t->n, by_position, t->arena, sc, t->sm_count, s, &tally.n));
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -1871,7 +1868,7 @@ extern "C" int wfcu_tokenize_docs_host(const uint8_t* const* docs, const uint64_
     }
     if (total == 0) return wfcu_tokenize_dev(nullptr, 0, nullptr, out);
     DevBuf text;
-    CUDA_TRY(text.alloc(total));
+    CUDA_TRY(text.alloc(total + 16));     // + 16: see upload()
     // every byte that no document overwrites is a separator
     CUDA_TRY(cudaMemsetAsync(text.p, '\n', total, nullptr));
     u64 off = 0;

@@ -350,7 +350,6 @@ struct SortScratch {
     TokenRec* alt;   // n records
     u64* hist;       // 256 * n_tiles
     u64* tmp;        // scan scratch
-    int* flag;       // skip flag
 };
 
 u64 sort_n_tiles(u64 n) { return (n + kTileItems - 1) / kTileItems; }
