@@ -282,7 +282,8 @@ WFCU_API int wfcu_utf8_sanitize_host(const uint8_t* text, uint64_t n, uint8_t* o
 WFCU_API int wfcu_normalize_words_host(const uint8_t* bytes, const uint32_t* lens, uint64_t n_frag,
                                        uint8_t* out_bytes, uint64_t out_cap, uint32_t* out_lens);
 
-/* wfc::tokenize on a device buffer: tokens in text order. */
+/* wfc::tokenize on a device buffer: tokens in text order.  dev_text is 16-byte aligned and its last, partial 16-byte
+ * chunk lies inside the allocation (any cudaMalloc'd buffer does; only the bytes below n are read). */
 WFCU_API int wfcu_tokenize_dev(const uint8_t* dev_text, uint64_t n, void* stream, wfcu_tokens** out);
 WFCU_API int wfcu_tokenize_host(const uint8_t* text, uint64_t n, wfcu_tokens** out);
 /* The tokens of several documents as ONE list (a worker's map stage, proj/src/pipeline.cpp:25-33: the tokens of its
