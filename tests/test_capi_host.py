@@ -121,3 +121,91 @@ def test_async_exchange_region_capacity():
     assert AsyncExchange(Table(), Ops(), Dist(4)).cap == 524288 + 1                 # no hint: cannot overflow
     assert AsyncExchange(Table(), Ops(), Dist(1), entries_hint=10 ** 9).cap == 524288 + 1
     assert AsyncExchange(Table(), Ops(), Dist(8), entries_hint=50000).send.rows == 8 * (2 * 6250 + 1024 + 1)
+
+
+def test_async_exchange_overlap_protocol():
+    """AsyncExchange(overlap=True) with recording stand-ins for the device steps: the collective and the merge of a step
+    are issued on the second stream behind an event recorded after the partition; the two send buffers alternate; the
+    partition that reuses a buffer first waits for the event of the merge that read it two steps earlier; slot_ready()
+    waits for the same event before the caller resets the owned table; finish() joins the streams before reading the
+    flags."""
+    import contextlib
+    from paper_2206_05269_b200.exchange import AsyncExchange
+
+    log = []
+
+    class Table:
+        def __init__(self, name): self.name = name
+        def max_entries(self): return 4096
+
+    class Flags(list):
+        def clone(self): return Flags(self)
+        def cpu(self): return self
+        def tolist(self): return list(self)
+        def zero_(self):
+            for i in range(len(self)): self[i] = 0
+
+    class Counts:
+        def __init__(self, n): self.v = Flags([0] * n)
+        def __getitem__(self, s): return Flags(self.v[s]) if isinstance(s, slice) and s.stop is not None else self
+        def zero_(self): self.v.zero_()
+
+    class Torch:
+        int64 = "i64"
+        @staticmethod
+        def zeros(n, dtype=None, device=None): return Counts(n)
+
+    class Entries:
+        device = "cpu"
+        def __init__(self, name): self.name = name
+
+    class Ops:
+        torch = Torch
+        def __init__(self): self.cur, self.n_buf, self.n_ev = "main", 0, 0
+        def empty_entries(self, n):
+            self.n_buf += 1
+            return Entries(f"buf{self.n_buf}")
+        def new_stream(self): return "comm"
+        def record(self):
+            self.n_ev += 1
+            log.append(("record", self.cur, self.n_ev))
+            return self.n_ev
+        def wait(self, ev): log.append(("wait", self.cur, ev))
+        @contextlib.contextmanager
+        def on(self, stream):
+            prev, self.cur = self.cur, stream
+            try: yield
+            finally: self.cur = prev
+        def partition_framed(self, local, world, send, cap, counts): log.append(("partition", self.cur, send.name))
+        def merge_regions(self, owned, recv, world, cap, counts): log.append(("merge", self.cur, owned.name))
+
+    class Dist:
+        def get_world_size(self, group=None): return 2
+        def all_to_all_single(self, recv, send, group=None): log.append(("a2a", ops.cur, send.name))
+        def all_reduce(self, t, group=None): log.append(("all_reduce", ops.cur))
+
+    ops = Ops()
+    ax = AsyncExchange(Table("local"), ops, Dist(), entries_hint=100, overlap=True)
+    assert ax.overlap
+    owned = [Table("own0"), Table("own1")]
+    for k in range(4):
+        ax.slot_ready()
+        log.append(("reset", ops.cur, owned[k & 1].name))
+        ax.step(Table("local"), owned[k & 1])
+    ax.finish()
+    sends = [e[2] for e in log if e[0] == "partition"]
+    assert sends[0] != sends[1] and sends == [sends[0], sends[1]] * 2                 # two send buffers alternate
+    assert all(e[1] == "comm" for e in log if e[0] in ("a2a", "merge"))               # collective + merge: second stream
+    assert all(e[1] == "main" for e in log if e[0] in ("partition", "reset"))         # count side: the caller's stream
+    # step k: partition, record(main)=r, [comm: wait(r), a2a, merge, record(comm)=m_k]
+    merged_ev = [e[2] for e in log if e[0] == "record" and e[1] == "comm"]
+    assert len(merged_ev) == 4
+    for k in (2, 3):     # reuse of slot k & 1: both the reset of the owned table and the partition wait for m_{k-2} first
+        start = [i for i, e in enumerate(log) if e[0] == "reset"][k]
+        before = log[:start]
+        assert ("wait", "main", merged_ev[k - 2]) in before[-3:]
+        part = [i for i, e in enumerate(log) if e[0] == "partition"][k]
+        assert ("wait", "main", merged_ev[k - 2]) in log[start:part]
+    # finish(): the caller's stream waits for the last merge before the flags are reduced
+    i_red = log.index(("all_reduce", "main"))
+    assert ("wait", "main", merged_ev[-1]) in log[:i_red] and log.index(("wait", "main", merged_ev[-1])) > [i for i, e in enumerate(log) if e[0] == "merge"][-1]
