@@ -220,6 +220,30 @@ __global__ void sort_fill_window_kernel(TokenRec* __restrict__ recs, u64 n, cons
     }
 }
 
+// out[0] = longest length below `longest`, out[1] = records whose length equals `longest`: windows behind the end of
+// the SECOND longest string cannot order anything (at most one record has bytes there), so one 30 KB token in a list
+// does not cost 3 700 window rounds.
+__global__ void sort_second_longest_kernel(const TokenRec* __restrict__ recs, u64 n, const uint8_t* __restrict__ arena,
+                                           u64 longest, u64* __restrict__ out) {
+    u64 below = 0, equal = 0;
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const u64 ext = recs[i].ext;
+        if (!ext) continue;
+        const u64 len = *reinterpret_cast<const u32*>(arena + ext);
+        if (len == longest) ++equal;
+        else below = below > len ? below : len;
+    }
+    for (int d = 16; d > 0; d >>= 1) {
+        const u64 ob = __shfl_xor_sync(0xFFFFFFFFu, below, d);
+        below = below > ob ? below : ob;
+        equal += __shfl_xor_sync(0xFFFFFFFFu, equal, d);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(reinterpret_cast<unsigned long long*>(out), (unsigned long long)below);
+        atomicAdd(reinterpret_cast<unsigned long long*>(out + 1), (unsigned long long)equal);
+    }
+}
+
 // Safety net behind the window passes (which stop at kLongWindows * 8 bytes): every long record compares itself with
 // its predecessor, in parallel, and only if some pair with the same prefix descends (*descents != 0 -- strings that
 // agree in their first 32 KiB) does the fix-up run: a stable insertion sort by the full string, one thread per run.
@@ -427,7 +451,17 @@ cudaError_t tokens_sort(TokenRec* recs, u64 n, bool by_position, const uint8_t* 
                 }
                 if (w < 0) {
                     const u64 longest = r3[0];
-                    windows = (int)std::min<u64>((longest > 16 ? (longest - 16 + 7) / 8 : 0), (u64)kLongWindows);
+                    const u64 zero2[2] = {0, 0};
+                    e = cudaMemcpyAsync(sc.tmp + 4, zero2, sizeof(zero2), cudaMemcpyHostToDevice, s);
+                    if (e != cudaSuccess) break;
+                    sort_second_longest_kernel<<<blocks_for(m, 256, sm), 256, 0, s>>>(sa, m, arena, longest, sc.tmp + 4);
+                    *launches += 1;
+                    u64 r2[2];
+                    e = cudaMemcpyAsync(r2, sc.tmp + 4, sizeof(r2), cudaMemcpyDeviceToHost, s);
+                    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+                    if (e != cudaSuccess) break;
+                    const u64 second = r2[1] >= 2 ? longest : r2[0];     // where two strings can still differ
+                    windows = (int)std::min<u64>((second > 16 ? (second - 16 + 7) / 8 : 0), (u64)kLongWindows);
                     w = windows;
                 }
                 if (--w < 0) break;

@@ -9,8 +9,9 @@ cases = {
     "accented": b"hello world " * 20 + "zzzéabcdefghijklmnop ".encode(),
     "shared 24": b"hello world " * 20 + b"abcdefghijklmnopqrstuvwxYZ " + b"abcdefghijklmnopqrstuvwxAB ",
 }
+cases["one 30 KB token"] = None
 for name, unit in cases.items():
-    text = unit * (4_000_000 // len(unit))
+    text = unit * (4_000_000 // len(unit)) if unit else b"hello world " * 300000 + b"k" * 30000 + b" " + b"zzzabcdefghijklmnopq " * 1000
     tk = capi.Tokens.tokenize_host(text)
     torch.cuda.synchronize(); t0 = time.perf_counter()
     tk.sort()
