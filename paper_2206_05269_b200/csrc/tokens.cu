@@ -174,7 +174,10 @@ __device__ __forceinline__ int long_compare(const uint8_t* arena, u64 a, u64 b) 
     const uint8_t* pa = arena + a + 8;
     const uint8_t* pb = arena + b + 8;
     const u32 m = la < lb ? la : lb;
-    for (u32 i = 16; i < m; ++i) {   // the first 16 bytes are known equal
+    u32 i = 16;                      // the first 16 bytes are known equal
+    for (; i + 8 <= m; i += 8)       // records are 8-byte aligned: a word at a time up to the first difference
+        if (*reinterpret_cast<const u64*>(pa + i) != *reinterpret_cast<const u64*>(pb + i)) break;
+    for (; i < m; ++i) {
         if (pa[i] != pb[i]) return pa[i] < pb[i] ? -1 : 1;
     }
     return la < lb ? -1 : (la > lb ? 1 : 0);
@@ -186,6 +189,7 @@ __device__ __forceinline__ int long_compare(const uint8_t* arena, u64 a, u64 b) 
 // significant pass of all, with the length (a string sorts behind its own prefixes; zero padding alone cannot tell
 // "ab" from "ab\0").  range[5] / range[6] collect OR / AND of the key so that constant digit positions are skipped,
 // range[4] the longest string (window < 0 only).
+__device__ __forceinline__ u64 long_window_key(const uint8_t* arena, u64 ext, int window);
 __global__ void sort_fill_window_kernel(TokenRec* __restrict__ recs, u64 n, const uint8_t* __restrict__ arena, int window,
                                         u64* __restrict__ range) {
     u64 o = 0, a = ~0ull, longest = 0;
@@ -198,10 +202,7 @@ __global__ void sort_fill_window_kernel(TokenRec* __restrict__ recs, u64 n, cons
                 key = len;
                 longest = longest > len ? longest : len;
             } else {
-                const uint8_t* p = arena + ext + 8;
-                const u32 lo = 16u + 8u * (u32)window;
-                const u32 hi = len < lo + 8u ? len : lo + 8u;
-                for (u32 j = lo; j < hi; ++j) key |= (u64)p[j] << (8 * (lo + 7 - j));
+                key = long_window_key(arena, ext, window);
             }
         }
         recs[i].pos = key;
@@ -217,6 +218,36 @@ __global__ void sort_fill_window_kernel(TokenRec* __restrict__ recs, u64 n, cons
         atomicOr(range + 5, o);
         atomicAnd(range + 6, a);
         if (window < 0) atomicMax(reinterpret_cast<unsigned long long*>(range + 4), (unsigned long long)longest);
+    }
+}
+
+// OR / AND of the window keys of windows [w0, w0 + count) over all long records: out[2 * j] |= key, out[2 * j + 1] &= key
+// for window w0 + j.  One launch and one host read decide for a batch of windows which of them need a pass at all
+// (a pair of identical 8 MiB tokens is 4096 windows in which nothing varies).
+constexpr int kWindowBatch = 64;
+__device__ __forceinline__ u64 long_window_key(const uint8_t* arena, u64 ext, int window) {
+    const u32 len = *reinterpret_cast<const u32*>(arena + ext);
+    const uint8_t* p = arena + ext + 8;
+    const u32 lo = 16u + 8u * (u32)window;
+    const u32 hi = len < lo + 8u ? len : lo + 8u;
+    u64 key = 0;
+    for (u32 j = lo; j < hi; ++j) key |= (u64)p[j] << (8 * (lo + 7 - j));
+    return key;
+}
+__global__ void sort_window_range_kernel(const TokenRec* __restrict__ recs, u64 n, const uint8_t* __restrict__ arena, int w0,
+                                         int count, u64* __restrict__ out) {
+    for (int j = 0; j < count; ++j) {
+        u64 o = 0, a = ~0ull;
+        for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+            const u64 ext = recs[i].ext;
+            const u64 key = ext ? long_window_key(arena, ext, w0 + j) : 0;
+            o |= key; a &= key;
+        }
+        for (int d = 16; d > 0; d >>= 1) {
+            o |= __shfl_xor_sync(0xFFFFFFFFu, o, d);
+            a &= __shfl_xor_sync(0xFFFFFFFFu, a, d);
+        }
+        if ((threadIdx.x & 31) == 0) { atomicOr(out + 2 * j, o); atomicAnd(out + 2 * j + 1, a); }
     }
 }
 
@@ -432,39 +463,59 @@ cudaError_t tokens_sort(TokenRec* recs, u64 n, bool by_position, const uint8_t* 
             // last one to the first; the stable passes over k1 / k0 below keep that order inside equal prefixes
             TokenRec* sa = a + (n - m);
             TokenRec* sb = b + (n - m);
-            int windows = 0;
-            for (int w = -1; e == cudaSuccess; ) {
+            auto fill = [&](int w, u64* r3) {              // keys of window w into pos; r3 (if asked for): longest, OR, AND
                 const u64 init2[3] = {0, 0, ~0ull};
                 e = cudaMemcpyAsync(sc.tmp + 4, init2, sizeof(init2), cudaMemcpyHostToDevice, s);
-                if (e != cudaSuccess) break;
+                if (e != cudaSuccess) return;
                 sort_fill_window_kernel<<<blocks_for(m, 256, sm), 256, 0, s>>>(sa, m, arena, w, sc.tmp);
                 *launches += 1;
-                u64 r3[3];
-                e = cudaMemcpyAsync(r3, sc.tmp + 4, sizeof(r3), cudaMemcpyDeviceToHost, s);
+                if (!r3) return;
+                e = cudaMemcpyAsync(r3, sc.tmp + 4, 3 * sizeof(u64), cudaMemcpyDeviceToHost, s);
                 if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-                if (e != cudaSuccess) break;
-                const u64 vary = r3[1] ^ r3[2];
+            };
+            auto passes = [&](u64 vary) {
                 for (int p = 0; p < 8 && e == cudaSuccess; ++p) {
                     if (!((vary >> (8 * p)) & 0xFF)) continue;
                     e = radix_pass(sa, sb, m, 1, p, sc, sm, s, launches);
                     TokenRec* t = sa; sa = sb; sb = t;
                 }
-                if (w < 0) {
-                    const u64 longest = r3[0];
-                    const u64 zero2[2] = {0, 0};
-                    e = cudaMemcpyAsync(sc.tmp + 4, zero2, sizeof(zero2), cudaMemcpyHostToDevice, s);
-                    if (e != cudaSuccess) break;
+            };
+            u64 r3[3] = {0, 0, 0};
+            fill(-1, r3);                                   // least significant: the length
+            if (e == cudaSuccess) passes(r3[1] ^ r3[2]);
+            int windows = 0;
+            if (e == cudaSuccess) {
+                const u64 longest = r3[0];
+                const u64 zero2[2] = {0, 0};
+                e = cudaMemcpyAsync(sc.tmp + 4, zero2, sizeof(zero2), cudaMemcpyHostToDevice, s);
+                if (e == cudaSuccess) {
                     sort_second_longest_kernel<<<blocks_for(m, 256, sm), 256, 0, s>>>(sa, m, arena, longest, sc.tmp + 4);
                     *launches += 1;
                     u64 r2[2];
                     e = cudaMemcpyAsync(r2, sc.tmp + 4, sizeof(r2), cudaMemcpyDeviceToHost, s);
                     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-                    if (e != cudaSuccess) break;
                     const u64 second = r2[1] >= 2 ? longest : r2[0];     // where two strings can still differ
                     windows = (int)std::min<u64>((second > 16 ? (second - 16 + 7) / 8 : 0), (u64)kLongWindows);
-                    w = windows;
                 }
-                if (--w < 0) break;
+            }
+            // the windows from the last one to the first, a batch at a time: which of them vary at all is one launch
+            // and one host read per batch (sc.hist is free between passes)
+            for (int hi = windows; hi > 0 && e == cudaSuccess; hi -= kWindowBatch) {
+                const int lo = hi > kWindowBatch ? hi - kWindowBatch : 0;
+                u64 init[2 * kWindowBatch], got[2 * kWindowBatch];
+                for (int j = 0; j < kWindowBatch; ++j) { init[2 * j] = 0; init[2 * j + 1] = ~0ull; }
+                e = cudaMemcpyAsync(sc.hist, init, sizeof(init), cudaMemcpyHostToDevice, s);
+                if (e != cudaSuccess) break;
+                sort_window_range_kernel<<<blocks_for(m, 256, sm), 256, 0, s>>>(sa, m, arena, lo, hi - lo, sc.hist);
+                *launches += 1;
+                e = cudaMemcpyAsync(got, sc.hist, sizeof(got), cudaMemcpyDeviceToHost, s);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+                for (int w = hi - 1; w >= lo && e == cudaSuccess; --w) {
+                    const u64 vary = got[2 * (w - lo)] ^ got[2 * (w - lo) + 1];
+                    if (!vary) continue;
+                    fill(w, nullptr);
+                    passes(vary);
+                }
             }
             if (e == cudaSuccess && sa != a + (n - m))
                 e = cudaMemcpyAsync(a + (n - m), sa, sizeof(TokenRec) * m, cudaMemcpyDeviceToDevice, s);

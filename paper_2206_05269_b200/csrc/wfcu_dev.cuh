@@ -200,9 +200,10 @@ __device__ __forceinline__ void long_add(const TableView& t, u64 rec, u64 add) {
             const uint8_t* a = t.arena + r + 8;
             const uint8_t* b = t.arena + rec + 8;
             bool same = true;
-            for (u32 k = 0; k < len; ++k) {
-                if (a[k] != b[k]) { same = false; break; }
-            }
+            u32 k = 0;
+            for (; k + 8 <= len && same; k += 8)      // records are 8-byte aligned
+                same = *reinterpret_cast<const u64*>(a + k) == *reinterpret_cast<const u64*>(b + k);
+            for (; k < len && same; ++k) same = a[k] == b[k];
             if (same) {
                 atomicAdd(t.long_count + i, add);
                 return;
