@@ -839,10 +839,7 @@ __device__ void giant_fragment(const uint8_t* text, u64 n, u64 e, const TableVie
 __global__ void wc_slow_kernel(const uint8_t* __restrict__ text, u64 n, TableView gt, EmitView em, int emit) {
     u64 count = *gt.n_deferred;
     if (count > gt.deferred_cap) count = gt.deferred_cap;
-    if (count == 0) {
-        slow_kernel_done(gt);
-        return;
-    }
+    if (count == 0) return;     // nothing to consume, nothing to reset: every CTA sees the same zero (no ticket traffic)
     u32 tokens = 0, inserted = 0;
     const EmitView* emp = emit ? &em : nullptr;
     const u32 lane = threadIdx.x & 31;
